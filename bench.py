@@ -1,0 +1,462 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Hive table hot path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "static build + lookup"): a step clears the
+table, inserts 2^26 unique uniform keys into 2,207,529 buckets (LF 0.95,
+growth off) and runs 2^26 finds with 50% hits.  Inputs (256 MiB keys, 256 MiB
+values, 256 MiB queries) and the 565 MB table are all larger than L2, so no L2
+flush is needed between steps.
+
+`python bench.py [--gpus N --steps K --warmup W] [--impl reference]`
+N > 1 runs under torchrun: each rank owns a hash-partitioned shard and its own
+2^26-key batch (weak scaling); keys are routed by an NCCL all-to-all.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import gen  # noqa: E402
+
+METRIC = "G lookups/s and G updates/s at 95% load, 1/2/4/8 B200, % of HBM roofline"
+UNIT = "G ops/s"
+N_LOG2 = 26
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n-log2", type=int, default=N_LOG2, help="keys per rank (debug only)")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------------------
+# clocks sampled during the timed region (NVML)
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons)}
+
+
+# ---------------------------------------------------------------------------------------
+# CPU oracle baseline / reference arm
+# ---------------------------------------------------------------------------------------
+def oracle_sample(n_log2: int):
+    """Oracle (as it stands) on a bounded sample of the workload: build 2^n_log2
+    keys to LF 0.95, then 2^n_log2 finds with 50% hits. Returns (ops, seconds)."""
+    import oracle
+    n = 1 << n_log2
+    nb = -(-n * 100 // (95 * 32))
+    ids = np.arange(n, dtype=np.uint32)
+    keys, vals = gen.keys_of(ids), gen.vals_of(ids)
+    qids, _ = gen.mixed_queries(n // 2, n // 2, n, seed=202)
+    q = gen.keys_of(qids)
+    t = oracle.OracleTable(nb * 32, lf_grow=2.0, lf_shrink=0)
+    t0 = time.perf_counter()
+    t.insert(keys, vals)
+    t.find(q)
+    dt = time.perf_counter() - t0
+    return 2 * n, dt
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    n_log2 = 20
+    for _ in range(args.warmup):
+        oracle_sample(n_log2)
+    tot_ops, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        ops, s = oracle_sample(n_log2)
+        tot_ops += ops
+        tot_s += s
+    v = tot_ops / tot_s / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": "cfg2 build+lookup at LF 0.95 (oracle sample: 2^20 keys + 2^20 finds per step)",
+                   "parallelism": "single host core"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": "2^20 inserts to LF 0.95 + 2^20 finds (50% hits) per step"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+# algorithmic bytes
+# ---------------------------------------------------------------------------------------
+def alg_bytes_find(n_hit, n_miss, p_h1, stash_nonempty):
+    hit = 256.0 * (2.0 - p_h1) + 9.0
+    miss = 512.0 + 9.0 + (32.0 if stash_nonempty else 0.0)
+    return n_hit * hit + n_miss * miss
+
+
+def alg_bytes_insert_fast(n_new, dedup):
+    # Step 1 probes b1 and b2 (new key) + one CAS sector + key/value/status I/O;
+    # with owner election: + owner_of write (4 B) + one election-table sector (32 B).
+    per = 512.0 + 32.0 + 9.0 + (36.0 if dedup else 0.0)
+    return n_new * per
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_15095_b200 import HiveTable, u32
+    from paper_2510_15095_b200.build import build as build_lib
+
+    if rank == 0:
+        build_lib()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    n = 1 << args.n_log2
+    nb = -(-n * 100 // (95 * 32)) if args.n_log2 != 26 else gen.CFG2_BUCKETS
+    ids = (np.arange(n, dtype=np.uint64) + rank * n).astype(np.uint32)
+    keys = u32(gen.keys_of(ids), dev)
+    vals = u32(gen.vals_of(ids), dev)
+    if world == 1:
+        qids, _ = gen.mixed_queries(n // 2, n // 2, n, seed=202)
+    else:
+        rng = np.random.default_rng(202 + rank)
+        hit_ids = rng.integers(0, n * world, n // 2, dtype=np.uint64)
+        miss_ids = np.arange(n // 2, dtype=np.uint64) + (1 << 31) + rank * (n // 2)
+        qids = np.concatenate([hit_ids, miss_ids])[rng.permutation(n)].astype(np.uint32)
+    queries = u32(gen.keys_of(qids), dev)
+    status = torch.empty(n, dtype=torch.uint8, device=dev)
+    vals_out = torch.empty(n, dtype=torch.uint32, device=dev)
+    found = torch.empty(n, dtype=torch.uint8, device=dev)
+
+    if world > 1:
+        from paper_2510_15095_b200.sharded import ShardedHive
+        sh = ShardedHive(nb * 32, lf_grow=2.0, lf_shrink=0)
+        table = sh.table
+
+        def step():
+            table.clear()
+            sh.insert(keys, vals)
+            sh.find(queries)
+    else:
+        table = HiveTable(nb * 32, lf_grow=2.0, lf_shrink=0)
+        sh = None
+
+        def step(ev=None):
+            table.clear()
+            if ev: ev[0].record()
+            table.insert(keys, vals, status)
+            if ev: ev[1].record()
+            table.find(queries, vals_out, found)
+            if ev: ev[2].record()
+
+    # ---- warm-up ---------------------------------------------------------------------
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, barrier + sync on both sides, max over ranks -------------
+    phase = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start.record()
+        for i in range(args.steps):
+            if world > 1:
+                step()
+            else:
+                step(phase[i])
+        end.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    total_ops = 2 * n * world
+    value = total_ops / (ms_per_step * 1e-3) / 1e9
+
+    # correctness guard on the last step (no outputs are trusted blindly)
+    if world == 1:
+        hit = np.zeros(1)
+        st_bad = int((status != 0).sum().item())
+        fnd = int(found.sum().item())
+        assert st_bad == 0 and fnd == n // 2, (st_bad, fnd)
+
+    out = {}
+    if world == 1:
+        ins_ms = statistics.mean(p[0].elapsed_time(p[1]) for p in phase)
+        find_ms = statistics.mean(p[1].elapsed_time(p[2]) for p in phase)
+        out["updates_gps"] = n / (ins_ms * 1e-3) / 1e9
+        out["lookups_gps"] = n / (find_ms * 1e-3) / 1e9
+        out["phase_ms"] = {"insert": ins_ms, "find": find_ms,
+                           "clear": ms_per_step - ins_ms - find_ms}
+
+    # ---- one profiled (untimed) step: per-kernel device times and launch counts ------------
+    table.profile(True)
+    if world > 1:
+        step()
+    else:
+        step()
+    torch.cuda.synchronize()
+    prof = table.profile_read(reset=True)
+    table.profile(False)
+    launches_per_step = sum(c for _, c in prof.values())
+    st = table.stats()
+    bucket_keys = max(1, st["count"] - st["stash_used"])
+    p_h1 = st["in_b1"] / bucket_keys
+    hbm_peak, peak_kind = peaks()
+
+    kern = {k: v[0] / v[1] for k, v in prof.items()}           # avg ms per launch
+    dominant = max(prof, key=lambda k: prof[k][0])
+    n_local = st["count"]
+    if dominant == "k_find":
+        algb = alg_bytes_find(n_local // 2 if world > 1 else n // 2, n // 2, p_h1, st["stash_used"] > 0)
+    else:
+        algb = alg_bytes_insert_fast(n_local if world > 1 else n, dedup=True)
+    achieved = algb / (kern[dominant] * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dominant)
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": hbm_peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": traffic, "alg_bytes_per_launch": algb, "p_h1": p_h1,
+                "kernel_ms": kern[dominant]}
+
+    # ---- e2e through the public API with host buffers (pinned) ---------------------------
+    e2e = None
+    if world == 1:
+        keys_h = keys.cpu().pin_memory()
+        vals_h = vals.cpu().pin_memory()
+        q_h = queries.cpu().pin_memory()
+        st_h = torch.empty(n, dtype=torch.uint8).pin_memory()
+        vo_h = torch.empty(n, dtype=torch.uint32).pin_memory()
+        fo_h = torch.empty(n, dtype=torch.uint8).pin_memory()
+        kd = torch.empty_like(keys)
+        vd = torch.empty_like(vals)
+        qd = torch.empty_like(queries)
+
+        def e2e_step():
+            table.clear()
+            kd.copy_(keys_h, non_blocking=True)
+            vd.copy_(vals_h, non_blocking=True)
+            table.insert(kd, vd, status)
+            st_h.copy_(status, non_blocking=True)
+            qd.copy_(q_h, non_blocking=True)
+            table.find(qd, vals_out, found)
+            vo_h.copy_(vals_out, non_blocking=True)
+            fo_h.copy_(found, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            e2e_step()
+        b.record()
+        torch.cuda.synchronize()
+        e_ms = a.elapsed_time(b) / args.steps
+        assert int(fo_h.sum().item()) == n // 2
+        e2e = {"value": total_ops / (e_ms * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 3 * 4 * n, "d2h_bytes_per_step": (1 + 4 + 1) * n,
+               "ms_per_step": e_ms}
+
+    # ---- secondary measurements (N = 1, untimed for `value`) ------------------------------
+    secondary = {}
+    if world == 1 and not args.no_secondary:
+        secondary = secondary_measurements(table, keys, vals, queries, n, nb, dev, prof)
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        s_log2 = min(22, args.n_log2)
+        ops, sec = oracle_sample(s_log2)
+        cpu = {"value": ops / sec / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"2^{s_log2} inserts to LF 0.95 + 2^{s_log2} finds (50% hits), sequential oracle",
+               "seconds": sec, "host_nproc": os.cpu_count()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": "cfg2: clear + insert 2^%d unique uniform keys into %d buckets "
+                                   "(LF 0.95, growth off) + 2^%d finds (50%% hits) per rank"
+                                   % (args.n_log2, nb, args.n_log2),
+                       "keys_per_rank": n, "buckets_per_rank": nb,
+                       "parallelism": "single GPU" if world == 1 else f"hash-sharded x{world} (NCCL all-to-all)",
+                       "l2": "inputs and table larger than L2 (no flush)", "owner_election": "on"},
+            **out,
+            "clocks": clk.summary(),
+            "gpu_launches": launches_per_step * args.steps,
+            "kernels_ms_per_step": {k: v[0] for k, v in prof.items()},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "secondary": secondary,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def secondary_measurements(table, keys, vals, queries, n, nb, dev, prof_main):
+    """Extra single-GPU numbers reported beside `value`: the keys-unique fast
+    path (no owner election), erase throughput on the full table, and the
+    config-3 mixed workload with linear-hashing grow/shrink."""
+    import torch
+
+    from paper_2510_15095_b200 import HiveTable, u8, u32
+    res = {}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+    # keys-unique fast path (HIVE_KEYS_UNIQUE)
+    tu = HiveTable(nb * 32, lf_grow=2.0, lf_shrink=0, keys_unique=True)
+    for _ in range(2):
+        tu.clear(); tu.insert(keys, vals); tu.find(queries)
+    times = []
+    for _ in range(3):
+        tu.clear()
+        ev[0].record(); tu.insert(keys, vals); ev[1].record(); tu.find(queries); ev[2].record()
+        torch.cuda.synchronize()
+        times.append((ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])))
+    res["unique_updates_gps"] = n / (statistics.mean(t[0] for t in times) * 1e-3) / 1e9
+    # erase half of the keys from the full table (dedup on)
+    half = keys[: n // 2]
+    table.clear(); table.insert(keys, vals)
+    ev[0].record(); table.erase(half); ev[1].record()
+    torch.cuda.synchronize()
+    res["erase_gps"] = (n // 2) / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9
+    del tu
+
+    # config 3: 64 batches x 2^20 mixed ops (40/20/40) over U = 2^26, 1K buckets
+    # start, growth + shrink, then the id-order drain tail.
+    nbat, bsz, U = 64, 1 << 20, 1 << 26
+    ops_all = [u8(gen.bernoulli_ops(bsz, 0.4, 0.2, seed=1000 + b), dev) for b in range(nbat)]
+    ids_all = [gen.uniform_ids(bsz, U, seed=2000 + b) for b in range(nbat)]
+    k_all = [u32(gen.keys_of(i), dev) for i in ids_all]
+    v_all = [u32(gen.vals_of(i), dev) for i in ids_all]
+    vo = torch.empty(bsz, dtype=torch.uint32, device=dev)
+    rr = torch.empty(bsz, dtype=torch.uint8, device=dev)
+    t3 = HiveTable(1024 * 32)
+    t3.profile(True)
+    torch.cuda.synchronize()
+    ev[0].record()
+    for b in range(nbat):
+        t3.mixed(ops_all[b], k_all[b], v_all[b], vo, rr)
+    ev[1].record()
+    torch.cuda.synchronize()
+    s3 = t3.stats()
+    mixed_ms = ev[0].elapsed_time(ev[1])
+    drain_keys = [u32(gen.keys_of(np.arange(lo, lo + bsz, dtype=np.uint32)), dev) for lo in range(0, U, bsz)]
+    ev[2].record()
+    for dk in drain_keys:
+        t3.erase(dk)
+    ev[3].record()
+    torch.cuda.synchronize()
+    s3b = t3.stats()
+    p3 = t3.profile_read(reset=True)
+    res["cfg3_mixed"] = {
+        "gops": nbat * bsz / (mixed_ms * 1e-3) / 1e9, "ms": mixed_ms,
+        "final_buckets": s3["n_buckets"], "final_count": s3["count"], "grows": s3["grows"],
+        "drain_tail_gops": U / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9,
+        "after_drain_buckets": s3b["n_buckets"], "shrinks": s3b["shrinks"],
+        "merge_aborts": s3b["merge_aborts"],
+        "split_ms": p3.get("k_split", (0, 0))[0], "merge_ms": p3.get("k_merge", (0, 0))[0],
+        "split_launches": p3.get("k_split", (0, 0))[1], "merge_launches": p3.get("k_merge", (0, 0))[1],
+    }
+    return res
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,200 @@
+/*
+ * hive.h — C ABI of the B200-native Hive hash table (arXiv 2510.15095).
+ *
+ * The data-parallel hot path of the paper — batched, warp-cooperative insert /
+ * lookup / delete over a packed bucket array of 64-bit key-value words, WABC
+ * slot claiming, WCME matching, the four-step insert, and load-factor-triggered
+ * linear-hashing split/merge — implemented as hand-written sm_100a CUDA in
+ * libhive.so.  No torch types appear here: all arguments are plain integers and
+ * pointers.  Citations: PAPER:L = reference PAPER.md line; SURVEY §x = the
+ * blueprint section; A-n = reading n of DESIGN.md "Readings of the paper".
+ *
+ * Conventions for every call
+ *  - d_* arguments are DEVICE pointers owned by the caller; they must stay
+ *    alive until the work on `stream` completes.  h_* are HOST pointers.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Calls are stream-ordered and asynchronous unless noted "sync".
+ *  - Keys and values are uint32.  Key 0xFFFFFFFF is reserved (it encodes the
+ *    EMPTY slot word, A-9): insert reports status 2, find reports not-found,
+ *    erase reports 0 for it.
+ *  - n == 0 is a no-op returning HIVE_OK.
+ *  - A handle is used by one stream at a time (phases never overlap); a call
+ *    made while another call on the same handle is still being issued returns
+ *    HIVE_EBUSY.  Different handles are independent.
+ *  - Errors: argument errors return immediately without launching work
+ *    (HIVE_EINVAL); CUDA errors map to HIVE_ECUDA with the text available from
+ *    hive_last_error(); a stash overflow (never expected at LF <= 0.95) sets
+ *    per-op status 3 and a sticky flag reported by hive_stats / hive_size as
+ *    HIVE_ESTASHFULL.
+ *
+ * Batch semantics (PHASED contract): a batch applies all INSERT
+ * ops, then all ERASE ops, then all FIND ops.  Insert status and erase output
+ * are present(k) at the start of their phase and identical for in-batch
+ * duplicates; after an insert phase k holds the value of the LAST op (highest
+ * index) inserting k in the batch — one member of the accepted set.  Find
+ * returns (present, value) at the FIND-phase start.  Resize happens only at
+ * phase boundaries: grow before INSERT while count + n_ins > lf_grow * slots
+ * (PAPER:482), shrink after ERASE while count < lf_shrink * slots.
+ */
+#ifndef HIVE_H
+#define HIVE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hive_table_s* hive_t;
+
+typedef enum {
+    HIVE_OK = 0,
+    HIVE_EINVAL = 1,      /* bad argument / config                          */
+    HIVE_ENOMEM = 2,      /* device or VA allocation failed                 */
+    HIVE_ECUDA = 3,       /* CUDA runtime / driver error                    */
+    HIVE_ENCCL = 4,       /* reserved (collectives run in the binding)      */
+    HIVE_ESTASHFULL = 5,  /* sticky: an entry could not be stored           */
+    HIVE_EBUSY = 6        /* handle already in use by a concurrent call     */
+} hive_status;
+
+/* Flags for hive_config.flags */
+#define HIVE_KEYS_UNIQUE 1u   /* caller asserts: no duplicate keys inside any one
+                                 insert or erase batch -> the owner-election
+                                 pass is skipped.  Results
+                                 are undefined if the assertion is false. */
+
+typedef struct {
+    uint64_t capacity;       /* initial slots; rounded up to 32-slot buckets
+                                (>= 2 buckets); any count (A-20)              */
+    uint64_t max_capacity;   /* slots reserved (virtual) for growth; 0 = half
+                                of device memory                             */
+    float    lf_grow;        /* 0.90; >= 1.0 disables growth      */
+    float    lf_shrink;      /* 0.25; <= 0 disables contraction   */
+    uint32_t max_evictions;  /* Step-3 bound, 16 (value A-8)       */
+    uint32_t resize_k;       /* K buckets per split/merge batch, 1024
+                                (value A-8)                        */
+    float    stash_fraction; /* stash capacity / slots, 0.02,
+                                floor 1024 entries                           */
+    uint32_t flags;          /* HIVE_KEYS_UNIQUE                              */
+} hive_config;
+
+/* Stats snapshot (sync). */
+typedef struct {
+    uint64_t n_buckets;      /* 2^m + split_ptr                               */
+    uint32_t m;              /* round level; index_mask = 2^m - 1 */
+    uint32_t split;          /* split pointer                     */
+    uint64_t count;          /* live keys (buckets + stash)                   */
+    uint64_t stash_used;     /* stash ring slots used since the last drain    */
+    uint64_t stash_cap;      /* stash ring capacity                           */
+    uint64_t evictions;      /* Step-3 victim swaps, cumulative               */
+    uint64_t max_depth;      /* deepest Step-3 round count of one insert      */
+    uint64_t stash_pushes;   /* Step-4 pushes, cumulative                     */
+    uint64_t leftovers;      /* inserts that reached Step 3, cumulative       */
+    uint64_t grows;          /* split batches run                             */
+    uint64_t shrinks;        /* merge batches run                             */
+    uint64_t merge_aborts;   /* merges aborted for lack of space  */
+    uint64_t failed;         /* entries lost to a full stash (must be 0)      */
+    uint64_t in_b1;          /* live bucket keys resident in addr(h1)         */
+    uint64_t mapped_bytes;   /* physical bytes mapped for buckets             */
+} hive_stats_t;
+
+/* Fill *cfg with the defaults above. */
+void hive_config_default(hive_config* cfg);
+
+/* Create a table (sync).  Reserves virtual address space for max_capacity
+ * and maps physical 2 MiB chunks for the initial buckets (EMPTY-filled).
+ * Returns HIVE_EINVAL for cfg == NULL, out == NULL, capacity == 0,
+ * lf_shrink >= lf_grow (when both are enabled), stash_fraction < 0. */
+hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out);
+
+/* Destroy (sync on the table's last stream); frees everything it owns. */
+hive_status hive_destroy(hive_t h);
+
+/* Four-step insert / replace.  d_keys, d_vals: uint32[n].
+ * d_status (nullable): uint8[n]; 0 = absent at phase start (inserted),
+ * 1 = present (value replaced), 2 = reserved key, 3 = failed (stash full).
+ * May grow the table first (one small D2H of the counters when growth is
+ * enabled). */
+hive_status hive_insert(hive_t h, const uint32_t* d_keys, const uint32_t* d_vals,
+                        uint64_t n, uint8_t* d_status, void* stream);
+
+/* Lookup by WCME over the two candidate buckets, then the stash index
+ * (PAPER:444-445).  d_vals_out: uint32[n] (value or 0 when absent);
+ * d_found (nullable): uint8[n] 1/0. */
+hive_status hive_find(hive_t h, const uint32_t* d_keys, uint64_t n,
+                      uint32_t* d_vals_out, uint8_t* d_found, void* stream);
+
+/* Delete (Alg. 4).  d_erased (nullable): uint8[n], 1 if the
+ * key was present at phase start.  May shrink the table afterwards. */
+hive_status hive_erase(hive_t h, const uint32_t* d_keys, uint64_t n,
+                       uint8_t* d_erased, void* stream);
+
+/* Mixed batch: d_op uint8[n] with 0 = find, 1 = insert, 2 = erase (other
+ * codes: result 0).  Runs INSERT, ERASE, FIND phases.
+ * d_vals_out uint32[n]: find value (0 for misses and non-find ops);
+ * d_result uint8[n]: the op's own status code as above. */
+hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys,
+                       const uint32_t* d_vals, uint64_t n, uint32_t* d_vals_out,
+                       uint8_t* d_result, void* stream);
+
+/* Reset to the freshly created state (all slots EMPTY, initial size, stash
+ * empty, counters zero); keeps allocations.  Async. */
+hive_status hive_clear(hive_t h, void* stream);
+
+/* Live key count (sync). */
+hive_status hive_size(hive_t h, uint64_t* out);
+
+/* Stats snapshot (sync); returns HIVE_ESTASHFULL if the sticky flag is set. */
+hive_status hive_stats(hive_t h, hive_stats_t* out);
+
+/* Export all live pairs (sync) into caller DEVICE buffers of capacity cap
+ * (order unspecified).  *n_out = number of live pairs (may exceed cap, in
+ * which case only cap are written). */
+hive_status hive_dump(hive_t h, uint32_t* d_keys, uint32_t* d_vals, uint64_t cap,
+                      uint64_t* n_out, void* stream);
+
+/* Per-kernel device timing (CUDA events around every launch on the call's
+ * stream).  Enabled by hive_profile(h, 1); hive_profile_read fills up to
+ * max entries of names (pointers to static strings), total milliseconds and
+ * launch counts, returns the number of kernels seen, and resets when
+ * reset != 0.  Sync. */
+hive_status hive_profile(hive_t h, int enable);
+int hive_profile_read(hive_t h, const char** names, double* ms, uint64_t* launches,
+                      int max, int reset);
+
+/* ---- stable partition (used for mixed classification and for routing a
+ * batch across hash-partitioned shards) -------------------- */
+
+/* Route a batch to n_shards shards: shard(k) = (fmix32(k ^ seed) * n_shards)
+ * >> 32.  Stable (rank order preserved inside each shard).
+ *   d_keys, d_vals (nullable), d_ops (nullable): the batch, length n.
+ *   d_send_kv: uint64[n] packed (value << 32 | key) in shard order;
+ *   d_send_ops (nullable): uint8[n] in shard order;
+ *   d_pos: uint32[n], d_pos[i] = position of op i in the send buffer;
+ *   d_counts: uint64[n_shards] ops per shard.
+ * n_shards in [1, 64].  n must be < 2^32. */
+hive_status hive_route(uint32_t n_shards, uint32_t seed, const uint32_t* d_keys,
+                       const uint32_t* d_vals, const uint8_t* d_ops, uint64_t n,
+                       uint64_t* d_send_kv, uint8_t* d_send_ops, uint32_t* d_pos,
+                       uint64_t* d_counts, void* stream);
+
+/* Inverse permutation gather after the results come back:
+ * d_out8[i] = d_in8[d_pos[i]] and d_out32[i] = d_in32[d_pos[i]]
+ * (either pair may be NULL). */
+hive_status hive_unroute(const uint32_t* d_pos, uint64_t n, const uint8_t* d_in8,
+                         uint8_t* d_out8, const uint32_t* d_in32, uint32_t* d_out32,
+                         void* stream);
+
+/* Split packed records (value << 32 | key) into key / value arrays. */
+hive_status hive_unpack_kv(const uint64_t* d_kv, uint64_t n, uint32_t* d_keys,
+                           uint32_t* d_vals, void* stream);
+
+/* Human-readable text of a status / of the last CUDA error seen. */
+const char* hive_status_string(hive_status s);
+const char* hive_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HIVE_H */

@@ -1,0 +1,229 @@
+// hive_device.cuh — device-side layout, hashing and warp-group primitives of the
+// B200 Hive table (arXiv 2510.15095).  Header-only, included by hive_kernels.cu.
+//
+// Layout: the bucket array is one virtually
+// contiguous range of n_b buckets x 32 slots x 8 B (256 B per bucket, 256 B
+// aligned), each slot the packed word (value << 32) | key with
+// EMPTY = all ones (A-9).  There is no separate freeMask array: the WABC
+// claim mask is the ballot of EMPTY slots over the bucket that Step 1 has
+// already loaded (PAPER:291-292 with the claim RMW moved onto the slot word
+// itself, one 64-bit CAS).
+//
+// Warp groups: one operation is served by a group of G lanes (G = 8 by
+// default), each lane holding 32/G slots loaded with one 256-bit (G = 8) or
+// 128-bit (G = 16) vector load, so a warp keeps 32/G independent bucket probes
+// in flight (PAPER:304's one-lane-per-slot WCME is G = 32).
+#pragma once
+#include <cstdint>
+
+namespace hive {
+
+constexpr uint64_t EMPTY = ~0ull;
+constexpr uint32_t INVALID_KEY = 0xFFFFFFFFu;
+constexpr int SLOTS = 32;                 // S = 32 slots per bucket
+constexpr uint32_t FULL = 0xFFFFFFFFu;
+constexpr uint32_t DEDUP_SEED = 0x2545F491u;
+
+// ---- packed word, PAPER:180-187 --------------------------------------------------
+__device__ __forceinline__ uint64_t pack(uint32_t k, uint32_t v) {
+    return ((uint64_t)v << 32) | (uint64_t)k;
+}
+__device__ __forceinline__ uint32_t key_of(uint64_t p) { return (uint32_t)p; }
+__device__ __forceinline__ uint32_t val_of(uint64_t p) { return (uint32_t)(p >> 32); }
+
+// ---- Listing 1, PAPER:229-249 (full 32-bit output, reduction in addr(), A-1) ----
+__device__ __forceinline__ uint32_t bithash1(uint32_t key) {
+    key = ~key + (key << 15);
+    key ^= (key >> 12);
+    key += (key << 2);
+    key ^= (key >> 4);
+    key *= 2057u;
+    key ^= (key >> 16);
+    return key;
+}
+__device__ __forceinline__ uint32_t bithash2(uint32_t key) {
+    key = (key + 0x7ed55d16u) + (key << 12);
+    key = (key ^ 0xc761c23cu) ^ (key >> 19);
+    key = (key + 0x165667b1u) + (key << 5);
+    key = (key + 0xd3a2646cu) ^ (key << 9);
+    key = (key + 0xfd7046c5u) + (key << 3);
+    key = (key ^ 0xb55a4f09u) ^ (key >> 16);
+    return key;
+}
+// MurmurHash3 finaliser: shard routing and the per-batch owner-election table
+// (independent of BitHash1/2).
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    h ^= h >> 16;
+    return h;
+}
+
+// ---- device control block --------------------------------------------------------
+struct Ctrl {
+    unsigned long long count;          // live keys (buckets + stash), A-19
+    unsigned long long stash_tail;     // ring slots used since the last drain
+    unsigned long long n_left;         // Step-3 leftover list length (this phase)
+    unsigned long long evictions;      // Step-3 victim swaps
+    unsigned long long max_depth;      // deepest Step-3 round count
+    unsigned long long stash_pushes;   // Step-4 pushes
+    unsigned long long leftovers;      // ops that reached Step 3
+    unsigned long long failed;         // entries lost to a full stash (sticky)
+    unsigned long long first_abort;    // merge: first aborting pair (LIFO index)
+    unsigned long long dump_n;         // dump cursor
+    unsigned long long in_b1;          // stats: keys resident in addr(h1)
+    unsigned long long pad[5];
+};
+
+// ---- linear-hashing addressing, PAPER:485-503 (Litwin rule, A-2) ----------------
+struct TableView {
+    uint64_t* buckets;   // n_b * 32 packed words
+    uint32_t mask;       // index_mask = 2^m - 1
+    uint32_t split;      // split pointer
+    __device__ __forceinline__ uint32_t addr(uint32_t h) const {
+        uint32_t b = h & mask;
+        if (b < split) b = h & ((mask << 1) | 1u);
+        return b;
+    }
+    // AltBucket (Alg. 3 line 34): the other candidate, equal -> cur,
+    // neither -> first.
+    __device__ __forceinline__ uint32_t alt(uint32_t k, uint32_t cur) const {
+        uint32_t c1 = addr(bithash1(k)), c2 = addr(bithash2(k));
+        return cur == c1 ? c2 : (cur == c2 ? c1 : c1);
+    }
+    __device__ __forceinline__ uint64_t* bucket(uint32_t b) const {
+        return buckets + (uint64_t)b * SLOTS;
+    }
+};
+
+// Overflow stash: a ring of packed words filled by fetch-add on
+// tail, plus an open-addressing index key -> ring position so finds, erases
+// and Step 1 can see stashed keys (A-10, A-11).
+struct StashView {
+    uint64_t* ring;      // cap words, EMPTY-initialised
+    uint64_t* index;     // idx_mask + 1 words: (key << 32) | ring_pos, EMPTY = free
+    uint64_t cap;
+    uint64_t idx_mask;
+    Ctrl* ctrl;
+};
+
+// Per-batch owner election table: (key << 32) | op, max op
+// per key wins (= the oracle's last write).
+struct DedupView {
+    uint64_t* slots;     // nullptr = election disabled (HIVE_KEYS_UNIQUE)
+    uint64_t mask;
+};
+
+// ---- memory access -----------------------------------------------------------------
+// Bucket loads bypass L1 allocation (random, no reuse; also no stale L1 lines
+// across the CAS traffic of other SMs).  SPL = slots per lane.
+template <int SPL>
+__device__ __forceinline__ void load_slots(const uint64_t* p, uint64_t (&s)[SPL]) {
+    if constexpr (SPL == 4) {
+        asm volatile("ld.global.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(s[0]), "=l"(s[1]), "=l"(s[2]), "=l"(s[3]) : "l"(p) : "memory");
+    } else if constexpr (SPL == 2) {
+        asm volatile("ld.global.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
+                     : "=l"(s[0]), "=l"(s[1]) : "l"(p) : "memory");
+    } else {
+        asm volatile("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(s[0]) : "l"(p) : "memory");
+    }
+}
+// Read-only phase variant (FIND): the table is immutable for the whole kernel.
+template <int SPL>
+__device__ __forceinline__ void load_slots_ro(const uint64_t* p, uint64_t (&s)[SPL]) {
+    if constexpr (SPL == 4) {
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(s[0]), "=l"(s[1]), "=l"(s[2]), "=l"(s[3]) : "l"(p));
+    } else if constexpr (SPL == 2) {
+        asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
+                     : "=l"(s[0]), "=l"(s[1]) : "l"(p));
+    } else {
+        asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(s[0]) : "l"(p));
+    }
+}
+
+// ---- warp-group view ---------------------------------------------------------------
+template <int G>
+struct WarpGroup {
+    static constexpr int SPL = SLOTS / G;          // slots per lane
+    static constexpr int GPW = 32 / G;             // groups per warp
+    static constexpr uint32_t GMASK = (G == 32) ? FULL : ((1u << G) - 1u);
+    int lane, gi, gl;
+    __device__ __forceinline__ WarpGroup() {
+        lane = threadIdx.x & 31;
+        gi = lane / G;
+        gl = lane % G;
+    }
+    __device__ __forceinline__ int base() const { return gi * G; }
+    // this group's bits of a full-warp ballot
+    __device__ __forceinline__ uint32_t bits(uint32_t bal) const {
+        return (bal >> (gi * G)) & GMASK;
+    }
+    __device__ __forceinline__ uint32_t ballot(bool p) const {
+        return bits(__ballot_sync(FULL, p));
+    }
+    template <typename T>
+    __device__ __forceinline__ T bcast(T v, int src_gl) const {
+        return __shfl_sync(FULL, v, base() + src_gl);
+    }
+    __device__ __forceinline__ uint64_t* slot_ptr(uint64_t* bucket) const {
+        return bucket + gl * SPL;
+    }
+};
+
+// Select s[j] for a runtime j without local-memory indexing.
+template <int SPL>
+__device__ __forceinline__ uint64_t pick(const uint64_t (&s)[SPL], int j) {
+    uint64_t w = s[0];
+#pragma unroll
+    for (int i = 1; i < SPL; ++i)
+        if (i == j) w = s[i];
+    return w;
+}
+template <int SPL>
+__device__ __forceinline__ void put(uint64_t (&s)[SPL], int j, uint64_t w) {
+#pragma unroll
+    for (int i = 0; i < SPL; ++i)
+        if (i == j) s[i] = w;
+}
+
+// Per-lane match mask of key k over the lane's slots (WCME compare).
+template <int SPL>
+__device__ __forceinline__ uint32_t match_bits(const uint64_t (&s)[SPL], uint32_t k) {
+    uint32_t mm = 0;
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) mm |= (key_of(s[j]) == k ? 1u : 0u) << j;
+    return mm;
+}
+// Per-lane free mask (slot == EMPTY): the WABC claim predicate.
+template <int SPL>
+__device__ __forceinline__ uint32_t free_bits(const uint64_t (&s)[SPL]) {
+    uint32_t fm = 0;
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) fm |= (s[j] == EMPTY ? 1u : 0u) << j;
+    return fm;
+}
+
+// WCME: match-and-elect.  Returns true (group-uniform) if key k is in the
+// cached bucket view; *winner_slot = lowest matching slot index (0..31) and
+// *word = its packed word.  `valid` must be false for k == INVALID_KEY
+// (EMPTY slots carry key 0xFFFFFFFF).  All 32 lanes must call this.
+template <int G>
+__device__ __forceinline__ bool wcme(const WarpGroup<G>& wg,
+                                     const uint64_t (&s)[WarpGroup<G>::SPL], uint32_t k,
+                                     bool valid, int* winner_slot, uint64_t* word) {
+    constexpr int SPL = WarpGroup<G>::SPL;
+    uint32_t mm = valid ? match_bits<SPL>(s, k) : 0u;
+    uint32_t M = wg.ballot(mm != 0);                       // match mask (lanes)
+    int w = M ? __ffs(M) - 1 : 0;                          // FirstSet
+    int j = mm ? __ffs(mm) - 1 : 0;
+    uint64_t my = pick<SPL>(s, j);
+    *word = wg.bcast(my, w);
+    *winner_slot = w * SPL + wg.bcast(j, w);
+    return M != 0;
+}
+
+}  // namespace hive

@@ -1,0 +1,738 @@
+// hive_host.cu — C-ABI implementation (include/hive.h): handle lifecycle, the
+// PHASED batch contract (INSERT -> ERASE -> FIND), the
+// load-factor triggers of PAPER:480-483 at phase boundaries (reading A-19),
+// and bucket-array growth by CUDA virtual memory: the whole max_capacity is
+// reserved as one virtual range and 2 MiB physical chunks are mapped as the
+// split pointer advances, so a split never copies or rehashes the table
+// ("allocates K new buckets").
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hive.h"
+#include "hive_kernels.cuh"
+
+using namespace hive;
+
+namespace {
+
+thread_local std::string g_err;
+
+void set_err(cudaError_t e, const char* what, int line) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s at hive_host.cu:%d: %s", what, line, cudaGetErrorString(e));
+    g_err = buf;
+}
+void set_err_drv(CUresult r, const char* what, int line) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s at hive_host.cu:%d: CUresult %d", what, line, (int)r);
+    g_err = buf;
+}
+
+#define CK(x)                                         \
+    do {                                              \
+        cudaError_t _e = (x);                         \
+        if (_e != cudaSuccess) {                      \
+            set_err(_e, #x, __LINE__);                \
+            return HIVE_ECUDA;                        \
+        }                                             \
+    } while (0)
+#define CKS(x)                                        \
+    do {                                              \
+        hive_status _s = (x);                         \
+        if (_s != HIVE_OK) return _s;                 \
+    } while (0)
+
+// ---- CUDA driver VMM entry points (resolved through the runtime, so the
+// library does not link libcuda and loads on GPU-less hosts) ----------------
+struct Vmm {
+    CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+    CUresult (*release)(CUmemGenericAllocationHandle);
+    CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+    CUresult (*free_va)(CUdeviceptr, size_t);
+    CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+    CUresult (*unmap)(CUdeviceptr, size_t);
+    CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+    CUresult (*granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags);
+    bool ok = false;
+};
+
+bool load_vmm(Vmm& v) {
+    if (v.ok) return true;
+    struct { const char* name; void** fn; } tab[] = {
+        {"cuMemCreate", (void**)&v.create},       {"cuMemRelease", (void**)&v.release},
+        {"cuMemAddressReserve", (void**)&v.reserve}, {"cuMemAddressFree", (void**)&v.free_va},
+        {"cuMemMap", (void**)&v.map},             {"cuMemUnmap", (void**)&v.unmap},
+        {"cuMemSetAccess", (void**)&v.set_access},
+        {"cuMemGetAllocationGranularity", (void**)&v.granularity},
+    };
+    for (auto& e : tab) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint(e.name, e.fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !*e.fn) {
+            g_err = std::string("driver entry point missing: ") + e.name;
+            return false;
+        }
+    }
+    v.ok = true;
+    return true;
+}
+Vmm g_vmm;
+
+uint64_t pow2_at_least(uint64_t x) {
+    uint64_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+}  // namespace
+
+struct hive_table_s {
+    hive_config cfg{};
+    int dev = 0, num_sms = 0;
+    Grids grids{};
+
+    // bucket array: one reserved VA range, 2 MiB chunks mapped on demand
+    CUdeviceptr va = 0;
+    size_t va_bytes = 0, gran = 0;
+    std::vector<CUmemGenericAllocationHandle> chunks;
+    uint64_t max_buckets = 0, nb_min = 0;
+    uint32_t m0 = 0, split0 = 0, m = 0, split = 0;
+
+    // stash ring + index (A-10)
+    uint64_t* ring = nullptr;
+    uint64_t ring_alloc = 0, stash_cap = 0;
+    uint64_t* sidx = nullptr;
+    uint64_t idx_cap = 0;
+
+    Ctrl* ctrl = nullptr;
+    Ctrl* ctrl_h = nullptr;            // pinned mirror
+    uint64_t* stage_h = nullptr;       // pinned staging words
+
+    // per-batch scratch (grown on demand)
+    uint64_t* dd = nullptr;   uint64_t dd_cap = 0;
+    uint32_t* owner = nullptr; uint64_t owner_cap = 0;
+    uint32_t* left = nullptr; uint64_t left_cap = 0;
+    uint32_t* cls = nullptr;  uint64_t cls_cap = 0;
+    uint64_t* cnt = nullptr;  uint64_t cnt_cap = 0;
+    uint64_t* pinfo = nullptr;
+    uint64_t* tmpkv = nullptr; uint64_t tmpkv_cap = 0;
+
+    uint64_t grows = 0, shrinks = 0, merge_aborts = 0;
+    uint64_t tail_known = 0;           // last stash_tail read from the device
+
+    // profiling
+    struct Rec { const char* name; cudaEvent_t a, b; };
+    bool prof = false;
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    struct Agg { const char* name; double ms; uint64_t n; };
+    std::vector<Agg> agg;
+
+    std::atomic<int> busy{0};
+    cudaStream_t last = nullptr;
+
+    uint64_t nb() const { return (1ull << m) + split; }
+    TableView tv() const {
+        return TableView{(uint64_t*)va, (uint32_t)((1ull << m) - 1), split};
+    }
+    StashView sv() const { return StashView{ring, sidx, stash_cap, idx_cap - 1, ctrl}; }
+    bool dedup_on() const { return !(cfg.flags & HIVE_KEYS_UNIQUE); }
+    uint64_t stash_cap_for(uint64_t n_b) const {
+        uint64_t c = (uint64_t)llround((double)cfg.stash_fraction * (double)n_b * SLOTS);
+        return std::max<uint64_t>(1024, c);
+    }
+};
+
+namespace {
+
+struct BusyGuard {
+    hive_table_s* h;
+    bool ok;
+    explicit BusyGuard(hive_table_s* t) : h(t) { ok = h->busy.exchange(1) == 0; }
+    ~BusyGuard() { if (ok) h->busy.store(0); }
+};
+
+cudaEvent_t get_event(hive_table_s* h) {
+    if (!h->pool.empty()) {
+        cudaEvent_t e = h->pool.back();
+        h->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Event pair around one launch when profiling is on.
+struct Prof {
+    hive_table_s* h;
+    const char* name;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    Prof(hive_table_s* t, const char* nm, cudaStream_t st) : h(t), name(nm), s(st) {
+        if (h->prof) {
+            a = get_event(h);
+            cudaEventRecord(a, s);
+        }
+    }
+    ~Prof() {
+        if (h->prof) {
+            cudaEvent_t b = get_event(h);
+            cudaEventRecord(b, s);
+            h->recs.push_back({name, a, b});
+        }
+    }
+};
+
+template <typename T>
+hive_status ensure(T*& p, uint64_t& cap, uint64_t need) {
+    if (need <= cap && p) return HIVE_OK;
+    uint64_t n = std::max<uint64_t>(need, cap * 3 / 2);
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc((void**)&p, n * sizeof(T));
+    if (e != cudaSuccess) {
+        set_err(e, "cudaMalloc(scratch)", __LINE__);
+        return HIVE_ENOMEM;
+    }
+    cap = n;
+    return HIVE_OK;
+}
+
+hive_status map_buckets(hive_table_s* h, uint64_t n_buckets) {
+    const size_t need = ((size_t)n_buckets * SLOTS * 8 + h->gran - 1) / h->gran * h->gran;
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = h->dev;
+    CUmemAccessDesc acc{};
+    acc.location = prop.location;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    while (h->chunks.size() * h->gran < need) {
+        const size_t off = h->chunks.size() * h->gran;
+        if (off + h->gran > h->va_bytes) {
+            g_err = "bucket array exceeds the reserved max_capacity";
+            return HIVE_ENOMEM;
+        }
+        CUmemGenericAllocationHandle mh;
+        CUresult r = g_vmm.create(&mh, h->gran, &prop, 0);
+        if (r != CUDA_SUCCESS) { set_err_drv(r, "cuMemCreate", __LINE__); return HIVE_ENOMEM; }
+        r = g_vmm.map(h->va + off, h->gran, 0, mh, 0);
+        if (r != CUDA_SUCCESS) { g_vmm.release(mh); set_err_drv(r, "cuMemMap", __LINE__); return HIVE_ENOMEM; }
+        r = g_vmm.set_access(h->va + off, h->gran, &acc, 1);
+        if (r != CUDA_SUCCESS) { set_err_drv(r, "cuMemSetAccess", __LINE__); return HIVE_ECUDA; }
+        h->chunks.push_back(mh);
+    }
+    return HIVE_OK;
+}
+
+hive_status read_ctrl(hive_table_s* h, cudaStream_t s) {
+    CK(cudaMemcpyAsync(h->ctrl_h, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    h->tail_known = h->ctrl_h->stash_tail;
+    return HIVE_OK;
+}
+
+hive_status set_ctrl_word(hive_table_s* h, unsigned long long* field, uint64_t value, cudaStream_t s) {
+    if (value == 0) {
+        CK(cudaMemsetAsync(field, 0, sizeof(uint64_t), s));
+        return HIVE_OK;
+    }
+    // only used right before a synchronising read, so one staging word suffices
+    h->stage_h[0] = value;
+    CK(cudaMemcpyAsync(field, h->stage_h, sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    return HIVE_OK;
+}
+
+// (Re)size the stash for `cap` entries and clear it (ring + index EMPTY, tail 0).
+hive_status stash_reset(hive_table_s* h, uint64_t cap, cudaStream_t s) {
+    if (cap > h->ring_alloc) {
+        // grow geometrically: the capacity follows n_b at every resize (A-8)
+        const uint64_t ra = std::max<uint64_t>(cap, h->ring_alloc * 2);
+        const uint64_t ic = pow2_at_least(2 * ra);
+        if (h->ring) cudaFree(h->ring);
+        if (h->sidx) cudaFree(h->sidx);
+        h->ring = nullptr;
+        h->sidx = nullptr;
+        h->ring_alloc = 0;
+        CK(cudaMalloc((void**)&h->ring, ra * sizeof(uint64_t)));
+        CK(cudaMalloc((void**)&h->sidx, ic * sizeof(uint64_t)));
+        h->ring_alloc = ra;
+        h->idx_cap = ic;
+    }
+    h->stash_cap = cap;
+    CK(launch_stash_reset(s, StashView{h->ring, h->sidx, h->ring_alloc, h->idx_cap - 1, h->ctrl}));
+    CKS(set_ctrl_word(h, &h->ctrl->stash_tail, 0, s));
+    h->tail_known = 0;
+    return HIVE_OK;
+}
+
+// ---- the INSERT phase (Steps 1-4, owner election, duplicate fix-up) ---------------
+hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* vals,
+                         const uint64_t* kvs, const uint32_t* idx, uint64_t n_upper,
+                         const uint64_t* n_dev, uint64_t n_batch, uint8_t* status,
+                         uint32_t* vals_zero, cudaStream_t s) {
+    const bool dedup = !kvs && h->dedup_on();
+    DedupView dd{nullptr, 0};
+    if (dedup) {
+        const uint64_t cap = pow2_at_least(std::max<uint64_t>(1024, 2 * n_upper));
+        CKS(ensure(h->dd, h->dd_cap, cap));
+        CKS(ensure(h->owner, h->owner_cap, n_batch));
+        dd = DedupView{h->dd, cap - 1};
+        CK(cudaMemsetAsync(h->dd, 0xFF, cap * sizeof(uint64_t), s));
+        Prof p(h, "k_dedup_elect", s);
+        CK(launch_dedup_elect(h->grids.dedup, s, keys, idx, n_upper, n_dev, dd));
+    }
+    CKS(ensure(h->left, h->left_cap, std::max<uint64_t>(n_upper, 1)));
+    CKS(set_ctrl_word(h, &h->ctrl->n_left, 0, s));
+    {
+        Prof p(h, kvs ? "k_insert_fast(reinsert)" : "k_insert_fast", s);
+        CK(launch_insert_fast(h->grids.insert_fast, s, keys, vals, kvs, idx, n_upper, n_dev, h->tv(),
+                              h->sv(), dd, h->owner, status, vals_zero, h->left));
+    }
+    {
+        Prof p(h, kvs ? "k_insert_slow(reinsert)" : "k_insert_slow", s);
+        CK(launch_insert_slow(h->grids.insert_slow, s, keys, vals, kvs, h->left, h->tv(), h->sv(),
+                              h->cfg.max_evictions, status));
+    }
+    if (dedup && status) {
+        Prof p(h, "k_dup_copy", s);
+        CK(launch_dup_copy(h->grids.stream, s, idx, n_upper, n_dev, h->owner, status));
+    }
+    return HIVE_OK;
+}
+
+// Drain the stash and reinsert its entries with Steps 2-4 after a resize
+// (PAPER:214, 443); the capacity follows the new size (reading A-8).
+hive_status drain_reinsert(hive_table_s* h, cudaStream_t s) {
+    const uint64_t new_cap = h->stash_cap_for(h->nb());
+    if (h->tail_known == 0) {
+        if (new_cap != h->stash_cap) CKS(stash_reset(h, new_cap, s));
+        return HIVE_OK;
+    }
+    const uint64_t used = std::min<uint64_t>(h->tail_known, h->stash_cap);
+    CKS(ensure(h->tmpkv, h->tmpkv_cap, used));
+    CK(cudaMemcpyAsync(h->tmpkv, h->ring, used * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    CKS(stash_reset(h, new_cap, s));
+    CKS(insert_phase(h, nullptr, nullptr, h->tmpkv, nullptr, used, nullptr, used, nullptr, nullptr, s));
+    CKS(read_ctrl(h, s));
+    return HIVE_OK;
+}
+
+// expand_batch: split min(K, 2^m - split) buckets from split_ptr.
+hive_status expand_batch(hive_table_s* h, cudaStream_t s, bool* grew) {
+    const uint64_t round_end = 1ull << h->m;
+    uint64_t n = std::min<uint64_t>(h->cfg.resize_k, round_end - h->split);
+    n = std::min<uint64_t>(n, h->max_buckets - h->nb());
+    *grew = n > 0;
+    if (!n) return HIVE_OK;
+    CKS(map_buckets(h, h->nb() + n));
+    {
+        Prof p(h, "k_split", s);
+        CK(launch_split(s, h->tv(), (uint32_t)n, h->ctrl));
+    }
+    h->split += (uint32_t)n;
+    if (h->split == round_end) {
+        h->m += 1;
+        h->split = 0;
+    }
+    h->grows++;
+    return drain_reinsert(h, s);
+}
+
+// contract_batch (readings A-7, A-25).  *aborted on a failed merge.
+hive_status contract_batch(hive_table_s* h, cudaStream_t s, bool* aborted) {
+    *aborted = false;
+    if (h->nb() <= h->nb_min) return HIVE_OK;
+    if (h->split == 0) {                  // regress: (m, 0) == (m-1, 2^(m-1))
+        h->m -= 1;
+        h->split = 1u << h->m;
+    }
+    uint64_t n = std::min<uint64_t>(h->cfg.resize_k, h->split);
+    n = std::min<uint64_t>(n, h->nb() - h->nb_min);
+    CKS(set_ctrl_word(h, &h->ctrl->first_abort, n, s));
+    {
+        Prof p(h, "k_merge", s);
+        CK(launch_merge(s, h->tv(), (uint32_t)n, h->ctrl));
+    }
+    CKS(read_ctrl(h, s));
+    const uint64_t merged = std::min<uint64_t>(h->ctrl_h->first_abort, n);
+    h->split -= (uint32_t)merged;
+    if (merged < n) {
+        *aborted = true;
+        h->merge_aborts++;
+    }
+    h->shrinks++;
+    return drain_reinsert(h, s);
+}
+
+hive_status grow_before(hive_table_s* h, uint64_t n_ins, cudaStream_t s) {
+    if (h->cfg.lf_grow >= 1.0f || n_ins == 0) return HIVE_OK;
+    CKS(read_ctrl(h, s));
+    const uint64_t count = h->ctrl_h->count;
+    while ((double)(count + n_ins) > (double)h->cfg.lf_grow * (double)h->nb() * SLOTS) {
+        bool grew = false;
+        CKS(expand_batch(h, s, &grew));
+        if (!grew) break;                 // max_capacity reached
+    }
+    return HIVE_OK;
+}
+
+hive_status shrink_after(hive_table_s* h, cudaStream_t s) {
+    if (h->cfg.lf_shrink <= 0.0f) return HIVE_OK;
+    CKS(read_ctrl(h, s));
+    const uint64_t count = h->ctrl_h->count;
+    while ((double)count < (double)h->cfg.lf_shrink * (double)h->nb() * SLOTS && h->nb() > h->nb_min) {
+        bool aborted = false;
+        CKS(contract_batch(h, s, &aborted));
+        if (aborted) break;
+    }
+    return HIVE_OK;
+}
+
+hive_status erase_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* idx, uint64_t n_upper,
+                        const uint64_t* n_dev, uint64_t n_batch, uint8_t* out, uint32_t* vals_zero,
+                        cudaStream_t s) {
+    const bool dedup = h->dedup_on();
+    DedupView dd{nullptr, 0};
+    if (dedup) {
+        const uint64_t cap = pow2_at_least(std::max<uint64_t>(1024, 2 * n_upper));
+        CKS(ensure(h->dd, h->dd_cap, cap));
+        CKS(ensure(h->owner, h->owner_cap, n_batch));
+        dd = DedupView{h->dd, cap - 1};
+        CK(cudaMemsetAsync(h->dd, 0xFF, cap * sizeof(uint64_t), s));
+        Prof p(h, "k_dedup_elect", s);
+        CK(launch_dedup_elect(h->grids.dedup, s, keys, idx, n_upper, n_dev, dd));
+    }
+    {
+        Prof p(h, "k_erase", s);
+        CK(launch_erase(h->grids.erase, s, keys, idx, n_upper, n_dev, h->tv(), h->sv(), dd, h->owner,
+                        out, vals_zero));
+    }
+    if (dedup && out) {
+        Prof p(h, "k_dup_copy", s);
+        CK(launch_dup_copy(h->grids.stream, s, idx, n_upper, n_dev, h->owner, out));
+    }
+    return HIVE_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+extern "C" {
+
+void hive_config_default(hive_config* c) {
+    if (!c) return;
+    c->capacity = 1024ull * SLOTS;
+    c->max_capacity = 0;
+    c->lf_grow = 0.90f;
+    c->lf_shrink = 0.25f;
+    c->max_evictions = 16;
+    c->resize_k = 1024;
+    c->stash_fraction = 0.02f;
+    c->flags = 0;
+}
+
+const char* hive_status_string(hive_status s) {
+    switch (s) {
+        case HIVE_OK: return "ok";
+        case HIVE_EINVAL: return "invalid argument";
+        case HIVE_ENOMEM: return "out of memory";
+        case HIVE_ECUDA: return "CUDA error";
+        case HIVE_ENCCL: return "NCCL error";
+        case HIVE_ESTASHFULL: return "stash full (entries lost)";
+        case HIVE_EBUSY: return "handle busy";
+    }
+    return "unknown";
+}
+
+const char* hive_last_error(void) { return g_err.c_str(); }
+
+hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
+    if (!cfg || !out || cfg->capacity == 0 || cfg->stash_fraction < 0.0f) return HIVE_EINVAL;
+    if (cfg->lf_grow < 1.0f && cfg->lf_shrink > 0.0f && cfg->lf_shrink >= cfg->lf_grow) return HIVE_EINVAL;
+    if (cfg->lf_grow <= 0.0f) return HIVE_EINVAL;
+    *out = nullptr;
+    if (!load_vmm(g_vmm)) return HIVE_ECUDA;
+    cudaStream_t s = (cudaStream_t)stream;
+    auto* h = new hive_table_s();
+    h->cfg = *cfg;
+    if (!h->cfg.max_evictions) h->cfg.max_evictions = 16;
+    if (!h->cfg.resize_k) h->cfg.resize_k = 1024;
+    auto fail = [&](hive_status st) { hive_destroy(h); return st; };
+    if (cudaGetDevice(&h->dev) != cudaSuccess) return fail(HIVE_ECUDA);
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev);
+    h->grids = query_grids(h->num_sms);
+
+    // A-20: any n_b >= 2, held as (m = floor(log2 n_b), split = n_b - 2^m)
+    const uint64_t nb = std::max<uint64_t>(2, (cfg->capacity + SLOTS - 1) / SLOTS);
+    uint32_t m = 0;
+    while ((2ull << m) <= nb) ++m;
+    h->m = h->m0 = m;
+    h->split = h->split0 = (uint32_t)(nb - (1ull << m));
+    h->nb_min = nb;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    uint64_t maxb = cfg->max_capacity ? (cfg->max_capacity + SLOTS - 1) / SLOTS
+                                      : (uint64_t)(total_b / 2 / (SLOTS * 8));
+    if (cfg->lf_grow >= 1.0f) maxb = nb;     // growth disabled: reserve exactly the table
+    h->max_buckets = std::min<uint64_t>(std::max<uint64_t>(maxb, nb), 1ull << 31);
+
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = h->dev;
+    CUresult r = g_vmm.granularity(&h->gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
+    if (r != CUDA_SUCCESS || !h->gran) { set_err_drv(r, "cuMemGetAllocationGranularity", __LINE__); return fail(HIVE_ECUDA); }
+    h->va_bytes = ((size_t)h->max_buckets * SLOTS * 8 + h->gran - 1) / h->gran * h->gran;
+    r = g_vmm.reserve(&h->va, h->va_bytes, 0, 0, 0);
+    if (r != CUDA_SUCCESS) { set_err_drv(r, "cuMemAddressReserve", __LINE__); return fail(HIVE_ENOMEM); }
+    hive_status st = map_buckets(h, nb);
+    if (st != HIVE_OK) return fail(st);
+
+    if (cudaMalloc((void**)&h->ctrl, sizeof(Ctrl)) != cudaSuccess) return fail(HIVE_ENOMEM);
+    if (cudaMallocHost((void**)&h->ctrl_h, sizeof(Ctrl)) != cudaSuccess) return fail(HIVE_ENOMEM);
+    if (cudaMallocHost((void**)&h->stage_h, 8 * sizeof(uint64_t)) != cudaSuccess) return fail(HIVE_ENOMEM);
+    if (cudaMalloc((void**)&h->pinfo, 2 * MAX_PARTS * sizeof(uint64_t)) != cudaSuccess) return fail(HIVE_ENOMEM);
+    memset(h->ctrl_h, 0, sizeof(Ctrl));
+    st = hive_clear(h, stream);
+    if (st != HIVE_OK) return fail(st);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return fail(HIVE_ECUDA);
+    *out = h;
+    return HIVE_OK;
+}
+
+hive_status hive_clear(hive_t h, void* stream) {
+    if (!h) return HIVE_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    h->m = h->m0;
+    h->split = h->split0;
+    CK(cudaMemsetAsync((void*)h->va, 0xFF, (size_t)h->nb_min * SLOTS * 8, s));
+    CK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), s));
+    CKS(stash_reset(h, h->stash_cap_for(h->nb_min), s));
+    h->grows = h->shrinks = h->merge_aborts = 0;
+    h->last = s;
+    return HIVE_OK;
+}
+
+hive_status hive_destroy(hive_t h) {
+    if (!h) return HIVE_EINVAL;
+    cudaStreamSynchronize(h->last);
+    cudaDeviceSynchronize();
+    if (h->va) {
+        for (size_t i = 0; i < h->chunks.size(); ++i) {
+            g_vmm.unmap(h->va + i * h->gran, h->gran);
+            g_vmm.release(h->chunks[i]);
+        }
+        g_vmm.free_va(h->va, h->va_bytes);
+    }
+    void* bufs[] = {h->ring, h->sidx, h->ctrl, h->dd, h->owner, h->left, h->cls, h->cnt, h->pinfo, h->tmpkv};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    if (h->ctrl_h) cudaFreeHost(h->ctrl_h);
+    if (h->stage_h) cudaFreeHost(h->stage_h);
+    for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : h->pool) cudaEventDestroy(e);
+    delete h;
+    return HIVE_OK;
+}
+
+hive_status hive_insert(hive_t h, const uint32_t* d_keys, const uint32_t* d_vals, uint64_t n,
+                        uint8_t* d_status, void* stream) {
+    if (!h) return HIVE_EINVAL;
+    if (n == 0) return HIVE_OK;
+    if (!d_keys || !d_vals || n >= (1ull << 32)) return HIVE_EINVAL;
+    BusyGuard g(h);
+    if (!g.ok) return HIVE_EBUSY;
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last = s;
+    CKS(grow_before(h, n, s));
+    return insert_phase(h, d_keys, d_vals, nullptr, nullptr, n, nullptr, n, d_status, nullptr, s);
+}
+
+hive_status hive_find(hive_t h, const uint32_t* d_keys, uint64_t n, uint32_t* d_vals_out,
+                      uint8_t* d_found, void* stream) {
+    if (!h) return HIVE_EINVAL;
+    if (n == 0) return HIVE_OK;
+    if (!d_keys || !d_vals_out) return HIVE_EINVAL;
+    BusyGuard g(h);
+    if (!g.ok) return HIVE_EBUSY;
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last = s;
+    Prof p(h, "k_find", s);
+    CK(launch_find(h->grids.find, s, d_keys, nullptr, n, nullptr, h->tv(), h->sv(), d_vals_out, d_found));
+    return HIVE_OK;
+}
+
+hive_status hive_erase(hive_t h, const uint32_t* d_keys, uint64_t n, uint8_t* d_erased, void* stream) {
+    if (!h) return HIVE_EINVAL;
+    if (n == 0) return HIVE_OK;
+    if (!d_keys || n >= (1ull << 32)) return HIVE_EINVAL;
+    BusyGuard g(h);
+    if (!g.ok) return HIVE_EBUSY;
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last = s;
+    CKS(erase_phase(h, d_keys, nullptr, n, nullptr, n, d_erased, nullptr, s));
+    return shrink_after(h, s);
+}
+
+hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, const uint32_t* d_vals,
+                       uint64_t n, uint32_t* d_vals_out, uint8_t* d_result, void* stream) {
+    if (!h) return HIVE_EINVAL;
+    if (n == 0) return HIVE_OK;
+    if (!d_op || !d_keys || !d_vals || !d_vals_out || !d_result || n >= (1ull << 32)) return HIVE_EINVAL;
+    BusyGuard g(h);
+    if (!g.ok) return HIVE_EBUSY;
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last = s;
+    // classify: stable partition of op indices by opcode (3 regions of n)
+    CKS(ensure(h->cls, h->cls_cap, 3 * n));
+    CKS(ensure(h->cnt, h->cnt_cap, 3 * part_warps(n) + 1));
+    {
+        Prof p(h, "k_classify", s);
+        CK(launch_partition(s, PART_CLASSIFY, 3, 0, d_keys, d_vals, d_op, n, h->cnt, h->pinfo, h->cls, n,
+                            nullptr, nullptr, nullptr, d_result, d_vals_out));
+    }
+    const uint64_t* n_find = h->pinfo + 0;
+    const uint64_t* n_ins = h->pinfo + 1;
+    const uint64_t* n_era = h->pinfo + 2;
+    if (h->cfg.lf_grow < 1.0f) {
+        CK(cudaMemcpyAsync(h->stage_h, h->pinfo, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        CKS(grow_before(h, h->stage_h[1], s));
+    }
+    CKS(insert_phase(h, d_keys, d_vals, nullptr, h->cls + n, n, n_ins, n, d_result, d_vals_out, s));
+    CKS(erase_phase(h, d_keys, h->cls + 2 * n, n, n_era, n, d_result, d_vals_out, s));
+    CKS(shrink_after(h, s));
+    Prof p(h, "k_find", s);
+    CK(launch_find(h->grids.find, s, d_keys, h->cls, n, n_find, h->tv(), h->sv(), d_vals_out, d_result));
+    return HIVE_OK;
+}
+
+hive_status hive_size(hive_t h, uint64_t* out) {
+    if (!h || !out) return HIVE_EINVAL;
+    CKS(read_ctrl(h, h->last));
+    *out = h->ctrl_h->count;
+    return h->ctrl_h->failed ? HIVE_ESTASHFULL : HIVE_OK;
+}
+
+hive_status hive_stats(hive_t h, hive_stats_t* o) {
+    if (!h || !o) return HIVE_EINVAL;
+    cudaStream_t s = h->last;
+    CKS(set_ctrl_word(h, &h->ctrl->in_b1, 0, s));
+    CK(launch_count_b1(h->grids.stream, s, h->tv(), h->nb(), h->ctrl));
+    CKS(read_ctrl(h, s));
+    const Ctrl& c = *h->ctrl_h;
+    memset(o, 0, sizeof *o);
+    o->n_buckets = h->nb();
+    o->m = h->m;
+    o->split = h->split;
+    o->count = c.count;
+    o->stash_used = std::min<uint64_t>(c.stash_tail, h->stash_cap);
+    o->stash_cap = h->stash_cap;
+    o->evictions = c.evictions;
+    o->max_depth = c.max_depth;
+    o->stash_pushes = c.stash_pushes;
+    o->leftovers = c.leftovers;
+    o->grows = h->grows;
+    o->shrinks = h->shrinks;
+    o->merge_aborts = h->merge_aborts;
+    o->failed = c.failed;
+    o->in_b1 = c.in_b1;
+    o->mapped_bytes = h->chunks.size() * h->gran;
+    return c.failed ? HIVE_ESTASHFULL : HIVE_OK;
+}
+
+hive_status hive_dump(hive_t h, uint32_t* d_keys, uint32_t* d_vals, uint64_t cap, uint64_t* n_out,
+                      void* stream) {
+    if (!h || !n_out || (cap && (!d_keys || !d_vals))) return HIVE_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    CKS(set_ctrl_word(h, &h->ctrl->dump_n, 0, s));
+    CK(launch_dump(h->grids.stream, s, h->tv(), h->nb(), h->sv(), d_keys, d_vals, cap));
+    CKS(read_ctrl(h, s));
+    *n_out = h->ctrl_h->dump_n;
+    return HIVE_OK;
+}
+
+hive_status hive_profile(hive_t h, int enable) {
+    if (!h) return HIVE_EINVAL;
+    h->prof = enable != 0;
+    return HIVE_OK;
+}
+
+int hive_profile_read(hive_t h, const char** names, double* ms, uint64_t* launches, int max, int reset) {
+    if (!h) return -1;
+    for (auto& r : h->recs) {
+        float t = 0.f;
+        cudaEventSynchronize(r.b);
+        cudaEventElapsedTime(&t, r.a, r.b);
+        bool hit = false;
+        for (auto& a : h->agg)
+            if (strcmp(a.name, r.name) == 0) { a.ms += t; a.n++; hit = true; break; }
+        if (!hit) h->agg.push_back({r.name, (double)t, 1});
+        h->pool.push_back(r.a);
+        h->pool.push_back(r.b);
+    }
+    h->recs.clear();
+    int k = 0;
+    for (auto& a : h->agg) {
+        if (k < max) {
+            if (names) names[k] = a.name;
+            if (ms) ms[k] = a.ms;
+            if (launches) launches[k] = a.n;
+        }
+        ++k;
+    }
+    if (reset) h->agg.clear();
+    return k;
+}
+
+hive_status hive_route(uint32_t n_shards, uint32_t seed, const uint32_t* d_keys, const uint32_t* d_vals,
+                       const uint8_t* d_ops, uint64_t n, uint64_t* d_send_kv, uint8_t* d_send_ops,
+                       uint32_t* d_pos, uint64_t* d_counts, void* stream) {
+    if (n_shards == 0 || n_shards > (uint32_t)MAX_PARTS || !d_counts) return HIVE_EINVAL;
+    if (n >= (1ull << 32)) return HIVE_EINVAL;
+    if (n && (!d_keys || !d_send_kv || !d_pos || (d_send_ops && !d_ops))) return HIVE_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint64_t* cnt = nullptr;
+    uint64_t* info = nullptr;
+    const uint64_t E = (uint64_t)n_shards * part_warps(n) + 1;
+    CK(cudaMallocAsync((void**)&cnt, E * sizeof(uint64_t), s));
+    CK(cudaMallocAsync((void**)&info, 2 * MAX_PARTS * sizeof(uint64_t), s));
+    CK(launch_partition(s, PART_ROUTE, n_shards, seed, d_keys, d_vals, d_ops, n, cnt, info, nullptr, 0,
+                        d_send_kv, d_send_ops, d_pos, nullptr, nullptr));
+    CK(cudaMemcpyAsync(d_counts, info, n_shards * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    CK(cudaFreeAsync(cnt, s));
+    CK(cudaFreeAsync(info, s));
+    return HIVE_OK;
+}
+
+hive_status hive_unroute(const uint32_t* d_pos, uint64_t n, const uint8_t* d_in8, uint8_t* d_out8,
+                         const uint32_t* d_in32, uint32_t* d_out32, void* stream) {
+    if (n == 0) return HIVE_OK;
+    if (!d_pos || ((d_out8 != nullptr) != (d_in8 != nullptr)) || ((d_out32 != nullptr) != (d_in32 != nullptr)))
+        return HIVE_EINVAL;
+    CK(launch_unroute((cudaStream_t)stream, d_pos, n, d_in8, d_out8, d_in32, d_out32));
+    return HIVE_OK;
+}
+
+hive_status hive_unpack_kv(const uint64_t* d_kv, uint64_t n, uint32_t* d_keys, uint32_t* d_vals,
+                           void* stream) {
+    if (n == 0) return HIVE_OK;
+    if (!d_kv) return HIVE_EINVAL;
+    CK(launch_unpack((cudaStream_t)stream, d_kv, n, d_keys, d_vals));
+    return HIVE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,954 @@
+// hive_kernels.cu — sm_100a kernels of the B200 Hive table (arXiv 2510.15095).
+//
+// Every kernel here is HBM-bound integer work (DESIGN.md "Kernels and their
+// rooflines"): no tensor cores, no shared-memory tiling of the table (each
+// 256 B bucket is touched once per probe).  Persistent grid-stride kernels of
+// 256 threads; one operation per 8-lane group (4 slots = one 256-bit load per
+// lane), so each warp keeps four independent bucket probes in flight.
+#include <cuda_runtime.h>
+
+#include "hive_kernels.cuh"
+
+namespace hive {
+
+// --------------------------------------------------------------------------------
+// small helpers
+// --------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t cas64(uint64_t* p, uint64_t cmp, uint64_t val) {
+    return (uint64_t)atomicCAS((unsigned long long*)p, (unsigned long long)cmp,
+                               (unsigned long long)val);
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_max(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long u = __shfl_xor_sync(FULL, v, o);
+        v = u > v ? u : v;
+    }
+    return v;
+}
+// One global atomic per block for a per-thread counter.  Every thread of the
+// block must call it (kernel epilogue, after the grid-stride loop).
+__device__ __forceinline__ void block_add(unsigned long long* dst, unsigned long long v) {
+    __shared__ unsigned long long acc;
+    if (threadIdx.x == 0) acc = 0;
+    __syncthreads();
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&acc, v);
+    __syncthreads();
+    if (threadIdx.x == 0 && acc) atomicAdd(dst, acc);
+}
+__device__ __forceinline__ void block_max(unsigned long long* dst, unsigned long long v) {
+    __shared__ unsigned long long accm;
+    if (threadIdx.x == 0) accm = 0;
+    __syncthreads();
+    v = warp_max(v);
+    if ((threadIdx.x & 31) == 0 && v) atomicMax(&accm, v);
+    __syncthreads();
+    if (threadIdx.x == 0 && accm) atomicMax(dst, accm);
+}
+
+// Per-warp staging of an index list in shared memory; one global atomic per
+// 32 items instead of one per warp-iteration.
+struct WarpList {
+    uint32_t* sbuf;   // 32 entries of this warp
+    int n;            // warp-uniform fill level
+    __device__ __forceinline__ void flush(uint32_t* out, unsigned long long* out_n) {
+        __syncwarp();
+        if (n == 0) return;
+        const int lane = threadIdx.x & 31;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(out_n, (unsigned long long)n);
+        base = __shfl_sync(FULL, base, 0);
+        if (lane < n) out[base + lane] = sbuf[lane];
+        __syncwarp();
+        n = 0;
+    }
+    __device__ __forceinline__ void push(bool flag, uint32_t item, uint32_t* out,
+                                         unsigned long long* out_n) {
+        uint32_t bal = __ballot_sync(FULL, flag);
+        int c = __popc(bal);
+        if (c == 0) return;
+        if (n + c > 32) flush(out, out_n);
+        if (flag) sbuf[n + __popc(bal & lanemask_lt())] = item;
+        n += c;
+        __syncwarp();
+    }
+};
+
+// --------------------------------------------------------------------------------
+// stash index (reading A-10): open addressing on fmix32(key)
+// --------------------------------------------------------------------------------
+__device__ __forceinline__ void stash_index_put(const StashView& sv, uint32_t k, uint64_t pos) {
+    uint64_t h = fmix32(k) & sv.idx_mask;
+    const uint64_t w = ((uint64_t)k << 32) | pos;
+    for (uint64_t probe = 0; probe <= sv.idx_mask; ++probe) {
+        uint64_t e = sv.index[h];
+        if (e == EMPTY) {
+            uint64_t prev = cas64(&sv.index[h], EMPTY, w);
+            if (prev == EMPTY) return;
+            e = prev;
+        }
+        if ((uint32_t)(e >> 32) == k) {          // re-point a stale entry for k
+            atomicExch((unsigned long long*)&sv.index[h], (unsigned long long)w);
+            return;
+        }
+        h = (h + 1) & sv.idx_mask;
+    }
+}
+// Ring position of the live stash entry holding k, or -1.
+__device__ __forceinline__ int64_t stash_lookup(const StashView& sv, uint32_t k, uint64_t* word) {
+    uint64_t h = fmix32(k) & sv.idx_mask;
+    for (uint64_t probe = 0; probe <= sv.idx_mask; ++probe) {
+        uint64_t e = sv.index[h];
+        if (e == EMPTY) return -1;
+        if ((uint32_t)(e >> 32) == k) {
+            uint64_t pos = e & 0xFFFFFFFFull;
+            uint64_t w = *(volatile uint64_t*)&sv.ring[pos];
+            if (w != EMPTY && key_of(w) == k) {
+                *word = w;
+                return (int64_t)pos;
+            }
+            return -1;
+        }
+        h = (h + 1) & sv.idx_mask;
+    }
+    return -1;
+}
+
+// --------------------------------------------------------------------------------
+// group protocols
+// --------------------------------------------------------------------------------
+template <int SPL>
+__device__ __forceinline__ void fill_empty(uint64_t (&s)[SPL]) {
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) s[j] = EMPTY;
+}
+
+// Step 1 / Alg. 1 ReplacePath and Alg. 4's CAS-to-EMPTY
+// (PAPER:448-475): WCME on the cached bucket view, the elected lane CASes its
+// cached word to `newkv`.  On a lost CAS the winner refreshes its view and the
+// group re-elects (reading A-18).  Group-uniform result; all lanes call.
+template <int G>
+__device__ __forceinline__ bool wcme_cas(const WarpGroup<G>& wg, uint64_t (&s)[WarpGroup<G>::SPL],
+                                         uint64_t* bucket, uint32_t k, uint64_t newkv,
+                                         bool valid) {
+    constexpr int SPL = WarpGroup<G>::SPL;
+    bool trying = valid, done = false;
+    for (int iter = 0; iter <= SLOTS; ++iter) {
+        int ws;
+        uint64_t old;
+        bool hit = wcme<G>(wg, s, k, trying, &ws, &old);
+        trying = trying && hit;
+        if (!__any_sync(FULL, trying)) break;
+        const int wl = ws / SPL;
+        bool ok = false;
+        if (trying && wg.gl == wl) {
+            uint64_t prev = cas64(bucket + ws, old, newkv);
+            ok = (prev == old);
+            if (!ok) put<SPL>(s, ws % SPL, prev);
+        }
+        ok = wg.bcast(ok, wl);
+        if (trying && ok) {
+            done = true;
+            trying = false;
+        }
+    }
+    return done;
+}
+
+// Step 2 / WABC claim-and-commit: ballot of EMPTY
+// slots in the cached view = claim mask; the lowest free lane elects its
+// lowest free slot and publishes kv with ONE 64-bit CAS(EMPTY -> kv).  A lost
+// CAS marks that slot taken in the view and the group re-elects.
+template <int G>
+__device__ __forceinline__ bool wabc_claim(const WarpGroup<G>& wg, uint64_t (&s)[WarpGroup<G>::SPL],
+                                           uint64_t* bucket, uint64_t kv, bool want) {
+    constexpr int SPL = WarpGroup<G>::SPL;
+    bool trying = want, placed = false;
+    for (int iter = 0; iter <= SLOTS; ++iter) {
+        uint32_t fm = trying ? free_bits<SPL>(s) : 0u;
+        uint32_t F = wg.ballot(fm != 0);
+        trying = trying && F != 0;
+        if (!__any_sync(FULL, trying)) break;
+        const int wl = F ? __ffs(F) - 1 : 0;
+        bool ok = false;
+        if (trying && wg.gl == wl) {
+            const int j = __ffs(fm) - 1;
+            uint64_t prev = cas64(bucket + wl * SPL + j, EMPTY, kv);
+            ok = (prev == EMPTY);
+            if (!ok) put<SPL>(s, j, prev);
+        }
+        ok = wg.bcast(ok, wl);
+        if (trying && ok) {
+            placed = true;
+            trying = false;
+        }
+    }
+    return placed;
+}
+
+// --------------------------------------------------------------------------------
+// FIND: WCME on b1, then b2 only on a miss, then the stash
+// index only when the stash is non-empty.  Read-only phase.
+// --------------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(BLOCK)
+k_find(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
+       const uint64_t* __restrict__ n_dev, TableView tv, StashView sv,
+       uint32_t* __restrict__ vals_out, uint8_t* __restrict__ found_out) {
+    using WG = WarpGroup<G>;
+    constexpr int SPL = WG::SPL;
+    WG wg;
+    if (n_dev) n = *n_dev;
+    const bool stash_on = sv.ctrl->stash_tail != 0;
+    const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
+    for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
+        const uint64_t t = t0 + wg.gi;
+        const bool active = t < n;
+        const uint64_t op = active ? (idx ? (uint64_t)idx[t] : t) : 0;
+        const uint32_t k = active ? keys[op] : INVALID_KEY;
+        const bool valid = k != INVALID_KEY;
+        uint32_t b1 = 0, b2 = 0;
+        if (valid) {
+            b1 = tv.addr(bithash1(k));
+            b2 = tv.addr(bithash2(k));
+        }
+        uint64_t s[SPL];
+        if (valid) load_slots_ro<SPL>(wg.slot_ptr(tv.bucket(b1)), s);
+        else fill_empty<SPL>(s);
+        int ws;
+        uint64_t w;
+        bool found = wcme<G>(wg, s, k, valid, &ws, &w);
+        const bool need2 = valid && !found && b2 != b1;
+        if (__any_sync(FULL, need2)) {
+            if (need2) load_slots_ro<SPL>(wg.slot_ptr(tv.bucket(b2)), s);
+            else fill_empty<SPL>(s);
+            uint64_t w2;
+            bool f2 = wcme<G>(wg, s, k, need2, &ws, &w2);
+            if (need2 && f2) {
+                found = true;
+                w = w2;
+            }
+        }
+        if (stash_on && valid && !found && wg.gl == 0) {
+            uint64_t sw;
+            if (stash_lookup(sv, k, &sw) >= 0) {
+                found = true;
+                w = sw;
+            }
+        }
+        if (active && wg.gl == 0) {
+            vals_out[op] = found ? val_of(w) : 0u;
+            if (found_out) found_out[op] = found ? 1 : 0;
+        }
+    }
+}
+
+// --------------------------------------------------------------------------------
+// Owner election for in-batch duplicates (reading A-15):
+// insert-if-absent of (key << 32 | op) into a per-batch table with atomicMax,
+// so the surviving op per key is the highest index (the oracle's last write).
+// Ops inside a warp are increasing with the lane (identity or stable lists), so
+// __match_any_sync's highest lane is the warp-local maximum.
+// --------------------------------------------------------------------------------
+__global__ void __launch_bounds__(BLOCK)
+k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
+              const uint64_t* __restrict__ n_dev, DedupView dd) {
+    if (n_dev) n = *n_dev;
+    const int lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u); t0 < n; t0 += stride) {
+        const uint64_t t = t0 + lane;
+        const bool active = t < n;
+        const uint64_t op = active ? (idx ? (uint64_t)idx[t] : t) : 0;
+        const uint32_t k = active ? keys[op] : INVALID_KEY;
+        const uint32_t grp = __match_any_sync(FULL, k);
+        const bool leader = (31 - __clz(grp)) == lane;
+        if (k == INVALID_KEY || !leader) continue;
+        const uint64_t word = ((uint64_t)k << 32) | op;
+        uint64_t h = fmix32(k ^ DEDUP_SEED) & dd.mask;
+        for (uint64_t probe = 0; probe <= dd.mask; ++probe) {
+            uint64_t e = dd.slots[h];
+            if (e == EMPTY) {
+                uint64_t prev = cas64(&dd.slots[h], EMPTY, word);
+                if (prev == EMPTY) break;
+                e = prev;
+            }
+            if ((uint32_t)(e >> 32) == k) {
+                if (word > e) atomicMax((unsigned long long*)&dd.slots[h], (unsigned long long)word);
+                break;
+            }
+            h = (h + 1) & dd.mask;
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t dedup_owner(const DedupView& dd, uint32_t k, uint32_t self) {
+    uint64_t h = fmix32(k ^ DEDUP_SEED) & dd.mask;
+    for (uint64_t probe = 0; probe <= dd.mask; ++probe) {
+        uint64_t e = dd.slots[h];
+        if (e == EMPTY) return self;
+        if ((uint32_t)(e >> 32) == k) return (uint32_t)e;
+        h = (h + 1) & dd.mask;
+    }
+    return self;
+}
+
+// --------------------------------------------------------------------------------
+// INSERT fast path: Step 1 (replace) + Step 2 (claim-and-commit,
+// PAPER:348-381) in one pass; ops whose candidate buckets are both full go to
+// the leftover list for Steps 3-4.  `kvs != nullptr` = place-only mode used to
+// reinsert drained stash entries after a resize: Step 1 is skipped
+// (those keys are in no bucket) and nothing is counted.
+// --------------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(BLOCK)
+k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+              const uint64_t* __restrict__ kvs, const uint32_t* __restrict__ idx, uint64_t n,
+              const uint64_t* __restrict__ n_dev, TableView tv, StashView sv, DedupView dd,
+              uint32_t* __restrict__ owner_of, uint8_t* __restrict__ status,
+              uint32_t* __restrict__ vals_zero, uint32_t* __restrict__ leftover) {
+    using WG = WarpGroup<G>;
+    constexpr int SPL = WG::SPL;
+    __shared__ uint32_t lbuf[WARPS_PER_BLOCK][32];
+    WG wg;
+    WarpList wl{lbuf[threadIdx.x >> 5], 0};
+    if (n_dev) n = *n_dev;
+    const bool place_only = kvs != nullptr;
+    const bool stash_on = !place_only && sv.ctrl->stash_tail != 0;
+    unsigned long long added = 0;
+    const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
+    for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
+        const uint64_t t = t0 + wg.gi;
+        const bool active = t < n;
+        uint64_t op = t;
+        uint32_t k = INVALID_KEY, v = 0;
+        if (active) {
+            if (place_only) {
+                const uint64_t w = kvs[t];
+                k = key_of(w);
+                v = val_of(w);
+            } else {
+                op = idx ? (uint64_t)idx[t] : t;
+                k = keys[op];
+                v = vals[op];
+            }
+        }
+        bool valid = active && k != INVALID_KEY;
+        if (!place_only && active && wg.gl == 0) {
+            if (vals_zero) vals_zero[op] = 0;
+            if (!valid && status) status[op] = 2;
+        }
+        // owner election (duplicates copy the owner's outcome afterwards)
+        if (dd.slots) {
+            uint32_t owner = (uint32_t)op;
+            if (valid && wg.gl == 0) owner = dedup_owner(dd, k, (uint32_t)op);
+            owner = wg.bcast(owner, 0);
+            if (active && wg.gl == 0) owner_of[op] = valid ? owner : (uint32_t)op;
+            if (owner != (uint32_t)op) valid = false;
+        }
+        const uint64_t kv = pack(k, v);
+        uint32_t b1 = 0, b2 = 0;
+        if (valid) {
+            b1 = tv.addr(bithash1(k));
+            b2 = tv.addr(bithash2(k));
+        }
+        const bool two = valid && b2 != b1;
+        uint64_t s1[SPL], s2[SPL];
+        if (valid) load_slots<SPL>(wg.slot_ptr(tv.bucket(b1)), s1);
+        else fill_empty<SPL>(s1);
+        bool done = false;
+        if (!place_only) {
+            // Step 1 on b1, then b2 (loaded only on a miss), then the stash.
+            done = wcme_cas<G>(wg, s1, tv.bucket(b1), k, kv, valid);
+            const bool need2 = two && !done;
+            if (need2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
+            else fill_empty<SPL>(s2);
+            if (__any_sync(FULL, need2)) done |= wcme_cas<G>(wg, s2, tv.bucket(b2), k, kv, need2);
+            if (stash_on) {
+                bool sdone = false;
+                if (valid && !done && wg.gl == 0) {
+                    uint64_t sw;
+                    int64_t pos = stash_lookup(sv, k, &sw);
+                    while (pos >= 0) {
+                        uint64_t prev = cas64(&sv.ring[pos], sw, kv);
+                        if (prev == sw) { sdone = true; break; }
+                        pos = stash_lookup(sv, k, &sw);
+                    }
+                }
+                done |= wg.bcast(sdone, 0);
+            }
+        } else {
+            if (two) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
+            else fill_empty<SPL>(s2);
+        }
+        // Step 2: WABC claim in b1, then b2 (first-fit, A-21)
+        bool placed = wabc_claim<G>(wg, s1, tv.bucket(b1), kv, valid && !done);
+        const bool want2 = two && !done && !placed;
+        if (__any_sync(FULL, want2)) placed |= wabc_claim<G>(wg, s2, tv.bucket(b2), kv, want2);
+        const bool left = valid && !done && !placed;
+        if (!place_only && valid && wg.gl == 0) {
+            if (status) status[op] = done ? 1 : 0;
+            if (!done) ++added;
+        }
+        wl.push(left && wg.gl == 0, (uint32_t)(place_only ? t : op), leftover, &sv.ctrl->n_left);
+    }
+    wl.flush(leftover, &sv.ctrl->n_left);
+    block_add(&sv.ctrl->count, added);
+}
+
+// --------------------------------------------------------------------------------
+// INSERT slow path: Step 3 bounded cuckoo eviction (Alg. 3)
+// then Step 4 stash for the leftovers of the fast pass.
+// B200 variant: no bucket lock -- the victim is swapped out with
+// one 64-bit CAS(victim -> newcomer) (reading A-14) and the victim slot
+// rotates with the round (reading A-6 allows any victim rule; placement is not
+// observable).
+// --------------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(BLOCK)
+k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+              const uint64_t* __restrict__ kvs, const uint32_t* __restrict__ leftover,
+              TableView tv, StashView sv, uint32_t max_evictions, uint8_t* __restrict__ status) {
+    using WG = WarpGroup<G>;
+    constexpr int SPL = WG::SPL;
+    WG wg;
+    const uint64_t n = sv.ctrl->n_left;
+    if (!kvs && blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(&sv.ctrl->leftovers, (unsigned long long)n);
+    unsigned long long evict = 0, depth = 0, pushes = 0, lost = 0;
+    const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
+    for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
+        const uint64_t t = t0 + wg.gi;
+        const bool active = t < n;
+        uint64_t item = active ? leftover[t] : 0;
+        uint64_t kv = EMPTY;
+        if (active) kv = kvs ? kvs[item] : pack(keys[item], vals[item]);
+        bool trying = active;
+        uint32_t b = active ? tv.addr(bithash1(key_of(kv))) : 0;   // start at b1
+        const uint32_t seed = active ? bithash2(key_of(kv)) : 0;
+        uint32_t rounds = 0;
+        for (uint32_t r = 0; r < max_evictions; ++r) {
+            if (!__any_sync(FULL, trying)) break;
+            uint64_t s[SPL];
+            if (trying) load_slots<SPL>(wg.slot_ptr(tv.bucket(b)), s);
+            else fill_empty<SPL>(s);
+            if (trying) ++rounds;
+            bool placed = wabc_claim<G>(wg, s, tv.bucket(b), kv, trying);   // line 3
+            if (placed) trying = false;
+            // evict a victim: rotating slot, CAS-swap (lines 17-21, A-14)
+            const int vs = (int)((seed + r * 11u) & 31u);
+            const int vl = vs / SPL;
+            uint64_t victim = wg.bcast(pick<SPL>(s, vs % SPL), vl);
+            bool ok = false;
+            if (trying && wg.gl == vl && victim != EMPTY) {
+                uint64_t prev = cas64(tv.bucket(b) + vs, victim, kv);
+                ok = (prev == victim);
+            }
+            ok = wg.bcast(ok, vl);
+            if (trying && ok) {
+                kv = victim;                                 // line 33
+                b = tv.alt(key_of(kv), b);                   // line 34
+                if (wg.gl == 0) ++evict;
+            }
+        }
+        if (wg.gl == 0 && active) depth = rounds > depth ? rounds : depth;
+        // Step 4: stash push of the in-hand entry
+        if (trying && wg.gl == 0) {
+            unsigned long long pos = atomicAdd(&sv.ctrl->stash_tail, 1ull);
+            if (pos < sv.cap) {
+                sv.ring[pos] = kv;
+                stash_index_put(sv, key_of(kv), pos);
+                ++pushes;
+            } else {
+                ++lost;
+                if (status && !kvs) status[item] = 3;
+            }
+        }
+    }
+    block_add(&sv.ctrl->evictions, evict);
+    block_add(&sv.ctrl->stash_pushes, pushes);
+    block_add(&sv.ctrl->failed, lost);
+    block_add(&sv.ctrl->count, (unsigned long long)(0ull - lost));
+    block_max(&sv.ctrl->max_depth, depth);
+}
+
+// --------------------------------------------------------------------------------
+// ERASE (Alg. 4 ScanBucketAndDelete): WCME, winner CAS -> EMPTY;
+// b2 only on a miss; then the stash.
+// --------------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(BLOCK)
+k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
+        const uint64_t* __restrict__ n_dev, TableView tv, StashView sv, DedupView dd,
+        uint32_t* __restrict__ owner_of, uint8_t* __restrict__ erased_out,
+        uint32_t* __restrict__ vals_zero) {
+    using WG = WarpGroup<G>;
+    constexpr int SPL = WG::SPL;
+    WG wg;
+    if (n_dev) n = *n_dev;
+    const bool stash_on = sv.ctrl->stash_tail != 0;
+    unsigned long long removed = 0;
+    const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
+    for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
+        const uint64_t t = t0 + wg.gi;
+        const bool active = t < n;
+        const uint64_t op = active ? (idx ? (uint64_t)idx[t] : t) : 0;
+        const uint32_t k = active ? keys[op] : INVALID_KEY;
+        bool valid = k != INVALID_KEY;
+        if (active && wg.gl == 0 && vals_zero) vals_zero[op] = 0;
+        if (dd.slots) {
+            uint32_t owner = (uint32_t)op;
+            if (valid && wg.gl == 0) owner = dedup_owner(dd, k, (uint32_t)op);
+            owner = wg.bcast(owner, 0);
+            if (active && wg.gl == 0) owner_of[op] = valid ? owner : (uint32_t)op;
+            if (owner != (uint32_t)op) valid = false;
+        }
+        uint32_t b1 = 0, b2 = 0;
+        if (valid) {
+            b1 = tv.addr(bithash1(k));
+            b2 = tv.addr(bithash2(k));
+        }
+        uint64_t s[SPL];
+        if (valid) load_slots<SPL>(wg.slot_ptr(tv.bucket(b1)), s);
+        else fill_empty<SPL>(s);
+        bool done = wcme_cas<G>(wg, s, tv.bucket(b1), k, EMPTY, valid);
+        const bool need2 = valid && !done && b2 != b1;
+        if (__any_sync(FULL, need2)) {
+            if (need2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s);
+            else fill_empty<SPL>(s);
+            done |= wcme_cas<G>(wg, s, tv.bucket(b2), k, EMPTY, need2);
+        }
+        if (stash_on && valid && !done && wg.gl == 0) {
+            uint64_t sw;
+            int64_t pos = stash_lookup(sv, k, &sw);
+            while (pos >= 0) {
+                uint64_t prev = cas64(&sv.ring[pos], sw, EMPTY);
+                if (prev == sw) { done = true; break; }
+                pos = stash_lookup(sv, k, &sw);
+            }
+        }
+        if (active && wg.gl == 0 && (valid || !dd.slots || k == INVALID_KEY)) {
+            if (erased_out) erased_out[op] = done ? 1 : 0;
+            if (done) ++removed;
+        }
+    }
+    block_add(&sv.ctrl->count, 0ull - removed);
+}
+
+// Duplicates copy their owner's outcome (PHASED contract, A-17).
+__global__ void __launch_bounds__(BLOCK)
+k_dup_copy(const uint32_t* __restrict__ idx, uint64_t n, const uint64_t* __restrict__ n_dev,
+           const uint32_t* __restrict__ owner_of, uint8_t* __restrict__ out) {
+    if (n_dev) n = *n_dev;
+    for (uint64_t t = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; t < n;
+         t += (uint64_t)gridDim.x * BLOCK) {
+        const uint64_t op = idx ? (uint64_t)idx[t] : t;
+        const uint32_t o = owner_of[op];
+        if (o != (uint32_t)op) out[op] = out[o];
+    }
+}
+
+// --------------------------------------------------------------------------------
+// Linear-hashing split: one warp per (b_src, b_dst) pair, one
+// lane per slot as in the paper's listing.  The destination bucket is written
+// whole (movers compacted into slots 0..n-1, EMPTY after), so new buckets need
+// no separate initialisation.  Residence hash: reading A-3.
+// --------------------------------------------------------------------------------
+__global__ void __launch_bounds__(BLOCK)
+k_split(TableView tv, uint32_t n_pairs, Ctrl* ctrl) {
+    const uint32_t pair = (blockIdx.x * BLOCK + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (pair >= n_pairs) return;
+    const uint32_t b_src = tv.split + pair;
+    const uint32_t b_dst = b_src + tv.mask + 1u;
+    const uint32_t next_mask = (tv.mask << 1) | 1u;
+    uint64_t* src = tv.bucket(b_src);
+    uint64_t* dst = tv.bucket(b_dst);
+    const uint64_t kv = src[lane];
+    bool should_move = false;
+    if (kv != EMPTY) {
+        const uint32_t k = key_of(kv);
+        const uint32_t h1 = bithash1(k);
+        const uint32_t h = ((h1 & tv.mask) == b_src) ? h1 : bithash2(k);
+        should_move = (h & next_mask) == b_dst;
+    }
+    const uint32_t move_mask = __ballot_sync(FULL, should_move);
+    const uint32_t my_rank = __popc(move_mask & lanemask_lt());
+    const int n_movers = __popc(move_mask);
+    if (should_move) {
+        dst[my_rank] = kv;
+        src[lane] = EMPTY;
+    }
+    if (lane >= n_movers) dst[lane] = EMPTY;                      // rest of the new bucket
+}
+
+// Contraction, LIFO pairs t = 0..n_pairs-1 with
+// b_dst = split-1-t, b_src = b_dst + 2^m.  Pass 1 finds the first pair that
+// must abort (n_move > n_free); pass 2 merges the pairs before it
+// (the sequential LIFO loop stops at its first abort, reading A-25).
+__global__ void __launch_bounds__(BLOCK)
+k_merge_check(TableView tv, uint32_t n_pairs, Ctrl* ctrl) {
+    const uint32_t t = (blockIdx.x * BLOCK + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= n_pairs) return;
+    const uint32_t b_dst = tv.split - 1u - t;
+    const uint32_t b_src = b_dst + tv.mask + 1u;
+    const uint32_t occ = __ballot_sync(FULL, tv.bucket(b_src)[lane] != EMPTY);
+    const uint32_t fre = __ballot_sync(FULL, tv.bucket(b_dst)[lane] == EMPTY);
+    if (lane == 0 && __popc(occ) > __popc(fre)) atomicMin(&ctrl->first_abort, (unsigned long long)t);
+}
+__global__ void __launch_bounds__(BLOCK)
+k_merge_apply(TableView tv, uint32_t n_pairs, Ctrl* ctrl) {
+    const uint32_t t = (blockIdx.x * BLOCK + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= n_pairs || t >= ctrl->first_abort) return;
+    const uint32_t b_dst = tv.split - 1u - t;
+    const uint32_t b_src = b_dst + tv.mask + 1u;
+    uint64_t* src = tv.bucket(b_src);
+    uint64_t* dst = tv.bucket(b_dst);
+    const uint64_t kv = src[lane];
+    const bool live = kv != EMPTY;
+    const uint32_t occ_mask = __ballot_sync(FULL, live);
+    const uint32_t my_rank = __popc(occ_mask & lanemask_lt());
+    const uint32_t dst_free = __ballot_sync(FULL, dst[lane] == EMPTY);
+    if (live) {
+        // pos = select_nth_one(dst_free, my_rank)
+        uint32_t m = dst_free;
+        for (uint32_t r = 0; r < my_rank; ++r) m &= m - 1;
+        const int pos = __ffs(m) - 1;
+        dst[pos] = kv;
+        src[lane] = EMPTY;
+    }
+}
+
+// --------------------------------------------------------------------------------
+// misc: dump, stats, partition / routing
+// --------------------------------------------------------------------------------
+__global__ void __launch_bounds__(BLOCK)
+k_dump(TableView tv, uint64_t n_slots, StashView sv, uint64_t ring_n, uint32_t* __restrict__ keys,
+       uint32_t* __restrict__ vals, uint64_t cap) {
+    const uint64_t total = n_slots + ring_n;
+    const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u); i0 < total; i0 += stride) {
+        const uint64_t i = i0 + (threadIdx.x & 31);
+        uint64_t w = EMPTY;
+        if (i < n_slots) w = tv.buckets[i];
+        else if (i < total) w = sv.ring[i - n_slots];
+        const bool live = w != EMPTY;
+        const uint32_t bal = __ballot_sync(FULL, live);
+        unsigned long long base = 0;
+        if ((threadIdx.x & 31) == 0 && bal) base = atomicAdd(&sv.ctrl->dump_n, (unsigned long long)__popc(bal));
+        base = __shfl_sync(FULL, base, 0);
+        if (live) {
+            const uint64_t p = base + __popc(bal & lanemask_lt());
+            if (p < cap) {
+                keys[p] = key_of(w);
+                vals[p] = val_of(w);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK)
+k_count_b1(TableView tv, uint64_t n_slots, Ctrl* ctrl) {
+    unsigned long long c = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < n_slots;
+         i += (uint64_t)gridDim.x * BLOCK) {
+        const uint64_t w = tv.buckets[i];
+        if (w != EMPTY && tv.addr(bithash1(key_of(w))) == (uint32_t)(i / SLOTS)) ++c;
+    }
+    block_add(&ctrl->in_b1, c);
+}
+
+__device__ __forceinline__ uint32_t part_of(int mode, uint32_t n_parts, uint32_t seed,
+                                            const uint32_t* keys, const uint8_t* ops, uint64_t i) {
+    if (mode == PART_CLASSIFY) {
+        const uint32_t o = ops[i];
+        return o < 3 ? o : 3u;
+    }
+    // shard(k) = (fmix32(k ^ seed) * G) >> 32
+    return (uint32_t)(((uint64_t)fmix32(keys[i] ^ seed) * (uint64_t)n_parts) >> 32);
+}
+
+// Stable partition pass 1: per-warp, per-part counts (part-major layout).
+__global__ void __launch_bounds__(BLOCK)
+k_part_count(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __restrict__ keys,
+             const uint8_t* __restrict__ ops, uint64_t n, uint64_t n_warps,
+             uint64_t* __restrict__ cnt) {
+    __shared__ uint32_t sc[WARPS_PER_BLOCK][MAX_PARTS + 1];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t w = (uint64_t)blockIdx.x * WARPS_PER_BLOCK + wib;
+    for (int p = lane; p <= MAX_PARTS; p += 32) sc[wib][p] = 0;
+    __syncwarp();
+    if (w < n_warps) {
+        const uint64_t lo = w * PART_CHUNK;
+        const uint64_t hi = lo + PART_CHUNK < n ? lo + PART_CHUNK : n;
+        for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
+            const uint64_t i = i0 + lane;
+            const uint32_t p = i < hi ? part_of(mode, n_parts, seed, keys, ops, i) : MAX_PARTS;
+            const uint32_t grp = __match_any_sync(FULL, p);
+            if ((__ffs(grp) - 1) == lane) sc[wib][p] += __popc(grp);
+            __syncwarp();
+        }
+        for (uint32_t p = lane; p < n_parts; p += 32) cnt[(uint64_t)p * n_warps + w] = sc[wib][p];
+    }
+}
+
+// Pass 2: exclusive scan over cnt (single block); part_info[p] = total of part
+// p, part_info[MAX_PARTS + p] = global start of part p.
+__global__ void __launch_bounds__(1024)
+k_part_scan(uint64_t* __restrict__ cnt, uint64_t E, uint32_t n_parts, uint64_t n_warps,
+            uint64_t* __restrict__ part_info) {
+    __shared__ uint64_t ssum[1024];
+    const int tid = threadIdx.x;
+    const uint64_t per = (E + 1023) / 1024;
+    const uint64_t lo = tid * per, hi = (lo + per < E) ? lo + per : E;
+    uint64_t s = 0;
+    for (uint64_t i = lo; i < hi; ++i) s += cnt[i];
+    ssum[tid] = s;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        uint64_t v = tid >= off ? ssum[tid - off] : 0;
+        __syncthreads();
+        ssum[tid] += v;
+        __syncthreads();
+    }
+    uint64_t run = ssum[tid] - s;      // exclusive prefix of this segment
+    for (uint64_t i = lo; i < hi; ++i) {
+        uint64_t c = cnt[i];
+        cnt[i] = run;
+        run += c;
+    }
+    __syncthreads();
+    const uint64_t total = ssum[1023];
+    if (tid < (int)n_parts) {
+        const uint64_t start = n_warps ? cnt[(uint64_t)tid * n_warps] : 0;
+        const uint64_t end = (tid + 1 < (int)n_parts) ? cnt[(uint64_t)(tid + 1) * n_warps] : total;
+        part_info[tid] = end - start;
+        part_info[MAX_PARTS + tid] = start;
+    }
+}
+
+// Pass 3: stable scatter.  CLASSIFY writes op indices into per-part regions
+// out_idx + p * idx_stride (invalid opcodes: result 0 / value 0 in place).
+// ROUTE writes packed records, opcodes and the inverse positions.
+__global__ void __launch_bounds__(BLOCK)
+k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __restrict__ keys,
+               const uint32_t* __restrict__ vals, const uint8_t* __restrict__ ops, uint64_t n,
+               uint64_t n_warps, const uint64_t* __restrict__ off,
+               const uint64_t* __restrict__ part_info, uint32_t* __restrict__ out_idx,
+               uint64_t idx_stride, uint64_t* __restrict__ send_kv, uint8_t* __restrict__ send_ops,
+               uint32_t* __restrict__ pos_out, uint8_t* __restrict__ result_zero,
+               uint32_t* __restrict__ vals_zero) {
+    __shared__ uint64_t run[WARPS_PER_BLOCK][MAX_PARTS + 1];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t w = (uint64_t)blockIdx.x * WARPS_PER_BLOCK + wib;
+    if (w >= n_warps) return;
+    for (uint32_t p = lane; p < n_parts; p += 32) run[wib][p] = off[(uint64_t)p * n_warps + w];
+    __syncwarp();
+    const uint64_t lo = w * PART_CHUNK;
+    const uint64_t hi = lo + PART_CHUNK < n ? lo + PART_CHUNK : n;
+    for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
+        const uint64_t i = i0 + lane;
+        const bool in = i < hi;
+        const uint32_t p = in ? part_of(mode, n_parts, seed, keys, ops, i) : MAX_PARTS;
+        const uint32_t grp = __match_any_sync(FULL, p);
+        const uint32_t rank = __popc(grp & lanemask_lt());
+        uint64_t pos = 0;
+        if (in && p < n_parts) pos = run[wib][p] + rank;
+        __syncwarp();
+        if (in && p < n_parts && (__ffs(grp) - 1) == lane) run[wib][p] += __popc(grp);
+        __syncwarp();
+        if (!in) continue;
+        if (mode == PART_CLASSIFY) {
+            if (p < n_parts) {
+                out_idx[(uint64_t)p * idx_stride + (pos - part_info[MAX_PARTS + p])] = (uint32_t)i;
+            } else {
+                if (result_zero) result_zero[i] = 0;
+                if (vals_zero) vals_zero[i] = 0;
+            }
+        } else {
+            send_kv[pos] = ((uint64_t)(vals ? vals[i] : 0u) << 32) | keys[i];
+            if (send_ops) send_ops[pos] = ops[i];
+            pos_out[i] = (uint32_t)pos;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK)
+k_unroute(const uint32_t* __restrict__ pos, uint64_t n, const uint8_t* __restrict__ in8,
+          uint8_t* __restrict__ out8, const uint32_t* __restrict__ in32, uint32_t* __restrict__ out32) {
+    for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (uint64_t)gridDim.x * BLOCK) {
+        const uint32_t p = pos[i];
+        if (out8) out8[i] = in8[p];
+        if (out32) out32[i] = in32[p];
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK)
+k_unpack(const uint64_t* __restrict__ kv, uint64_t n, uint32_t* __restrict__ keys,
+         uint32_t* __restrict__ vals) {
+    for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (uint64_t)gridDim.x * BLOCK) {
+        const uint64_t w = kv[i];
+        if (keys) keys[i] = key_of(w);
+        if (vals) vals[i] = val_of(w);
+    }
+}
+
+// --------------------------------------------------------------------------------
+// launchers
+// --------------------------------------------------------------------------------
+static int occ(const void* fn) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BLOCK, 0);
+    return nb > 0 ? nb : 1;
+}
+
+Grids query_grids(int num_sms) {
+    Grids g;
+    g.find = occ((const void*)k_find<GROUP>) * num_sms;
+    g.insert_fast = occ((const void*)k_insert_fast<GROUP>) * num_sms;
+    g.insert_slow = occ((const void*)k_insert_slow<GROUP>) * num_sms;
+    g.erase = occ((const void*)k_erase<GROUP>) * num_sms;
+    g.dedup = occ((const void*)k_dedup_elect) * num_sms;
+    g.stream = 4 * num_sms;
+    return g;
+}
+
+static inline int clamp_grid(int grid, uint64_t n, uint64_t per_block) {
+    uint64_t need = (n + per_block - 1) / per_block;
+    if (need < 1) need = 1;
+    return (int)(need < (uint64_t)grid ? need : (uint64_t)grid);
+}
+
+constexpr uint64_t OPS_PER_BLOCK = BLOCK / GROUP;
+
+cudaError_t launch_find(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
+                        uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
+                        uint32_t* vals_out, uint8_t* found) {
+    if (!n_dev) grid = clamp_grid(grid, n, OPS_PER_BLOCK);
+    k_find<GROUP><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, vals_out, found);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dedup_elect(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
+                               uint64_t n, const uint64_t* n_dev, DedupView dd) {
+    if (!n_dev) grid = clamp_grid(grid, n, BLOCK);
+    k_dedup_elect<<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, dd);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_insert_fast(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
+                               const uint64_t* kvs, const uint32_t* idx, uint64_t n,
+                               const uint64_t* n_dev, TableView tv, StashView sv, DedupView dd,
+                               uint32_t* owner_of, uint8_t* status, uint32_t* vals_zero,
+                               uint32_t* leftover) {
+    if (!n_dev) grid = clamp_grid(grid, n, OPS_PER_BLOCK);
+    k_insert_fast<GROUP><<<grid, BLOCK, 0, s>>>(keys, vals, kvs, idx, n, n_dev, tv, sv, dd, owner_of,
+                                                status, vals_zero, leftover);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_insert_slow(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
+                               const uint64_t* kvs, const uint32_t* leftover, TableView tv,
+                               StashView sv, uint32_t max_evictions, uint8_t* status) {
+    k_insert_slow<GROUP><<<grid, BLOCK, 0, s>>>(keys, vals, kvs, leftover, tv, sv, max_evictions, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_erase(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
+                         uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
+                         DedupView dd, uint32_t* owner_of, uint8_t* erased, uint32_t* vals_zero) {
+    if (!n_dev) grid = clamp_grid(grid, n, OPS_PER_BLOCK);
+    k_erase<GROUP><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, dd, owner_of, erased, vals_zero);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dup_copy(int grid, cudaStream_t s, const uint32_t* idx, uint64_t n,
+                            const uint64_t* n_dev, const uint32_t* owner_of, uint8_t* out) {
+    if (!n_dev) grid = clamp_grid(grid, n, BLOCK);
+    k_dup_copy<<<grid, BLOCK, 0, s>>>(idx, n, n_dev, owner_of, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_split(cudaStream_t s, TableView tv, uint32_t n_pairs, Ctrl* ctrl) {
+    if (n_pairs == 0) return cudaSuccess;
+    const int grid = (int)((n_pairs + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK);
+    k_split<<<grid, BLOCK, 0, s>>>(tv, n_pairs, ctrl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_merge(cudaStream_t s, TableView tv, uint32_t n_pairs, Ctrl* ctrl) {
+    if (n_pairs == 0) return cudaSuccess;
+    const int grid = (int)((n_pairs + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK);
+    k_merge_check<<<grid, BLOCK, 0, s>>>(tv, n_pairs, ctrl);
+    k_merge_apply<<<grid, BLOCK, 0, s>>>(tv, n_pairs, ctrl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dump(int grid, cudaStream_t s, TableView tv, uint64_t n_buckets, StashView sv,
+                        uint32_t* keys, uint32_t* vals, uint64_t cap) {
+    const uint64_t ring_n = sv.cap;
+    k_dump<<<grid, BLOCK, 0, s>>>(tv, n_buckets * SLOTS, sv, ring_n, keys, vals, cap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_count_b1(int grid, cudaStream_t s, TableView tv, uint64_t n_buckets, Ctrl* ctrl) {
+    k_count_b1<<<grid, BLOCK, 0, s>>>(tv, n_buckets * SLOTS, ctrl);
+    return cudaGetLastError();
+}
+
+uint64_t part_warps(uint64_t n) { return (n + PART_CHUNK - 1) / PART_CHUNK; }
+
+cudaError_t launch_partition(cudaStream_t s, int mode, uint32_t n_parts, uint32_t seed,
+                             const uint32_t* keys, const uint32_t* vals, const uint8_t* ops,
+                             uint64_t n, uint64_t* cnt, uint64_t* part_info,
+                             uint32_t* out_idx, uint64_t idx_stride, uint64_t* send_kv,
+                             uint8_t* send_ops, uint32_t* pos, uint8_t* result_zero,
+                             uint32_t* vals_zero) {
+    const uint64_t nw = part_warps(n);
+    const int grid = (int)((nw + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK);
+    if (nw) k_part_count<<<grid, BLOCK, 0, s>>>(mode, n_parts, seed, keys, ops, n, nw, cnt);
+    k_part_scan<<<1, 1024, 0, s>>>(cnt, (uint64_t)n_parts * nw, n_parts, nw, part_info);
+    if (nw)
+        k_part_scatter<<<grid, BLOCK, 0, s>>>(mode, n_parts, seed, keys, vals, ops, n, nw, cnt, part_info,
+                                              out_idx, idx_stride, send_kv, send_ops, pos, result_zero,
+                                              vals_zero);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unroute(cudaStream_t s, const uint32_t* pos, uint64_t n, const uint8_t* in8,
+                           uint8_t* out8, const uint32_t* in32, uint32_t* out32) {
+    const int grid = clamp_grid(1184, n, BLOCK);
+    k_unroute<<<grid, BLOCK, 0, s>>>(pos, n, in8, out8, in32, out32);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(cudaStream_t s, const uint64_t* kv, uint64_t n, uint32_t* keys,
+                          uint32_t* vals) {
+    const int grid = clamp_grid(1184, n, BLOCK);
+    k_unpack<<<grid, BLOCK, 0, s>>>(kv, n, keys, vals);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stash_reset(cudaStream_t s, StashView sv) {
+    cudaError_t e = cudaMemsetAsync(sv.ring, 0xFF, sv.cap * sizeof(uint64_t), s);
+    if (e != cudaSuccess) return e;
+    return cudaMemsetAsync(sv.index, 0xFF, (sv.idx_mask + 1) * sizeof(uint64_t), s);
+}
+
+}  // namespace hive

@@ -1,0 +1,73 @@
+// hive_kernels.cuh — launcher interface between the host orchestration
+// (hive_host.cu) and the sm_100a kernels (hive_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "hive_device.cuh"
+
+namespace hive {
+
+constexpr int BLOCK = 256;
+constexpr int WARPS_PER_BLOCK = BLOCK / 32;
+constexpr int GROUP = 8;                 // lanes per operation
+constexpr int PART_CHUNK = 2048;         // elements per warp in the stable partition
+constexpr int MAX_PARTS = 64;
+
+enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1 };
+
+struct Grids {                           // persistent grid sizes (blocks)
+    int find, insert_fast, insert_slow, erase, dedup, stream;
+};
+
+// Occupancy-derived persistent grid sizes for this device.
+Grids query_grids(int num_sms);
+
+cudaError_t launch_find(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
+                        uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
+                        uint32_t* vals_out, uint8_t* found);
+
+cudaError_t launch_dedup_elect(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
+                               uint64_t n, const uint64_t* n_dev, DedupView dd);
+
+cudaError_t launch_insert_fast(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
+                               const uint64_t* kvs, const uint32_t* idx, uint64_t n,
+                               const uint64_t* n_dev, TableView tv, StashView sv, DedupView dd,
+                               uint32_t* owner_of, uint8_t* status, uint32_t* vals_zero,
+                               uint32_t* leftover);
+
+cudaError_t launch_insert_slow(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
+                               const uint64_t* kvs, const uint32_t* leftover, TableView tv,
+                               StashView sv, uint32_t max_evictions, uint8_t* status);
+
+cudaError_t launch_erase(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
+                         uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
+                         DedupView dd, uint32_t* owner_of, uint8_t* erased, uint32_t* vals_zero);
+
+cudaError_t launch_dup_copy(int grid, cudaStream_t s, const uint32_t* idx, uint64_t n,
+                            const uint64_t* n_dev, const uint32_t* owner_of, uint8_t* out);
+
+cudaError_t launch_split(cudaStream_t s, TableView tv, uint32_t n_pairs, Ctrl* ctrl);
+cudaError_t launch_merge(cudaStream_t s, TableView tv, uint32_t n_pairs, Ctrl* ctrl);
+
+cudaError_t launch_stash_reset(cudaStream_t s, StashView sv);
+
+cudaError_t launch_dump(int grid, cudaStream_t s, TableView tv, uint64_t n_buckets, StashView sv,
+                        uint32_t* keys, uint32_t* vals, uint64_t cap);
+cudaError_t launch_count_b1(int grid, cudaStream_t s, TableView tv, uint64_t n_buckets, Ctrl* ctrl);
+
+// Stable partition: count -> scan -> scatter.  cnt must hold n_parts * n_warps
+// words, part_info 2 * MAX_PARTS words (totals, bases).
+uint64_t part_warps(uint64_t n);
+cudaError_t launch_partition(cudaStream_t s, int mode, uint32_t n_parts, uint32_t seed,
+                             const uint32_t* keys, const uint32_t* vals, const uint8_t* ops,
+                             uint64_t n, uint64_t* cnt, uint64_t* part_info,
+                             uint32_t* out_idx, uint64_t idx_stride, uint64_t* send_kv,
+                             uint8_t* send_ops, uint32_t* pos, uint8_t* result_zero,
+                             uint32_t* vals_zero);
+
+cudaError_t launch_unroute(cudaStream_t s, const uint32_t* pos, uint64_t n, const uint8_t* in8,
+                           uint8_t* out8, const uint32_t* in32, uint32_t* out32);
+cudaError_t launch_unpack(cudaStream_t s, const uint64_t* kv, uint64_t n, uint32_t* keys,
+                          uint32_t* vals);
+
+}  // namespace hive

@@ -1,0 +1,291 @@
+"""Thin ctypes binding over libhive.so (include/hive.h).
+
+Argument marshalling only: torch tensors supply device memory and the current
+CUDA stream; every step of the hot path runs in the library's sm_100a kernels.
+There is no CPU fallback: without a built libhive.so or a CUDA device every
+entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libhive.so")
+
+HIVE_KEYS_UNIQUE = 1
+OP_FIND, OP_INSERT, OP_ERASE = 0, 1, 2
+INVALID_KEY = 0xFFFFFFFF
+
+_STATUS = {0: "ok", 1: "invalid argument", 2: "out of memory", 3: "CUDA error", 4: "NCCL error",
+           5: "stash full", 6: "handle busy"}
+
+
+class HiveError(RuntimeError):
+    pass
+
+
+class HiveConfig(ctypes.Structure):
+    _fields_ = [("capacity", ctypes.c_uint64), ("max_capacity", ctypes.c_uint64),
+                ("lf_grow", ctypes.c_float), ("lf_shrink", ctypes.c_float),
+                ("max_evictions", ctypes.c_uint32), ("resize_k", ctypes.c_uint32),
+                ("stash_fraction", ctypes.c_float), ("flags", ctypes.c_uint32)]
+
+
+class HiveStats(ctypes.Structure):
+    _fields_ = [("n_buckets", ctypes.c_uint64), ("m", ctypes.c_uint32), ("split", ctypes.c_uint32)] + [
+        (n, ctypes.c_uint64) for n in (
+            "count", "stash_used", "stash_cap", "evictions", "max_depth", "stash_pushes", "leftovers",
+            "grows", "shrinks", "merge_aborts", "failed", "in_b1", "mapped_bytes")]
+
+
+# every exported symbol of include/hive.h, with its ctypes signature
+_vp, _u32, _u64, _int = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
+SIGNATURES = {
+    "hive_config_default": (None, [ctypes.POINTER(HiveConfig)]),
+    "hive_create": (_int, [ctypes.POINTER(HiveConfig), _vp, ctypes.POINTER(_vp)]),
+    "hive_destroy": (_int, [_vp]),
+    "hive_insert": (_int, [_vp, _vp, _vp, _u64, _vp, _vp]),
+    "hive_find": (_int, [_vp, _vp, _u64, _vp, _vp, _vp]),
+    "hive_erase": (_int, [_vp, _vp, _u64, _vp, _vp]),
+    "hive_mixed": (_int, [_vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp]),
+    "hive_clear": (_int, [_vp, _vp]),
+    "hive_size": (_int, [_vp, ctypes.POINTER(_u64)]),
+    "hive_stats": (_int, [_vp, ctypes.POINTER(HiveStats)]),
+    "hive_dump": (_int, [_vp, _vp, _vp, _u64, ctypes.POINTER(_u64), _vp]),
+    "hive_profile": (_int, [_vp, _int]),
+    "hive_profile_read": (_int, [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
+                                 ctypes.POINTER(_u64), _int, _int]),
+    "hive_route": (_int, [_u32, _u32, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp]),
+    "hive_unroute": (_int, [_vp, _u64, _vp, _vp, _vp, _vp, _vp]),
+    "hive_unpack_kv": (_int, [_vp, _u64, _vp, _vp, _vp]),
+    "hive_status_string": (ctypes.c_char_p, [_int]),
+    "hive_last_error": (ctypes.c_char_p, []),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libhive.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise HiveError(f"{LIB_PATH} is missing: run `python -m paper_2510_15095_b200.build` "
+                            "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        detail = lib().hive_last_error().decode(errors="replace")
+        raise HiveError(f"{what}: {_STATUS.get(rc, rc)} {detail}")
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _dev(t: torch.Tensor, nbytes_per: int) -> torch.Tensor:
+    if not t.is_cuda:
+        raise HiveError("expected a CUDA tensor")
+    if t.element_size() != nbytes_per or not t.is_contiguous():
+        raise HiveError(f"expected a contiguous {nbytes_per}-byte dtype tensor, got {t.dtype}")
+    return t
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def u32(x, device="cuda") -> torch.Tensor:
+    """uint32 tensor on `device` from numpy / list / tensor."""
+    if isinstance(x, torch.Tensor):
+        if x.element_size() == 4:
+            return x.contiguous().view(torch.uint32).to(device)
+        return x.to(torch.int64).to(torch.uint32).to(device)
+    import numpy as np
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.uint32))
+    return torch.from_numpy(a.view(np.int32)).view(torch.uint32).to(device)
+
+
+def u8(x, device="cuda") -> torch.Tensor:
+    import numpy as np
+    if isinstance(x, torch.Tensor):
+        return x.to(torch.uint8).to(device)
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.uint8))).to(device)
+
+
+class HiveTable:
+    """One Hive table on the current CUDA device (a handle of include/hive.h)."""
+
+    def __init__(self, capacity: int, max_capacity: int = 0, lf_grow: float = 0.9,
+                 lf_shrink: float = 0.25, max_evictions: int = 16, resize_k: int = 1024,
+                 stash_fraction: float = 0.02, keys_unique: bool = False, stream=None):
+        L = lib()
+        if not torch.cuda.is_available():
+            raise HiveError("no CUDA device: the Hive table runs only on the GPU")
+        cfg = HiveConfig()
+        L.hive_config_default(ctypes.byref(cfg))
+        cfg.capacity, cfg.max_capacity = capacity, max_capacity
+        cfg.lf_grow, cfg.lf_shrink = lf_grow, lf_shrink
+        cfg.max_evictions, cfg.resize_k, cfg.stash_fraction = max_evictions, resize_k, stash_fraction
+        cfg.flags = HIVE_KEYS_UNIQUE if keys_unique else 0
+        self.cfg = cfg
+        h = ctypes.c_void_p()
+        _check(L.hive_create(ctypes.byref(cfg), ctypes.c_void_p(_stream(stream)), ctypes.byref(h)), "hive_create")
+        self._h = h
+        self._L = L
+
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            self._L.hive_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- device-resident batch ops --------------------------------------------------
+    def insert(self, keys: torch.Tensor, vals: torch.Tensor, status: torch.Tensor | None = None,
+               stream=None) -> torch.Tensor:
+        keys, vals = _dev(keys, 4), _dev(vals, 4)
+        n = keys.numel()
+        if vals.numel() != n:
+            raise HiveError("keys and vals differ in length")
+        if status is None:
+            status = torch.empty(n, dtype=torch.uint8, device=keys.device)
+        _check(self._L.hive_insert(self._h, _p(keys), _p(vals), n, _p(status), _stream(stream)), "hive_insert")
+        return status
+
+    def find(self, keys: torch.Tensor, vals_out=None, found=None, stream=None):
+        keys = _dev(keys, 4)
+        n = keys.numel()
+        if vals_out is None:
+            vals_out = torch.empty(n, dtype=torch.uint32, device=keys.device)
+        if found is None:
+            found = torch.empty(n, dtype=torch.uint8, device=keys.device)
+        _check(self._L.hive_find(self._h, _p(keys), n, _p(vals_out), _p(found), _stream(stream)), "hive_find")
+        return vals_out, found
+
+    def erase(self, keys: torch.Tensor, erased=None, stream=None) -> torch.Tensor:
+        keys = _dev(keys, 4)
+        n = keys.numel()
+        if erased is None:
+            erased = torch.empty(n, dtype=torch.uint8, device=keys.device)
+        _check(self._L.hive_erase(self._h, _p(keys), n, _p(erased), _stream(stream)), "hive_erase")
+        return erased
+
+    def mixed(self, ops: torch.Tensor, keys: torch.Tensor, vals: torch.Tensor, vals_out=None,
+              result=None, stream=None):
+        ops, keys, vals = _dev(ops, 1), _dev(keys, 4), _dev(vals, 4)
+        n = keys.numel()
+        if vals_out is None:
+            vals_out = torch.empty(n, dtype=torch.uint32, device=keys.device)
+        if result is None:
+            result = torch.empty(n, dtype=torch.uint8, device=keys.device)
+        _check(self._L.hive_mixed(self._h, _p(ops), _p(keys), _p(vals), n, _p(vals_out), _p(result),
+                                  _stream(stream)), "hive_mixed")
+        return vals_out, result
+
+    # ---- end-to-end variants: host tensors in, host tensors out -----------------------
+    def insert_host(self, keys_h: torch.Tensor, vals_h: torch.Tensor) -> torch.Tensor:
+        k = keys_h.to("cuda", non_blocking=True)
+        v = vals_h.to("cuda", non_blocking=True)
+        st = self.insert(k, v)
+        out = torch.empty(st.shape, dtype=st.dtype, pin_memory=True)
+        out.copy_(st, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out
+
+    def find_host(self, keys_h: torch.Tensor):
+        k = keys_h.to("cuda", non_blocking=True)
+        v, f = self.find(k)
+        vo = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+        fo = torch.empty(f.shape, dtype=f.dtype, pin_memory=True)
+        vo.copy_(v, non_blocking=True)
+        fo.copy_(f, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return vo, fo
+
+    # ---- inspection -----------------------------------------------------------------
+    def clear(self, stream=None):
+        _check(self._L.hive_clear(self._h, _stream(stream)), "hive_clear")
+
+    def size(self) -> int:
+        n = ctypes.c_uint64()
+        _check(self._L.hive_size(self._h, ctypes.byref(n)), "hive_size")
+        return n.value
+
+    def stats(self, allow_failed: bool = False) -> dict:
+        s = HiveStats()
+        rc = self._L.hive_stats(self._h, ctypes.byref(s))
+        if not (allow_failed and rc == 5):
+            _check(rc, "hive_stats")
+        return {n: getattr(s, n) for n, _ in HiveStats._fields_}
+
+    def dump(self):
+        n = ctypes.c_uint64()
+        _check(self._L.hive_dump(self._h, None, None, 0, ctypes.byref(n), _stream()), "hive_dump")
+        k = torch.empty(max(n.value, 1), dtype=torch.uint32, device="cuda")
+        v = torch.empty(max(n.value, 1), dtype=torch.uint32, device="cuda")
+        _check(self._L.hive_dump(self._h, _p(k), _p(v), n.value, ctypes.byref(n), _stream()), "hive_dump")
+        return k[:n.value], v[:n.value]
+
+    def profile(self, enable: bool = True):
+        _check(self._L.hive_profile(self._h, 1 if enable else 0), "hive_profile")
+
+    def profile_read(self, reset: bool = True) -> dict:
+        m = 64
+        names = (ctypes.c_char_p * m)()
+        ms = (ctypes.c_double * m)()
+        cnt = (ctypes.c_uint64 * m)()
+        k = self._L.hive_profile_read(self._h, names, ms, cnt, m, 1 if reset else 0)
+        return {names[i].decode(): (ms[i], cnt[i]) for i in range(min(k, m))}
+
+
+# ---- routing for the hash-partitioned table ---------------------------
+def route(keys: torch.Tensor, vals: torch.Tensor | None, ops: torch.Tensor | None, n_shards: int,
+          seed: int, stream=None):
+    """Stable partition of a batch by shard(k) = (fmix32(k ^ seed) * G) >> 32.
+    Returns (send_kv int64[n] packed value<<32|key, send_ops uint8[n] | None,
+    pos int32[n] (op i -> send position), counts int64[G])."""
+    keys = _dev(keys, 4)
+    n = keys.numel()
+    dev = keys.device
+    send_kv = torch.empty(n, dtype=torch.int64, device=dev)
+    send_ops = torch.empty(n, dtype=torch.uint8, device=dev) if ops is not None else None
+    pos = torch.empty(n, dtype=torch.int32, device=dev)
+    counts = torch.empty(n_shards, dtype=torch.int64, device=dev)
+    _check(lib().hive_route(n_shards, seed, _p(keys), _p(vals), _p(ops), n, _p(send_kv), _p(send_ops),
+                            _p(pos), _p(counts), _stream(stream)), "hive_route")
+    return send_kv, send_ops, pos, counts
+
+
+def unroute(pos: torch.Tensor, in8: torch.Tensor | None = None, in32: torch.Tensor | None = None,
+            stream=None):
+    n = pos.numel()
+    out8 = torch.empty(n, dtype=torch.uint8, device=pos.device) if in8 is not None else None
+    out32 = torch.empty(n, dtype=torch.uint32, device=pos.device) if in32 is not None else None
+    _check(lib().hive_unroute(_p(pos), n, _p(in8), _p(out8), _p(in32), _p(out32), _stream(stream)),
+           "hive_unroute")
+    return out8, out32
+
+
+def unpack_kv(kv: torch.Tensor, stream=None):
+    n = kv.numel()
+    k = torch.empty(n, dtype=torch.uint32, device=kv.device)
+    v = torch.empty(n, dtype=torch.uint32, device=kv.device)
+    _check(lib().hive_unpack_kv(_p(kv), n, _p(k), _p(v), _stream(stream)), "hive_unpack_kv")
+    return k, v
