@@ -381,6 +381,8 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "kernels_ms_per_step": {k: v[0] for k, v in prof.items()},
             "roofline": roofline,
+            "table_stats": {k: st[k] for k in ("count", "n_buckets", "stash_used", "evictions", "max_depth",
+                                               "stash_pushes", "leftovers", "in_b1")},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "secondary": secondary,

@@ -110,38 +110,53 @@ struct StashView {
 };
 
 // Per-batch owner election table: (key << 32) | op, max op
-// per key wins (= the oracle's last write).
+// per key wins (= the oracle's last write).  `flag[op]` is set only for ops
+// whose key occurs more than once in the phase, so only those consult the
+// table again (uniform batches pay the election pass alone).
 struct DedupView {
     uint64_t* slots;     // nullptr = election disabled (HIVE_KEYS_UNIQUE)
     uint64_t mask;
+    uint8_t* flag;       // per op (indexed like the keys), zeroed per phase
+    uint32_t* owner_of;  // per op, written for flagged ops only
 };
 
 // ---- memory access -----------------------------------------------------------------
-// Bucket loads bypass L1 allocation (random, no reuse; also no stale L1 lines
-// across the CAS traffic of other SMs).  SPL = slots per lane.
-template <int SPL>
-__device__ __forceinline__ void load_slots(const uint64_t* p, uint64_t (&s)[SPL]) {
-    if constexpr (SPL == 4) {
-        asm volatile("ld.global.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
-                     : "=l"(s[0]), "=l"(s[1]), "=l"(s[2]), "=l"(s[3]) : "l"(p) : "memory");
-    } else if constexpr (SPL == 2) {
-        asm volatile("ld.global.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
-                     : "=l"(s[0]), "=l"(s[1]) : "l"(p) : "memory");
-    } else {
-        asm volatile("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(s[0]) : "l"(p) : "memory");
-    }
+// Bucket loads: 256-bit vector loads (LDG.E.ENL2.256 on sm_100a), bypassing L1
+// allocation (random, no reuse; also no stale L1 lines across the CAS traffic of
+// other SMs).  A lane holding SPL slots issues SPL/4 of them back to back, so all
+// of a probe's bytes are in flight at once.  `volatile` keeps re-probes of the
+// same bucket (after a lost CAS) from being merged by the compiler.
+__device__ __forceinline__ void ld4(const uint64_t* p, uint64_t& a, uint64_t& b, uint64_t& c,
+                                    uint64_t& d) {
+    asm volatile("ld.global.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
 }
 // Read-only phase variant (FIND): the table is immutable for the whole kernel.
+__device__ __forceinline__ void ld4_ro(const uint64_t* p, uint64_t& a, uint64_t& b, uint64_t& c,
+                                       uint64_t& d) {
+    asm("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+        : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+template <int SPL>
+__device__ __forceinline__ void load_slots(const uint64_t* p, uint64_t (&s)[SPL]) {
+    if constexpr (SPL >= 4) {
+#pragma unroll
+        for (int i = 0; i < SPL; i += 4) ld4(p + i, s[i], s[i + 1], s[i + 2], s[i + 3]);
+    } else if constexpr (SPL == 2) {
+        asm volatile("ld.global.L1::no_allocate.v2.u64 {%0,%1}, [%2];" : "=l"(s[0]), "=l"(s[1]) : "l"(p));
+    } else {
+        asm volatile("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(s[0]) : "l"(p));
+    }
+}
 template <int SPL>
 __device__ __forceinline__ void load_slots_ro(const uint64_t* p, uint64_t (&s)[SPL]) {
-    if constexpr (SPL == 4) {
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
-                     : "=l"(s[0]), "=l"(s[1]), "=l"(s[2]), "=l"(s[3]) : "l"(p));
+    if constexpr (SPL >= 4) {
+#pragma unroll
+        for (int i = 0; i < SPL; i += 4) ld4_ro(p + i, s[i], s[i + 1], s[i + 2], s[i + 3]);
     } else if constexpr (SPL == 2) {
-        asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
-                     : "=l"(s[0]), "=l"(s[1]) : "l"(p));
+        asm("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];" : "=l"(s[0]), "=l"(s[1]) : "l"(p));
     } else {
-        asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(s[0]) : "l"(p));
+        asm("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(s[0]) : "l"(p));
     }
 }
 
@@ -205,25 +220,6 @@ __device__ __forceinline__ uint32_t free_bits(const uint64_t (&s)[SPL]) {
 #pragma unroll
     for (int j = 0; j < SPL; ++j) fm |= (s[j] == EMPTY ? 1u : 0u) << j;
     return fm;
-}
-
-// WCME: match-and-elect.  Returns true (group-uniform) if key k is in the
-// cached bucket view; *winner_slot = lowest matching slot index (0..31) and
-// *word = its packed word.  `valid` must be false for k == INVALID_KEY
-// (EMPTY slots carry key 0xFFFFFFFF).  All 32 lanes must call this.
-template <int G>
-__device__ __forceinline__ bool wcme(const WarpGroup<G>& wg,
-                                     const uint64_t (&s)[WarpGroup<G>::SPL], uint32_t k,
-                                     bool valid, int* winner_slot, uint64_t* word) {
-    constexpr int SPL = WarpGroup<G>::SPL;
-    uint32_t mm = valid ? match_bits<SPL>(s, k) : 0u;
-    uint32_t M = wg.ballot(mm != 0);                       // match mask (lanes)
-    int w = M ? __ffs(M) - 1 : 0;                          // FirstSet
-    int j = mm ? __ffs(mm) - 1 : 0;
-    uint64_t my = pick<SPL>(s, j);
-    *word = wg.bcast(my, w);
-    *winner_slot = w * SPL + wg.bcast(j, w);
-    return M != 0;
 }
 
 }  // namespace hive

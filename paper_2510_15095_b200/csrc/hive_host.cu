@@ -119,6 +119,7 @@ struct hive_table_s {
     // per-batch scratch (grown on demand)
     uint64_t* dd = nullptr;   uint64_t dd_cap = 0;
     uint32_t* owner = nullptr; uint64_t owner_cap = 0;
+    uint8_t* flag = nullptr;  uint64_t flag_cap = 0;
     uint32_t* left = nullptr; uint64_t left_cap = 0;
     uint32_t* cls = nullptr;  uint64_t cls_cap = 0;
     uint64_t* cnt = nullptr;  uint64_t cnt_cap = 0;
@@ -276,37 +277,44 @@ hive_status stash_reset(hive_table_s* h, uint64_t cap, cudaStream_t s) {
     return HIVE_OK;
 }
 
+// ---- owner election for in-batch duplicates -------------------
+hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* idx, uint64_t n_upper,
+                         const uint64_t* n_dev, uint64_t n_batch, DedupView* dd, cudaStream_t s) {
+    const uint64_t cap = pow2_at_least(std::max<uint64_t>(1024, 2 * n_upper));
+    CKS(ensure(h->dd, h->dd_cap, cap));
+    CKS(ensure(h->owner, h->owner_cap, n_batch));
+    CKS(ensure(h->flag, h->flag_cap, n_batch));
+    *dd = DedupView{h->dd, cap - 1, h->flag, h->owner};
+    CK(cudaMemsetAsync(h->dd, 0xFF, cap * sizeof(uint64_t), s));
+    CK(cudaMemsetAsync(h->flag, 0, n_batch, s));
+    Prof p(h, "k_dedup_elect", s);
+    CK(launch_dedup_elect(h->grids.dedup, s, keys, idx, n_upper, n_dev, *dd));
+    return HIVE_OK;
+}
+
 // ---- the INSERT phase (Steps 1-4, owner election, duplicate fix-up) ---------------
 hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* vals,
                          const uint64_t* kvs, const uint32_t* idx, uint64_t n_upper,
                          const uint64_t* n_dev, uint64_t n_batch, uint8_t* status,
                          uint32_t* vals_zero, cudaStream_t s) {
     const bool dedup = !kvs && h->dedup_on();
-    DedupView dd{nullptr, 0};
-    if (dedup) {
-        const uint64_t cap = pow2_at_least(std::max<uint64_t>(1024, 2 * n_upper));
-        CKS(ensure(h->dd, h->dd_cap, cap));
-        CKS(ensure(h->owner, h->owner_cap, n_batch));
-        dd = DedupView{h->dd, cap - 1};
-        CK(cudaMemsetAsync(h->dd, 0xFF, cap * sizeof(uint64_t), s));
-        Prof p(h, "k_dedup_elect", s);
-        CK(launch_dedup_elect(h->grids.dedup, s, keys, idx, n_upper, n_dev, dd));
-    }
+    DedupView dd{nullptr, 0, nullptr, nullptr};
+    if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
     CKS(ensure(h->left, h->left_cap, std::max<uint64_t>(n_upper, 1)));
     CKS(set_ctrl_word(h, &h->ctrl->n_left, 0, s));
     {
         Prof p(h, kvs ? "k_insert_fast(reinsert)" : "k_insert_fast", s);
-        CK(launch_insert_fast(h->grids.insert_fast, s, keys, vals, kvs, idx, n_upper, n_dev, h->tv(),
-                              h->sv(), dd, h->owner, status, vals_zero, h->left));
+        CK(launch_insert_fast(h->grids, s, keys, vals, kvs, idx, n_upper, n_dev, h->tv(),
+                              h->sv(), dd, status, vals_zero, h->left));
     }
     {
         Prof p(h, kvs ? "k_insert_slow(reinsert)" : "k_insert_slow", s);
-        CK(launch_insert_slow(h->grids.insert_slow, s, keys, vals, kvs, h->left, h->tv(), h->sv(),
+        CK(launch_insert_slow(h->grids, s, keys, vals, kvs, h->left, h->tv(), h->sv(),
                               h->cfg.max_evictions, status));
     }
     if (dedup && status) {
         Prof p(h, "k_dup_copy", s);
-        CK(launch_dup_copy(h->grids.stream, s, idx, n_upper, n_dev, h->owner, status));
+        CK(launch_dup_copy(h->grids.stream, s, idx, n_upper, n_dev, dd, status));
     }
     return HIVE_OK;
 }
@@ -403,24 +411,16 @@ hive_status erase_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* i
                         const uint64_t* n_dev, uint64_t n_batch, uint8_t* out, uint32_t* vals_zero,
                         cudaStream_t s) {
     const bool dedup = h->dedup_on();
-    DedupView dd{nullptr, 0};
-    if (dedup) {
-        const uint64_t cap = pow2_at_least(std::max<uint64_t>(1024, 2 * n_upper));
-        CKS(ensure(h->dd, h->dd_cap, cap));
-        CKS(ensure(h->owner, h->owner_cap, n_batch));
-        dd = DedupView{h->dd, cap - 1};
-        CK(cudaMemsetAsync(h->dd, 0xFF, cap * sizeof(uint64_t), s));
-        Prof p(h, "k_dedup_elect", s);
-        CK(launch_dedup_elect(h->grids.dedup, s, keys, idx, n_upper, n_dev, dd));
-    }
+    DedupView dd{nullptr, 0, nullptr, nullptr};
+    if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
     {
         Prof p(h, "k_erase", s);
-        CK(launch_erase(h->grids.erase, s, keys, idx, n_upper, n_dev, h->tv(), h->sv(), dd, h->owner,
-                        out, vals_zero));
+        CK(launch_erase(h->grids, s, keys, idx, n_upper, n_dev, h->tv(), h->sv(), dd, out,
+                        vals_zero));
     }
     if (dedup && out) {
         Prof p(h, "k_dup_copy", s);
-        CK(launch_dup_copy(h->grids.stream, s, idx, n_upper, n_dev, h->owner, out));
+        CK(launch_dup_copy(h->grids.stream, s, idx, n_upper, n_dev, dd, out));
     }
     return HIVE_OK;
 }
@@ -537,7 +537,8 @@ hive_status hive_destroy(hive_t h) {
         }
         g_vmm.free_va(h->va, h->va_bytes);
     }
-    void* bufs[] = {h->ring, h->sidx, h->ctrl, h->dd, h->owner, h->left, h->cls, h->cnt, h->pinfo, h->tmpkv};
+    void* bufs[] = {h->ring, h->sidx, h->ctrl, h->dd, h->owner, h->flag, h->left, h->cls, h->cnt, h->pinfo,
+                    h->tmpkv};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (h->ctrl_h) cudaFreeHost(h->ctrl_h);
@@ -571,7 +572,7 @@ hive_status hive_find(hive_t h, const uint32_t* d_keys, uint64_t n, uint32_t* d_
     cudaStream_t s = (cudaStream_t)stream;
     h->last = s;
     Prof p(h, "k_find", s);
-    CK(launch_find(h->grids.find, s, d_keys, nullptr, n, nullptr, h->tv(), h->sv(), d_vals_out, d_found));
+    CK(launch_find(h->grids, s, d_keys, nullptr, n, nullptr, h->tv(), h->sv(), d_vals_out, d_found));
     return HIVE_OK;
 }
 
@@ -616,7 +617,7 @@ hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
     CKS(erase_phase(h, d_keys, h->cls + 2 * n, n, n_era, n, d_result, d_vals_out, s));
     CKS(shrink_after(h, s));
     Prof p(h, "k_find", s);
-    CK(launch_find(h->grids.find, s, d_keys, h->cls, n, n_find, h->tv(), h->sv(), d_vals_out, d_result));
+    CK(launch_find(h->grids, s, d_keys, h->cls, n, n_find, h->tv(), h->sv(), d_vals_out, d_result));
     return HIVE_OK;
 }
 

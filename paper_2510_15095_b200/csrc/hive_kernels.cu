@@ -7,6 +7,8 @@
 // lane), so each warp keeps four independent bucket probes in flight.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "hive_kernels.cuh"
 
 namespace hive {
@@ -135,8 +137,10 @@ __device__ __forceinline__ void fill_empty(uint64_t (&s)[SPL]) {
 }
 
 // Step 1 / Alg. 1 ReplacePath and Alg. 4's CAS-to-EMPTY
-// (PAPER:448-475): WCME on the cached bucket view, the elected lane CASes its
-// cached word to `newkv`.  On a lost CAS the winner refreshes its view and the
+// (PAPER:448-475): WCME on the cached bucket view -- per-lane match bits, a
+// group ballot = match mask M, FirstSet(M) elects the winner lane, which CASes
+// its own cached word (lowest matching slot) to `newkv`; the outcome is
+// broadcast by ballot.  On a lost CAS the winner refreshes its view and the
 // group re-elects (reading A-18).  Group-uniform result; all lanes call.
 template <int G>
 __device__ __forceinline__ bool wcme_cas(const WarpGroup<G>& wg, uint64_t (&s)[WarpGroup<G>::SPL],
@@ -145,20 +149,20 @@ __device__ __forceinline__ bool wcme_cas(const WarpGroup<G>& wg, uint64_t (&s)[W
     constexpr int SPL = WarpGroup<G>::SPL;
     bool trying = valid, done = false;
     for (int iter = 0; iter <= SLOTS; ++iter) {
-        int ws;
-        uint64_t old;
-        bool hit = wcme<G>(wg, s, k, trying, &ws, &old);
-        trying = trying && hit;
+        const uint32_t mm = trying ? match_bits<SPL>(s, k) : 0u;
+        const uint32_t M = wg.ballot(mm != 0);                    // match mask
+        trying = trying && M != 0;                                // early exit
         if (!__any_sync(FULL, trying)) break;
-        const int wl = ws / SPL;
         bool ok = false;
-        if (trying && wg.gl == wl) {
-            uint64_t prev = cas64(bucket + ws, old, newkv);
+        if (trying && wg.gl == __ffs(M) - 1) {                    // FirstSet winner
+            const int j = __ffs(mm) - 1;
+            const uint64_t old = pick<SPL>(s, j);
+            const uint64_t prev = cas64(wg.slot_ptr(bucket) + j, old, newkv);
             ok = (prev == old);
-            if (!ok) put<SPL>(s, ws % SPL, prev);
+            if (!ok) put<SPL>(s, j, prev);
         }
-        ok = wg.bcast(ok, wl);
-        if (trying && ok) {
+        const bool any_ok = wg.ballot(ok) != 0;                   // broadcast (all lanes)
+        if (trying && any_ok) {
             done = true;
             trying = false;
         }
@@ -166,8 +170,8 @@ __device__ __forceinline__ bool wcme_cas(const WarpGroup<G>& wg, uint64_t (&s)[W
     return done;
 }
 
-// Step 2 / WABC claim-and-commit: ballot of EMPTY
-// slots in the cached view = claim mask; the lowest free lane elects its
+// Step 2 / WABC claim-and-commit: the ballot of EMPTY
+// slots in the cached view is the claim mask; the lowest free lane elects its
 // lowest free slot and publishes kv with ONE 64-bit CAS(EMPTY -> kv).  A lost
 // CAS marks that slot taken in the view and the group re-elects.
 template <int G>
@@ -176,25 +180,38 @@ __device__ __forceinline__ bool wabc_claim(const WarpGroup<G>& wg, uint64_t (&s)
     constexpr int SPL = WarpGroup<G>::SPL;
     bool trying = want, placed = false;
     for (int iter = 0; iter <= SLOTS; ++iter) {
-        uint32_t fm = trying ? free_bits<SPL>(s) : 0u;
-        uint32_t F = wg.ballot(fm != 0);
+        const uint32_t fm = trying ? free_bits<SPL>(s) : 0u;
+        const uint32_t F = wg.ballot(fm != 0);
         trying = trying && F != 0;
         if (!__any_sync(FULL, trying)) break;
-        const int wl = F ? __ffs(F) - 1 : 0;
         bool ok = false;
-        if (trying && wg.gl == wl) {
+        if (trying && wg.gl == __ffs(F) - 1) {
             const int j = __ffs(fm) - 1;
-            uint64_t prev = cas64(bucket + wl * SPL + j, EMPTY, kv);
+            const uint64_t prev = cas64(wg.slot_ptr(bucket) + j, EMPTY, kv);
             ok = (prev == EMPTY);
             if (!ok) put<SPL>(s, j, prev);
         }
-        ok = wg.bcast(ok, wl);
-        if (trying && ok) {
+        const bool any_ok = wg.ballot(ok) != 0;                   // all lanes vote
+        if (trying && any_ok) {
             placed = true;
             trying = false;
         }
     }
     return placed;
+}
+
+// Read-only WCME for FIND: the value of the lowest matching slot (one 32-bit
+// shuffle from the elected lane).
+template <int G>
+__device__ __forceinline__ bool wcme_value(const WarpGroup<G>& wg, const uint64_t (&s)[WarpGroup<G>::SPL],
+                                           uint32_t k, bool valid, uint32_t* val) {
+    constexpr int SPL = WarpGroup<G>::SPL;
+    const uint32_t mm = valid ? match_bits<SPL>(s, k) : 0u;
+    const uint32_t M = wg.ballot(mm != 0);
+    const uint32_t mine = mm ? val_of(pick<SPL>(s, __ffs(mm) - 1)) : 0u;
+    const uint32_t v = wg.bcast(mine, M ? __ffs(M) - 1 : 0);
+    if (M) *val = v;
+    return M != 0;
 }
 
 // --------------------------------------------------------------------------------
@@ -227,29 +244,22 @@ k_find(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint
         uint64_t s[SPL];
         if (valid) load_slots_ro<SPL>(wg.slot_ptr(tv.bucket(b1)), s);
         else fill_empty<SPL>(s);
-        int ws;
-        uint64_t w;
-        bool found = wcme<G>(wg, s, k, valid, &ws, &w);
+        uint32_t val = 0;
+        bool found = wcme_value<G>(wg, s, k, valid, &val);
         const bool need2 = valid && !found && b2 != b1;
         if (__any_sync(FULL, need2)) {
             if (need2) load_slots_ro<SPL>(wg.slot_ptr(tv.bucket(b2)), s);
-            else fill_empty<SPL>(s);
-            uint64_t w2;
-            bool f2 = wcme<G>(wg, s, k, need2, &ws, &w2);
-            if (need2 && f2) {
-                found = true;
-                w = w2;
-            }
+            found |= wcme_value<G>(wg, s, k, need2, &val);
         }
         if (stash_on && valid && !found && wg.gl == 0) {
             uint64_t sw;
             if (stash_lookup(sv, k, &sw) >= 0) {
                 found = true;
-                w = sw;
+                val = val_of(sw);
             }
         }
         if (active && wg.gl == 0) {
-            vals_out[op] = found ? val_of(w) : 0u;
+            vals_out[op] = found ? val : 0u;
             if (found_out) found_out[op] = found ? 1 : 0;
         }
     }
@@ -257,10 +267,12 @@ k_find(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint
 
 // --------------------------------------------------------------------------------
 // Owner election for in-batch duplicates (reading A-15):
-// insert-if-absent of (key << 32 | op) into a per-batch table with atomicMax,
-// so the surviving op per key is the highest index (the oracle's last write).
-// Ops inside a warp are increasing with the lane (identity or stable lists), so
-// __match_any_sync's highest lane is the warp-local maximum.
+// insert-if-absent of (key << 32 | op) into a per-batch table; atomicMax keeps
+// the highest op per key (the oracle's last write).  Ops inside a warp are
+// increasing with the lane (identity or stable lists), so __match_any_sync's
+// highest lane is the warp-local maximum.  Every op whose key occurs more than
+// once gets flag[op] = 1 (the first conflicting arrival flags the creator), so
+// the phase kernels consult the table only for those ops.
 // --------------------------------------------------------------------------------
 __global__ void __launch_bounds__(BLOCK)
 k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
@@ -274,19 +286,18 @@ k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ id
         const uint64_t op = active ? (idx ? (uint64_t)idx[t] : t) : 0;
         const uint32_t k = active ? keys[op] : INVALID_KEY;
         const uint32_t grp = __match_any_sync(FULL, k);
-        const bool leader = (31 - __clz(grp)) == lane;
-        if (k == INVALID_KEY || !leader) continue;
+        if (k == INVALID_KEY) continue;
+        if (__popc(grp) > 1) dd.flag[op] = 1;
+        if ((31 - __clz(grp)) != lane) continue;
         const uint64_t word = ((uint64_t)k << 32) | op;
         uint64_t h = fmix32(k ^ DEDUP_SEED) & dd.mask;
         for (uint64_t probe = 0; probe <= dd.mask; ++probe) {
-            uint64_t e = dd.slots[h];
-            if (e == EMPTY) {
-                uint64_t prev = cas64(&dd.slots[h], EMPTY, word);
-                if (prev == EMPTY) break;
-                e = prev;
-            }
-            if ((uint32_t)(e >> 32) == k) {
-                if (word > e) atomicMax((unsigned long long*)&dd.slots[h], (unsigned long long)word);
+            const uint64_t prev = cas64(&dd.slots[h], EMPTY, word);
+            if (prev == EMPTY) break;
+            if ((uint32_t)(prev >> 32) == k) {
+                dd.flag[op] = 1;
+                dd.flag[(uint32_t)prev] = 1;
+                if (word > prev) atomicMax((unsigned long long*)&dd.slots[h], (unsigned long long)word);
                 break;
             }
             h = (h + 1) & dd.mask;
@@ -305,20 +316,41 @@ __device__ __forceinline__ uint32_t dedup_owner(const DedupView& dd, uint32_t k,
     return self;
 }
 
+// Owner check of one group (all lanes call): only flagged ops probe the table.
+template <int G>
+__device__ __forceinline__ bool owns(const WarpGroup<G>& wg, const DedupView& dd, bool valid,
+                                     uint32_t k, uint64_t op) {
+    if (!dd.slots) return true;
+    uint32_t owner = (uint32_t)op;
+    if (valid && wg.gl == 0 && dd.flag[op]) {
+        owner = dedup_owner(dd, k, (uint32_t)op);
+        dd.owner_of[op] = owner;
+    }
+    return wg.bcast(owner, 0) == (uint32_t)op;
+}
+
 // --------------------------------------------------------------------------------
 // INSERT fast path: Step 1 (replace) + Step 2 (claim-and-commit,
 // PAPER:348-381) in one pass; ops whose candidate buckets are both full go to
-// the leftover list for Steps 3-4.  `kvs != nullptr` = place-only mode used to
-// reinsert drained stash entries after a resize: Step 1 is skipped
-// (those keys are in no bucket) and nothing is counted.
+// the leftover list for Steps 3-4.
+//
+// The b2 probe is speculative — issued together with b1 — while the warp's
+// observed rate of Step-1 hits in b1 stays below 1/4 (a new key must read both
+// buckets anyway, so this only removes a dependent round trip); once a batch
+// looks replace-heavy the warp switches to the bytes-optimal lazy order of the
+// paper (b2 only after a miss in b1).
+//
+// `kvs != nullptr` = place-only mode used to reinsert drained stash entries
+// after a resize: Step 1 is skipped (those keys are in no bucket)
+// and nothing is counted.
 // --------------------------------------------------------------------------------
 template <int G>
 __global__ void __launch_bounds__(BLOCK)
 k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
               const uint64_t* __restrict__ kvs, const uint32_t* __restrict__ idx, uint64_t n,
               const uint64_t* __restrict__ n_dev, TableView tv, StashView sv, DedupView dd,
-              uint32_t* __restrict__ owner_of, uint8_t* __restrict__ status,
-              uint32_t* __restrict__ vals_zero, uint32_t* __restrict__ leftover) {
+              uint8_t* __restrict__ status, uint32_t* __restrict__ vals_zero,
+              uint32_t* __restrict__ leftover) {
     using WG = WarpGroup<G>;
     constexpr int SPL = WG::SPL;
     __shared__ uint32_t lbuf[WARPS_PER_BLOCK][32];
@@ -328,6 +360,7 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     const bool place_only = kvs != nullptr;
     const bool stash_on = !place_only && sv.ctrl->stash_tail != 0;
     unsigned long long added = 0;
+    uint32_t seen = 0, hits1 = 0;              // warp-uniform replace-rate estimate
     const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
     for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
@@ -347,36 +380,37 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             }
         }
         bool valid = active && k != INVALID_KEY;
-        if (!place_only && active && wg.gl == 0) {
-            if (vals_zero) vals_zero[op] = 0;
-            if (!valid && status) status[op] = 2;
-        }
-        // owner election (duplicates copy the owner's outcome afterwards)
-        if (dd.slots) {
-            uint32_t owner = (uint32_t)op;
-            if (valid && wg.gl == 0) owner = dedup_owner(dd, k, (uint32_t)op);
-            owner = wg.bcast(owner, 0);
-            if (active && wg.gl == 0) owner_of[op] = valid ? owner : (uint32_t)op;
-            if (owner != (uint32_t)op) valid = false;
-        }
-        const uint64_t kv = pack(k, v);
+        const bool spec = place_only || (hits1 * 4u <= seen);
         uint32_t b1 = 0, b2 = 0;
         if (valid) {
             b1 = tv.addr(bithash1(k));
             b2 = tv.addr(bithash2(k));
         }
-        const bool two = valid && b2 != b1;
+        bool two = valid && b2 != b1;
         uint64_t s1[SPL], s2[SPL];
         if (valid) load_slots<SPL>(wg.slot_ptr(tv.bucket(b1)), s1);
         else fill_empty<SPL>(s1);
+        if (two && spec) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
+        else fill_empty<SPL>(s2);
+        if (!place_only && active && wg.gl == 0) {
+            if (vals_zero) vals_zero[op] = 0;
+            if (!valid && status) status[op] = 2;
+        }
+        // owner election: duplicates copy the owner's outcome afterwards
+        if (!owns<G>(wg, dd, valid, k, op)) {
+            valid = false;
+            two = false;
+        }
+        const uint64_t kv = pack(k, v);
         bool done = false;
         if (!place_only) {
-            // Step 1 on b1, then b2 (loaded only on a miss), then the stash.
+            // Step 1 on b1, then b2, then the stash.
             done = wcme_cas<G>(wg, s1, tv.bucket(b1), k, kv, valid);
             const bool need2 = two && !done;
-            if (need2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
-            else fill_empty<SPL>(s2);
-            if (__any_sync(FULL, need2)) done |= wcme_cas<G>(wg, s2, tv.bucket(b2), k, kv, need2);
+            if (__any_sync(FULL, need2)) {                 // spec is warp-uniform
+                if (!spec && need2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
+                done |= wcme_cas<G>(wg, s2, tv.bucket(b2), k, kv, need2);
+            }
             if (stash_on) {
                 bool sdone = false;
                 if (valid && !done && wg.gl == 0) {
@@ -390,14 +424,17 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
                 }
                 done |= wg.bcast(sdone, 0);
             }
-        } else {
-            if (two) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
-            else fill_empty<SPL>(s2);
+            const uint32_t vb = __ballot_sync(FULL, valid && wg.gl == 0);
+            seen += __popc(vb);
+            hits1 += __popc(vb & __ballot_sync(FULL, done));
         }
         // Step 2: WABC claim in b1, then b2 (first-fit, A-21)
         bool placed = wabc_claim<G>(wg, s1, tv.bucket(b1), kv, valid && !done);
         const bool want2 = two && !done && !placed;
-        if (__any_sync(FULL, want2)) placed |= wabc_claim<G>(wg, s2, tv.bucket(b2), kv, want2);
+        if (__any_sync(FULL, want2)) {
+            if (place_only && !spec && want2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
+            placed |= wabc_claim<G>(wg, s2, tv.bucket(b2), kv, want2);
+        }
         const bool left = valid && !done && !placed;
         if (!place_only && valid && wg.gl == 0) {
             if (status) status[op] = done ? 1 : 0;
@@ -493,8 +530,7 @@ template <int G>
 __global__ void __launch_bounds__(BLOCK)
 k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
         const uint64_t* __restrict__ n_dev, TableView tv, StashView sv, DedupView dd,
-        uint32_t* __restrict__ owner_of, uint8_t* __restrict__ erased_out,
-        uint32_t* __restrict__ vals_zero) {
+        uint8_t* __restrict__ erased_out, uint32_t* __restrict__ vals_zero) {
     using WG = WarpGroup<G>;
     constexpr int SPL = WG::SPL;
     WG wg;
@@ -509,14 +545,6 @@ k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uin
         const uint64_t op = active ? (idx ? (uint64_t)idx[t] : t) : 0;
         const uint32_t k = active ? keys[op] : INVALID_KEY;
         bool valid = k != INVALID_KEY;
-        if (active && wg.gl == 0 && vals_zero) vals_zero[op] = 0;
-        if (dd.slots) {
-            uint32_t owner = (uint32_t)op;
-            if (valid && wg.gl == 0) owner = dedup_owner(dd, k, (uint32_t)op);
-            owner = wg.bcast(owner, 0);
-            if (active && wg.gl == 0) owner_of[op] = valid ? owner : (uint32_t)op;
-            if (owner != (uint32_t)op) valid = false;
-        }
         uint32_t b1 = 0, b2 = 0;
         if (valid) {
             b1 = tv.addr(bithash1(k));
@@ -525,6 +553,9 @@ k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uin
         uint64_t s[SPL];
         if (valid) load_slots<SPL>(wg.slot_ptr(tv.bucket(b1)), s);
         else fill_empty<SPL>(s);
+        if (active && wg.gl == 0 && vals_zero) vals_zero[op] = 0;
+        const bool owner = owns<G>(wg, dd, valid, k, op);
+        valid = valid && owner;
         bool done = wcme_cas<G>(wg, s, tv.bucket(b1), k, EMPTY, valid);
         const bool need2 = valid && !done && b2 != b1;
         if (__any_sync(FULL, need2)) {
@@ -541,7 +572,7 @@ k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uin
                 pos = stash_lookup(sv, k, &sw);
             }
         }
-        if (active && wg.gl == 0 && (valid || !dd.slots || k == INVALID_KEY)) {
+        if (active && wg.gl == 0 && owner) {
             if (erased_out) erased_out[op] = done ? 1 : 0;
             if (done) ++removed;
         }
@@ -552,12 +583,13 @@ k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uin
 // Duplicates copy their owner's outcome (PHASED contract, A-17).
 __global__ void __launch_bounds__(BLOCK)
 k_dup_copy(const uint32_t* __restrict__ idx, uint64_t n, const uint64_t* __restrict__ n_dev,
-           const uint32_t* __restrict__ owner_of, uint8_t* __restrict__ out) {
+           DedupView dd, uint8_t* __restrict__ out) {
     if (n_dev) n = *n_dev;
     for (uint64_t t = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; t < n;
          t += (uint64_t)gridDim.x * BLOCK) {
         const uint64_t op = idx ? (uint64_t)idx[t] : t;
-        const uint32_t o = owner_of[op];
+        if (!dd.flag[op]) continue;
+        const uint32_t o = dd.owner_of[op];
         if (o != (uint32_t)op) out[op] = out[o];
     }
 }
@@ -818,12 +850,35 @@ static int occ(const void* fn) {
     return nb > 0 ? nb : 1;
 }
 
+static int env_g(const char* name, int dflt) {
+    const char* e = getenv(name);
+    if (!e) return dflt;
+    const int g = atoi(e);
+    return (g == 1 || g == 2 || g == 4 || g == 8) ? g : dflt;
+}
+
+#define HIVE_DISPATCH_G(g, X) \
+    switch (g) {              \
+        case 1: X(1); break;  \
+        case 2: X(2); break;  \
+        case 4: X(4); break;  \
+        default: X(8); break; \
+    }
+
 Grids query_grids(int num_sms) {
     Grids g;
-    g.find = occ((const void*)k_find<GROUP>) * num_sms;
-    g.insert_fast = occ((const void*)k_insert_fast<GROUP>) * num_sms;
-    g.insert_slow = occ((const void*)k_insert_slow<GROUP>) * num_sms;
-    g.erase = occ((const void*)k_erase<GROUP>) * num_sms;
+    g.g_find = env_g("HIVE_G_FIND", G_FIND);
+    g.g_insert = env_g("HIVE_G_INSERT", G_INSERT);
+    g.g_slow = env_g("HIVE_G_SLOW", G_SLOW);
+    g.g_erase = env_g("HIVE_G_ERASE", G_ERASE);
+#define OCC_FIND(G) g.find = occ((const void*)k_find<G>) * num_sms
+#define OCC_INS(G) g.insert_fast = occ((const void*)k_insert_fast<G>) * num_sms
+#define OCC_SLOW(G) g.insert_slow = occ((const void*)k_insert_slow<G>) * num_sms
+#define OCC_ERA(G) g.erase = occ((const void*)k_erase<G>) * num_sms
+    HIVE_DISPATCH_G(g.g_find, OCC_FIND)
+    HIVE_DISPATCH_G(g.g_insert, OCC_INS)
+    HIVE_DISPATCH_G(g.g_slow, OCC_SLOW)
+    HIVE_DISPATCH_G(g.g_erase, OCC_ERA)
     g.dedup = occ((const void*)k_dedup_elect) * num_sms;
     g.stream = 4 * num_sms;
     return g;
@@ -835,13 +890,12 @@ static inline int clamp_grid(int grid, uint64_t n, uint64_t per_block) {
     return (int)(need < (uint64_t)grid ? need : (uint64_t)grid);
 }
 
-constexpr uint64_t OPS_PER_BLOCK = BLOCK / GROUP;
-
-cudaError_t launch_find(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
+cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                         uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
                         uint32_t* vals_out, uint8_t* found) {
-    if (!n_dev) grid = clamp_grid(grid, n, OPS_PER_BLOCK);
-    k_find<GROUP><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, vals_out, found);
+    const int grid = n_dev ? gr.find : clamp_grid(gr.find, n, BLOCK / gr.g_find);
+#define L_FIND(G) k_find<G><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, vals_out, found)
+    HIVE_DISPATCH_G(gr.g_find, L_FIND)
     return cudaGetLastError();
 }
 
@@ -852,36 +906,39 @@ cudaError_t launch_dedup_elect(int grid, cudaStream_t s, const uint32_t* keys, c
     return cudaGetLastError();
 }
 
-cudaError_t launch_insert_fast(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
+cudaError_t launch_insert_fast(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
                                const uint64_t* kvs, const uint32_t* idx, uint64_t n,
                                const uint64_t* n_dev, TableView tv, StashView sv, DedupView dd,
-                               uint32_t* owner_of, uint8_t* status, uint32_t* vals_zero,
-                               uint32_t* leftover) {
-    if (!n_dev) grid = clamp_grid(grid, n, OPS_PER_BLOCK);
-    k_insert_fast<GROUP><<<grid, BLOCK, 0, s>>>(keys, vals, kvs, idx, n, n_dev, tv, sv, dd, owner_of,
-                                                status, vals_zero, leftover);
+                               uint8_t* status, uint32_t* vals_zero, uint32_t* leftover) {
+    const int grid = n_dev ? gr.insert_fast : clamp_grid(gr.insert_fast, n, BLOCK / gr.g_insert);
+#define L_INS(G) k_insert_fast<G><<<grid, BLOCK, 0, s>>>(keys, vals, kvs, idx, n, n_dev, tv, sv, dd, \
+                                                         status, vals_zero, leftover)
+    HIVE_DISPATCH_G(gr.g_insert, L_INS)
     return cudaGetLastError();
 }
 
-cudaError_t launch_insert_slow(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
+cudaError_t launch_insert_slow(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
                                const uint64_t* kvs, const uint32_t* leftover, TableView tv,
                                StashView sv, uint32_t max_evictions, uint8_t* status) {
-    k_insert_slow<GROUP><<<grid, BLOCK, 0, s>>>(keys, vals, kvs, leftover, tv, sv, max_evictions, status);
+#define L_SLOW(G) k_insert_slow<G><<<gr.insert_slow, BLOCK, 0, s>>>(keys, vals, kvs, leftover, tv, sv, \
+                                                                    max_evictions, status)
+    HIVE_DISPATCH_G(gr.g_slow, L_SLOW)
     return cudaGetLastError();
 }
 
-cudaError_t launch_erase(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
+cudaError_t launch_erase(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                          uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
-                         DedupView dd, uint32_t* owner_of, uint8_t* erased, uint32_t* vals_zero) {
-    if (!n_dev) grid = clamp_grid(grid, n, OPS_PER_BLOCK);
-    k_erase<GROUP><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, dd, owner_of, erased, vals_zero);
+                         DedupView dd, uint8_t* erased, uint32_t* vals_zero) {
+    const int grid = n_dev ? gr.erase : clamp_grid(gr.erase, n, BLOCK / gr.g_erase);
+#define L_ERA(G) k_erase<G><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, dd, erased, vals_zero)
+    HIVE_DISPATCH_G(gr.g_erase, L_ERA)
     return cudaGetLastError();
 }
 
 cudaError_t launch_dup_copy(int grid, cudaStream_t s, const uint32_t* idx, uint64_t n,
-                            const uint64_t* n_dev, const uint32_t* owner_of, uint8_t* out) {
+                            const uint64_t* n_dev, DedupView dd, uint8_t* out) {
     if (!n_dev) grid = clamp_grid(grid, n, BLOCK);
-    k_dup_copy<<<grid, BLOCK, 0, s>>>(idx, n, n_dev, owner_of, out);
+    k_dup_copy<<<grid, BLOCK, 0, s>>>(idx, n, n_dev, dd, out);
     return cudaGetLastError();
 }
 

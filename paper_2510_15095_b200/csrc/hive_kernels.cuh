@@ -9,7 +9,10 @@ namespace hive {
 
 constexpr int BLOCK = 256;
 constexpr int WARPS_PER_BLOCK = BLOCK / 32;
-constexpr int GROUP = 8;                 // lanes per operation
+// Lanes per operation for each probe kernel: defaults
+// chosen by ncu measurement; HIVE_G_FIND / HIVE_G_INSERT / HIVE_G_ERASE /
+// HIVE_G_SLOW (1, 2, 4 or 8) override them for experiments.
+constexpr int G_FIND = 4, G_INSERT = 4, G_ERASE = 2, G_SLOW = 2;
 constexpr int PART_CHUNK = 2048;         // elements per warp in the stable partition
 constexpr int MAX_PARTS = 64;
 
@@ -17,34 +20,34 @@ enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1 };
 
 struct Grids {                           // persistent grid sizes (blocks)
     int find, insert_fast, insert_slow, erase, dedup, stream;
+    int g_find, g_insert, g_slow, g_erase;   // lanes per operation
 };
 
 // Occupancy-derived persistent grid sizes for this device.
 Grids query_grids(int num_sms);
 
-cudaError_t launch_find(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
+cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                         uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
                         uint32_t* vals_out, uint8_t* found);
 
 cudaError_t launch_dedup_elect(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                                uint64_t n, const uint64_t* n_dev, DedupView dd);
 
-cudaError_t launch_insert_fast(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
+cudaError_t launch_insert_fast(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
                                const uint64_t* kvs, const uint32_t* idx, uint64_t n,
                                const uint64_t* n_dev, TableView tv, StashView sv, DedupView dd,
-                               uint32_t* owner_of, uint8_t* status, uint32_t* vals_zero,
-                               uint32_t* leftover);
+                               uint8_t* status, uint32_t* vals_zero, uint32_t* leftover);
 
-cudaError_t launch_insert_slow(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
+cudaError_t launch_insert_slow(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
                                const uint64_t* kvs, const uint32_t* leftover, TableView tv,
                                StashView sv, uint32_t max_evictions, uint8_t* status);
 
-cudaError_t launch_erase(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
+cudaError_t launch_erase(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                          uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
-                         DedupView dd, uint32_t* owner_of, uint8_t* erased, uint32_t* vals_zero);
+                         DedupView dd, uint8_t* erased, uint32_t* vals_zero);
 
 cudaError_t launch_dup_copy(int grid, cudaStream_t s, const uint32_t* idx, uint64_t n,
-                            const uint64_t* n_dev, const uint32_t* owner_of, uint8_t* out);
+                            const uint64_t* n_dev, DedupView dd, uint8_t* out);
 
 cudaError_t launch_split(cudaStream_t s, TableView tv, uint32_t n_pairs, Ctrl* ctrl);
 cudaError_t launch_merge(cudaStream_t s, TableView tv, uint32_t n_pairs, Ctrl* ctrl);
