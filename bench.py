@@ -430,12 +430,17 @@ def secondary_measurements(table, keys, vals, queries, n, nb, dev, prof_main):
     v_all = [u32(gen.vals_of(i), dev) for i in ids_all]
     vo = torch.empty(bsz, dtype=torch.uint32, device=dev)
     rr = torch.empty(bsz, dtype=torch.uint8, device=dev)
+    if os.environ.get("HIVE_TRACE_CFG3"):
+        os.environ["HIVE_TRACE"] = "1"
     t3 = HiveTable(1024 * 32)
     t3.profile(True)
     torch.cuda.synchronize()
+    walls = []
     ev[0].record()
     for b in range(nbat):
+        w0 = time.perf_counter()
         t3.mixed(ops_all[b], k_all[b], v_all[b], vo, rr)
+        walls.append(time.perf_counter() - w0)
     ev[1].record()
     torch.cuda.synchronize()
     s3 = t3.stats()
@@ -450,6 +455,8 @@ def secondary_measurements(table, keys, vals, queries, n, nb, dev, prof_main):
     p3 = t3.profile_read(reset=True)
     res["cfg3_mixed"] = {
         "gops": nbat * bsz / (mixed_ms * 1e-3) / 1e9, "ms": mixed_ms,
+        "host_wall_ms_max": 1e3 * max(walls), "host_wall_ms_sum": 1e3 * sum(walls),
+        "kern_ms": {k: round(v[0], 3) for k, v in p3.items()},
         "final_buckets": s3["n_buckets"], "final_count": s3["count"], "grows": s3["grows"],
         "drain_tail_gops": U / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9,
         "after_drain_buckets": s3b["n_buckets"], "shrinks": s3b["shrinks"],

@@ -10,8 +10,10 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -24,6 +26,20 @@ using namespace hive;
 namespace {
 
 thread_local std::string g_err;
+
+// HIVE_TRACE=1: host-side timing of allocation / mapping / sync points (stderr).
+const bool g_trace = getenv("HIVE_TRACE") != nullptr;
+struct Trace {
+    const char* what;
+    uint64_t arg;
+    std::chrono::steady_clock::time_point t0;
+    Trace(const char* w, uint64_t a) : what(w), arg(a), t0(std::chrono::steady_clock::now()) {}
+    ~Trace() {
+        if (!g_trace) return;
+        const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        fprintf(stderr, "[hive] %-14s %12llu %9.1f us\n", what, (unsigned long long)arg, us);
+    }
+};
 
 void set_err(cudaError_t e, const char* what, int line) {
     char buf[512];
@@ -92,6 +108,14 @@ uint64_t pow2_at_least(uint64_t x) {
     return p;
 }
 
+// A reserved virtual range whose prefix is backed by physical memory.
+struct VRange {
+    struct Chunk { CUmemGenericAllocationHandle h; size_t off, bytes; };
+    CUdeviceptr va = 0;
+    size_t reserved = 0, mapped = 0;
+    std::vector<Chunk> chunks;
+};
+
 }  // namespace
 
 struct hive_table_s {
@@ -99,16 +123,20 @@ struct hive_table_s {
     int dev = 0, num_sms = 0;
     Grids grids{};
 
-    // bucket array: one reserved VA range, 2 MiB chunks mapped on demand
-    CUdeviceptr va = 0;
-    size_t va_bytes = 0, gran = 0;
-    std::vector<CUmemGenericAllocationHandle> chunks;
+    // Growable device arrays: each a reserved VA range backed on demand by
+    // physical chunks (never moved, never freed while the table lives).
+    size_t gran = 0;
+    VRange bk;                         // bucket array
+    VRange rg;                         // stash ring
+    VRange ix;                         // stash index
+    VRange dr;                         // drain staging (stash entries to reinsert)
+    CUdeviceptr va = 0;                // == bk.va
     uint64_t max_buckets = 0, nb_min = 0;
     uint32_t m0 = 0, split0 = 0, m = 0, split = 0;
 
     // stash ring + index (A-10)
     uint64_t* ring = nullptr;
-    uint64_t ring_alloc = 0, stash_cap = 0;
+    uint64_t stash_cap = 0;
     uint64_t* sidx = nullptr;
     uint64_t idx_cap = 0;
 
@@ -124,10 +152,10 @@ struct hive_table_s {
     uint32_t* cls = nullptr;  uint64_t cls_cap = 0;
     uint64_t* cnt = nullptr;  uint64_t cnt_cap = 0;
     uint64_t* pinfo = nullptr;
-    uint64_t* tmpkv = nullptr; uint64_t tmpkv_cap = 0;
 
     uint64_t grows = 0, shrinks = 0, merge_aborts = 0;
-    uint64_t tail_known = 0;           // last stash_tail read from the device
+    uint64_t tail_known = 0;           // stash_tail at the last synchronising read
+    unsigned long long* aborts = nullptr;   // per-segment first aborting merge pair
 
     // profiling
     struct Rec { const char* name; cudaEvent_t a, b; };
@@ -196,6 +224,7 @@ struct Prof {
 template <typename T>
 hive_status ensure(T*& p, uint64_t& cap, uint64_t need) {
     if (need <= cap && p) return HIVE_OK;
+    Trace tr("ensure", need * sizeof(T));
     uint64_t n = std::max<uint64_t>(need, cap * 3 / 2);
     if (p) cudaFree(p);
     p = nullptr;
@@ -209,8 +238,27 @@ hive_status ensure(T*& p, uint64_t& cap, uint64_t need) {
     return HIVE_OK;
 }
 
-hive_status map_buckets(hive_table_s* h, uint64_t n_buckets) {
-    const size_t need = ((size_t)n_buckets * SLOTS * 8 + h->gran - 1) / h->gran * h->gran;
+hive_status vrange_reserve(hive_table_s* h, VRange& r, size_t bytes) {
+    r.reserved = std::max<size_t>(h->gran, (bytes + h->gran - 1) / h->gran * h->gran);
+    CUresult e = g_vmm.reserve(&r.va, r.reserved, 0, 0, 0);
+    if (e != CUDA_SUCCESS) { set_err_drv(e, "cuMemAddressReserve", __LINE__); return HIVE_ENOMEM; }
+    return HIVE_OK;
+}
+
+// Back the first `need` bytes of a range with physical memory.  Growth maps
+// geometrically (>= 1/4 of what is mapped, whole 2 MiB granules, one
+// cuMemCreate per step), so a long run of K-bucket splits or stash growth
+// costs few driver calls, and nothing is ever copied or freed on the way.
+hive_status vrange_map(hive_table_s* h, VRange& r, size_t need) {
+    need = (need + h->gran - 1) / h->gran * h->gran;
+    if (need <= r.mapped) return HIVE_OK;
+    Trace tr("vrange_map", need);
+    size_t target = std::max(need, r.mapped + r.mapped / 4);
+    target = std::min((target + h->gran - 1) / h->gran * h->gran, r.reserved);
+    if (target < need) {
+        g_err = "request exceeds the reserved max_capacity";
+        return HIVE_ENOMEM;
+    }
     CUmemAllocationProp prop{};
     prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
@@ -218,25 +266,35 @@ hive_status map_buckets(hive_table_s* h, uint64_t n_buckets) {
     CUmemAccessDesc acc{};
     acc.location = prop.location;
     acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    while (h->chunks.size() * h->gran < need) {
-        const size_t off = h->chunks.size() * h->gran;
-        if (off + h->gran > h->va_bytes) {
-            g_err = "bucket array exceeds the reserved max_capacity";
-            return HIVE_ENOMEM;
-        }
-        CUmemGenericAllocationHandle mh;
-        CUresult r = g_vmm.create(&mh, h->gran, &prop, 0);
-        if (r != CUDA_SUCCESS) { set_err_drv(r, "cuMemCreate", __LINE__); return HIVE_ENOMEM; }
-        r = g_vmm.map(h->va + off, h->gran, 0, mh, 0);
-        if (r != CUDA_SUCCESS) { g_vmm.release(mh); set_err_drv(r, "cuMemMap", __LINE__); return HIVE_ENOMEM; }
-        r = g_vmm.set_access(h->va + off, h->gran, &acc, 1);
-        if (r != CUDA_SUCCESS) { set_err_drv(r, "cuMemSetAccess", __LINE__); return HIVE_ECUDA; }
-        h->chunks.push_back(mh);
-    }
+    const size_t off = r.mapped, bytes = target - r.mapped;
+    CUmemGenericAllocationHandle mh;
+    CUresult e = g_vmm.create(&mh, bytes, &prop, 0);
+    if (e != CUDA_SUCCESS) { set_err_drv(e, "cuMemCreate", __LINE__); return HIVE_ENOMEM; }
+    e = g_vmm.map(r.va + off, bytes, 0, mh, 0);
+    if (e != CUDA_SUCCESS) { g_vmm.release(mh); set_err_drv(e, "cuMemMap", __LINE__); return HIVE_ENOMEM; }
+    r.chunks.push_back({mh, off, bytes});
+    e = g_vmm.set_access(r.va + off, bytes, &acc, 1);
+    if (e != CUDA_SUCCESS) { set_err_drv(e, "cuMemSetAccess", __LINE__); return HIVE_ECUDA; }
+    r.mapped = target;
     return HIVE_OK;
 }
 
+void vrange_free(VRange& r) {
+    if (!r.va) return;
+    for (auto& c : r.chunks) {
+        g_vmm.unmap(r.va + c.off, c.bytes);
+        g_vmm.release(c.h);
+    }
+    g_vmm.free_va(r.va, r.reserved);
+    r = VRange{};
+}
+
+hive_status map_buckets(hive_table_s* h, uint64_t n_buckets) {
+    return vrange_map(h, h->bk, (size_t)n_buckets * SLOTS * 8);
+}
+
 hive_status read_ctrl(hive_table_s* h, cudaStream_t s) {
+    Trace tr("read_ctrl", 0);
     CK(cudaMemcpyAsync(h->ctrl_h, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     h->tail_known = h->ctrl_h->stash_tail;
@@ -255,23 +313,17 @@ hive_status set_ctrl_word(hive_table_s* h, unsigned long long* field, uint64_t v
 }
 
 // (Re)size the stash for `cap` entries and clear it (ring + index EMPTY, tail 0).
+// Ring and index live in reserved VA ranges: growing maps more memory, the
+// index capacity is the power of two >= 2 cap (rebuilt at every drain).
 hive_status stash_reset(hive_table_s* h, uint64_t cap, cudaStream_t s) {
-    if (cap > h->ring_alloc) {
-        // grow geometrically: the capacity follows n_b at every resize (A-8)
-        const uint64_t ra = std::max<uint64_t>(cap, h->ring_alloc * 2);
-        const uint64_t ic = pow2_at_least(2 * ra);
-        if (h->ring) cudaFree(h->ring);
-        if (h->sidx) cudaFree(h->sidx);
-        h->ring = nullptr;
-        h->sidx = nullptr;
-        h->ring_alloc = 0;
-        CK(cudaMalloc((void**)&h->ring, ra * sizeof(uint64_t)));
-        CK(cudaMalloc((void**)&h->sidx, ic * sizeof(uint64_t)));
-        h->ring_alloc = ra;
-        h->idx_cap = ic;
-    }
+    const uint64_t ic = pow2_at_least(2 * cap);
+    CKS(vrange_map(h, h->rg, cap * sizeof(uint64_t)));
+    CKS(vrange_map(h, h->ix, ic * sizeof(uint64_t)));
+    h->ring = (uint64_t*)h->rg.va;
+    h->sidx = (uint64_t*)h->ix.va;
     h->stash_cap = cap;
-    CK(launch_stash_reset(s, StashView{h->ring, h->sidx, h->ring_alloc, h->idx_cap - 1, h->ctrl}));
+    h->idx_cap = ic;
+    CK(launch_stash_reset(s, h->sv()));
     CKS(set_ctrl_word(h, &h->ctrl->stash_tail, 0, s));
     h->tail_known = 0;
     return HIVE_OK;
@@ -320,7 +372,10 @@ hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* 
 }
 
 // Drain the stash and reinsert its entries with Steps 2-4 after a resize
-// (PAPER:214, 443); the capacity follows the new size (reading A-8).
+// (PAPER:214, 443); the capacity follows the new size (reading A-8).  Uses the
+// stash tail of the synchronising read that preceded the resize.  The oracle
+// drains after every K-bucket batch; the GPU drains once per resize phase
+// (stash membership is not observable, count is unchanged either way).
 hive_status drain_reinsert(hive_table_s* h, cudaStream_t s) {
     const uint64_t new_cap = h->stash_cap_for(h->nb());
     if (h->tail_known == 0) {
@@ -328,83 +383,100 @@ hive_status drain_reinsert(hive_table_s* h, cudaStream_t s) {
         return HIVE_OK;
     }
     const uint64_t used = std::min<uint64_t>(h->tail_known, h->stash_cap);
-    CKS(ensure(h->tmpkv, h->tmpkv_cap, used));
-    CK(cudaMemcpyAsync(h->tmpkv, h->ring, used * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    Trace tr("drain", used);
+    CKS(vrange_map(h, h->dr, used * sizeof(uint64_t)));
+    uint64_t* tmpkv = (uint64_t*)h->dr.va;
+    CK(cudaMemcpyAsync(tmpkv, h->ring, used * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
     CKS(stash_reset(h, new_cap, s));
-    CKS(insert_phase(h, nullptr, nullptr, h->tmpkv, nullptr, used, nullptr, used, nullptr, nullptr, s));
-    CKS(read_ctrl(h, s));
+    CKS(insert_phase(h, nullptr, nullptr, tmpkv, nullptr, used, nullptr, used, nullptr, nullptr, s));
+    h->tail_known = ~0ull;             // unknown until the next read
     return HIVE_OK;
 }
 
-// expand_batch: split min(K, 2^m - split) buckets from split_ptr.
-hive_status expand_batch(hive_table_s* h, cudaStream_t s, bool* grew) {
-    const uint64_t round_end = 1ull << h->m;
-    uint64_t n = std::min<uint64_t>(h->cfg.resize_k, round_end - h->split);
-    n = std::min<uint64_t>(n, h->max_buckets - h->nb());
-    *grew = n > 0;
-    if (!n) return HIVE_OK;
-    CKS(map_buckets(h, h->nb() + n));
-    {
-        Prof p(h, "k_split", s);
-        CK(launch_split(s, h->tv(), (uint32_t)n, h->ctrl));
+// Grow before an INSERT phase (reading A-19): the K-bucket
+// expand_batch loop of the oracle is simulated on the host from `count` (it
+// depends on nothing else), then executed as one k_split launch per
+// linear-hashing round it crosses -- pairs of one round are independent, and a
+// round's sources were written by the previous round's launch.
+hive_status grow_known(hive_table_s* h, uint64_t count, uint64_t n_ins, cudaStream_t s) {
+    uint32_t m = h->m, split = h->split;
+    uint64_t batches = 0;
+    auto nb = [&]() { return (1ull << m) + split; };
+    while ((double)(count + n_ins) > (double)h->cfg.lf_grow * (double)nb() * SLOTS) {
+        uint64_t n = std::min<uint64_t>(h->cfg.resize_k, (1ull << m) - split);
+        n = std::min<uint64_t>(n, h->max_buckets - nb());
+        if (n == 0) break;                // max_capacity reached
+        split += (uint32_t)n;
+        if (split == (1u << m)) { ++m; split = 0; }
+        ++batches;
     }
-    h->split += (uint32_t)n;
-    if (h->split == round_end) {
-        h->m += 1;
-        h->split = 0;
+    if (!batches) return HIVE_OK;
+    CKS(map_buckets(h, nb()));
+    while (h->m != m || h->split != split) {
+        const uint32_t round_end = 1u << h->m;
+        const uint32_t stop = (h->m == m) ? split : round_end;
+        {
+            Prof p(h, "k_split", s);
+            CK(launch_split(s, h->tv(), stop - h->split, h->ctrl));
+        }
+        h->split = stop;
+        if (h->split == round_end) { h->m += 1; h->split = 0; }
     }
-    h->grows++;
-    return drain_reinsert(h, s);
-}
-
-// contract_batch (readings A-7, A-25).  *aborted on a failed merge.
-hive_status contract_batch(hive_table_s* h, cudaStream_t s, bool* aborted) {
-    *aborted = false;
-    if (h->nb() <= h->nb_min) return HIVE_OK;
-    if (h->split == 0) {                  // regress: (m, 0) == (m-1, 2^(m-1))
-        h->m -= 1;
-        h->split = 1u << h->m;
-    }
-    uint64_t n = std::min<uint64_t>(h->cfg.resize_k, h->split);
-    n = std::min<uint64_t>(n, h->nb() - h->nb_min);
-    CKS(set_ctrl_word(h, &h->ctrl->first_abort, n, s));
-    {
-        Prof p(h, "k_merge", s);
-        CK(launch_merge(s, h->tv(), (uint32_t)n, h->ctrl));
-    }
-    CKS(read_ctrl(h, s));
-    const uint64_t merged = std::min<uint64_t>(h->ctrl_h->first_abort, n);
-    h->split -= (uint32_t)merged;
-    if (merged < n) {
-        *aborted = true;
-        h->merge_aborts++;
-    }
-    h->shrinks++;
+    h->grows += batches;
     return drain_reinsert(h, s);
 }
 
 hive_status grow_before(hive_table_s* h, uint64_t n_ins, cudaStream_t s) {
     if (h->cfg.lf_grow >= 1.0f || n_ins == 0) return HIVE_OK;
     CKS(read_ctrl(h, s));
-    const uint64_t count = h->ctrl_h->count;
-    while ((double)(count + n_ins) > (double)h->cfg.lf_grow * (double)h->nb() * SLOTS) {
-        bool grew = false;
-        CKS(expand_batch(h, s, &grew));
-        if (!grew) break;                 // max_capacity reached
-    }
-    return HIVE_OK;
+    return grow_known(h, h->ctrl_h->count, n_ins, s);
 }
 
+// Shrink after an ERASE phase: the oracle's
+// contract_batch loop is simulated from `count` into per-round segments of
+// LIFO pairs; each segment is one check+apply launch pair that stops at its
+// first aborting pair (and merges nothing if an earlier segment aborted);
+// one synchronising read returns how far the merges got.
 hive_status shrink_after(hive_table_s* h, cudaStream_t s) {
-    if (h->cfg.lf_shrink <= 0.0f) return HIVE_OK;
+    if (h->cfg.lf_shrink <= 0.0f || h->nb() <= h->nb_min) return HIVE_OK;
     CKS(read_ctrl(h, s));
     const uint64_t count = h->ctrl_h->count;
-    while ((double)count < (double)h->cfg.lf_shrink * (double)h->nb() * SLOTS && h->nb() > h->nb_min) {
-        bool aborted = false;
-        CKS(contract_batch(h, s, &aborted));
-        if (aborted) break;
+    struct Seg { uint32_t m, split0; uint64_t pairs; };
+    std::vector<Seg> segs;
+    uint32_t m = h->m, split = h->split;
+    uint64_t batches = 0;
+    auto nb = [&]() { return (1ull << m) + split; };
+    while ((double)count < (double)h->cfg.lf_shrink * (double)nb() * SLOTS && nb() > h->nb_min) {
+        if (split == 0) { --m; split = 1u << m; }              // regress, A-7
+        uint64_t n = std::min<uint64_t>(h->cfg.resize_k, split);
+        n = std::min<uint64_t>(n, nb() - h->nb_min);
+        if (segs.empty() || segs.back().m != m) {
+            if ((int)segs.size() == MAX_SEGMENTS) break;
+            segs.push_back({m, split, 0});
+        }
+        segs.back().pairs += n;
+        split -= (uint32_t)n;
+        ++batches;
     }
-    return HIVE_OK;
+    if (segs.empty()) return HIVE_OK;
+    for (size_t i = 0; i < segs.size(); ++i) h->stage_h[8 + i] = segs[i].pairs;
+    CK(cudaMemcpyAsync(h->aborts, h->stage_h + 8, segs.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    for (size_t i = 0; i < segs.size(); ++i) {
+        TableView tv{(uint64_t*)h->va, (uint32_t)((1ull << segs[i].m) - 1), segs[i].split0};
+        Prof p(h, "k_merge", s);
+        CK(launch_merge(s, tv, (uint32_t)segs[i].pairs, h->aborts + i, i ? h->aborts + i - 1 : nullptr,
+                        i ? segs[i - 1].pairs : 0));
+    }
+    CK(cudaMemcpyAsync(h->stage_h + 8, h->aborts, segs.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < segs.size(); ++i) {
+        const uint64_t merged = std::min<uint64_t>(h->stage_h[8 + i], segs[i].pairs);
+        h->m = segs[i].m;
+        h->split = segs[i].split0 - (uint32_t)merged;
+        if (merged < segs[i].pairs) { h->merge_aborts++; break; }
+    }
+    h->shrinks += batches;
+    return drain_reinsert(h, s);
 }
 
 hive_status erase_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* idx, uint64_t n_upper,
@@ -495,16 +567,23 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     prop.location.id = h->dev;
     CUresult r = g_vmm.granularity(&h->gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
     if (r != CUDA_SUCCESS || !h->gran) { set_err_drv(r, "cuMemGetAllocationGranularity", __LINE__); return fail(HIVE_ECUDA); }
-    h->va_bytes = ((size_t)h->max_buckets * SLOTS * 8 + h->gran - 1) / h->gran * h->gran;
-    r = g_vmm.reserve(&h->va, h->va_bytes, 0, 0, 0);
-    if (r != CUDA_SUCCESS) { set_err_drv(r, "cuMemAddressReserve", __LINE__); return fail(HIVE_ENOMEM); }
-    hive_status st = map_buckets(h, nb);
+    const uint64_t max_stash = h->stash_cap_for(h->max_buckets);
+    hive_status st = vrange_reserve(h, h->bk, (size_t)h->max_buckets * SLOTS * 8);
+    if (st == HIVE_OK) st = vrange_reserve(h, h->rg, max_stash * sizeof(uint64_t));
+    if (st == HIVE_OK) st = vrange_reserve(h, h->ix, pow2_at_least(2 * max_stash) * sizeof(uint64_t));
+    if (st == HIVE_OK) st = vrange_reserve(h, h->dr, max_stash * sizeof(uint64_t));
+    if (st != HIVE_OK) return fail(st);
+    h->va = h->bk.va;
+    st = map_buckets(h, nb);
     if (st != HIVE_OK) return fail(st);
 
     if (cudaMalloc((void**)&h->ctrl, sizeof(Ctrl)) != cudaSuccess) return fail(HIVE_ENOMEM);
     if (cudaMallocHost((void**)&h->ctrl_h, sizeof(Ctrl)) != cudaSuccess) return fail(HIVE_ENOMEM);
-    if (cudaMallocHost((void**)&h->stage_h, 8 * sizeof(uint64_t)) != cudaSuccess) return fail(HIVE_ENOMEM);
+    if (cudaMallocHost((void**)&h->stage_h, (8 + MAX_SEGMENTS) * sizeof(uint64_t)) != cudaSuccess)
+        return fail(HIVE_ENOMEM);
     if (cudaMalloc((void**)&h->pinfo, 2 * MAX_PARTS * sizeof(uint64_t)) != cudaSuccess) return fail(HIVE_ENOMEM);
+    if (cudaMalloc((void**)&h->aborts, MAX_SEGMENTS * sizeof(unsigned long long)) != cudaSuccess)
+        return fail(HIVE_ENOMEM);
     memset(h->ctrl_h, 0, sizeof(Ctrl));
     st = hive_clear(h, stream);
     if (st != HIVE_OK) return fail(st);
@@ -530,15 +609,11 @@ hive_status hive_destroy(hive_t h) {
     if (!h) return HIVE_EINVAL;
     cudaStreamSynchronize(h->last);
     cudaDeviceSynchronize();
-    if (h->va) {
-        for (size_t i = 0; i < h->chunks.size(); ++i) {
-            g_vmm.unmap(h->va + i * h->gran, h->gran);
-            g_vmm.release(h->chunks[i]);
-        }
-        g_vmm.free_va(h->va, h->va_bytes);
-    }
-    void* bufs[] = {h->ring, h->sidx, h->ctrl, h->dd, h->owner, h->flag, h->left, h->cls, h->cnt, h->pinfo,
-                    h->tmpkv};
+    vrange_free(h->bk);
+    vrange_free(h->rg);
+    vrange_free(h->ix);
+    vrange_free(h->dr);
+    void* bufs[] = {h->ctrl, h->dd, h->owner, h->flag, h->left, h->cls, h->cnt, h->pinfo, h->aborts};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (h->ctrl_h) cudaFreeHost(h->ctrl_h);
@@ -608,10 +683,10 @@ hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
     const uint64_t* n_find = h->pinfo + 0;
     const uint64_t* n_ins = h->pinfo + 1;
     const uint64_t* n_era = h->pinfo + 2;
-    if (h->cfg.lf_grow < 1.0f) {
+    if (h->cfg.lf_grow < 1.0f) {           // one sync: phase sizes + counters
         CK(cudaMemcpyAsync(h->stage_h, h->pinfo, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        CKS(grow_before(h, h->stage_h[1], s));
+        CKS(read_ctrl(h, s));
+        if (h->stage_h[1]) CKS(grow_known(h, h->ctrl_h->count, h->stage_h[1], s));
     }
     CKS(insert_phase(h, d_keys, d_vals, nullptr, h->cls + n, n, n_ins, n, d_result, d_vals_out, s));
     CKS(erase_phase(h, d_keys, h->cls + 2 * n, n, n_era, n, d_result, d_vals_out, s));
@@ -651,7 +726,7 @@ hive_status hive_stats(hive_t h, hive_stats_t* o) {
     o->merge_aborts = h->merge_aborts;
     o->failed = c.failed;
     o->in_b1 = c.in_b1;
-    o->mapped_bytes = h->chunks.size() * h->gran;
+    o->mapped_bytes = h->bk.mapped;
     return c.failed ? HIVE_ESTASHFULL : HIVE_OK;
 }
 

@@ -630,24 +630,32 @@ k_split(TableView tv, uint32_t n_pairs, Ctrl* ctrl) {
 
 // Contraction, LIFO pairs t = 0..n_pairs-1 with
 // b_dst = split-1-t, b_src = b_dst + 2^m.  Pass 1 finds the first pair that
-// must abort (n_move > n_free); pass 2 merges the pairs before it
-// (the sequential LIFO loop stops at its first abort, reading A-25).
+// must abort (n_move > n_free) -> *abort_at (initialised to n_pairs
+// by the host); pass 2 merges the pairs before it (the sequential LIFO loop
+// stops at its first abort, reading A-25).  A segment whose predecessor
+// segment (the previous linear-hashing round of the same shrink phase)
+// aborted merges nothing.
 __global__ void __launch_bounds__(BLOCK)
-k_merge_check(TableView tv, uint32_t n_pairs, Ctrl* ctrl) {
+k_merge_check(TableView tv, uint32_t n_pairs, unsigned long long* abort_at,
+              const unsigned long long* prev_abort, uint64_t prev_pairs) {
     const uint32_t t = (blockIdx.x * BLOCK + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (t >= n_pairs) return;
+    if (prev_abort && *prev_abort < prev_pairs) {
+        if (t == 0 && lane == 0) *abort_at = 0;
+        return;
+    }
     const uint32_t b_dst = tv.split - 1u - t;
     const uint32_t b_src = b_dst + tv.mask + 1u;
     const uint32_t occ = __ballot_sync(FULL, tv.bucket(b_src)[lane] != EMPTY);
     const uint32_t fre = __ballot_sync(FULL, tv.bucket(b_dst)[lane] == EMPTY);
-    if (lane == 0 && __popc(occ) > __popc(fre)) atomicMin(&ctrl->first_abort, (unsigned long long)t);
+    if (lane == 0 && __popc(occ) > __popc(fre)) atomicMin(abort_at, (unsigned long long)t);
 }
 __global__ void __launch_bounds__(BLOCK)
-k_merge_apply(TableView tv, uint32_t n_pairs, Ctrl* ctrl) {
+k_merge_apply(TableView tv, uint32_t n_pairs, const unsigned long long* abort_at) {
     const uint32_t t = (blockIdx.x * BLOCK + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (t >= n_pairs || t >= ctrl->first_abort) return;
+    if (t >= n_pairs || t >= *abort_at) return;
     const uint32_t b_dst = tv.split - 1u - t;
     const uint32_t b_src = b_dst + tv.mask + 1u;
     uint64_t* src = tv.bucket(b_src);
@@ -949,11 +957,12 @@ cudaError_t launch_split(cudaStream_t s, TableView tv, uint32_t n_pairs, Ctrl* c
     return cudaGetLastError();
 }
 
-cudaError_t launch_merge(cudaStream_t s, TableView tv, uint32_t n_pairs, Ctrl* ctrl) {
+cudaError_t launch_merge(cudaStream_t s, TableView tv, uint32_t n_pairs, unsigned long long* abort_at,
+                         const unsigned long long* prev_abort, uint64_t prev_pairs) {
     if (n_pairs == 0) return cudaSuccess;
     const int grid = (int)((n_pairs + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK);
-    k_merge_check<<<grid, BLOCK, 0, s>>>(tv, n_pairs, ctrl);
-    k_merge_apply<<<grid, BLOCK, 0, s>>>(tv, n_pairs, ctrl);
+    k_merge_check<<<grid, BLOCK, 0, s>>>(tv, n_pairs, abort_at, prev_abort, prev_pairs);
+    k_merge_apply<<<grid, BLOCK, 0, s>>>(tv, n_pairs, abort_at);
     return cudaGetLastError();
 }
 

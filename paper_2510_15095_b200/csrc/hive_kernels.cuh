@@ -50,7 +50,9 @@ cudaError_t launch_dup_copy(int grid, cudaStream_t s, const uint32_t* idx, uint6
                             const uint64_t* n_dev, DedupView dd, uint8_t* out);
 
 cudaError_t launch_split(cudaStream_t s, TableView tv, uint32_t n_pairs, Ctrl* ctrl);
-cudaError_t launch_merge(cudaStream_t s, TableView tv, uint32_t n_pairs, Ctrl* ctrl);
+cudaError_t launch_merge(cudaStream_t s, TableView tv, uint32_t n_pairs, unsigned long long* abort_at,
+                         const unsigned long long* prev_abort, uint64_t prev_pairs);
+constexpr int MAX_SEGMENTS = 64;        // linear-hashing rounds crossed by one resize phase
 
 cudaError_t launch_stash_reset(cudaStream_t s, StashView sv);
 
