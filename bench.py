@@ -359,7 +359,7 @@ def main():
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        s_log2 = min(22, args.n_log2)
+        s_log2 = min(24, args.n_log2)
         ops, sec = oracle_sample(s_log2)
         cpu = {"value": ops / sec / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"2^{s_log2} inserts to LF 0.95 + 2^{s_log2} finds (50% hits), sequential oracle",
