@@ -344,8 +344,8 @@ __device__ __forceinline__ bool owns(const WarpGroup<G>& wg, const DedupView& dd
 // after a resize: Step 1 is skipped (those keys are in no bucket)
 // and nothing is counted.
 // --------------------------------------------------------------------------------
-template <int G>
-__global__ void __launch_bounds__(BLOCK)
+template <int G, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
 k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
               const uint64_t* __restrict__ kvs, const uint32_t* __restrict__ idx, uint64_t n,
               const uint64_t* __restrict__ n_dev, TableView tv, StashView sv, DedupView dd,
@@ -454,8 +454,8 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
 // rotates with the round (reading A-6 allows any victim rule; placement is not
 // observable).
 // --------------------------------------------------------------------------------
-template <int G>
-__global__ void __launch_bounds__(BLOCK)
+template <int G, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
 k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
               const uint64_t* __restrict__ kvs, const uint32_t* __restrict__ leftover,
               TableView tv, StashView sv, uint32_t max_evictions, uint8_t* __restrict__ status) {
@@ -485,7 +485,9 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             if (trying) ++rounds;
             bool placed = wabc_claim<G>(wg, s, tv.bucket(b), kv, trying);   // line 3
             if (placed) trying = false;
-            // evict a victim: rotating slot, CAS-swap (lines 17-21, A-14)
+            // Victim (lines 17-21): a rotating slot (reading A-6: any victim rule;
+            // preferring residents in their second bucket raised p_h1 to 0.93 but
+            // doubled evictions and grew the stash 5x -- a net loss).
             const int vs = (int)((seed + r * 11u) & 31u);
             const int vl = vs / SPL;
             uint64_t victim = wg.bcast(pick<SPL>(s, vs % SPL), vl);
@@ -526,8 +528,8 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
 // ERASE (Alg. 4 ScanBucketAndDelete): WCME, winner CAS -> EMPTY;
 // b2 only on a miss; then the stash.
 // --------------------------------------------------------------------------------
-template <int G>
-__global__ void __launch_bounds__(BLOCK)
+template <int G, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
 k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
         const uint64_t* __restrict__ n_dev, TableView tv, StashView sv, DedupView dd,
         uint8_t* __restrict__ erased_out, uint32_t* __restrict__ vals_zero) {
@@ -873,20 +875,38 @@ static int env_g(const char* name, int dflt) {
         default: X(8); break; \
     }
 
+#define HIVE_DISPATCH_GM(g, mb, X)           \
+    if (mb >= 4) {                            \
+        switch (g) {                          \
+            case 1: X(1, 4); break;           \
+            case 2: X(2, 4); break;           \
+            case 4: X(4, 4); break;           \
+            default: X(8, 4); break;          \
+        }                                     \
+    } else {                                  \
+        switch (g) {                          \
+            case 1: X(1, 1); break;           \
+            case 2: X(2, 1); break;           \
+            case 4: X(4, 1); break;           \
+            default: X(8, 1); break;          \
+        }                                     \
+    }
+
 Grids query_grids(int num_sms) {
     Grids g;
     g.g_find = env_g("HIVE_G_FIND", G_FIND);
     g.g_insert = env_g("HIVE_G_INSERT", G_INSERT);
     g.g_slow = env_g("HIVE_G_SLOW", G_SLOW);
     g.g_erase = env_g("HIVE_G_ERASE", G_ERASE);
+    g.minb = getenv("HIVE_MINB") ? atoi(getenv("HIVE_MINB")) : MINB_DEFAULT;
 #define OCC_FIND(G) g.find = occ((const void*)k_find<G>) * num_sms
-#define OCC_INS(G) g.insert_fast = occ((const void*)k_insert_fast<G>) * num_sms
-#define OCC_SLOW(G) g.insert_slow = occ((const void*)k_insert_slow<G>) * num_sms
-#define OCC_ERA(G) g.erase = occ((const void*)k_erase<G>) * num_sms
+#define OCC_INS(G, MB) g.insert_fast = occ((const void*)k_insert_fast<G, MB>) * num_sms
+#define OCC_SLOW(G, MB) g.insert_slow = occ((const void*)k_insert_slow<G, MB>) * num_sms
+#define OCC_ERA(G, MB) g.erase = occ((const void*)k_erase<G, MB>) * num_sms
     HIVE_DISPATCH_G(g.g_find, OCC_FIND)
-    HIVE_DISPATCH_G(g.g_insert, OCC_INS)
-    HIVE_DISPATCH_G(g.g_slow, OCC_SLOW)
-    HIVE_DISPATCH_G(g.g_erase, OCC_ERA)
+    HIVE_DISPATCH_GM(g.g_insert, g.minb, OCC_INS)
+    HIVE_DISPATCH_GM(g.g_slow, g.minb, OCC_SLOW)
+    HIVE_DISPATCH_GM(g.g_erase, g.minb, OCC_ERA)
     g.dedup = occ((const void*)k_dedup_elect) * num_sms;
     g.stream = 4 * num_sms;
     return g;
@@ -919,18 +939,18 @@ cudaError_t launch_insert_fast(const Grids& gr, cudaStream_t s, const uint32_t* 
                                const uint64_t* n_dev, TableView tv, StashView sv, DedupView dd,
                                uint8_t* status, uint32_t* vals_zero, uint32_t* leftover) {
     const int grid = n_dev ? gr.insert_fast : clamp_grid(gr.insert_fast, n, BLOCK / gr.g_insert);
-#define L_INS(G) k_insert_fast<G><<<grid, BLOCK, 0, s>>>(keys, vals, kvs, idx, n, n_dev, tv, sv, dd, \
+#define L_INS(G, MB) k_insert_fast<G, MB><<<grid, BLOCK, 0, s>>>(keys, vals, kvs, idx, n, n_dev, tv, sv, dd, \
                                                          status, vals_zero, leftover)
-    HIVE_DISPATCH_G(gr.g_insert, L_INS)
+    HIVE_DISPATCH_GM(gr.g_insert, gr.minb, L_INS)
     return cudaGetLastError();
 }
 
 cudaError_t launch_insert_slow(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
                                const uint64_t* kvs, const uint32_t* leftover, TableView tv,
                                StashView sv, uint32_t max_evictions, uint8_t* status) {
-#define L_SLOW(G) k_insert_slow<G><<<gr.insert_slow, BLOCK, 0, s>>>(keys, vals, kvs, leftover, tv, sv, \
+#define L_SLOW(G, MB) k_insert_slow<G, MB><<<gr.insert_slow, BLOCK, 0, s>>>(keys, vals, kvs, leftover, tv, sv, \
                                                                     max_evictions, status)
-    HIVE_DISPATCH_G(gr.g_slow, L_SLOW)
+    HIVE_DISPATCH_GM(gr.g_slow, gr.minb, L_SLOW)
     return cudaGetLastError();
 }
 
@@ -938,8 +958,8 @@ cudaError_t launch_erase(const Grids& gr, cudaStream_t s, const uint32_t* keys, 
                          uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
                          DedupView dd, uint8_t* erased, uint32_t* vals_zero) {
     const int grid = n_dev ? gr.erase : clamp_grid(gr.erase, n, BLOCK / gr.g_erase);
-#define L_ERA(G) k_erase<G><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, dd, erased, vals_zero)
-    HIVE_DISPATCH_G(gr.g_erase, L_ERA)
+#define L_ERA(G, MB) k_erase<G, MB><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, dd, erased, vals_zero)
+    HIVE_DISPATCH_GM(gr.g_erase, gr.minb, L_ERA)
     return cudaGetLastError();
 }
 

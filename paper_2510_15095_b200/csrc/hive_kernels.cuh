@@ -13,6 +13,7 @@ constexpr int WARPS_PER_BLOCK = BLOCK / 32;
 // chosen by ncu measurement; HIVE_G_FIND / HIVE_G_INSERT / HIVE_G_ERASE /
 // HIVE_G_SLOW (1, 2, 4 or 8) override them for experiments.
 constexpr int G_FIND = 4, G_INSERT = 4, G_ERASE = 2, G_SLOW = 2;
+constexpr int MINB_DEFAULT = 4;          // 4 blocks/SM => <= 64 registers (ncu: 74-80 regs left 36% warps active)
 constexpr int PART_CHUNK = 2048;         // elements per warp in the stable partition
 constexpr int MAX_PARTS = 64;
 
@@ -21,6 +22,7 @@ enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1 };
 struct Grids {                           // persistent grid sizes (blocks)
     int find, insert_fast, insert_slow, erase, dedup, stream;
     int g_find, g_insert, g_slow, g_erase;   // lanes per operation
+    int minb;                                // min resident blocks/SM for the mutating kernels
 };
 
 // Occupancy-derived persistent grid sizes for this device.
