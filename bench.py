@@ -153,22 +153,6 @@ def run_reference(args, rank: int, world: int):
 
 
 # ---------------------------------------------------------------------------------------
-# algorithmic bytes
-# ---------------------------------------------------------------------------------------
-def alg_bytes_find(n_hit, n_miss, p_h1, stash_nonempty):
-    hit = 256.0 * (2.0 - p_h1) + 9.0
-    miss = 512.0 + 9.0 + (32.0 if stash_nonempty else 0.0)
-    return n_hit * hit + n_miss * miss
-
-
-def alg_bytes_insert_fast(n_new, dedup):
-    # Step 1 probes b1 and b2 (new key) + one CAS sector + key/value/status I/O;
-    # with owner election: + owner_of write (4 B) + one election-table sector (32 B).
-    per = 512.0 + 32.0 + 9.0 + (36.0 if dedup else 0.0)
-    return n_new * per
-
-
-# ---------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------
 def main():
@@ -295,13 +279,20 @@ def main():
     hbm_peak, peak_kind = peaks()
 
     kern = {k: v[0] / v[1] for k, v in prof.items()}           # avg ms per launch
-    dominant = max(prof, key=lambda k: prof[k][0])
-    n_local = st["count"]
-    if dominant == "k_find":
-        algb = alg_bytes_find(n_local // 2 if world > 1 else n // 2, n // 2, p_h1, st["stash_used"] > 0)
-    else:
-        algb = alg_bytes_insert_fast(n_local if world > 1 else n, dedup=True)
-    achieved = algb / (kern[dominant] * 1e-3) / 1e9
+    launches = {k: v[1] for k, v in prof.items()}
+    fam = {"k_find": "find", "k_insert_fast": "insert", "k_insert_slow": "evict", "k_erase": "erase",
+           "k_dedup_elect": "elect"}
+    ab = st["alg_bytes"]                                       # counted by the kernels in this step
+    per_kernel = {}
+    for k in kern:
+        if k in fam and ab.get(fam[k]):
+            per_launch = ab[fam[k]] / launches[k]
+            per_kernel[k] = {"ms": kern[k], "alg_bytes_per_launch": per_launch,
+                             "achieved_GBps": per_launch / (kern[k] * 1e-3) / 1e9,
+                             "frac": per_launch / (kern[k] * 1e-3) / 1e9 / hbm_peak}
+    dominant = max(per_kernel, key=lambda k: prof[k][0])
+    algb = per_kernel[dominant]["alg_bytes_per_launch"]
+    achieved = per_kernel[dominant]["achieved_GBps"]
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -311,7 +302,9 @@ def main():
     roofline = {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": hbm_peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
                 "traffic": traffic, "alg_bytes_per_launch": algb, "p_h1": p_h1,
-                "kernel_ms": kern[dominant]}
+                "kernel_ms": kern[dominant], "per_kernel": per_kernel,
+                "alg_bytes_rule": "counted in-kernel: 256 B per bucket probe, 32 B per CAS sector, "
+                                  "8 B per spill/stash word, exact key/value/result streams"}
 
     # ---- e2e through the public API with host buffers (pinned) ---------------------------
     e2e = None

@@ -97,6 +97,13 @@ typedef struct {
     uint64_t failed;         /* entries lost to a full stash (must be 0)      */
     uint64_t in_b1;          /* live bucket keys resident in addr(h1)         */
     uint64_t mapped_bytes;   /* physical bytes mapped for buckets             */
+    uint64_t alg_bytes[8];   /* algorithmic bytes touched since create/clear,
+                                per kernel family: [0] find, [1] insert fast
+                                path, [2] eviction + stash, [3] erase,
+                                [4] owner election (256 B per bucket probe,
+                                32 B per CAS sector, 8 B per spill / stash
+                                word, exact key / value / result stream
+                                bytes)                          */
 } hive_stats_t;
 
 /* Fill *cfg with the defaults above. */

@@ -61,6 +61,14 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
     return h;
 }
 
+// Three fingerprint bits of a key in its bucket's spill word (independent of
+// BitHash1/2).
+constexpr uint32_t SPILL_SEED = 0x3C6EF372u;
+__device__ __forceinline__ uint64_t spill_fp(uint32_t k) {
+    const uint32_t x = fmix32(k ^ SPILL_SEED);
+    return (1ull << (x & 63)) | (1ull << ((x >> 6) & 63)) | (1ull << ((x >> 12) & 63));
+}
+
 // ---- device control block --------------------------------------------------------
 struct Ctrl {
     unsigned long long count;          // live keys (buckets + stash), A-19
@@ -75,13 +83,24 @@ struct Ctrl {
     unsigned long long dump_n;         // dump cursor
     unsigned long long in_b1;          // stats: keys resident in addr(h1)
     unsigned long long pad[5];
+    // Algorithmic bytes touched, per kernel family: 256 per
+    // bucket probe, 32 per CAS / atomic sector, 8 per spill word or stash word,
+    // exact bytes of the key / value / result streams.
+    unsigned long long abytes[8];
 };
+enum AlgBytes { AB_FIND = 0, AB_INSERT = 1, AB_EVICT = 2, AB_ERASE = 3, AB_ELECT = 4, AB_RESIZE = 5 };
 
 // ---- linear-hashing addressing, PAPER:485-503 (Litwin rule, A-2) ----------------
 struct TableView {
     uint64_t* buckets;   // n_b * 32 packed words
     uint32_t mask;       // index_mask = 2^m - 1
     uint32_t split;      // split pointer
+    // Spill filter (B200 addition): one 64-bit word per bucket b;
+    // for every live key k NOT stored in bucket addr(h1(k)) (it sits in b2 or
+    // the stash) the bits spill_fp(k) are set in spill[addr(h1(k))].  Bits are
+    // only ever added (erase leaves them; split copies, merge ORs), so a word
+    // missing any of k's bits proves k is in no place but b1.
+    uint64_t* spill;
     __device__ __forceinline__ uint32_t addr(uint32_t h) const {
         uint32_t b = h & mask;
         if (b < split) b = h & ((mask << 1) | 1u);

@@ -130,6 +130,7 @@ struct hive_table_s {
     VRange rg;                         // stash ring
     VRange ix;                         // stash index
     VRange dr;                         // drain staging (stash entries to reinsert)
+    VRange sp;                         // spill filter: one u64 per bucket
     CUdeviceptr va = 0;                // == bk.va
     uint64_t max_buckets = 0, nb_min = 0;
     uint32_t m0 = 0, split0 = 0, m = 0, split = 0;
@@ -170,7 +171,7 @@ struct hive_table_s {
 
     uint64_t nb() const { return (1ull << m) + split; }
     TableView tv() const {
-        return TableView{(uint64_t*)va, (uint32_t)((1ull << m) - 1), split};
+        return TableView{(uint64_t*)va, (uint32_t)((1ull << m) - 1), split, (uint64_t*)sp.va};
     }
     StashView sv() const { return StashView{ring, sidx, stash_cap, idx_cap - 1, ctrl}; }
     bool dedup_on() const { return !(cfg.flags & HIVE_KEYS_UNIQUE); }
@@ -290,7 +291,8 @@ void vrange_free(VRange& r) {
 }
 
 hive_status map_buckets(hive_table_s* h, uint64_t n_buckets) {
-    return vrange_map(h, h->bk, (size_t)n_buckets * SLOTS * 8);
+    CKS(vrange_map(h, h->bk, (size_t)n_buckets * SLOTS * 8));
+    return vrange_map(h, h->sp, (size_t)n_buckets * sizeof(uint64_t));
 }
 
 hive_status read_ctrl(hive_table_s* h, cudaStream_t s) {
@@ -340,7 +342,7 @@ hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* 
     CK(cudaMemsetAsync(h->dd, 0xFF, cap * sizeof(uint64_t), s));
     CK(cudaMemsetAsync(h->flag, 0, n_batch, s));
     Prof p(h, "k_dedup_elect", s);
-    CK(launch_dedup_elect(h->grids.dedup, s, keys, idx, n_upper, n_dev, *dd));
+    CK(launch_dedup_elect(h->grids.dedup, s, keys, idx, n_upper, n_dev, *dd, h->ctrl));
     return HIVE_OK;
 }
 
@@ -462,7 +464,7 @@ hive_status shrink_after(hive_table_s* h, cudaStream_t s) {
     for (size_t i = 0; i < segs.size(); ++i) h->stage_h[8 + i] = segs[i].pairs;
     CK(cudaMemcpyAsync(h->aborts, h->stage_h + 8, segs.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
     for (size_t i = 0; i < segs.size(); ++i) {
-        TableView tv{(uint64_t*)h->va, (uint32_t)((1ull << segs[i].m) - 1), segs[i].split0};
+        TableView tv{(uint64_t*)h->va, (uint32_t)((1ull << segs[i].m) - 1), segs[i].split0, (uint64_t*)h->sp.va};
         Prof p(h, "k_merge", s);
         CK(launch_merge(s, tv, (uint32_t)segs[i].pairs, h->aborts + i, i ? h->aborts + i - 1 : nullptr,
                         i ? segs[i - 1].pairs : 0));
@@ -572,6 +574,7 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     if (st == HIVE_OK) st = vrange_reserve(h, h->rg, max_stash * sizeof(uint64_t));
     if (st == HIVE_OK) st = vrange_reserve(h, h->ix, pow2_at_least(2 * max_stash) * sizeof(uint64_t));
     if (st == HIVE_OK) st = vrange_reserve(h, h->dr, max_stash * sizeof(uint64_t));
+    if (st == HIVE_OK) st = vrange_reserve(h, h->sp, (size_t)h->max_buckets * sizeof(uint64_t));
     if (st != HIVE_OK) return fail(st);
     h->va = h->bk.va;
     st = map_buckets(h, nb);
@@ -598,6 +601,7 @@ hive_status hive_clear(hive_t h, void* stream) {
     h->m = h->m0;
     h->split = h->split0;
     CK(cudaMemsetAsync((void*)h->va, 0xFF, (size_t)h->nb_min * SLOTS * 8, s));
+    CK(cudaMemsetAsync((void*)h->sp.va, 0, (size_t)h->nb_min * sizeof(uint64_t), s));
     CK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), s));
     CKS(stash_reset(h, h->stash_cap_for(h->nb_min), s));
     h->grows = h->shrinks = h->merge_aborts = 0;
@@ -613,6 +617,7 @@ hive_status hive_destroy(hive_t h) {
     vrange_free(h->rg);
     vrange_free(h->ix);
     vrange_free(h->dr);
+    vrange_free(h->sp);
     void* bufs[] = {h->ctrl, h->dd, h->owner, h->flag, h->left, h->cls, h->cnt, h->pinfo, h->aborts};
     for (void* b : bufs)
         if (b) cudaFree(b);
@@ -727,6 +732,7 @@ hive_status hive_stats(hive_t h, hive_stats_t* o) {
     o->failed = c.failed;
     o->in_b1 = c.in_b1;
     o->mapped_bytes = h->bk.mapped;
+    for (int i = 0; i < 8; ++i) o->alg_bytes[i] = c.abytes[i];
     return c.failed ? HIVE_ESTASHFULL : HIVE_OK;
 }
 

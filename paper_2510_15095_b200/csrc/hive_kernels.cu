@@ -145,7 +145,7 @@ __device__ __forceinline__ void fill_empty(uint64_t (&s)[SPL]) {
 template <int G>
 __device__ __forceinline__ bool wcme_cas(const WarpGroup<G>& wg, uint64_t (&s)[WarpGroup<G>::SPL],
                                          uint64_t* bucket, uint32_t k, uint64_t newkv,
-                                         bool valid) {
+                                         bool valid, unsigned long long& ab) {
     constexpr int SPL = WarpGroup<G>::SPL;
     bool trying = valid, done = false;
     for (int iter = 0; iter <= SLOTS; ++iter) {
@@ -158,6 +158,7 @@ __device__ __forceinline__ bool wcme_cas(const WarpGroup<G>& wg, uint64_t (&s)[W
             const int j = __ffs(mm) - 1;
             const uint64_t old = pick<SPL>(s, j);
             const uint64_t prev = cas64(wg.slot_ptr(bucket) + j, old, newkv);
+            ab += 32;
             ok = (prev == old);
             if (!ok) put<SPL>(s, j, prev);
         }
@@ -176,7 +177,8 @@ __device__ __forceinline__ bool wcme_cas(const WarpGroup<G>& wg, uint64_t (&s)[W
 // CAS marks that slot taken in the view and the group re-elects.
 template <int G>
 __device__ __forceinline__ bool wabc_claim(const WarpGroup<G>& wg, uint64_t (&s)[WarpGroup<G>::SPL],
-                                           uint64_t* bucket, uint64_t kv, bool want) {
+                                           uint64_t* bucket, uint64_t kv, bool want,
+                                           unsigned long long& ab) {
     constexpr int SPL = WarpGroup<G>::SPL;
     bool trying = want, placed = false;
     for (int iter = 0; iter <= SLOTS; ++iter) {
@@ -188,6 +190,7 @@ __device__ __forceinline__ bool wabc_claim(const WarpGroup<G>& wg, uint64_t (&s)
         if (trying && wg.gl == __ffs(F) - 1) {
             const int j = __ffs(fm) - 1;
             const uint64_t prev = cas64(wg.slot_ptr(bucket) + j, EMPTY, kv);
+            ab += 32;
             ok = (prev == EMPTY);
             if (!ok) put<SPL>(s, j, prev);
         }
@@ -218,8 +221,8 @@ __device__ __forceinline__ bool wcme_value(const WarpGroup<G>& wg, const uint64_
 // FIND: WCME on b1, then b2 only on a miss, then the stash
 // index only when the stash is non-empty.  Read-only phase.
 // --------------------------------------------------------------------------------
-template <int G>
-__global__ void __launch_bounds__(BLOCK)
+template <int G, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
 k_find(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
        const uint64_t* __restrict__ n_dev, TableView tv, StashView sv,
        uint32_t* __restrict__ vals_out, uint8_t* __restrict__ found_out) {
@@ -228,12 +231,13 @@ k_find(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint
     WG wg;
     if (n_dev) n = *n_dev;
     const bool stash_on = sv.ctrl->stash_tail != 0;
+    unsigned long long ab = 0;
     const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
     for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
         const uint64_t t = t0 + wg.gi;
         const bool active = t < n;
-        const uint64_t op = active ? (idx ? (uint64_t)idx[t] : t) : 0;
+        const uint32_t op = active ? (idx ? idx[t] : (uint32_t)t) : 0u;   // < 2^32 (API)
         const uint32_t k = active ? keys[op] : INVALID_KEY;
         const bool valid = k != INVALID_KEY;
         uint32_t b1 = 0, b2 = 0;
@@ -242,27 +246,38 @@ k_find(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint
             b2 = tv.addr(bithash2(k));
         }
         uint64_t s[SPL];
-        if (valid) load_slots_ro<SPL>(wg.slot_ptr(tv.bucket(b1)), s);
-        else fill_empty<SPL>(s);
+        uint64_t spill_w = 0;
+        if (valid) {
+            load_slots_ro<SPL>(wg.slot_ptr(tv.bucket(b1)), s);
+            spill_w = __ldg((const unsigned long long*)&tv.spill[b1]);
+        } else {
+            fill_empty<SPL>(s);
+        }
         uint32_t val = 0;
         bool found = wcme_value<G>(wg, s, k, valid, &val);
-        const bool need2 = valid && !found && b2 != b1;
+        // beyond b1 only if b1's spill word allows k to live elsewhere
+        const bool maybe = valid && !found && (spill_w & spill_fp(k)) == spill_fp(k);
+        const bool need2 = maybe && b2 != b1;
         if (__any_sync(FULL, need2)) {
             if (need2) load_slots_ro<SPL>(wg.slot_ptr(tv.bucket(b2)), s);
             found |= wcme_value<G>(wg, s, k, need2, &val);
         }
-        if (stash_on && valid && !found && wg.gl == 0) {
+        if (stash_on && maybe && !found && wg.gl == 0) {
             uint64_t sw;
             if (stash_lookup(sv, k, &sw) >= 0) {
                 found = true;
                 val = val_of(sw);
             }
+            ab += 16;
         }
+        if (active && wg.gl == 0)
+            ab += 8 + (found_out ? 1 : 0) + (valid ? 256 + 8 : 0) + (need2 ? 256 : 0);
         if (active && wg.gl == 0) {
             vals_out[op] = found ? val : 0u;
             if (found_out) found_out[op] = found ? 1 : 0;
         }
     }
+    block_add(&sv.ctrl->abytes[AB_FIND], ab);
 }
 
 // --------------------------------------------------------------------------------
@@ -276,8 +291,9 @@ k_find(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint
 // --------------------------------------------------------------------------------
 __global__ void __launch_bounds__(BLOCK)
 k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
-              const uint64_t* __restrict__ n_dev, DedupView dd) {
+              const uint64_t* __restrict__ n_dev, DedupView dd, Ctrl* ctrl) {
     if (n_dev) n = *n_dev;
+    unsigned long long ab = 0;
     const int lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
     for (uint64_t t0 = (uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u); t0 < n; t0 += stride) {
@@ -286,6 +302,7 @@ k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ id
         const uint64_t op = active ? (idx ? (uint64_t)idx[t] : t) : 0;
         const uint32_t k = active ? keys[op] : INVALID_KEY;
         const uint32_t grp = __match_any_sync(FULL, k);
+        if (active) ab += 4 + (idx ? 4 : 0);
         if (k == INVALID_KEY) continue;
         if (__popc(grp) > 1) dd.flag[op] = 1;
         if ((31 - __clz(grp)) != lane) continue;
@@ -293,6 +310,7 @@ k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ id
         uint64_t h = fmix32(k ^ DEDUP_SEED) & dd.mask;
         for (uint64_t probe = 0; probe <= dd.mask; ++probe) {
             const uint64_t prev = cas64(&dd.slots[h], EMPTY, word);
+            ab += 32;
             if (prev == EMPTY) break;
             if ((uint32_t)(prev >> 32) == k) {
                 dd.flag[op] = 1;
@@ -303,6 +321,7 @@ k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ id
             h = (h + 1) & dd.mask;
         }
     }
+    block_add(&ctrl->abytes[AB_ELECT], ab);
 }
 
 __device__ __forceinline__ uint32_t dedup_owner(const DedupView& dd, uint32_t k, uint32_t self) {
@@ -319,26 +338,25 @@ __device__ __forceinline__ uint32_t dedup_owner(const DedupView& dd, uint32_t k,
 // Owner check of one group (all lanes call): only flagged ops probe the table.
 template <int G>
 __device__ __forceinline__ bool owns(const WarpGroup<G>& wg, const DedupView& dd, bool valid,
-                                     uint32_t k, uint64_t op) {
+                                     uint32_t k, uint32_t op, unsigned long long& ab) {
     if (!dd.slots) return true;
     uint32_t owner = (uint32_t)op;
-    if (valid && wg.gl == 0 && dd.flag[op]) {
-        owner = dedup_owner(dd, k, (uint32_t)op);
-        dd.owner_of[op] = owner;
+    if (valid && wg.gl == 0) {
+        ab += 1;
+        if (dd.flag[op]) {
+            owner = dedup_owner(dd, k, op);
+            dd.owner_of[op] = owner;
+            ab += 8 + 4;
+        }
     }
-    return wg.bcast(owner, 0) == (uint32_t)op;
+    return wg.bcast(owner, 0) == op;
 }
 
 // --------------------------------------------------------------------------------
 // INSERT fast path: Step 1 (replace) + Step 2 (claim-and-commit,
 // PAPER:348-381) in one pass; ops whose candidate buckets are both full go to
-// the leftover list for Steps 3-4.
-//
-// The b2 probe is speculative — issued together with b1 — while the warp's
-// observed rate of Step-1 hits in b1 stays below 1/4 (a new key must read both
-// buckets anyway, so this only removes a dependent round trip); once a batch
-// looks replace-heavy the warp switches to the bytes-optimal lazy order of the
-// paper (b2 only after a miss in b1).
+// the leftover list for Steps 3-4.  The spill filter decides whether Step 1
+// must look beyond b1; Step 2 reads b2 only when b1 is full.
 //
 // `kvs != nullptr` = place-only mode used to reinsert drained stash entries
 // after a resize: Step 1 is skipped (those keys are in no bucket)
@@ -359,14 +377,13 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     if (n_dev) n = *n_dev;
     const bool place_only = kvs != nullptr;
     const bool stash_on = !place_only && sv.ctrl->stash_tail != 0;
-    unsigned long long added = 0;
-    uint32_t seen = 0, hits1 = 0;              // warp-uniform replace-rate estimate
+    unsigned long long added = 0, ab = 0;
     const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
     for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
         const uint64_t t = t0 + wg.gi;
         const bool active = t < n;
-        uint64_t op = t;
+        uint32_t op = (uint32_t)t;                  // op indices < 2^32 (API contract)
         uint32_t k = INVALID_KEY, v = 0;
         if (active) {
             if (place_only) {
@@ -374,47 +391,60 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
                 k = key_of(w);
                 v = val_of(w);
             } else {
-                op = idx ? (uint64_t)idx[t] : t;
+                op = idx ? idx[t] : (uint32_t)t;
                 k = keys[op];
                 v = vals[op];
             }
         }
         bool valid = active && k != INVALID_KEY;
-        const bool spec = place_only || (hits1 * 4u <= seen);
         uint32_t b1 = 0, b2 = 0;
         if (valid) {
             b1 = tv.addr(bithash1(k));
             b2 = tv.addr(bithash2(k));
         }
         bool two = valid && b2 != b1;
+        const uint64_t fp = spill_fp(k);
         uint64_t s1[SPL], s2[SPL];
-        if (valid) load_slots<SPL>(wg.slot_ptr(tv.bucket(b1)), s1);
-        else fill_empty<SPL>(s1);
-        if (two && spec) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
-        else fill_empty<SPL>(s2);
-        if (!place_only && active && wg.gl == 0) {
-            if (vals_zero) vals_zero[op] = 0;
-            if (!valid && status) status[op] = 2;
+        uint64_t spill_w = 0;
+        if (valid) {
+            load_slots<SPL>(wg.slot_ptr(tv.bucket(b1)), s1);
+            spill_w = tv.spill[b1];
+        } else {
+            fill_empty<SPL>(s1);
+        }
+        fill_empty<SPL>(s2);
+        if (active && wg.gl == 0) {
+            ab += (place_only ? 8 : 8 + (status ? 1 : 0) + (vals_zero ? 4 : 0) + (idx ? 4 : 0)) +
+                  (valid ? 256 + 8 : 0);
+            if (!place_only) {
+                if (vals_zero) vals_zero[op] = 0;
+                if (!valid && status) status[op] = 2;
+            }
         }
         // owner election: duplicates copy the owner's outcome afterwards
-        if (!owns<G>(wg, dd, valid, k, op)) {
+        if (!owns<G>(wg, dd, valid, k, op, ab)) {
             valid = false;
             two = false;
         }
         const uint64_t kv = pack(k, v);
-        bool done = false;
+        bool done = false, have2 = false;
         if (!place_only) {
-            // Step 1 on b1, then b2, then the stash.
-            done = wcme_cas<G>(wg, s1, tv.bucket(b1), k, kv, valid);
-            const bool need2 = two && !done;
-            if (__any_sync(FULL, need2)) {                 // spec is warp-uniform
-                if (!spec && need2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
-                done |= wcme_cas<G>(wg, s2, tv.bucket(b2), k, kv, need2);
+            // Step 1: b1; then -- only if b1's spill word allows k to live
+            // elsewhere -- b2 and the stash.
+            done = wcme_cas<G>(wg, s1, tv.bucket(b1), k, kv, valid, ab);
+            const bool maybe = valid && !done && (spill_w & fp) == fp;
+            const bool need2 = two && maybe;
+            if (__any_sync(FULL, need2)) {
+                if (need2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
+                if (need2 && wg.gl == 0) ab += 256;
+                have2 = need2;
+                done |= wcme_cas<G>(wg, s2, tv.bucket(b2), k, kv, need2, ab);
             }
             if (stash_on) {
                 bool sdone = false;
-                if (valid && !done && wg.gl == 0) {
+                if (maybe && !done && wg.gl == 0) {
                     uint64_t sw;
+                    ab += 16;
                     int64_t pos = stash_lookup(sv, k, &sw);
                     while (pos >= 0) {
                         uint64_t prev = cas64(&sv.ring[pos], sw, kv);
@@ -424,26 +454,31 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
                 }
                 done |= wg.bcast(sdone, 0);
             }
-            const uint32_t vb = __ballot_sync(FULL, valid && wg.gl == 0);
-            seen += __popc(vb);
-            hits1 += __popc(vb & __ballot_sync(FULL, done));
         }
-        // Step 2: WABC claim in b1, then b2 (first-fit, A-21)
-        bool placed = wabc_claim<G>(wg, s1, tv.bucket(b1), kv, valid && !done);
+        // Step 2: WABC claim in b1, then b2 (first-fit, A-21); b2 is read only
+        // if b1 is full.
+        bool placed = wabc_claim<G>(wg, s1, tv.bucket(b1), kv, valid && !done, ab);
         const bool want2 = two && !done && !placed;
         if (__any_sync(FULL, want2)) {
-            if (place_only && !spec && want2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
-            placed |= wabc_claim<G>(wg, s2, tv.bucket(b2), kv, want2);
+            if (want2 && !have2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
+            if (want2 && !have2 && wg.gl == 0) ab += 256;
+            const bool p2 = wabc_claim<G>(wg, s2, tv.bucket(b2), kv, want2, ab);
+            if (p2 && wg.gl == 0) {
+                atomicOr((unsigned long long*)&tv.spill[b1], (unsigned long long)fp);
+                ab += 8;
+            }
+            placed |= p2;
         }
         const bool left = valid && !done && !placed;
         if (!place_only && valid && wg.gl == 0) {
             if (status) status[op] = done ? 1 : 0;
             if (!done) ++added;
         }
-        wl.push(left && wg.gl == 0, (uint32_t)(place_only ? t : op), leftover, &sv.ctrl->n_left);
+        wl.push(left && wg.gl == 0, op, leftover, &sv.ctrl->n_left);
     }
     wl.flush(leftover, &sv.ctrl->n_left);
     block_add(&sv.ctrl->count, added);
+    block_add(&sv.ctrl->abytes[AB_INSERT], ab);
 }
 
 // --------------------------------------------------------------------------------
@@ -464,7 +499,7 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     WG wg;
     const uint64_t n = sv.ctrl->n_left;
     if (!kvs && blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(&sv.ctrl->leftovers, (unsigned long long)n);
-    unsigned long long evict = 0, depth = 0, pushes = 0, lost = 0;
+    unsigned long long evict = 0, depth = 0, pushes = 0, lost = 0, ab = 0;
     const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
     for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
@@ -483,8 +518,16 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             if (trying) load_slots<SPL>(wg.slot_ptr(tv.bucket(b)), s);
             else fill_empty<SPL>(s);
             if (trying) ++rounds;
-            bool placed = wabc_claim<G>(wg, s, tv.bucket(b), kv, trying);   // line 3
-            if (placed) trying = false;
+            if (trying && wg.gl == 0) ab += 256;
+            bool placed = wabc_claim<G>(wg, s, tv.bucket(b), kv, trying, ab);   // line 3
+            if (placed) {
+                trying = false;
+                const uint32_t hb = tv.addr(bithash1(key_of(kv)));
+                if (wg.gl == 0 && hb != b) {
+                    atomicOr((unsigned long long*)&tv.spill[hb], (unsigned long long)spill_fp(key_of(kv)));
+                    ab += 8;
+                }
+            }
             // Victim (lines 17-21): a rotating slot (reading A-6: any victim rule;
             // preferring residents in their second bucket raised p_h1 to 0.93 but
             // doubled evictions and grew the stash 5x -- a net loss).
@@ -494,23 +537,35 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             bool ok = false;
             if (trying && wg.gl == vl && victim != EMPTY) {
                 uint64_t prev = cas64(tv.bucket(b) + vs, victim, kv);
+                ab += 32;
                 ok = (prev == victim);
             }
             ok = wg.bcast(ok, vl);
             if (trying && ok) {
+                const uint32_t hb = tv.addr(bithash1(key_of(kv)));      // kv now lives in b
+                if (wg.gl == 0 && hb != b) {
+                    atomicOr((unsigned long long*)&tv.spill[hb], (unsigned long long)spill_fp(key_of(kv)));
+                    ab += 8;
+                }
                 kv = victim;                                 // line 33
                 b = tv.alt(key_of(kv), b);                   // line 34
                 if (wg.gl == 0) ++evict;
             }
         }
-        if (wg.gl == 0 && active) depth = rounds > depth ? rounds : depth;
+        if (wg.gl == 0 && active) {
+            depth = rounds > depth ? rounds : depth;
+            ab += 4 + 8;
+        }
         // Step 4: stash push of the in-hand entry
         if (trying && wg.gl == 0) {
             unsigned long long pos = atomicAdd(&sv.ctrl->stash_tail, 1ull);
             if (pos < sv.cap) {
+                atomicOr((unsigned long long*)&tv.spill[tv.addr(bithash1(key_of(kv)))],
+                         (unsigned long long)spill_fp(key_of(kv)));
                 sv.ring[pos] = kv;
                 stash_index_put(sv, key_of(kv), pos);
                 ++pushes;
+                ab += 8 + 8 + 8;
             } else {
                 ++lost;
                 if (status && !kvs) status[item] = 3;
@@ -522,6 +577,7 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     block_add(&sv.ctrl->failed, lost);
     block_add(&sv.ctrl->count, (unsigned long long)(0ull - lost));
     block_max(&sv.ctrl->max_depth, depth);
+    block_add(&sv.ctrl->abytes[AB_EVICT], ab);
 }
 
 // --------------------------------------------------------------------------------
@@ -538,13 +594,13 @@ k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uin
     WG wg;
     if (n_dev) n = *n_dev;
     const bool stash_on = sv.ctrl->stash_tail != 0;
-    unsigned long long removed = 0;
+    unsigned long long removed = 0, ab = 0;
     const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
     for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
         const uint64_t t = t0 + wg.gi;
         const bool active = t < n;
-        const uint64_t op = active ? (idx ? (uint64_t)idx[t] : t) : 0;
+        const uint32_t op = active ? (idx ? idx[t] : (uint32_t)t) : 0u;   // < 2^32 (API)
         const uint32_t k = active ? keys[op] : INVALID_KEY;
         bool valid = k != INVALID_KEY;
         uint32_t b1 = 0, b2 = 0;
@@ -553,20 +609,31 @@ k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uin
             b2 = tv.addr(bithash2(k));
         }
         uint64_t s[SPL];
-        if (valid) load_slots<SPL>(wg.slot_ptr(tv.bucket(b1)), s);
-        else fill_empty<SPL>(s);
-        if (active && wg.gl == 0 && vals_zero) vals_zero[op] = 0;
-        const bool owner = owns<G>(wg, dd, valid, k, op);
+        uint64_t spill_w = 0;
+        if (valid) {
+            load_slots<SPL>(wg.slot_ptr(tv.bucket(b1)), s);
+            spill_w = tv.spill[b1];
+        } else {
+            fill_empty<SPL>(s);
+        }
+        if (active && wg.gl == 0) {
+            if (vals_zero) vals_zero[op] = 0;
+            ab += 4 + (erased_out ? 1 : 0) + (vals_zero ? 4 : 0) + (idx ? 4 : 0) + (valid ? 256 + 8 : 0);
+        }
+        const bool owner = owns<G>(wg, dd, valid, k, op, ab);
         valid = valid && owner;
-        bool done = wcme_cas<G>(wg, s, tv.bucket(b1), k, EMPTY, valid);
-        const bool need2 = valid && !done && b2 != b1;
+        bool done = wcme_cas<G>(wg, s, tv.bucket(b1), k, EMPTY, valid, ab);
+        const bool maybe = valid && !done && (spill_w & spill_fp(k)) == spill_fp(k);
+        const bool need2 = maybe && b2 != b1;
         if (__any_sync(FULL, need2)) {
             if (need2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s);
             else fill_empty<SPL>(s);
-            done |= wcme_cas<G>(wg, s, tv.bucket(b2), k, EMPTY, need2);
+            if (need2 && wg.gl == 0) ab += 256;
+            done |= wcme_cas<G>(wg, s, tv.bucket(b2), k, EMPTY, need2, ab);
         }
-        if (stash_on && valid && !done && wg.gl == 0) {
+        if (stash_on && maybe && !done && wg.gl == 0) {
             uint64_t sw;
+            ab += 16;
             int64_t pos = stash_lookup(sv, k, &sw);
             while (pos >= 0) {
                 uint64_t prev = cas64(&sv.ring[pos], sw, EMPTY);
@@ -580,6 +647,7 @@ k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uin
         }
     }
     block_add(&sv.ctrl->count, 0ull - removed);
+    block_add(&sv.ctrl->abytes[AB_ERASE], ab);
 }
 
 // Duplicates copy their owner's outcome (PHASED contract, A-17).
@@ -628,6 +696,9 @@ k_split(TableView tv, uint32_t n_pairs, Ctrl* ctrl) {
         src[lane] = EMPTY;
     }
     if (lane >= n_movers) dst[lane] = EMPTY;                      // rest of the new bucket
+    // keys whose b1 was b_src may now have b1 = b_dst: the new bucket inherits
+    // the spill word (conservative)
+    if (lane == 0) tv.spill[b_dst] = tv.spill[b_src];
 }
 
 // Contraction, LIFO pairs t = 0..n_pairs-1 with
@@ -675,6 +746,7 @@ k_merge_apply(TableView tv, uint32_t n_pairs, const unsigned long long* abort_at
         dst[pos] = kv;
         src[lane] = EMPTY;
     }
+    if (lane == 0) tv.spill[b_dst] |= tv.spill[b_src];           // spill words merge
 }
 
 // --------------------------------------------------------------------------------
@@ -892,6 +964,28 @@ static int env_g(const char* name, int dflt) {
         }                                     \
     }
 
+#define HIVE_DISPATCH_GM8(g, mb, X)          \
+    if (mb >= 8) {                            \
+        switch (g) {                          \
+            case 2: X(2, 8); break;           \
+            case 4: X(4, 8); break;           \
+            default: X(8, 8); break;          \
+        }                                     \
+    } else if (mb >= 6) {                     \
+        switch (g) {                          \
+            case 2: X(2, 6); break;           \
+            case 4: X(4, 6); break;           \
+            default: X(8, 6); break;          \
+        }                                     \
+    } else {                                  \
+        switch (g) {                          \
+            case 1: X(1, 1); break;           \
+            case 2: X(2, 1); break;           \
+            case 4: X(4, 1); break;           \
+            default: X(8, 1); break;          \
+        }                                     \
+    }
+
 Grids query_grids(int num_sms) {
     Grids g;
     g.g_find = env_g("HIVE_G_FIND", G_FIND);
@@ -899,11 +993,12 @@ Grids query_grids(int num_sms) {
     g.g_slow = env_g("HIVE_G_SLOW", G_SLOW);
     g.g_erase = env_g("HIVE_G_ERASE", G_ERASE);
     g.minb = getenv("HIVE_MINB") ? atoi(getenv("HIVE_MINB")) : MINB_DEFAULT;
-#define OCC_FIND(G) g.find = occ((const void*)k_find<G>) * num_sms
+    g.minb_find = getenv("HIVE_MINB_FIND") ? atoi(getenv("HIVE_MINB_FIND")) : MINB_FIND_DEFAULT;
+#define OCC_FIND(G, MB) g.find = occ((const void*)k_find<G, MB>) * num_sms
 #define OCC_INS(G, MB) g.insert_fast = occ((const void*)k_insert_fast<G, MB>) * num_sms
 #define OCC_SLOW(G, MB) g.insert_slow = occ((const void*)k_insert_slow<G, MB>) * num_sms
 #define OCC_ERA(G, MB) g.erase = occ((const void*)k_erase<G, MB>) * num_sms
-    HIVE_DISPATCH_G(g.g_find, OCC_FIND)
+    HIVE_DISPATCH_GM8(g.g_find, g.minb_find, OCC_FIND)
     HIVE_DISPATCH_GM(g.g_insert, g.minb, OCC_INS)
     HIVE_DISPATCH_GM(g.g_slow, g.minb, OCC_SLOW)
     HIVE_DISPATCH_GM(g.g_erase, g.minb, OCC_ERA)
@@ -922,15 +1017,15 @@ cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, c
                         uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
                         uint32_t* vals_out, uint8_t* found) {
     const int grid = n_dev ? gr.find : clamp_grid(gr.find, n, BLOCK / gr.g_find);
-#define L_FIND(G) k_find<G><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, vals_out, found)
-    HIVE_DISPATCH_G(gr.g_find, L_FIND)
+#define L_FIND(G, MB) k_find<G, MB><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, vals_out, found)
+    HIVE_DISPATCH_GM8(gr.g_find, gr.minb_find, L_FIND)
     return cudaGetLastError();
 }
 
 cudaError_t launch_dedup_elect(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
-                               uint64_t n, const uint64_t* n_dev, DedupView dd) {
+                               uint64_t n, const uint64_t* n_dev, DedupView dd, Ctrl* ctrl) {
     if (!n_dev) grid = clamp_grid(grid, n, BLOCK);
-    k_dedup_elect<<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, dd);
+    k_dedup_elect<<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, dd, ctrl);
     return cudaGetLastError();
 }
 

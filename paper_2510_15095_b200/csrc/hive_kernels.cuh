@@ -13,6 +13,7 @@ constexpr int WARPS_PER_BLOCK = BLOCK / 32;
 // chosen by ncu measurement; HIVE_G_FIND / HIVE_G_INSERT / HIVE_G_ERASE /
 // HIVE_G_SLOW (1, 2, 4 or 8) override them for experiments.
 constexpr int G_FIND = 4, G_INSERT = 4, G_ERASE = 2, G_SLOW = 2;
+constexpr int MINB_FIND_DEFAULT = 6;           // 40 regs: 3.60 ms vs 3.79 (48 regs) vs 4.60 (32, spills)
 constexpr int MINB_DEFAULT = 4;          // 4 blocks/SM => <= 64 registers (ncu: 74-80 regs left 36% warps active)
 constexpr int PART_CHUNK = 2048;         // elements per warp in the stable partition
 constexpr int MAX_PARTS = 64;
@@ -23,6 +24,7 @@ struct Grids {                           // persistent grid sizes (blocks)
     int find, insert_fast, insert_slow, erase, dedup, stream;
     int g_find, g_insert, g_slow, g_erase;   // lanes per operation
     int minb;                                // min resident blocks/SM for the mutating kernels
+    int minb_find;                           // ... and for k_find
 };
 
 // Occupancy-derived persistent grid sizes for this device.
@@ -33,7 +35,7 @@ cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, c
                         uint32_t* vals_out, uint8_t* found);
 
 cudaError_t launch_dedup_elect(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
-                               uint64_t n, const uint64_t* n_dev, DedupView dd);
+                               uint64_t n, const uint64_t* n_dev, DedupView dd, Ctrl* ctrl);
 
 cudaError_t launch_insert_fast(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
                                const uint64_t* kvs, const uint32_t* idx, uint64_t n,

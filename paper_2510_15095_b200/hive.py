@@ -38,7 +38,8 @@ class HiveStats(ctypes.Structure):
     _fields_ = [("n_buckets", ctypes.c_uint64), ("m", ctypes.c_uint32), ("split", ctypes.c_uint32)] + [
         (n, ctypes.c_uint64) for n in (
             "count", "stash_used", "stash_cap", "evictions", "max_depth", "stash_pushes", "leftovers",
-            "grows", "shrinks", "merge_aborts", "failed", "in_b1", "mapped_bytes")]
+            "grows", "shrinks", "merge_aborts", "failed", "in_b1", "mapped_bytes")] + [
+        ("alg_bytes", ctypes.c_uint64 * 8)]
 
 
 # every exported symbol of include/hive.h, with its ctypes signature
@@ -233,7 +234,9 @@ class HiveTable:
         rc = self._L.hive_stats(self._h, ctypes.byref(s))
         if not (allow_failed and rc == 5):
             _check(rc, "hive_stats")
-        return {n: getattr(s, n) for n, _ in HiveStats._fields_}
+        d = {n: getattr(s, n) for n, _ in HiveStats._fields_}
+        d["alg_bytes"] = dict(zip(("find", "insert", "evict", "erase", "elect"), list(s.alg_bytes)[:5]))
+        return d
 
     def dump(self):
         n = ctypes.c_uint64()
