@@ -132,11 +132,21 @@ struct StashView {
 // per key wins (= the oracle's last write).  `flag[op]` is set only for ops
 // whose key occurs more than once in the phase, so only those consult the
 // table again (uniform batches pay the election pass alone).
+//
+// For large phases the table is split into n_parts L2-sized sub-tables of
+// mask + 1 entries; a key's sub-table is the top bits of its election hash and
+// its home slot the low bits, so each per-part election launch works on an
+// L2-resident sub-table.
 struct DedupView {
     uint64_t* slots;     // nullptr = election disabled (HIVE_KEYS_UNIQUE)
-    uint64_t mask;
+    uint64_t mask;       // sub-table size - 1
     uint8_t* flag;       // per op (indexed like the keys), zeroed per phase
     uint32_t* owner_of;  // per op, written for flagged ops only
+    uint32_t n_parts;    // sub-tables (power of two)
+    __device__ __forceinline__ uint64_t* sub(uint32_t h) const {
+        const uint32_t part = n_parts > 1 ? (uint32_t)(((uint64_t)h * n_parts) >> 32) : 0u;
+        return slots + (uint64_t)part * (mask + 1);
+    }
 };
 
 // ---- memory access -----------------------------------------------------------------

@@ -149,6 +149,9 @@ struct hive_table_s {
     uint64_t* dd = nullptr;   uint64_t dd_cap = 0;
     uint32_t* owner = nullptr; uint64_t owner_cap = 0;
     uint8_t* flag = nullptr;  uint64_t flag_cap = 0;
+    uint64_t* erec = nullptr; uint64_t erec_cap = 0;     // election records (op << 32 | key)
+    unsigned long long* ecount = nullptr;                // per-part counts + cursors
+    uint64_t* einfo = nullptr;                           // per-part totals / bases
     uint32_t* left = nullptr; uint64_t left_cap = 0;
     uint32_t* cls = nullptr;  uint64_t cls_cap = 0;
     uint64_t* cnt = nullptr;  uint64_t cnt_cap = 0;
@@ -334,15 +337,33 @@ hive_status stash_reset(hive_table_s* h, uint64_t cap, cudaStream_t s) {
 // ---- owner election for in-batch duplicates -------------------
 hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* idx, uint64_t n_upper,
                          const uint64_t* n_dev, uint64_t n_batch, DedupView* dd, cudaStream_t s) {
-    const uint64_t cap = pow2_at_least(std::max<uint64_t>(1024, 2 * n_upper));
-    CKS(ensure(h->dd, h->dd_cap, cap));
+    // Large phases: hash-partition the ops so that each part's sub-table
+    // (~32 MB) stays in L2 during its election launch (ncu: 18.5 G elections/s
+    // with a 1 GiB table vs 49 G/s L2-resident).
+    uint32_t parts = 1;
+    while (parts < 32 && 2 * n_upper * sizeof(uint64_t) / parts > (32ull << 20)) parts *= 2;
+    const uint64_t sub = pow2_at_least(std::max<uint64_t>(1024, parts == 1 ? 2 * n_upper
+                                                                          : (5 * n_upper / parts) / 2));
+    CKS(ensure(h->dd, h->dd_cap, sub * parts));
     CKS(ensure(h->owner, h->owner_cap, n_batch));
     CKS(ensure(h->flag, h->flag_cap, n_batch));
-    *dd = DedupView{h->dd, cap - 1, h->flag, h->owner};
-    CK(cudaMemsetAsync(h->dd, 0xFF, cap * sizeof(uint64_t), s));
+    *dd = DedupView{h->dd, sub - 1, h->flag, h->owner, parts};
+    CK(cudaMemsetAsync(h->dd, 0xFF, sub * parts * sizeof(uint64_t), s));
     CK(cudaMemsetAsync(h->flag, 0, n_batch, s));
+    if (parts == 1) {
+        Prof p(h, "k_dedup_elect", s);
+        CK(launch_dedup_elect(h->grids.dedup, s, keys, idx, n_upper, n_dev, *dd, h->ctrl));
+        return HIVE_OK;
+    }
+    CKS(ensure(h->erec, h->erec_cap, n_upper));
+    {
+        Prof p(h, "k_elect_partition", s);
+        CK(launch_elect_partition(s, keys, idx, n_upper, n_dev, parts, h->ecount, h->ecount + MAX_PARTS,
+                                  h->einfo, h->erec, h->num_sms));
+    }
     Prof p(h, "k_dedup_elect", s);
-    CK(launch_dedup_elect(h->grids.dedup, s, keys, idx, n_upper, n_dev, *dd, h->ctrl));
+    for (uint32_t q = 0; q < parts; ++q)
+        CK(launch_dedup_elect_part(h->grids.dedup, s, h->erec, h->einfo, q, *dd, h->ctrl));
     return HIVE_OK;
 }
 
@@ -585,6 +606,9 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     if (cudaMallocHost((void**)&h->stage_h, (8 + MAX_SEGMENTS) * sizeof(uint64_t)) != cudaSuccess)
         return fail(HIVE_ENOMEM);
     if (cudaMalloc((void**)&h->pinfo, 2 * MAX_PARTS * sizeof(uint64_t)) != cudaSuccess) return fail(HIVE_ENOMEM);
+    if (cudaMalloc((void**)&h->einfo, 2 * MAX_PARTS * sizeof(uint64_t)) != cudaSuccess) return fail(HIVE_ENOMEM);
+    if (cudaMalloc((void**)&h->ecount, 2 * MAX_PARTS * sizeof(unsigned long long)) != cudaSuccess)
+        return fail(HIVE_ENOMEM);
     if (cudaMalloc((void**)&h->aborts, MAX_SEGMENTS * sizeof(unsigned long long)) != cudaSuccess)
         return fail(HIVE_ENOMEM);
     memset(h->ctrl_h, 0, sizeof(Ctrl));
@@ -618,7 +642,8 @@ hive_status hive_destroy(hive_t h) {
     vrange_free(h->ix);
     vrange_free(h->dr);
     vrange_free(h->sp);
-    void* bufs[] = {h->ctrl, h->dd, h->owner, h->flag, h->left, h->cls, h->cnt, h->pinfo, h->aborts};
+    void* bufs[] = {h->ctrl, h->dd, h->owner, h->flag, h->left, h->cls, h->cnt, h->pinfo, h->aborts,
+                    h->erec, h->ecount, h->einfo};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (h->ctrl_h) cudaFreeHost(h->ctrl_h);

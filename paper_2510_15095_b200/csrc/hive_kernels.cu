@@ -7,6 +7,7 @@
 // lane), so each warp keeps four independent bucket probes in flight.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "hive_kernels.cuh"
@@ -307,15 +308,17 @@ k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ id
         if (__popc(grp) > 1) dd.flag[op] = 1;
         if ((31 - __clz(grp)) != lane) continue;
         const uint64_t word = ((uint64_t)k << 32) | op;
-        uint64_t h = fmix32(k ^ DEDUP_SEED) & dd.mask;
+        const uint32_t hk = fmix32(k ^ DEDUP_SEED);
+        uint64_t* tab = dd.sub(hk);
+        uint64_t h = hk & dd.mask;
         for (uint64_t probe = 0; probe <= dd.mask; ++probe) {
-            const uint64_t prev = cas64(&dd.slots[h], EMPTY, word);
+            const uint64_t prev = cas64(&tab[h], EMPTY, word);
             ab += 32;
             if (prev == EMPTY) break;
             if ((uint32_t)(prev >> 32) == k) {
                 dd.flag[op] = 1;
                 dd.flag[(uint32_t)prev] = 1;
-                if (word > prev) atomicMax((unsigned long long*)&dd.slots[h], (unsigned long long)word);
+                if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
                 break;
             }
             h = (h + 1) & dd.mask;
@@ -324,10 +327,144 @@ k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ id
     block_add(&ctrl->abytes[AB_ELECT], ab);
 }
 
+// Election over one part of a hash-partitioned phase: input = the part's
+// (op << 32 | key) records in op order (stable partition), sub-table L2-resident.
+__global__ void __launch_bounds__(BLOCK)
+k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict__ part_info, uint32_t part,
+                   DedupView dd, Ctrl* ctrl) {
+    const uint64_t n = part_info[part];
+    const uint64_t base = part_info[MAX_PARTS + part];
+    const int lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
+    unsigned long long ab = 0;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u); t0 < n; t0 += stride) {
+        const uint64_t t = t0 + lane;
+        const bool active = t < n;
+        const uint64_t w = active ? recs[base + t] : EMPTY;
+        const uint32_t k = (uint32_t)w, op = (uint32_t)(w >> 32);
+        const uint32_t grp = __match_any_sync(FULL, k);
+        if (active) ab += 8;
+        if (!active) continue;
+        // input order inside a warp is arbitrary here: elect the max op of the
+        // lanes holding the same key
+        uint32_t mx = op;
+        if (__popc(grp) > 1) {
+            dd.flag[op] = 1;
+            mx = __reduce_max_sync(grp, op);
+        }
+        if (op != mx) continue;
+        const uint64_t word = ((uint64_t)k << 32) | op;
+        const uint32_t hk = fmix32(k ^ DEDUP_SEED);
+        uint64_t* tab = dd.sub(hk);
+        uint64_t h = hk & dd.mask;
+        for (uint64_t probe = 0; probe <= dd.mask; ++probe) {
+            const uint64_t prev = cas64(&tab[h], EMPTY, word);
+            ab += 32;
+            if (prev == EMPTY) break;
+            if ((uint32_t)(prev >> 32) == k) {
+                dd.flag[op] = 1;
+                dd.flag[(uint32_t)prev] = 1;
+                if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
+                break;
+            }
+            h = (h + 1) & dd.mask;
+        }
+    }
+    block_add(&ctrl->abytes[AB_ELECT], ab);
+}
+
+// Hash partition of one phase's ops for the election (order inside a part is
+// arbitrary; the election is order-free): pass 1 per-block histograms,
+// pass 2 per-part bases, pass 3 a 4096-op tile per block written part by part
+// at a per-block reservation (runs of ~4096/P contiguous records).
+constexpr int ETILE = 4096;
+__device__ __forceinline__ uint32_t elect_part(uint32_t k, uint32_t n_parts) {
+    return (uint32_t)(((uint64_t)fmix32(k ^ DEDUP_SEED) * (uint64_t)n_parts) >> 32);
+}
+__global__ void __launch_bounds__(BLOCK)
+k_elect_hist(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
+             const uint64_t* __restrict__ n_dev, uint32_t n_parts, unsigned long long* __restrict__ gcount) {
+    __shared__ unsigned int hist[MAX_PARTS];
+    if (n_dev) n = *n_dev;
+    for (int p = threadIdx.x; p < MAX_PARTS; p += BLOCK) hist[p] = 0;
+    __syncthreads();
+    for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (uint64_t)gridDim.x * BLOCK) {
+        const uint32_t k = keys[idx ? idx[i] : i];
+        if (k != INVALID_KEY) atomicAdd(&hist[elect_part(k, n_parts)], 1u);
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < (int)n_parts; p += BLOCK)
+        if (hist[p]) atomicAdd(&gcount[p], (unsigned long long)hist[p]);
+}
+__global__ void k_elect_bases(const unsigned long long* __restrict__ gcount, uint32_t n_parts,
+                              uint64_t* __restrict__ part_info, unsigned long long* __restrict__ cursor) {
+    if (threadIdx.x != 0) return;
+    uint64_t run = 0;
+    for (uint32_t p = 0; p < n_parts; ++p) {
+        part_info[p] = gcount[p];
+        part_info[MAX_PARTS + p] = run;
+        cursor[p] = run;
+        run += gcount[p];
+    }
+}
+__global__ void __launch_bounds__(BLOCK)
+k_elect_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
+                const uint64_t* __restrict__ n_dev, uint32_t n_parts, unsigned long long* __restrict__ cursor,
+                uint64_t* __restrict__ recs) {
+    __shared__ unsigned int hist[MAX_PARTS];
+    __shared__ unsigned long long gbase[MAX_PARTS];
+    if (n_dev) n = *n_dev;
+    constexpr int PER = ETILE / BLOCK;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * ETILE; t0 < n; t0 += (uint64_t)gridDim.x * ETILE) {
+        for (int p = threadIdx.x; p < MAX_PARTS; p += BLOCK) hist[p] = 0;
+        __syncthreads();
+        uint64_t rec[PER];
+        uint32_t part[PER], rank[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const uint64_t i = t0 + (uint64_t)j * BLOCK + threadIdx.x;
+            part[j] = MAX_PARTS;
+            if (i < n) {
+                const uint32_t op = idx ? idx[i] : (uint32_t)i;
+                const uint32_t k = keys[op];
+                if (k != INVALID_KEY) {
+                    part[j] = elect_part(k, n_parts);
+                    rec[j] = ((uint64_t)op << 32) | k;
+                    rank[j] = atomicAdd(&hist[part[j]], 1u);
+                }
+            }
+        }
+        __syncthreads();
+        for (int p = threadIdx.x; p < (int)n_parts; p += BLOCK)
+            gbase[p] = hist[p] ? atomicAdd(&cursor[p], (unsigned long long)hist[p]) : 0ull;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if (part[j] < MAX_PARTS) recs[gbase[part[j]] + rank[j]] = rec[j];
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_elect_partition(cudaStream_t s, const uint32_t* keys, const uint32_t* idx, uint64_t n,
+                                   const uint64_t* n_dev, uint32_t n_parts, unsigned long long* gcount,
+                                   unsigned long long* cursor, uint64_t* part_info, uint64_t* recs,
+                                   int num_sms) {
+    cudaError_t e = cudaMemsetAsync(gcount, 0, MAX_PARTS * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    const int grid_h = (int)std::min<uint64_t>((n + BLOCK - 1) / BLOCK, (uint64_t)num_sms * 8);
+    k_elect_hist<<<grid_h, BLOCK, 0, s>>>(keys, idx, n, n_dev, n_parts, gcount);
+    k_elect_bases<<<1, 32, 0, s>>>(gcount, n_parts, part_info, cursor);
+    const int grid_s = (int)std::min<uint64_t>((n + ETILE - 1) / ETILE, (uint64_t)num_sms * 8);
+    k_elect_scatter<<<grid_s, BLOCK, 0, s>>>(keys, idx, n, n_dev, n_parts, cursor, recs);
+    return cudaGetLastError();
+}
+
 __device__ __forceinline__ uint32_t dedup_owner(const DedupView& dd, uint32_t k, uint32_t self) {
-    uint64_t h = fmix32(k ^ DEDUP_SEED) & dd.mask;
+    const uint32_t hk = fmix32(k ^ DEDUP_SEED);
+    const uint64_t* tab = dd.sub(hk);
+    uint64_t h = hk & dd.mask;
     for (uint64_t probe = 0; probe <= dd.mask; ++probe) {
-        uint64_t e = dd.slots[h];
+        uint64_t e = tab[h];
         if (e == EMPTY) return self;
         if ((uint32_t)(e >> 32) == k) return (uint32_t)e;
         h = (h + 1) & dd.mask;
@@ -794,6 +931,11 @@ __device__ __forceinline__ uint32_t part_of(int mode, uint32_t n_parts, uint32_t
         const uint32_t o = ops[i];
         return o < 3 ? o : 3u;
     }
+    if (mode == PART_ELECT) {                    // election sub-table of the key
+        const uint32_t k = keys[i];
+        if (k == INVALID_KEY) return MAX_PARTS;
+        return (uint32_t)(((uint64_t)fmix32(k ^ DEDUP_SEED) * (uint64_t)n_parts) >> 32);
+    }
     // shard(k) = (fmix32(k ^ seed) * G) >> 32
     return (uint32_t)(((uint64_t)fmix32(keys[i] ^ seed) * (uint64_t)n_parts) >> 32);
 }
@@ -802,7 +944,9 @@ __device__ __forceinline__ uint32_t part_of(int mode, uint32_t n_parts, uint32_t
 __global__ void __launch_bounds__(BLOCK)
 k_part_count(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __restrict__ keys,
              const uint8_t* __restrict__ ops, uint64_t n, uint64_t n_warps,
-             uint64_t* __restrict__ cnt) {
+             uint64_t* __restrict__ cnt, const uint32_t* __restrict__ idx,
+             const uint64_t* __restrict__ n_dev) {
+    if (n_dev) n = *n_dev;
     __shared__ uint32_t sc[WARPS_PER_BLOCK][MAX_PARTS + 1];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t w = (uint64_t)blockIdx.x * WARPS_PER_BLOCK + wib;
@@ -810,10 +954,11 @@ k_part_count(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __restri
     __syncwarp();
     if (w < n_warps) {
         const uint64_t lo = w * PART_CHUNK;
-        const uint64_t hi = lo + PART_CHUNK < n ? lo + PART_CHUNK : n;
+        const uint64_t hi = lo + PART_CHUNK < n ? lo + PART_CHUNK : (lo < n ? n : lo);
         for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
             const uint64_t i = i0 + lane;
-            const uint32_t p = i < hi ? part_of(mode, n_parts, seed, keys, ops, i) : MAX_PARTS;
+            const uint64_t e = i < hi ? (idx ? (uint64_t)idx[i] : i) : 0;
+            const uint32_t p = i < hi ? part_of(mode, n_parts, seed, keys, ops, e) : MAX_PARTS;
             const uint32_t grp = __match_any_sync(FULL, p);
             if ((__ffs(grp) - 1) == lane) sc[wib][p] += __popc(grp);
             __syncwarp();
@@ -822,33 +967,45 @@ k_part_count(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __restri
     }
 }
 
-// Pass 2: exclusive scan over cnt (single block); part_info[p] = total of part
-// p, part_info[MAX_PARTS + p] = global start of part p.
+// Pass 2: exclusive scan over cnt (single block, coalesced 1024-element tiles,
+// warp-shuffle scans); part_info[p] = total of part p,
+// part_info[MAX_PARTS + p] = global start of part p.
 __global__ void __launch_bounds__(1024)
 k_part_scan(uint64_t* __restrict__ cnt, uint64_t E, uint32_t n_parts, uint64_t n_warps,
             uint64_t* __restrict__ part_info) {
-    __shared__ uint64_t ssum[1024];
-    const int tid = threadIdx.x;
-    const uint64_t per = (E + 1023) / 1024;
-    const uint64_t lo = tid * per, hi = (lo + per < E) ? lo + per : E;
-    uint64_t s = 0;
-    for (uint64_t i = lo; i < hi; ++i) s += cnt[i];
-    ssum[tid] = s;
+    __shared__ uint64_t wsum[32];
+    __shared__ uint64_t carry;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) carry = 0;
     __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-        uint64_t v = tid >= off ? ssum[tid - off] : 0;
+    for (uint64_t base = 0; base < E; base += 1024) {
+        const uint64_t i = base + tid;
+        const uint64_t v = i < E ? cnt[i] : 0;
+        uint64_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[wid] = x;
         __syncthreads();
-        ssum[tid] += v;
+        if (wid == 0) {
+            uint64_t w = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t y = __shfl_up_sync(FULL, w, o);
+                if (lane >= o) w += y;
+            }
+            wsum[lane] = w;
+        }
+        __syncthreads();
+        const uint64_t c = carry;
+        if (i < E) cnt[i] = c + (wid ? wsum[wid - 1] : 0) + x - v;
+        __syncthreads();
+        if (tid == 0) carry = c + wsum[31];
         __syncthreads();
     }
-    uint64_t run = ssum[tid] - s;      // exclusive prefix of this segment
-    for (uint64_t i = lo; i < hi; ++i) {
-        uint64_t c = cnt[i];
-        cnt[i] = run;
-        run += c;
-    }
-    __syncthreads();
-    const uint64_t total = ssum[1023];
+    const uint64_t total = carry;
     if (tid < (int)n_parts) {
         const uint64_t start = n_warps ? cnt[(uint64_t)tid * n_warps] : 0;
         const uint64_t end = (tid + 1 < (int)n_parts) ? cnt[(uint64_t)(tid + 1) * n_warps] : total;
@@ -867,19 +1024,22 @@ k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __rest
                const uint64_t* __restrict__ part_info, uint32_t* __restrict__ out_idx,
                uint64_t idx_stride, uint64_t* __restrict__ send_kv, uint8_t* __restrict__ send_ops,
                uint32_t* __restrict__ pos_out, uint8_t* __restrict__ result_zero,
-               uint32_t* __restrict__ vals_zero) {
+               uint32_t* __restrict__ vals_zero, const uint32_t* __restrict__ idx,
+               const uint64_t* __restrict__ n_dev) {
     __shared__ uint64_t run[WARPS_PER_BLOCK][MAX_PARTS + 1];
+    if (n_dev) n = *n_dev;
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t w = (uint64_t)blockIdx.x * WARPS_PER_BLOCK + wib;
     if (w >= n_warps) return;
     for (uint32_t p = lane; p < n_parts; p += 32) run[wib][p] = off[(uint64_t)p * n_warps + w];
     __syncwarp();
     const uint64_t lo = w * PART_CHUNK;
-    const uint64_t hi = lo + PART_CHUNK < n ? lo + PART_CHUNK : n;
+    const uint64_t hi = lo + PART_CHUNK < n ? lo + PART_CHUNK : (lo < n ? n : lo);
     for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
         const uint64_t i = i0 + lane;
         const bool in = i < hi;
-        const uint32_t p = in ? part_of(mode, n_parts, seed, keys, ops, i) : MAX_PARTS;
+        const uint64_t e = in ? (idx ? (uint64_t)idx[i] : i) : 0;
+        const uint32_t p = in ? part_of(mode, n_parts, seed, keys, ops, e) : MAX_PARTS;
         const uint32_t grp = __match_any_sync(FULL, p);
         const uint32_t rank = __popc(grp & lanemask_lt());
         uint64_t pos = 0;
@@ -888,7 +1048,9 @@ k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __rest
         if (in && p < n_parts && (__ffs(grp) - 1) == lane) run[wib][p] += __popc(grp);
         __syncwarp();
         if (!in) continue;
-        if (mode == PART_CLASSIFY) {
+        if (mode == PART_ELECT) {
+            if (p < n_parts) send_kv[pos] = (e << 32) | keys[e];
+        } else if (mode == PART_CLASSIFY) {
             if (p < n_parts) {
                 out_idx[(uint64_t)p * idx_stride + (pos - part_info[MAX_PARTS + p])] = (uint32_t)i;
             } else {
@@ -936,7 +1098,7 @@ static int env_g(const char* name, int dflt) {
     const char* e = getenv(name);
     if (!e) return dflt;
     const int g = atoi(e);
-    return (g == 1 || g == 2 || g == 4 || g == 8) ? g : dflt;
+    return (g == 2 || g == 4 || g == 8) ? g : dflt;
 }
 
 #define HIVE_DISPATCH_G(g, X) \
@@ -947,22 +1109,17 @@ static int env_g(const char* name, int dflt) {
         default: X(8); break; \
     }
 
-#define HIVE_DISPATCH_GM(g, mb, X)           \
-    if (mb >= 4) {                            \
-        switch (g) {                          \
-            case 1: X(1, 4); break;           \
-            case 2: X(2, 4); break;           \
-            case 4: X(4, 4); break;           \
-            default: X(8, 4); break;          \
-        }                                     \
-    } else {                                  \
-        switch (g) {                          \
-            case 1: X(1, 1); break;           \
-            case 2: X(2, 1); break;           \
-            case 4: X(4, 1); break;           \
-            default: X(8, 1); break;          \
-        }                                     \
+#define HIVE_SWITCH_G(g, mb, X) \
+    switch (g) {                  \
+        case 2: X(2, mb); break;  \
+        case 4: X(4, mb); break;  \
+        default: X(8, mb); break; \
     }
+#define HIVE_DISPATCH_GM(g, mb, X)                     \
+    if (mb >= 6) { HIVE_SWITCH_G(g, 6, X) }             \
+    else if (mb == 5) { HIVE_SWITCH_G(g, 5, X) }        \
+    else if (mb >= 4) { HIVE_SWITCH_G(g, 4, X) }        \
+    else { HIVE_SWITCH_G(g, 1, X) }
 
 #define HIVE_DISPATCH_GM8(g, mb, X)          \
     if (mb >= 8) {                            \
@@ -979,7 +1136,6 @@ static int env_g(const char* name, int dflt) {
         }                                     \
     } else {                                  \
         switch (g) {                          \
-            case 1: X(1, 1); break;           \
             case 2: X(2, 1); break;           \
             case 4: X(4, 1); break;           \
             default: X(8, 1); break;          \
@@ -1019,6 +1175,12 @@ cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, c
     const int grid = n_dev ? gr.find : clamp_grid(gr.find, n, BLOCK / gr.g_find);
 #define L_FIND(G, MB) k_find<G, MB><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, vals_out, found)
     HIVE_DISPATCH_GM8(gr.g_find, gr.minb_find, L_FIND)
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dedup_elect_part(int grid, cudaStream_t s, const uint64_t* recs, const uint64_t* part_info,
+                                    uint32_t part, DedupView dd, Ctrl* ctrl) {
+    k_dedup_elect_part<<<grid, BLOCK, 0, s>>>(recs, part_info, part, dd, ctrl);
     return cudaGetLastError();
 }
 
@@ -1100,15 +1262,15 @@ cudaError_t launch_partition(cudaStream_t s, int mode, uint32_t n_parts, uint32_
                              uint64_t n, uint64_t* cnt, uint64_t* part_info,
                              uint32_t* out_idx, uint64_t idx_stride, uint64_t* send_kv,
                              uint8_t* send_ops, uint32_t* pos, uint8_t* result_zero,
-                             uint32_t* vals_zero) {
+                             uint32_t* vals_zero, const uint32_t* idx, const uint64_t* n_dev) {
     const uint64_t nw = part_warps(n);
     const int grid = (int)((nw + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK);
-    if (nw) k_part_count<<<grid, BLOCK, 0, s>>>(mode, n_parts, seed, keys, ops, n, nw, cnt);
+    if (nw) k_part_count<<<grid, BLOCK, 0, s>>>(mode, n_parts, seed, keys, ops, n, nw, cnt, idx, n_dev);
     k_part_scan<<<1, 1024, 0, s>>>(cnt, (uint64_t)n_parts * nw, n_parts, nw, part_info);
     if (nw)
         k_part_scatter<<<grid, BLOCK, 0, s>>>(mode, n_parts, seed, keys, vals, ops, n, nw, cnt, part_info,
                                               out_idx, idx_stride, send_kv, send_ops, pos, result_zero,
-                                              vals_zero);
+                                              vals_zero, idx, n_dev);
     return cudaGetLastError();
 }
 

@@ -18,7 +18,7 @@ constexpr int MINB_DEFAULT = 4;          // 4 blocks/SM => <= 64 registers (ncu:
 constexpr int PART_CHUNK = 2048;         // elements per warp in the stable partition
 constexpr int MAX_PARTS = 64;
 
-enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1 };
+enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1, PART_ELECT = 2 };
 
 struct Grids {                           // persistent grid sizes (blocks)
     int find, insert_fast, insert_slow, erase, dedup, stream;
@@ -72,7 +72,14 @@ cudaError_t launch_partition(cudaStream_t s, int mode, uint32_t n_parts, uint32_
                              uint64_t n, uint64_t* cnt, uint64_t* part_info,
                              uint32_t* out_idx, uint64_t idx_stride, uint64_t* send_kv,
                              uint8_t* send_ops, uint32_t* pos, uint8_t* result_zero,
-                             uint32_t* vals_zero);
+                             uint32_t* vals_zero, const uint32_t* idx = nullptr,
+                             const uint64_t* n_dev = nullptr);
+cudaError_t launch_elect_partition(cudaStream_t s, const uint32_t* keys, const uint32_t* idx, uint64_t n,
+                                   const uint64_t* n_dev, uint32_t n_parts, unsigned long long* gcount,
+                                   unsigned long long* cursor, uint64_t* part_info, uint64_t* recs,
+                                   int num_sms);
+cudaError_t launch_dedup_elect_part(int grid, cudaStream_t s, const uint64_t* recs, const uint64_t* part_info,
+                                    uint32_t part, DedupView dd, Ctrl* ctrl);
 
 cudaError_t launch_unroute(cudaStream_t s, const uint32_t* pos, uint64_t n, const uint8_t* in8,
                            uint8_t* out8, const uint32_t* in32, uint32_t* out32);

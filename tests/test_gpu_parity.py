@@ -195,3 +195,19 @@ def test_cfg2_full_scale_properties():
     v = v.cpu().numpy().astype(np.uint32)
     assert (f == hit).all()
     assert (v[hit] == gen.vals_of(qids[hit])).all() and (v[~hit] == 0).all()
+
+
+def test_partitioned_owner_election_large_batches():
+    """Batches large enough for the hash-partitioned election (2^22 ops ->
+    2 L2-sized sub-tables) with heavy duplicates: statuses, erase outputs and
+    the final dump equal the oracle's."""
+    rng = np.random.default_rng(77)
+    n = 1 << 22
+    p = _pair(-(-(1 << 21) * 100 // (80 * 32)) * 32, lf_grow=2.0, lf_shrink=0)
+    keys = rng.integers(0, 1 << 21, n, dtype=np.uint64).astype(np.uint32)
+    vals = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    p.insert(keys, vals)
+    p.check_state()
+    p.erase(rng.integers(0, 1 << 22, n, dtype=np.uint64).astype(np.uint32))
+    p.check_state()
+    p.find(rng.integers(0, 1 << 22, 1 << 20, dtype=np.uint64).astype(np.uint32))
