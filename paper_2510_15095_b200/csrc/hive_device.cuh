@@ -234,21 +234,32 @@ __device__ __forceinline__ void put(uint64_t (&s)[SPL], int j, uint64_t w) {
         if (i == j) s[i] = w;
 }
 
-// Per-lane match mask of key k over the lane's slots (WCME compare).
+// One pass over a lane's slots (WCME compare + WABC free test):
+// jm = first slot holding key k, jf = first EMPTY slot (SPL = none).  A slot is
+// EMPTY iff its key word is 0xFFFFFFFF (that key is reserved, A-9), so both
+// tests are 32-bit compares; the scan runs high to low so the lowest index wins.
 template <int SPL>
-__device__ __forceinline__ uint32_t match_bits(const uint64_t (&s)[SPL], uint32_t k) {
-    uint32_t mm = 0;
+__device__ __forceinline__ void scan_slots(const uint64_t (&s)[SPL], uint32_t k, int& jm, int& jf) {
+    jm = SPL;
+    jf = SPL;
 #pragma unroll
-    for (int j = 0; j < SPL; ++j) mm |= (key_of(s[j]) == k ? 1u : 0u) << j;
-    return mm;
+    for (int j = SPL - 1; j >= 0; --j) {
+        const uint32_t key = key_of(s[j]);
+        jm = (key == k) ? j : jm;
+        jf = (key == INVALID_KEY) ? j : jf;
+    }
 }
-// Per-lane free mask (slot == EMPTY): the WABC claim predicate.
+// First slot holding k and its value (find path).
 template <int SPL>
-__device__ __forceinline__ uint32_t free_bits(const uint64_t (&s)[SPL]) {
-    uint32_t fm = 0;
+__device__ __forceinline__ int scan_value(const uint64_t (&s)[SPL], uint32_t k, uint32_t& v) {
+    int jm = SPL;
 #pragma unroll
-    for (int j = 0; j < SPL; ++j) fm |= (s[j] == EMPTY ? 1u : 0u) << j;
-    return fm;
+    for (int j = SPL - 1; j >= 0; --j) {
+        const bool hit = key_of(s[j]) == k;
+        jm = hit ? j : jm;
+        v = hit ? val_of(s[j]) : v;
+    }
+    return jm;
 }
 
 }  // namespace hive

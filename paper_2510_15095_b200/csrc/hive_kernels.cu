@@ -138,11 +138,11 @@ __device__ __forceinline__ void fill_empty(uint64_t (&s)[SPL]) {
 }
 
 // Step 1 / Alg. 1 ReplacePath and Alg. 4's CAS-to-EMPTY
-// (PAPER:448-475): WCME on the cached bucket view -- per-lane match bits, a
+// (PAPER:448-475): WCME on the cached bucket view -- per-lane first match, a
 // group ballot = match mask M, FirstSet(M) elects the winner lane, which CASes
-// its own cached word (lowest matching slot) to `newkv`; the outcome is
-// broadcast by ballot.  On a lost CAS the winner refreshes its view and the
-// group re-elects (reading A-18).  Group-uniform result; all lanes call.
+// its cached word to `newkv`; the outcome is broadcast by ballot.  On a lost CAS
+// the winner refreshes its view and the group re-elects (reading A-18).
+// Group-uniform result; all lanes call.
 template <int G>
 __device__ __forceinline__ bool wcme_cas(const WarpGroup<G>& wg, uint64_t (&s)[WarpGroup<G>::SPL],
                                          uint64_t* bucket, uint32_t k, uint64_t newkv,
@@ -150,18 +150,18 @@ __device__ __forceinline__ bool wcme_cas(const WarpGroup<G>& wg, uint64_t (&s)[W
     constexpr int SPL = WarpGroup<G>::SPL;
     bool trying = valid, done = false;
     for (int iter = 0; iter <= SLOTS; ++iter) {
-        const uint32_t mm = trying ? match_bits<SPL>(s, k) : 0u;
-        const uint32_t M = wg.ballot(mm != 0);                    // match mask
+        int jm = SPL, jf;
+        if (trying) scan_slots<SPL>(s, k, jm, jf);
+        const uint32_t M = wg.ballot(jm < SPL);                   // match mask
         trying = trying && M != 0;                                // early exit
         if (!__any_sync(FULL, trying)) break;
         bool ok = false;
         if (trying && wg.gl == __ffs(M) - 1) {                    // FirstSet winner
-            const int j = __ffs(mm) - 1;
-            const uint64_t old = pick<SPL>(s, j);
-            const uint64_t prev = cas64(wg.slot_ptr(bucket) + j, old, newkv);
+            const uint64_t old = pick<SPL>(s, jm);
+            const uint64_t prev = cas64(wg.slot_ptr(bucket) + jm, old, newkv);
             ab += 32;
             ok = (prev == old);
-            if (!ok) put<SPL>(s, j, prev);
+            if (!ok) put<SPL>(s, jm, prev);
         }
         const bool any_ok = wg.ballot(ok) != 0;                   // broadcast (all lanes)
         if (trying && any_ok) {
@@ -183,17 +183,17 @@ __device__ __forceinline__ bool wabc_claim(const WarpGroup<G>& wg, uint64_t (&s)
     constexpr int SPL = WarpGroup<G>::SPL;
     bool trying = want, placed = false;
     for (int iter = 0; iter <= SLOTS; ++iter) {
-        const uint32_t fm = trying ? free_bits<SPL>(s) : 0u;
-        const uint32_t F = wg.ballot(fm != 0);
+        int jm, jf = SPL;
+        if (trying) scan_slots<SPL>(s, INVALID_KEY, jm, jf);
+        const uint32_t F = wg.ballot(jf < SPL);
         trying = trying && F != 0;
         if (!__any_sync(FULL, trying)) break;
         bool ok = false;
         if (trying && wg.gl == __ffs(F) - 1) {
-            const int j = __ffs(fm) - 1;
-            const uint64_t prev = cas64(wg.slot_ptr(bucket) + j, EMPTY, kv);
+            const uint64_t prev = cas64(wg.slot_ptr(bucket) + jf, EMPTY, kv);
             ab += 32;
             ok = (prev == EMPTY);
-            if (!ok) put<SPL>(s, j, prev);
+            if (!ok) put<SPL>(s, jf, prev);
         }
         const bool any_ok = wg.ballot(ok) != 0;                   // all lanes vote
         if (trying && any_ok) {
@@ -204,15 +204,35 @@ __device__ __forceinline__ bool wabc_claim(const WarpGroup<G>& wg, uint64_t (&s)
     return placed;
 }
 
+// Optimistic WABC claim for the insert fast path: the lowest free lane (jf =
+// its first free slot, from the Step-1 scan) issues CAS(EMPTY -> kv) but the
+// group does NOT wait for the outcome; the CAS result is checked one loop
+// iteration later (after the next op's loads are in flight) and a lost claim
+// is handed to Step 3.  Returns group-uniformly whether a claim was issued.
+template <int G>
+__device__ __forceinline__ bool wabc_claim_issue(const WarpGroup<G>& wg, int jf, uint64_t* bucket, uint64_t kv,
+                                                 bool want, bool& pend, uint64_t& pend_prev,
+                                                 uint32_t& pend_item, uint32_t item, unsigned long long& ab) {
+    constexpr int SPL = WarpGroup<G>::SPL;
+    const uint32_t F = wg.ballot(want && jf < SPL);
+    if (want && F && wg.gl == __ffs(F) - 1) {
+        pend_prev = cas64(wg.slot_ptr(bucket) + jf, EMPTY, kv);
+        pend = true;
+        pend_item = item;
+        ab += 32;
+    }
+    return want && F != 0;
+}
+
 // Read-only WCME for FIND: the value of the lowest matching slot (one 32-bit
 // shuffle from the elected lane).
 template <int G>
 __device__ __forceinline__ bool wcme_value(const WarpGroup<G>& wg, const uint64_t (&s)[WarpGroup<G>::SPL],
                                            uint32_t k, bool valid, uint32_t* val) {
     constexpr int SPL = WarpGroup<G>::SPL;
-    const uint32_t mm = valid ? match_bits<SPL>(s, k) : 0u;
-    const uint32_t M = wg.ballot(mm != 0);
-    const uint32_t mine = mm ? val_of(pick<SPL>(s, __ffs(mm) - 1)) : 0u;
+    uint32_t mine = 0;
+    const int jm = valid ? scan_value<SPL>(s, k, mine) : SPL;
+    const uint32_t M = wg.ballot(jm < SPL);
     const uint32_t v = wg.bcast(mine, M ? __ffs(M) - 1 : 0);
     if (M) *val = v;
     return M != 0;
@@ -515,6 +535,9 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     const bool place_only = kvs != nullptr;
     const bool stash_on = !place_only && sv.ctrl->stash_tail != 0;
     unsigned long long added = 0, ab = 0;
+    bool pend = false;                     // this lane issued a claim last iteration
+    uint64_t pend_prev = EMPTY;            // ... and this is its CAS result
+    uint32_t pend_item = 0;
     const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
     for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
@@ -565,10 +588,14 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         }
         const uint64_t kv = pack(k, v);
         bool done = false, have2 = false;
+        int jm1 = SPL, jf1 = SPL;
         if (!place_only) {
-            // Step 1: b1; then -- only if b1's spill word allows k to live
-            // elsewhere -- b2 and the stash.
-            done = wcme_cas<G>(wg, s1, tv.bucket(b1), k, kv, valid, ab);
+            // Step 1: b1 (one scan gives the match and the first free slot); then
+            // -- only if b1's spill word allows k to live elsewhere -- b2 and the
+            // stash.
+            if (valid) scan_slots<SPL>(s1, k, jm1, jf1);
+            if (__any_sync(FULL, wg.ballot(jm1 < SPL) != 0))
+                done = wcme_cas<G>(wg, s1, tv.bucket(b1), k, kv, valid, ab);
             const bool maybe = valid && !done && (spill_w & fp) == fp;
             const bool need2 = two && maybe;
             if (__any_sync(FULL, need2)) {
@@ -592,14 +619,23 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
                 done |= wg.bcast(sdone, 0);
             }
         }
-        // Step 2: WABC claim in b1, then b2 (first-fit, A-21); b2 is read only
-        // if b1 is full.
-        bool placed = wabc_claim<G>(wg, s1, tv.bucket(b1), kv, valid && !done, ab);
+        // resolve the claim issued in the previous iteration (its CAS has had
+        // this iteration's loads to come back); a lost claim goes to Step 3
+        wl.push(pend && pend_prev != EMPTY, pend_item, leftover, &sv.ctrl->n_left);
+        pend = false;
+        // Step 2: optimistic WABC claim in b1, then b2 (first-fit, A-21); b2 is
+        // read only if b1 is full.
+        if (place_only && valid) scan_slots<SPL>(s1, INVALID_KEY, jm1, jf1);
+        bool placed = wabc_claim_issue<G>(wg, jf1, tv.bucket(b1), kv, valid && !done, pend, pend_prev,
+                                          pend_item, op, ab);
         const bool want2 = two && !done && !placed;
         if (__any_sync(FULL, want2)) {
             if (want2 && !have2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
             if (want2 && !have2 && wg.gl == 0) ab += 256;
-            const bool p2 = wabc_claim<G>(wg, s2, tv.bucket(b2), kv, want2, ab);
+            int jm2, jf2 = SPL;
+            if (want2) scan_slots<SPL>(s2, INVALID_KEY, jm2, jf2);
+            const bool p2 = wabc_claim_issue<G>(wg, jf2, tv.bucket(b2), kv, want2, pend, pend_prev,
+                                                pend_item, op, ab);
             if (p2 && wg.gl == 0) {
                 atomicOr((unsigned long long*)&tv.spill[b1], (unsigned long long)fp);
                 ab += 8;
@@ -613,6 +649,7 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         }
         wl.push(left && wg.gl == 0, op, leftover, &sv.ctrl->n_left);
     }
+    wl.push(pend && pend_prev != EMPTY, pend_item, leftover, &sv.ctrl->n_left);
     wl.flush(leftover, &sv.ctrl->n_left);
     block_add(&sv.ctrl->count, added);
     block_add(&sv.ctrl->abytes[AB_INSERT], ab);
