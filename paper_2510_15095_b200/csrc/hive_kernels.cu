@@ -49,6 +49,7 @@ __device__ __forceinline__ void block_add(unsigned long long* dst, unsigned long
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(&acc, v);
     __syncthreads();
     if (threadIdx.x == 0 && acc) atomicAdd(dst, acc);
+    __syncthreads();                       // acc is reused by the next call
 }
 __device__ __forceinline__ void block_max(unsigned long long* dst, unsigned long long v) {
     __shared__ unsigned long long accm;
@@ -58,6 +59,7 @@ __device__ __forceinline__ void block_max(unsigned long long* dst, unsigned long
     if ((threadIdx.x & 31) == 0 && v) atomicMax(&accm, v);
     __syncthreads();
     if (threadIdx.x == 0 && accm) atomicMax(dst, accm);
+    __syncthreads();
 }
 
 // Per-warp staging of an index list in shared memory; one global atomic per
