@@ -376,7 +376,8 @@ hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* 
     DedupView dd{nullptr, 0, nullptr, nullptr};
     if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
     CKS(ensure(h->left, h->left_cap, std::max<uint64_t>(n_upper, 1)));
-    CKS(set_ctrl_word(h, &h->ctrl->n_left, 0, s));
+    CK(cudaMemsetAsync(&h->ctrl->n_left, 0, sizeof(uint64_t), s));
+    CK(cudaMemsetAsync(&h->ctrl->slow_next, 0, sizeof(uint64_t), s));
     {
         Prof p(h, kvs ? "k_insert_fast(reinsert)" : "k_insert_fast", s);
         CK(launch_insert_fast(h->grids, s, keys, vals, kvs, idx, n_upper, n_dev, h->tv(),

@@ -672,81 +672,111 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
               TableView tv, StashView sv, uint32_t max_evictions, uint8_t* __restrict__ status) {
     using WG = WarpGroup<G>;
     constexpr int SPL = WG::SPL;
+    constexpr uint32_t BATCH = 2 * WG::GPW;          // leftover positions claimed per refill
     WG wg;
     const uint64_t n = sv.ctrl->n_left;
     if (!kvs && blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(&sv.ctrl->leftovers, (unsigned long long)n);
     unsigned long long evict = 0, depth = 0, pushes = 0, lost = 0, ab = 0;
-    const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
-    for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
-        const uint64_t t = t0 + wg.gi;
-        const bool active = t < n;
-        uint64_t item = active ? leftover[t] : 0;
-        uint64_t kv = EMPTY;
-        if (active) kv = kvs ? kvs[item] : pack(keys[item], vals[item]);
-        bool trying = active;
-        uint32_t b = active ? tv.addr(bithash1(key_of(kv))) : 0;   // start at b1
-        const uint32_t seed = active ? bithash2(key_of(kv)) : 0;
-        uint32_t rounds = 0;
-        for (uint32_t r = 0; r < max_evictions; ++r) {
-            if (!__any_sync(FULL, trying)) break;
-            uint64_t s[SPL];
-            if (trying) load_slots<SPL>(wg.slot_ptr(tv.bucket(b)), s);
-            else fill_empty<SPL>(s);
-            if (trying) ++rounds;
-            if (trying && wg.gl == 0) ab += 256;
-            bool placed = wabc_claim<G>(wg, s, tv.bucket(b), kv, trying, ab);   // line 3
-            if (placed) {
-                trying = false;
-                const uint32_t hb = tv.addr(bithash1(key_of(kv)));
-                if (wg.gl == 0 && hb != b) {
-                    atomicOr((unsigned long long*)&tv.spill[hb], (unsigned long long)spill_fp(key_of(kv)));
-                    ab += 8;
-                }
-            }
-            // Victim (lines 17-21): a rotating slot (reading A-6: any victim rule;
-            // preferring residents in their second bucket raised p_h1 to 0.93 but
-            // doubled evictions and grew the stash 5x -- a net loss).
-            const int vs = (int)((seed + r * 11u) & 31u);
-            const int vl = vs / SPL;
-            uint64_t victim = wg.bcast(pick<SPL>(s, vs % SPL), vl);
-            bool ok = false;
-            if (trying && wg.gl == vl && victim != EMPTY) {
-                uint64_t prev = cas64(tv.bucket(b) + vs, victim, kv);
-                ab += 32;
-                ok = (prev == victim);
-            }
-            ok = wg.bcast(ok, vl);
-            if (trying && ok) {
-                const uint32_t hb = tv.addr(bithash1(key_of(kv)));      // kv now lives in b
-                if (wg.gl == 0 && hb != b) {
-                    atomicOr((unsigned long long*)&tv.spill[hb], (unsigned long long)spill_fp(key_of(kv)));
-                    ab += 8;
-                }
-                kv = victim;                                 // line 33
-                b = tv.alt(key_of(kv), b);                   // line 34
-                if (wg.gl == 0) ++evict;
-            }
-        }
-        if (wg.gl == 0 && active) {
-            depth = rounds > depth ? rounds : depth;
-            ab += 4 + 8;
-        }
-        // Step 4: stash push of the in-hand entry
-        if (trying && wg.gl == 0) {
-            unsigned long long pos = atomicAdd(&sv.ctrl->stash_tail, 1ull);
-            if (pos < sv.cap) {
-                atomicOr((unsigned long long*)&tv.spill[tv.addr(bithash1(key_of(kv)))],
-                         (unsigned long long)spill_fp(key_of(kv)));
-                sv.ring[pos] = kv;
-                stash_index_put(sv, key_of(kv), pos);
-                ++pushes;
-                ab += 8 + 8 + 8;
+    // Dynamic scheduling: every warp iteration advances each busy group by one
+    // eviction round; a group whose entry is placed (or stashed) immediately
+    // takes the next leftover, so a warp never idles behind its longest chain.
+    bool busy = false;                       // group-uniform job state
+    uint32_t item = 0, b = 0, seed = 0, r = 0;
+    uint64_t kv = EMPTY;
+    uint64_t qa = 0, qb = 0;                 // warp-uniform claimed range of leftover positions
+    bool drained = n == 0;
+    const uint32_t leaders = __ballot_sync(FULL, wg.gl == 0);
+    while (true) {
+        // ---- hand out work to idle groups ----
+        const uint32_t idle = __ballot_sync(FULL, !busy && wg.gl == 0);
+        if (drained && idle == leaders) break;
+        if (idle && !drained) {
+            const uint32_t need = __popc(idle);
+            const uint32_t rank = wg.bcast((uint32_t)__popc(idle & lanemask_lt()), 0);
+            const uint64_t avail = qb - qa;
+            uint64_t pos = ~0ull;
+            if (rank < avail) pos = qa + rank;
+            if (need > avail) {
+                unsigned long long base = 0;
+                if ((threadIdx.x & 31) == 0) base = atomicAdd(&sv.ctrl->slow_next, (unsigned long long)BATCH);
+                base = __shfl_sync(FULL, base, 0);
+                if (rank >= avail) pos = base + (rank - avail);
+                qa = base + (need - avail);
+                qb = base + BATCH;
+                if (base + (need - avail) >= n) drained = true;
             } else {
-                ++lost;
-                if (status && !kvs) status[item] = 3;
+                qa += need;
+            }
+            if (qa >= n) qa = qb = n;
+            const bool start = !busy && pos < n;
+            if (start) {
+                item = leftover[pos];
+                kv = kvs ? kvs[item] : pack(keys[item], vals[item]);
+                b = tv.addr(bithash1(key_of(kv)));               // start at b1
+                seed = bithash2(key_of(kv));
+                r = 0;
+                busy = true;
+                if (wg.gl == 0) ab += 4 + 8;
             }
         }
+        if (!__any_sync(FULL, busy)) continue;
+        // ---- one round of Alg. 3 for every busy group ----
+        uint64_t s[SPL];
+        if (busy) load_slots<SPL>(wg.slot_ptr(tv.bucket(b)), s);
+        else fill_empty<SPL>(s);
+        if (busy && wg.gl == 0) ab += 256;
+        const bool placed = wabc_claim<G>(wg, s, tv.bucket(b), kv, busy, ab);   // line 3
+        if (placed) {
+            const uint32_t hb = tv.addr(bithash1(key_of(kv)));
+            if (wg.gl == 0 && hb != b) {
+                atomicOr((unsigned long long*)&tv.spill[hb], (unsigned long long)spill_fp(key_of(kv)));
+                ab += 8;
+            }
+        }
+        // Victim (lines 17-21): a rotating slot (reading A-6: any victim rule;
+        // preferring residents in their second bucket raised p_h1 to 0.93 but
+        // doubled evictions and grew the stash 5x -- a net loss).
+        const bool evicting = busy && !placed;
+        const int vs = (int)((seed + r * 11u) & 31u);
+        const int vl = vs / SPL;
+        const uint64_t victim = wg.bcast(pick<SPL>(s, vs % SPL), vl);
+        bool ok = false;
+        if (evicting && wg.gl == vl && victim != EMPTY) {
+            const uint64_t prev = cas64(tv.bucket(b) + vs, victim, kv);
+            ab += 32;
+            ok = (prev == victim);
+        }
+        ok = wg.bcast(ok, vl);
+        if (evicting && ok) {
+            const uint32_t hb = tv.addr(bithash1(key_of(kv)));          // kv now lives in b
+            if (wg.gl == 0 && hb != b) {
+                atomicOr((unsigned long long*)&tv.spill[hb], (unsigned long long)spill_fp(key_of(kv)));
+                ab += 8;
+            }
+            kv = victim;                                     // line 33
+            b = tv.alt(key_of(kv), b);                       // line 34
+            if (wg.gl == 0) ++evict;
+        }
+        if (busy) ++r;
+        const bool finish = busy && (placed || r >= max_evictions);
+        if (finish && wg.gl == 0) {
+            depth = r > depth ? r : depth;
+            if (!placed) {                                   // Step 4: stash the in-hand entry
+                const unsigned long long pos = atomicAdd(&sv.ctrl->stash_tail, 1ull);
+                if (pos < sv.cap) {
+                    atomicOr((unsigned long long*)&tv.spill[tv.addr(bithash1(key_of(kv)))],
+                             (unsigned long long)spill_fp(key_of(kv)));
+                    sv.ring[pos] = kv;
+                    stash_index_put(sv, key_of(kv), pos);
+                    ++pushes;
+                    ab += 8 + 8 + 8;
+                } else {
+                    ++lost;
+                    if (status && !kvs) status[item] = 3;
+                }
+            }
+        }
+        if (finish) busy = false;
     }
     block_add(&sv.ctrl->evictions, evict);
     block_add(&sv.ctrl->stash_pushes, pushes);
