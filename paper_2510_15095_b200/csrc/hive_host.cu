@@ -28,14 +28,14 @@ namespace {
 thread_local std::string g_err;
 
 // HIVE_TRACE=1: host-side timing of allocation / mapping / sync points (stderr).
-const bool g_trace = getenv("HIVE_TRACE") != nullptr;
+inline bool g_trace() { return getenv("HIVE_TRACE") != nullptr; }
 struct Trace {
     const char* what;
     uint64_t arg;
     std::chrono::steady_clock::time_point t0;
     Trace(const char* w, uint64_t a) : what(w), arg(a), t0(std::chrono::steady_clock::now()) {}
     ~Trace() {
-        if (!g_trace) return;
+        if (!g_trace()) return;
         const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
         fprintf(stderr, "[hive] %-14s %12llu %9.1f us\n", what, (unsigned long long)arg, us);
     }
@@ -249,15 +249,16 @@ hive_status vrange_reserve(hive_table_s* h, VRange& r, size_t bytes) {
     return HIVE_OK;
 }
 
-// Back the first `need` bytes of a range with physical memory.  Growth maps
-// geometrically (>= 1/4 of what is mapped, whole 2 MiB granules, one
-// cuMemCreate per step), so a long run of K-bucket splits or stash growth
-// costs few driver calls, and nothing is ever copied or freed on the way.
+// Back the first `need` bytes of a range with physical memory.  Growth at least
+// doubles what is mapped (whole 2 MiB granules, one cuMemCreate per step):
+// cuMemSetAccess / cuMemCreate cost 5-95 ms per call on this system (measured,
+// HIVE_TRACE), so a long run of K-bucket splits must cost only a few calls.
+// Nothing is ever copied or freed on the way.
 hive_status vrange_map(hive_table_s* h, VRange& r, size_t need) {
     need = (need + h->gran - 1) / h->gran * h->gran;
     if (need <= r.mapped) return HIVE_OK;
     Trace tr("vrange_map", need);
-    size_t target = std::max(need, r.mapped + r.mapped / 4);
+    size_t target = std::max(need, 2 * r.mapped);
     target = std::min((target + h->gran - 1) / h->gran * h->gran, r.reserved);
     if (target < need) {
         g_err = "request exceeds the reserved max_capacity";
@@ -272,11 +273,19 @@ hive_status vrange_map(hive_table_s* h, VRange& r, size_t need) {
     acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
     const size_t off = r.mapped, bytes = target - r.mapped;
     CUmemGenericAllocationHandle mh;
-    CUresult e = g_vmm.create(&mh, bytes, &prop, 0);
+    CUresult e;
+    {
+        Trace t1("cuMemCreate", bytes);
+        e = g_vmm.create(&mh, bytes, &prop, 0);
+    }
     if (e != CUDA_SUCCESS) { set_err_drv(e, "cuMemCreate", __LINE__); return HIVE_ENOMEM; }
-    e = g_vmm.map(r.va + off, bytes, 0, mh, 0);
+    {
+        Trace t2("cuMemMap", bytes);
+        e = g_vmm.map(r.va + off, bytes, 0, mh, 0);
+    }
     if (e != CUDA_SUCCESS) { g_vmm.release(mh); set_err_drv(e, "cuMemMap", __LINE__); return HIVE_ENOMEM; }
     r.chunks.push_back({mh, off, bytes});
+    Trace t3("cuMemSetAccess", bytes);
     e = g_vmm.set_access(r.va + off, bytes, &acc, 1);
     if (e != CUDA_SUCCESS) { set_err_drv(e, "cuMemSetAccess", __LINE__); return HIVE_ECUDA; }
     r.mapped = target;
@@ -323,6 +332,7 @@ hive_status set_ctrl_word(hive_table_s* h, unsigned long long* field, uint64_t v
 hive_status stash_reset(hive_table_s* h, uint64_t cap, cudaStream_t s) {
     const uint64_t ic = pow2_at_least(2 * cap);
     CKS(vrange_map(h, h->rg, cap * sizeof(uint64_t)));
+    CKS(vrange_map(h, h->dr, cap * sizeof(uint64_t)));
     CKS(vrange_map(h, h->ix, ic * sizeof(uint64_t)));
     h->ring = (uint64_t*)h->rg.va;
     h->sidx = (uint64_t*)h->ix.va;
@@ -599,7 +609,10 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     if (st == HIVE_OK) st = vrange_reserve(h, h->sp, (size_t)h->max_buckets * sizeof(uint64_t));
     if (st != HIVE_OK) return fail(st);
     h->va = h->bk.va;
-    st = map_buckets(h, nb);
+    // growth-enabled tables start with >= 64 MiB of buckets backed (256 Ki
+    // buckets) so that early splits need no driver call
+    const uint64_t premap = cfg->lf_grow < 1.0f ? std::min<uint64_t>(h->max_buckets, 1ull << 18) : 0;
+    st = map_buckets(h, std::max<uint64_t>(nb, premap));
     if (st != HIVE_OK) return fail(st);
 
     if (cudaMalloc((void**)&h->ctrl, sizeof(Ctrl)) != cudaSuccess) return fail(HIVE_ENOMEM);
