@@ -315,20 +315,13 @@ def main():
         st_h = torch.empty(n, dtype=torch.uint8).pin_memory()
         vo_h = torch.empty(n, dtype=torch.uint32).pin_memory()
         fo_h = torch.empty(n, dtype=torch.uint8).pin_memory()
-        kd = torch.empty_like(keys)
-        vd = torch.empty_like(vals)
-        qd = torch.empty_like(queries)
 
         def e2e_step():
+            # public API with host buffers: hive_insert_host / hive_find_host
+            # pipeline the transfers against compute inside the library
             table.clear()
-            kd.copy_(keys_h, non_blocking=True)
-            vd.copy_(vals_h, non_blocking=True)
-            table.insert(kd, vd, status)
-            st_h.copy_(status, non_blocking=True)
-            qd.copy_(q_h, non_blocking=True)
-            table.find(qd, vals_out, found)
-            vo_h.copy_(vals_out, non_blocking=True)
-            fo_h.copy_(found, non_blocking=True)
+            table.insert_host(keys_h, vals_h, st_h)
+            table.find_host(q_h, vo_h, fo_h)
 
         for _ in range(2):
             e2e_step()

@@ -145,6 +145,22 @@ hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys,
                        const uint32_t* d_vals, uint64_t n, uint32_t* d_vals_out,
                        uint8_t* d_result, void* stream);
 
+/* Host-buffer variants (the end-to-end public path).  h_* are HOST pointers
+ * (page-locked memory recommended; pageable works but serialises copies).
+ * Stream-ordered like the device calls: the results are in the host buffers
+ * once `stream` has completed the call, and the host buffers must stay alive
+ * until then.  Semantics are those of hive_insert / hive_find.  Internally the
+ * transfers run on the handle's own upload / download streams in 4 Mi-op
+ * chunks so that copies overlap compute: the owner election starts once all
+ * keys are on the device and overlaps the value upload, insert chunks start as
+ * their values land, find chunks overlap the download of earlier results, and
+ * a find's upload may overlap a preceding insert's compute.  Device staging
+ * buffers are owned by the handle (allocated on first use, reused). */
+hive_status hive_insert_host(hive_t h, const uint32_t* h_keys, const uint32_t* h_vals,
+                             uint64_t n, uint8_t* h_status, void* stream);
+hive_status hive_find_host(hive_t h, const uint32_t* h_keys, uint64_t n,
+                           uint32_t* h_vals_out, uint8_t* h_found, void* stream);
+
 /* Reset to the freshly created state (all slots EMPTY, initial size, stash
  * empty, counters zero); keeps allocations.  Async. */
 hive_status hive_clear(hive_t h, void* stream);

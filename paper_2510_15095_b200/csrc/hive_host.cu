@@ -157,6 +157,18 @@ struct hive_table_s {
     uint64_t* cnt = nullptr;  uint64_t cnt_cap = 0;
     uint64_t* pinfo = nullptr;
 
+    // host-buffer pipeline (hive_insert_host / hive_find_host): staging buffers,
+    // upload / download streams, and "staging free" events
+    uint32_t* hk = nullptr; uint64_t hk_cap = 0;
+    uint32_t* hv = nullptr; uint64_t hv_cap = 0;
+    uint8_t* hst = nullptr; uint64_t hst_cap = 0;
+    uint32_t* fq = nullptr; uint64_t fq_cap = 0;
+    uint32_t* fv = nullptr; uint64_t fv_cap = 0;
+    uint8_t* ff = nullptr; uint64_t ff_cap = 0;
+    cudaStream_t up = nullptr, down = nullptr;
+    cudaEvent_t ins_free = nullptr, find_free = nullptr;
+    std::vector<cudaEvent_t> pipe_ev;
+
     uint64_t grows = 0, shrinks = 0, merge_aborts = 0;
     uint64_t tail_known = 0;           // stash_tail at the last synchronising read
     unsigned long long* aborts = nullptr;   // per-segment first aborting merge pair
@@ -378,17 +390,32 @@ hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* 
 }
 
 // ---- the INSERT phase (Steps 1-4, owner election, duplicate fix-up) ---------------
+// Chunked launch of the fast path for the host pipeline: chunk c covers ops
+// [c * chunk, ...) and waits for ready[c] (its values have been uploaded).
+struct InsertChunks {
+    uint64_t chunk;
+    const cudaEvent_t* ready;
+};
+
 hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* vals,
                          const uint64_t* kvs, const uint32_t* idx, uint64_t n_upper,
                          const uint64_t* n_dev, uint64_t n_batch, uint8_t* status,
-                         uint32_t* vals_zero, cudaStream_t s) {
+                         uint32_t* vals_zero, cudaStream_t s, const InsertChunks* chunks = nullptr) {
     const bool dedup = !kvs && h->dedup_on();
     DedupView dd{nullptr, 0, nullptr, nullptr};
     if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
     CKS(ensure(h->left, h->left_cap, std::max<uint64_t>(n_upper, 1)));
     CK(cudaMemsetAsync(&h->ctrl->n_left, 0, sizeof(uint64_t), s));
     CK(cudaMemsetAsync(&h->ctrl->slow_next, 0, sizeof(uint64_t), s));
-    {
+    if (chunks) {
+        Prof p(h, "k_insert_fast", s);
+        for (uint64_t off = 0, c = 0; off < n_upper; off += chunks->chunk, ++c) {
+            CK(cudaStreamWaitEvent(s, chunks->ready[c], 0));
+            CK(launch_insert_fast(h->grids, s, keys, vals, nullptr, nullptr,
+                                  std::min<uint64_t>(chunks->chunk, n_upper - off), nullptr, h->tv(), h->sv(),
+                                  dd, status, nullptr, h->left, (uint32_t)off));
+        }
+    } else {
         Prof p(h, kvs ? "k_insert_fast(reinsert)" : "k_insert_fast", s);
         CK(launch_insert_fast(h->grids, s, keys, vals, kvs, idx, n_upper, n_dev, h->tv(),
                               h->sv(), dd, status, vals_zero, h->left));
@@ -533,6 +560,28 @@ hive_status erase_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* i
 
 }  // namespace
 
+// ---- host-buffer pipeline -----------------------------------------------------------
+namespace {
+constexpr uint64_t HOST_CHUNK = 1ull << 22;   // ops per transfer / launch chunk
+
+hive_status pipe_init(hive_table_s* h, size_t n_events) {
+    if (!h->up) {
+        CK(cudaStreamCreateWithFlags(&h->up, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&h->down, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->ins_free, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->find_free, cudaEventDisableTiming));
+        CK(cudaEventRecord(h->ins_free, h->up));
+        CK(cudaEventRecord(h->find_free, h->up));
+    }
+    while (h->pipe_ev.size() < n_events) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->pipe_ev.push_back(e);
+    }
+    return HIVE_OK;
+}
+}  // namespace
+
 // =====================================================================================
 // C ABI
 // =====================================================================================
@@ -657,7 +706,12 @@ hive_status hive_destroy(hive_t h) {
     vrange_free(h->dr);
     vrange_free(h->sp);
     void* bufs[] = {h->ctrl, h->dd, h->owner, h->flag, h->left, h->cls, h->cnt, h->pinfo, h->aborts,
-                    h->erec, h->ecount, h->einfo};
+                    h->erec, h->ecount, h->einfo, h->hk, h->hv, h->hst, h->fq, h->fv, h->ff};
+    for (auto e : h->pipe_ev) cudaEventDestroy(e);
+    if (h->ins_free) cudaEventDestroy(h->ins_free);
+    if (h->find_free) cudaEventDestroy(h->find_free);
+    if (h->up) cudaStreamDestroy(h->up);
+    if (h->down) cudaStreamDestroy(h->down);
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (h->ctrl_h) cudaFreeHost(h->ctrl_h);
@@ -737,6 +791,84 @@ hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
     CKS(shrink_after(h, s));
     Prof p(h, "k_find", s);
     CK(launch_find(h->grids, s, d_keys, h->cls, n, n_find, h->tv(), h->sv(), d_vals_out, d_result));
+    return HIVE_OK;
+}
+
+hive_status hive_insert_host(hive_t h, const uint32_t* h_keys, const uint32_t* h_vals, uint64_t n,
+                             uint8_t* h_status, void* stream) {
+    if (!h) return HIVE_EINVAL;
+    if (n == 0) return HIVE_OK;
+    if (!h_keys || !h_vals || n >= (1ull << 32)) return HIVE_EINVAL;
+    BusyGuard g(h);
+    if (!g.ok) return HIVE_EBUSY;
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last = s;
+    const uint64_t nch = (n + HOST_CHUNK - 1) / HOST_CHUNK;
+    CKS(pipe_init(h, nch + 3));
+    CKS(ensure(h->hk, h->hk_cap, n));
+    CKS(ensure(h->hv, h->hv_cap, n));
+    CKS(ensure(h->hst, h->hst_cap, n));
+    cudaEvent_t* ev = h->pipe_ev.data();          // [0, nch): values ready; nch: keys ready; nch+1, nch+2
+    // uploads: all keys first (the election needs the whole batch), then values by chunk
+    CK(cudaStreamWaitEvent(h->up, h->ins_free, 0));
+    CK(cudaMemcpyAsync(h->hk, h_keys, n * 4, cudaMemcpyHostToDevice, h->up));
+    CK(cudaEventRecord(ev[nch], h->up));
+    for (uint64_t off = 0, c = 0; off < n; off += HOST_CHUNK, ++c) {
+        const uint64_t len = std::min(HOST_CHUNK, n - off);
+        CK(cudaMemcpyAsync(h->hv + off, h_vals + off, len * 4, cudaMemcpyHostToDevice, h->up));
+        CK(cudaEventRecord(ev[c], h->up));
+    }
+    CK(cudaStreamWaitEvent(s, ev[nch], 0));
+    CKS(grow_before(h, n, s));
+    InsertChunks ic{HOST_CHUNK, ev};
+    CKS(insert_phase(h, h->hk, h->hv, nullptr, nullptr, n, nullptr, n, h->hst, nullptr, s, &ic));
+    CK(cudaEventRecord(h->ins_free, s));
+    if (h_status) {
+        CK(cudaStreamWaitEvent(h->down, h->ins_free, 0));
+        CK(cudaMemcpyAsync(h_status, h->hst, n, cudaMemcpyDeviceToHost, h->down));
+        CK(cudaEventRecord(ev[nch + 1], h->down));
+        CK(cudaStreamWaitEvent(s, ev[nch + 1], 0));
+    }
+    return HIVE_OK;
+}
+
+hive_status hive_find_host(hive_t h, const uint32_t* h_keys, uint64_t n, uint32_t* h_vals_out,
+                           uint8_t* h_found, void* stream) {
+    if (!h) return HIVE_EINVAL;
+    if (n == 0) return HIVE_OK;
+    if (!h_keys || !h_vals_out) return HIVE_EINVAL;
+    BusyGuard g(h);
+    if (!g.ok) return HIVE_EBUSY;
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last = s;
+    const uint64_t nch = (n + HOST_CHUNK - 1) / HOST_CHUNK;
+    CKS(pipe_init(h, 2 * nch + 1));
+    CKS(ensure(h->fq, h->fq_cap, n));
+    CKS(ensure(h->fv, h->fv_cap, n));
+    CKS(ensure(h->ff, h->ff_cap, n));
+    cudaEvent_t* ev = h->pipe_ev.data();          // [0, nch): uploaded; [nch, 2nch): probed; 2nch: done
+    CK(cudaStreamWaitEvent(h->up, h->find_free, 0));
+    for (uint64_t off = 0, c = 0; off < n; off += HOST_CHUNK, ++c) {
+        const uint64_t len = std::min(HOST_CHUNK, n - off);
+        CK(cudaMemcpyAsync(h->fq + off, h_keys + off, len * 4, cudaMemcpyHostToDevice, h->up));
+        CK(cudaEventRecord(ev[c], h->up));
+    }
+    {
+        Prof p(h, "k_find", s);
+        for (uint64_t off = 0, c = 0; off < n; off += HOST_CHUNK, ++c) {
+            const uint64_t len = std::min(HOST_CHUNK, n - off);
+            CK(cudaStreamWaitEvent(s, ev[c], 0));
+            CK(launch_find(h->grids, s, h->fq + off, nullptr, len, nullptr, h->tv(), h->sv(), h->fv + off,
+                           h->ff + off));
+            CK(cudaEventRecord(ev[nch + c], s));
+            CK(cudaStreamWaitEvent(h->down, ev[nch + c], 0));
+            CK(cudaMemcpyAsync(h_vals_out + off, h->fv + off, len * 4, cudaMemcpyDeviceToHost, h->down));
+            if (h_found) CK(cudaMemcpyAsync(h_found + off, h->ff + off, len, cudaMemcpyDeviceToHost, h->down));
+        }
+    }
+    CK(cudaEventRecord(h->find_free, s));
+    CK(cudaEventRecord(ev[2 * nch], h->down));
+    CK(cudaStreamWaitEvent(s, ev[2 * nch], 0));
     return HIVE_OK;
 }
 

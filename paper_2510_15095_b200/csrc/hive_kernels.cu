@@ -527,7 +527,7 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
               const uint64_t* __restrict__ kvs, const uint32_t* __restrict__ idx, uint64_t n,
               const uint64_t* __restrict__ n_dev, TableView tv, StashView sv, DedupView dd,
               uint8_t* __restrict__ status, uint32_t* __restrict__ vals_zero,
-              uint32_t* __restrict__ leftover) {
+              uint32_t* __restrict__ leftover, uint32_t op_base) {
     using WG = WarpGroup<G>;
     constexpr int SPL = WG::SPL;
     __shared__ uint32_t lbuf[WARPS_PER_BLOCK][32];
@@ -553,7 +553,7 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
                 k = key_of(w);
                 v = val_of(w);
             } else {
-                op = idx ? idx[t] : (uint32_t)t;
+                op = idx ? idx[t] : op_base + (uint32_t)t;   // op_base: chunked launches
                 k = keys[op];
                 v = vals[op];
             }
@@ -1263,10 +1263,11 @@ cudaError_t launch_dedup_elect(int grid, cudaStream_t s, const uint32_t* keys, c
 cudaError_t launch_insert_fast(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
                                const uint64_t* kvs, const uint32_t* idx, uint64_t n,
                                const uint64_t* n_dev, TableView tv, StashView sv, DedupView dd,
-                               uint8_t* status, uint32_t* vals_zero, uint32_t* leftover) {
+                               uint8_t* status, uint32_t* vals_zero, uint32_t* leftover,
+                               uint32_t op_base) {
     const int grid = n_dev ? gr.insert_fast : clamp_grid(gr.insert_fast, n, BLOCK / gr.g_insert);
 #define L_INS(G, MB) k_insert_fast<G, MB><<<grid, BLOCK, 0, s>>>(keys, vals, kvs, idx, n, n_dev, tv, sv, dd, \
-                                                         status, vals_zero, leftover)
+                                                         status, vals_zero, leftover, op_base)
     HIVE_DISPATCH_GM(gr.g_insert, gr.minb, L_INS)
     return cudaGetLastError();
 }

@@ -40,7 +40,8 @@ cudaError_t launch_dedup_elect(int grid, cudaStream_t s, const uint32_t* keys, c
 cudaError_t launch_insert_fast(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
                                const uint64_t* kvs, const uint32_t* idx, uint64_t n,
                                const uint64_t* n_dev, TableView tv, StashView sv, DedupView dd,
-                               uint8_t* status, uint32_t* vals_zero, uint32_t* leftover);
+                               uint8_t* status, uint32_t* vals_zero, uint32_t* leftover,
+                               uint32_t op_base = 0);
 
 cudaError_t launch_insert_slow(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
                                const uint64_t* kvs, const uint32_t* leftover, TableView tv,

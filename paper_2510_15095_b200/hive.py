@@ -53,6 +53,8 @@ SIGNATURES = {
     "hive_erase": (_int, [_vp, _vp, _u64, _vp, _vp]),
     "hive_mixed": (_int, [_vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp]),
     "hive_clear": (_int, [_vp, _vp]),
+    "hive_insert_host": (_int, [_vp, _vp, _vp, _u64, _vp, _vp]),
+    "hive_find_host": (_int, [_vp, _vp, _u64, _vp, _vp, _vp]),
     "hive_size": (_int, [_vp, ctypes.POINTER(_u64)]),
     "hive_stats": (_int, [_vp, ctypes.POINTER(HiveStats)]),
     "hive_dump": (_int, [_vp, _vp, _vp, _u64, ctypes.POINTER(_u64), _vp]),
@@ -201,24 +203,33 @@ class HiveTable:
         return vals_out, result
 
     # ---- end-to-end variants: host tensors in, host tensors out -----------------------
-    def insert_host(self, keys_h: torch.Tensor, vals_h: torch.Tensor) -> torch.Tensor:
-        k = keys_h.to("cuda", non_blocking=True)
-        v = vals_h.to("cuda", non_blocking=True)
-        st = self.insert(k, v)
-        out = torch.empty(st.shape, dtype=st.dtype, pin_memory=True)
-        out.copy_(st, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        return out
+    # (pinned host tensors; asynchronous on the current stream: results are valid
+    # after torch.cuda.current_stream().synchronize())
+    @staticmethod
+    def _host(t: torch.Tensor, nbytes_per: int) -> torch.Tensor:
+        if t.is_cuda or t.element_size() != nbytes_per or not t.is_contiguous():
+            raise HiveError("expected a contiguous host tensor")
+        return t
 
-    def find_host(self, keys_h: torch.Tensor):
-        k = keys_h.to("cuda", non_blocking=True)
-        v, f = self.find(k)
-        vo = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
-        fo = torch.empty(f.shape, dtype=f.dtype, pin_memory=True)
-        vo.copy_(v, non_blocking=True)
-        fo.copy_(f, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        return vo, fo
+    def insert_host(self, keys_h, vals_h, status_h=None, stream=None):
+        keys_h, vals_h = self._host(keys_h, 4), self._host(vals_h, 4)
+        n = keys_h.numel()
+        if status_h is None:
+            status_h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        _check(self._L.hive_insert_host(self._h, _p(keys_h), _p(vals_h), n, _p(status_h), _stream(stream)),
+               "hive_insert_host")
+        return status_h
+
+    def find_host(self, keys_h, vals_h=None, found_h=None, stream=None):
+        keys_h = self._host(keys_h, 4)
+        n = keys_h.numel()
+        if vals_h is None:
+            vals_h = torch.empty(n, dtype=torch.uint32, pin_memory=True)
+        if found_h is None:
+            found_h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        _check(self._L.hive_find_host(self._h, _p(keys_h), n, _p(vals_h), _p(found_h), _stream(stream)),
+               "hive_find_host")
+        return vals_h, found_h
 
     # ---- inspection -----------------------------------------------------------------
     def clear(self, stream=None):
