@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--n-log2", type=int, default=N_LOG2, help="keys per rank (debug only)")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the hash-sharded (NCCL all-to-all) path even at world size 1 (testing)")
     return ap.parse_args()
 
 
@@ -173,7 +175,13 @@ def main():
     if rank == 0:
         build_lib()
     torch.cuda.set_device(local)
-    if world > 1:
+    sharded = world > 1 or args.force_sharded
+    if sharded:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
@@ -195,7 +203,7 @@ def main():
     vals_out = torch.empty(n, dtype=torch.uint32, device=dev)
     found = torch.empty(n, dtype=torch.uint8, device=dev)
 
-    if world > 1:
+    if sharded:
         from paper_2510_15095_b200.sharded import ShardedHive
         sh = ShardedHive(nb * 32, lf_grow=2.0, lf_shrink=0)
         table = sh.table
@@ -224,22 +232,22 @@ def main():
     # ---- timed region: K steps, barrier + sync on both sides, max over ranks -------------
     phase = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
+    if sharded:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         start.record()
         for i in range(args.steps):
-            if world > 1:
+            if sharded:
                 step()
             else:
                 step(phase[i])
         end.record()
         torch.cuda.synchronize()
-    if world > 1:
+    if sharded:
         dist.barrier()
     ms = start.elapsed_time(end)
-    if world > 1:
+    if sharded:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -248,14 +256,14 @@ def main():
     value = total_ops / (ms_per_step * 1e-3) / 1e9
 
     # correctness guard on the last step (no outputs are trusted blindly)
-    if world == 1:
+    if not sharded:
         hit = np.zeros(1)
         st_bad = int((status != 0).sum().item())
         fnd = int(found.sum().item())
         assert st_bad == 0 and fnd == n // 2, (st_bad, fnd)
 
     out = {}
-    if world == 1:
+    if not sharded:
         ins_ms = statistics.mean(p[0].elapsed_time(p[1]) for p in phase)
         find_ms = statistics.mean(p[1].elapsed_time(p[2]) for p in phase)
         out["updates_gps"] = n / (ins_ms * 1e-3) / 1e9
@@ -265,10 +273,7 @@ def main():
 
     # ---- one profiled (untimed) step: per-kernel device times and launch counts ------------
     table.profile(True)
-    if world > 1:
-        step()
-    else:
-        step()
+    step()
     torch.cuda.synchronize()
     prof = table.profile_read(reset=True)
     table.profile(False)
@@ -308,7 +313,7 @@ def main():
 
     # ---- e2e through the public API with host buffers (pinned) ---------------------------
     e2e = None
-    if world == 1:
+    if not sharded:
         keys_h = keys.cpu().pin_memory()
         vals_h = vals.cpu().pin_memory()
         q_h = queries.cpu().pin_memory()
@@ -338,13 +343,44 @@ def main():
                "h2d_bytes_per_step": 3 * 4 * n, "d2h_bytes_per_step": (1 + 4 + 1) * n,
                "ms_per_step": e_ms}
 
+    if sharded:
+        # sharded public API with host buffers: H2D inputs, collective insert +
+        # find, D2H results (every rank), max over ranks
+        keys_h, vals_h, q_h = keys.cpu().pin_memory(), vals.cpu().pin_memory(), queries.cpu().pin_memory()
+        st_h = torch.empty(n, dtype=torch.uint8).pin_memory()
+        vo_h = torch.empty(n, dtype=torch.uint32).pin_memory()
+        fo_h = torch.empty(n, dtype=torch.uint8).pin_memory()
+
+        def e2e_step_sh():
+            table.clear()
+            st = sh.insert(keys_h.to(dev, non_blocking=True), vals_h.to(dev, non_blocking=True))
+            st_h.copy_(st, non_blocking=True)
+            v, f = sh.find(q_h.to(dev, non_blocking=True))
+            vo_h.copy_(v, non_blocking=True)
+            fo_h.copy_(f, non_blocking=True)
+
+        e2e_step_sh()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            e2e_step_sh()
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / args.steps], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+        e2e = {"value": total_ops / (e_ms * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 3 * 4 * n, "d2h_bytes_per_step": (1 + 4 + 1) * n, "ms_per_step": e_ms}
+
     # ---- secondary measurements (N = 1, untimed for `value`) ------------------------------
     secondary = {}
-    if world == 1 and not args.no_secondary:
+    if not sharded and not args.no_secondary:
         secondary = secondary_measurements(table, keys, vals, queries, n, nb, dev, prof)
 
     cpu = None
-    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+    if world == 1 and not sharded and rank == 0 and not args.no_cpu_baseline:
         s_log2 = min(24, args.n_log2)
         ops, sec = oracle_sample(s_log2)
         cpu = {"value": ops / sec / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -360,7 +396,7 @@ def main():
                                    "(LF 0.95, growth off) + 2^%d finds (50%% hits) per rank"
                                    % (args.n_log2, nb, args.n_log2),
                        "keys_per_rank": n, "buckets_per_rank": nb,
-                       "parallelism": "single GPU" if world == 1 else f"hash-sharded x{world} (NCCL all-to-all)",
+                       "parallelism": "single GPU" if not sharded else f"hash-sharded x{world} (NCCL all-to-all)",
                        "l2": "inputs and table larger than L2 (no flush)", "owner_election": "on"},
             **out,
             "clocks": clk.summary(),
@@ -374,7 +410,7 @@ def main():
             "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 
