@@ -257,11 +257,25 @@ k_find(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint
     unsigned long long ab = 0;
     const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
-    for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
+    // software pipeline: next iteration's (op, key) loads while this one probes
+    const uint64_t stride = nw * WG::GPW;
+    uint32_t op_n = 0, k_n = INVALID_KEY;
+    {
+        const uint64_t t = warp * WG::GPW + wg.gi;
+        if (t < n) {
+            op_n = idx ? idx[t] : (uint32_t)t;
+            k_n = keys[op_n];
+        }
+    }
+    for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += stride) {
         const uint64_t t = t0 + wg.gi;
         const bool active = t < n;
-        const uint32_t op = active ? (idx ? idx[t] : (uint32_t)t) : 0u;   // < 2^32 (API)
-        const uint32_t k = active ? keys[op] : INVALID_KEY;
+        const uint32_t op = op_n;                      // < 2^32 (API)
+        const uint32_t k = active ? k_n : INVALID_KEY;
+        if (t + stride < n) {
+            op_n = idx ? idx[t + stride] : (uint32_t)(t + stride);
+            k_n = keys[op_n];
+        }
         const bool valid = k != INVALID_KEY;
         uint32_t b1 = 0, b2 = 0;
         if (valid) {
@@ -542,22 +556,31 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     uint32_t pend_item = 0;
     const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
-    for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
+    // software pipeline: the next iteration's (op, key, value) is loaded while
+    // this iteration probes
+    const uint64_t stride = nw * WG::GPW;
+    uint32_t op_n = 0, k_n = INVALID_KEY, v_n = 0;
+    auto fetch = [&](uint64_t tt) {
+        if (tt >= n) return;
+        if (place_only) {
+            const uint64_t w = kvs[tt];
+            op_n = (uint32_t)tt;
+            k_n = key_of(w);
+            v_n = val_of(w);
+        } else {
+            op_n = idx ? idx[tt] : op_base + (uint32_t)tt;   // op_base: chunked launches
+            k_n = keys[op_n];
+            v_n = vals[op_n];
+        }
+    };
+    fetch(warp * WG::GPW + wg.gi);
+    for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += stride) {
         const uint64_t t = t0 + wg.gi;
         const bool active = t < n;
-        uint32_t op = (uint32_t)t;                  // op indices < 2^32 (API contract)
-        uint32_t k = INVALID_KEY, v = 0;
-        if (active) {
-            if (place_only) {
-                const uint64_t w = kvs[t];
-                k = key_of(w);
-                v = val_of(w);
-            } else {
-                op = idx ? idx[t] : op_base + (uint32_t)t;   // op_base: chunked launches
-                k = keys[op];
-                v = vals[op];
-            }
-        }
+        const uint32_t op = op_n;                    // op indices < 2^32 (API contract)
+        const uint32_t k = active ? k_n : INVALID_KEY;
+        const uint32_t v = v_n;
+        fetch(t + stride);
         bool valid = active && k != INVALID_KEY;
         uint32_t b1 = 0, b2 = 0;
         if (valid) {
@@ -566,15 +589,16 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         }
         bool two = valid && b2 != b1;
         const uint64_t fp = spill_fp(k);
-        uint64_t s1[SPL], s2[SPL];
+        // one bucket view: b1, later overwritten by b2 (b1's scan results are
+        // kept in jm1 / jf1), so the two views never occupy registers together
+        uint64_t sv_[SPL];
         uint64_t spill_w = 0;
         if (valid) {
-            load_slots<SPL>(wg.slot_ptr(tv.bucket(b1)), s1);
+            load_slots<SPL>(wg.slot_ptr(tv.bucket(b1)), sv_);
             spill_w = tv.spill[b1];
         } else {
-            fill_empty<SPL>(s1);
+            fill_empty<SPL>(sv_);
         }
-        fill_empty<SPL>(s2);
         if (active && wg.gl == 0) {
             ab += (place_only ? 8 : 8 + (status ? 1 : 0) + (vals_zero ? 4 : 0) + (idx ? 4 : 0)) +
                   (valid ? 256 + 8 : 0);
@@ -595,16 +619,16 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             // Step 1: b1 (one scan gives the match and the first free slot); then
             // -- only if b1's spill word allows k to live elsewhere -- b2 and the
             // stash.
-            if (valid) scan_slots<SPL>(s1, k, jm1, jf1);
+            if (valid) scan_slots<SPL>(sv_, k, jm1, jf1);
             if (__any_sync(FULL, wg.ballot(jm1 < SPL) != 0))
-                done = wcme_cas<G>(wg, s1, tv.bucket(b1), k, kv, valid, ab);
+                done = wcme_cas<G>(wg, sv_, tv.bucket(b1), k, kv, valid, ab);
             const bool maybe = valid && !done && (spill_w & fp) == fp;
             const bool need2 = two && maybe;
             if (__any_sync(FULL, need2)) {
-                if (need2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
+                if (need2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), sv_);
                 if (need2 && wg.gl == 0) ab += 256;
                 have2 = need2;
-                done |= wcme_cas<G>(wg, s2, tv.bucket(b2), k, kv, need2, ab);
+                done |= wcme_cas<G>(wg, sv_, tv.bucket(b2), k, kv, need2, ab);
             }
             if (stash_on) {
                 bool sdone = false;
@@ -627,15 +651,15 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         pend = false;
         // Step 2: optimistic WABC claim in b1, then b2 (first-fit, A-21); b2 is
         // read only if b1 is full.
-        if (place_only && valid) scan_slots<SPL>(s1, INVALID_KEY, jm1, jf1);
+        if (place_only && valid) scan_slots<SPL>(sv_, INVALID_KEY, jm1, jf1);
         bool placed = wabc_claim_issue<G>(wg, jf1, tv.bucket(b1), kv, valid && !done, pend, pend_prev,
                                           pend_item, op, ab);
         const bool want2 = two && !done && !placed;
         if (__any_sync(FULL, want2)) {
-            if (want2 && !have2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), s2);
+            if (want2 && !have2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), sv_);
             if (want2 && !have2 && wg.gl == 0) ab += 256;
             int jm2, jf2 = SPL;
-            if (want2) scan_slots<SPL>(s2, INVALID_KEY, jm2, jf2);
+            if (want2) scan_slots<SPL>(sv_, INVALID_KEY, jm2, jf2);
             const bool p2 = wabc_claim_issue<G>(wg, jf2, tv.bucket(b2), kv, want2, pend, pend_prev,
                                                 pend_item, op, ab);
             if (p2 && wg.gl == 0) {
@@ -1187,7 +1211,7 @@ static int env_g(const char* name, int dflt) {
 #define HIVE_DISPATCH_GM(g, mb, X)                     \
     if (mb >= 6) { HIVE_SWITCH_G(g, 6, X) }             \
     else if (mb == 5) { HIVE_SWITCH_G(g, 5, X) }        \
-    else if (mb >= 4) { HIVE_SWITCH_G(g, 4, X) }        \
+    else if (mb == 4) { HIVE_SWITCH_G(g, 4, X) }        \
     else { HIVE_SWITCH_G(g, 1, X) }
 
 #define HIVE_DISPATCH_GM8(g, mb, X)          \
