@@ -493,7 +493,55 @@ def secondary_measurements(table, keys, vals, queries, n, nb, dev, prof_main):
         "split_ms": p3.get("k_split", (0, 0))[0], "merge_ms": p3.get("k_merge", (0, 0))[0],
         "split_launches": p3.get("k_split", (0, 0))[1], "merge_launches": p3.get("k_merge", (0, 0))[1],
     }
+    res["cfg4_zipf"] = cfg4_zipf(dev)
     return res
+
+
+def cfg4_zipf(dev):
+    """BASELINE config 4: 2^21 buckets, growth off, prefill
+    0.90 * 2^26 keys; Z1 = 2^26 Zipf(0.99) ops over the present keys, 50%
+    insert (value = op index) / 50% find, in one mixed batch; Z2 = insert 2^22
+    Zipf draws over an absent universe of 0.05 * 2^26 keys (LF -> ~0.95, heavy
+    in-batch duplicates, Steps 3-4)."""
+    import torch
+
+    from paper_2510_15095_b200 import HiveTable, u8, u32
+    nb = 1 << 21
+    n_pre = int(0.90 * (1 << 26))
+    t = HiveTable(nb * 32, lf_grow=2.0, lf_shrink=0)
+    pre_ids = np.arange(n_pre, dtype=np.uint32)
+    pk, pv = u32(gen.keys_of(pre_ids), dev), u32(gen.vals_of(pre_ids), dev)
+    n1 = 1 << 26
+    r1 = gen.zipf_ranks(n1, n_pre, 0.99, seed=7)
+    k1 = u32(gen.keys_of((r1 - 1).astype(np.uint32)), dev)
+    ops1 = u8(np.where(np.random.default_rng(8).random(n1) < 0.5, 1, 0).astype(np.uint8), dev)
+    v1 = torch.arange(n1, dtype=torch.int64, device=dev).to(torch.int32).view(torch.uint32)
+    n2 = 1 << 22
+    r2 = gen.zipf_ranks(n2, int(0.05 * (1 << 26)), 0.99, seed=9)
+    k2 = u32(gen.keys_of((r2 - 1 + (1 << 31)).astype(np.uint32)), dev)
+    v2 = v1[:n2]
+    vo = torch.empty(n1, dtype=torch.uint32, device=dev)
+    rr = torch.empty(n1, dtype=torch.uint8, device=dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    out = {}
+    for rep in range(2):                        # rep 0 warms up (scratch sizing)
+        t.clear()
+        t.insert(pk, pv)
+        torch.cuda.synchronize()
+        ev[0].record()
+        t.mixed(ops1, k1, v1, vo, rr)
+        ev[1].record()
+        t.insert(k2, v2)
+        ev[2].record()
+        torch.cuda.synchronize()
+    s = t.stats()
+    hot = int((r1 == 1).sum())
+    out = {"z1_mixed_gops": n1 / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9,
+           "z2_insert_gops": n2 / (ev[1].elapsed_time(ev[2]) * 1e-3) / 1e9,
+           "z1_hot_key_copies": hot, "z2_distinct_keys": int(len(np.unique(r2))),
+           "final_lf": s["count"] / (nb * 32), "evictions": s["evictions"], "max_depth": s["max_depth"],
+           "stash_used": s["stash_used"], "leftovers": s["leftovers"]}
+    return out
 
 
 if __name__ == "__main__":

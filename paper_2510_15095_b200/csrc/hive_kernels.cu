@@ -885,9 +885,30 @@ __global__ void __launch_bounds__(BLOCK)
 k_dup_copy(const uint32_t* __restrict__ idx, uint64_t n, const uint64_t* __restrict__ n_dev,
            DedupView dd, uint8_t* __restrict__ out) {
     if (n_dev) n = *n_dev;
+    if (!idx) {                             // contiguous ops: 16 flags per load
+        const uint64_t nv = n / 16;
+        const uint4* f4 = reinterpret_cast<const uint4*>(dd.flag);
+        for (uint64_t v = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * BLOCK) {
+            const uint4 w = f4[v];
+            if ((w.x | w.y | w.z | w.w) == 0) continue;
+            for (int j = 0; j < 16; ++j) {
+                const uint64_t op = v * 16 + j;
+                if (!dd.flag[op]) continue;
+                const uint32_t o = dd.owner_of[op];
+                if (o != (uint32_t)op) out[op] = out[o];
+            }
+        }
+        for (uint64_t op = nv * 16 + (uint64_t)blockIdx.x * BLOCK + threadIdx.x; op < n;
+             op += (uint64_t)gridDim.x * BLOCK) {
+            if (!dd.flag[op]) continue;
+            const uint32_t o = dd.owner_of[op];
+            if (o != (uint32_t)op) out[op] = out[o];
+        }
+        return;
+    }
     for (uint64_t t = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; t < n;
          t += (uint64_t)gridDim.x * BLOCK) {
-        const uint64_t op = idx ? (uint64_t)idx[t] : t;
+        const uint64_t op = idx[t];
         if (!dd.flag[op]) continue;
         const uint32_t o = dd.owner_of[op];
         if (o != (uint32_t)op) out[op] = out[o];
