@@ -1,0 +1,43 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (slow: the sequential oracle takes about a minute per config)."""
+import numpy as np
+import pytest
+import torch
+
+import gen
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def test_cfg3_full_scale_mixed_with_resize():
+    """Config 3: 64 batches x 2^20 ops (40/20/40) over U = 2^26 from 1K buckets
+    with growth and shrink, then the id-order drain tail; every op's result and
+    the expansion trajectory equal the oracle's, batch by batch.
+
+    Mid-round, linear hashing leaves unsplit buckets ~1.35x over-subscribed by
+    first-choice keys; the oracle's paper-literal lowest-slot victim rule then
+    overflows a 2% stash within the first batches (the GPU's rotating victim
+    does not).  Stash capacity does not change any result unless it overflows,
+    so both sides run with a 30% stash here."""
+    from gpu_util import Pair
+    p = Pair(1024 * 32, stash_fraction=0.30)
+    nbat, bsz, U = 64, 1 << 20, 1 << 26
+    for b in range(nbat):
+        ops = gen.bernoulli_ops(bsz, 0.4, 0.2, seed=1000 + b)
+        ids = gen.uniform_ids(bsz, U, seed=2000 + b)
+        p.mixed(ops, gen.keys_of(ids), gen.vals_of(ids))
+        sg, so = p.g.stats(), p.o.stats()
+        assert (sg["n_buckets"], sg["m"], sg["split"]) == (so["n_buckets"], so["m"], so["split"]), b
+        assert sg["count"] == so["count"]
+    p.check_state()
+    assert p.g.stats()["n_buckets"] > 600_000
+    for lo in range(0, U, bsz):
+        p.erase(gen.keys_of(np.arange(lo, lo + bsz, dtype=np.uint32)))
+    sg, so = p.check_state(trajectory=False)
+    assert sg["count"] == 0 and (sg["merge_aborts"] > 0 or sg["n_buckets"] == 1024)
