@@ -362,8 +362,10 @@ hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* 
     // Large phases: hash-partition the ops so that each part's sub-table
     // (~32 MB) stays in L2 during its election launch (ncu: 18.5 G elections/s
     // with a 1 GiB table vs 49 G/s L2-resident).
+    static const uint64_t sub_bytes = getenv("HIVE_ELECT_MB") ? (uint64_t)atoi(getenv("HIVE_ELECT_MB")) << 20
+                                                              : (32ull << 20);
     uint32_t parts = 1;
-    while (parts < 32 && 2 * n_upper * sizeof(uint64_t) / parts > (32ull << 20)) parts *= 2;
+    while (parts < MAX_PARTS && 2 * n_upper * sizeof(uint64_t) / parts > sub_bytes) parts *= 2;
     const uint64_t sub = pow2_at_least(std::max<uint64_t>(1024, parts == 1 ? 2 * n_upper
                                                                           : (5 * n_upper / parts) / 2));
     CKS(ensure(h->dd, h->dd_cap, sub * parts));
