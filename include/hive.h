@@ -104,6 +104,9 @@ typedef struct {
                                 32 B per CAS sector, 8 B per spill / stash
                                 word, exact key / value / result stream
                                 bytes)                          */
+    uint64_t step3;          /* entries placed by the Step-3 loop (new keys,
+                                reinserted stash entries, lost fast claims);
+                                Step-2 placements = new keys - leftovers      */
 } hive_stats_t;
 
 /* Fill *cfg with the defaults above. */

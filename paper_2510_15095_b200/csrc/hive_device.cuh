@@ -83,7 +83,8 @@ struct Ctrl {
     unsigned long long dump_n;         // dump cursor
     unsigned long long in_b1;          // stats: keys resident in addr(h1)
     unsigned long long slow_next;      // Step-3 work queue cursor (this phase)
-    unsigned long long pad[4];
+    unsigned long long step3;          // entries placed by the Step-3 loop (cumulative)
+    unsigned long long pad[3];
     // Algorithmic bytes touched, per kernel family: 256 per
     // bucket probe, 32 per CAS / atomic sector, 8 per spill word or stash word,
     // exact bytes of the key / value / result streams.

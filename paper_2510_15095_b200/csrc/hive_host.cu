@@ -906,6 +906,7 @@ hive_status hive_stats(hive_t h, hive_stats_t* o) {
     o->in_b1 = c.in_b1;
     o->mapped_bytes = h->bk.mapped;
     for (int i = 0; i < 8; ++i) o->alg_bytes[i] = c.abytes[i];
+    o->step3 = c.step3;
     return c.failed ? HIVE_ESTASHFULL : HIVE_OK;
 }
 

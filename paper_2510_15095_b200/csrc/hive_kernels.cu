@@ -679,6 +679,7 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     wl.flush(leftover, &sv.ctrl->n_left);
     block_add(&sv.ctrl->count, added);
     block_add(&sv.ctrl->abytes[AB_INSERT], ab);
+
 }
 
 // --------------------------------------------------------------------------------
@@ -700,7 +701,7 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     WG wg;
     const uint64_t n = sv.ctrl->n_left;
     if (!kvs && blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(&sv.ctrl->leftovers, (unsigned long long)n);
-    unsigned long long evict = 0, depth = 0, pushes = 0, lost = 0, ab = 0;
+    unsigned long long evict = 0, depth = 0, pushes = 0, lost = 0, ab = 0, st3 = 0;
     // Dynamic scheduling: every warp iteration advances each busy group by one
     // eviction round; a group whose entry is placed (or stashed) immediately
     // takes the next leftover, so a warp never idles behind its longest chain.
@@ -785,6 +786,7 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         const bool finish = busy && (placed || r >= max_evictions);
         if (finish && wg.gl == 0) {
             depth = r > depth ? r : depth;
+            if (placed) ++st3;
             if (!placed) {                                   // Step 4: stash the in-hand entry
                 const unsigned long long pos = atomicAdd(&sv.ctrl->stash_tail, 1ull);
                 if (pos < sv.cap) {
@@ -808,6 +810,7 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     block_add(&sv.ctrl->count, (unsigned long long)(0ull - lost));
     block_max(&sv.ctrl->max_depth, depth);
     block_add(&sv.ctrl->abytes[AB_EVICT], ab);
+    block_add(&sv.ctrl->step3, st3);
 }
 
 // --------------------------------------------------------------------------------

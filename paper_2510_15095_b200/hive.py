@@ -39,7 +39,8 @@ class HiveStats(ctypes.Structure):
         (n, ctypes.c_uint64) for n in (
             "count", "stash_used", "stash_cap", "evictions", "max_depth", "stash_pushes", "leftovers",
             "grows", "shrinks", "merge_aborts", "failed", "in_b1", "mapped_bytes")] + [
-        ("alg_bytes", ctypes.c_uint64 * 8)]
+        ("alg_bytes", ctypes.c_uint64 * 8)] + [
+        ("step3", ctypes.c_uint64)]
 
 
 # every exported symbol of include/hive.h, with its ctypes signature
