@@ -205,6 +205,11 @@ hive_status hive_route(uint32_t n_shards, uint32_t seed, const uint32_t* d_keys,
                        uint64_t* d_send_kv, uint8_t* d_send_ops, uint32_t* d_pos,
                        uint64_t* d_counts, void* stream);
 
+/* Keys-only variant for find / erase batches: d_send_keys uint32[n] in shard
+ * order (half the bytes of the packed records, no unpack pass). */
+hive_status hive_route_keys(uint32_t n_shards, uint32_t seed, const uint32_t* d_keys, uint64_t n,
+                            uint32_t* d_send_keys, uint32_t* d_pos, uint64_t* d_counts, void* stream);
+
 /* Inverse permutation gather after the results come back:
  * d_out8[i] = d_in8[d_pos[i]] and d_out32[i] = d_in32[d_pos[i]]
  * (either pair may be NULL). */

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -954,24 +955,43 @@ int hive_profile_read(hive_t h, const char** names, double* ms, uint64_t* launch
     return k;
 }
 
-hive_status hive_route(uint32_t n_shards, uint32_t seed, const uint32_t* d_keys, const uint32_t* d_vals,
-                       const uint8_t* d_ops, uint64_t n, uint64_t* d_send_kv, uint8_t* d_send_ops,
-                       uint32_t* d_pos, uint64_t* d_counts, void* stream) {
+static hive_status route_impl(int mode, uint32_t n_shards, uint32_t seed, const uint32_t* d_keys,
+                              const uint32_t* d_vals, const uint8_t* d_ops, uint64_t n, uint64_t* d_send_kv,
+                              uint8_t* d_send_ops, uint32_t* d_pos, uint64_t* d_counts, void* stream) {
     if (n_shards == 0 || n_shards > (uint32_t)MAX_PARTS || !d_counts) return HIVE_EINVAL;
     if (n >= (1ull << 32)) return HIVE_EINVAL;
     if (n && (!d_keys || !d_send_kv || !d_pos || (d_send_ops && !d_ops))) return HIVE_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
-    uint64_t* cnt = nullptr;
-    uint64_t* info = nullptr;
+    // Per-device scratch kept for the life of the process: allocator calls cost
+    // 5-95 ms on this system and a stream-ordered pool releases its memory at
+    // every synchronisation.  Calls on one device are serialised by the lock.
+    struct RouteScratch { uint64_t* cnt = nullptr; uint64_t cap = 0; uint64_t* info = nullptr; };
+    static std::mutex mu;
+    static RouteScratch scratch[64];
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    RouteScratch& rs = scratch[dev & 63];
     const uint64_t E = (uint64_t)n_shards * part_warps(n) + 1;
-    CK(cudaMallocAsync((void**)&cnt, E * sizeof(uint64_t), s));
-    CK(cudaMallocAsync((void**)&info, 2 * MAX_PARTS * sizeof(uint64_t), s));
-    CK(launch_partition(s, PART_ROUTE, n_shards, seed, d_keys, d_vals, d_ops, n, cnt, info, nullptr, 0,
+    CKS(ensure(rs.cnt, rs.cap, E));
+    if (!rs.info) CK(cudaMalloc((void**)&rs.info, 2 * MAX_PARTS * sizeof(uint64_t)));
+    CK(launch_partition(s, mode, n_shards, seed, d_keys, d_vals, d_ops, n, rs.cnt, rs.info, nullptr, 0,
                         d_send_kv, d_send_ops, d_pos, nullptr, nullptr));
-    CK(cudaMemcpyAsync(d_counts, info, n_shards * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-    CK(cudaFreeAsync(cnt, s));
-    CK(cudaFreeAsync(info, s));
+    CK(cudaMemcpyAsync(d_counts, rs.info, n_shards * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
     return HIVE_OK;
+}
+
+hive_status hive_route(uint32_t n_shards, uint32_t seed, const uint32_t* d_keys, const uint32_t* d_vals,
+                       const uint8_t* d_ops, uint64_t n, uint64_t* d_send_kv, uint8_t* d_send_ops,
+                       uint32_t* d_pos, uint64_t* d_counts, void* stream) {
+    return route_impl(PART_ROUTE, n_shards, seed, d_keys, d_vals, d_ops, n, d_send_kv, d_send_ops, d_pos,
+                      d_counts, stream);
+}
+
+hive_status hive_route_keys(uint32_t n_shards, uint32_t seed, const uint32_t* d_keys, uint64_t n,
+                            uint32_t* d_send_keys, uint32_t* d_pos, uint64_t* d_counts, void* stream) {
+    return route_impl(PART_ROUTE_KEYS, n_shards, seed, d_keys, nullptr, nullptr, n, (uint64_t*)d_send_keys,
+                      nullptr, d_pos, d_counts, stream);
 }
 
 hive_status hive_unroute(const uint32_t* d_pos, uint64_t n, const uint8_t* d_in8, uint8_t* d_out8,

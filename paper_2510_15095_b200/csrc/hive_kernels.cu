@@ -1174,6 +1174,9 @@ k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __rest
                 if (result_zero) result_zero[i] = 0;
                 if (vals_zero) vals_zero[i] = 0;
             }
+        } else if (mode == PART_ROUTE_KEYS) {
+            reinterpret_cast<uint32_t*>(send_kv)[pos] = keys[i];
+            pos_out[i] = (uint32_t)pos;
         } else {
             send_kv[pos] = ((uint64_t)(vals ? vals[i] : 0u) << 32) | keys[i];
             if (send_ops) send_ops[pos] = ops[i];

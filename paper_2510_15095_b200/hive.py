@@ -63,6 +63,7 @@ SIGNATURES = {
     "hive_profile_read": (_int, [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
                                  ctypes.POINTER(_u64), _int, _int]),
     "hive_route": (_int, [_u32, _u32, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp]),
+    "hive_route_keys": (_int, [_u32, _u32, _vp, _u64, _vp, _vp, _vp, _vp]),
     "hive_unroute": (_int, [_vp, _u64, _vp, _vp, _vp, _vp, _vp]),
     "hive_unpack_kv": (_int, [_vp, _u64, _vp, _vp, _vp]),
     "hive_status_string": (ctypes.c_char_p, [_int]),
@@ -286,6 +287,18 @@ def route(keys: torch.Tensor, vals: torch.Tensor | None, ops: torch.Tensor | Non
     _check(lib().hive_route(n_shards, seed, _p(keys), _p(vals), _p(ops), n, _p(send_kv), _p(send_ops),
                             _p(pos), _p(counts), _stream(stream)), "hive_route")
     return send_kv, send_ops, pos, counts
+
+
+def route_keys(keys: torch.Tensor, n_shards: int, seed: int, stream=None):
+    """Keys-only stable partition: (send_keys uint32[n], pos int32[n], counts int64[G])."""
+    keys = _dev(keys, 4)
+    n = keys.numel()
+    send = torch.empty(n, dtype=torch.uint32, device=keys.device)
+    pos = torch.empty(n, dtype=torch.int32, device=keys.device)
+    counts = torch.empty(n_shards, dtype=torch.int64, device=keys.device)
+    _check(lib().hive_route_keys(n_shards, seed, _p(keys), n, _p(send), _p(pos), _p(counts), _stream(stream)),
+           "hive_route_keys")
+    return send, pos, counts
 
 
 def unroute(pos: torch.Tensor, in8: torch.Tensor | None = None, in32: torch.Tensor | None = None,

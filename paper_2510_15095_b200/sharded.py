@@ -37,6 +37,10 @@ class CudaOps:
         return hive.route(keys, vals, ops, n_shards, seed)
 
     @staticmethod
+    def route_keys(keys, n_shards, seed):
+        return hive.route_keys(keys, n_shards, seed)
+
+    @staticmethod
     def unroute(pos, in8=None, in32=None):
         return hive.unroute(pos, in8=in8, in32=in32)
 
@@ -91,8 +95,13 @@ class ShardedHive:
         out8, _ = self.ops.unroute(pos, in8=back)
         return out8
 
+    def _forward_keys(self, keys):
+        send, pos, counts = self.ops.route_keys(keys, self.world, self.seed)
+        sc, rc = self._counts(counts)
+        return self._a2a_u32(send, rc, sc), pos, sc, rc
+
     def find(self, keys):
-        k, _, _, pos, sc, rc = self._forward(keys, None, None)
+        k, pos, sc, rc = self._forward_keys(keys)
         vals, found = self.table.find(k)
         bv = self._a2a_u32(vals, sc, rc)
         bf = self._a2a_u8(found, sc, rc)
@@ -100,7 +109,7 @@ class ShardedHive:
         return v, f
 
     def erase(self, keys):
-        k, _, _, pos, sc, rc = self._forward(keys, None, None)
+        k, pos, sc, rc = self._forward_keys(keys)
         er = self.table.erase(k)
         back = self._a2a_u8(er, sc, rc)
         out8, _ = self.ops.unroute(pos, in8=back)

@@ -64,6 +64,17 @@ class OracleOps:
         return torch.from_numpy(kv.view(np.int64)), send_ops, torch.from_numpy(pos), counts
 
     @staticmethod
+    def route_keys(keys, n_shards, seed):
+        import oracle
+        k = keys.numpy().view(np.uint32)
+        sh = oracle.shard_array(k, seed, n_shards)
+        order = np.argsort(sh, kind="stable")
+        pos = np.empty(len(k), np.int32)
+        pos[order] = np.arange(len(k), dtype=np.int32)
+        counts = torch.from_numpy(np.bincount(sh, minlength=n_shards).astype(np.int64))
+        return _t32(k[order]), torch.from_numpy(pos), counts
+
+    @staticmethod
     def unroute(pos, in8=None, in32=None):
         p = pos.numpy()
         o8 = torch.from_numpy(in8.numpy()[p].copy()) if in8 is not None else None
