@@ -148,7 +148,7 @@ __device__ __forceinline__ void fill_empty(uint64_t (&s)[SPL]) {
 template <int G>
 __device__ __forceinline__ bool wcme_cas(const WarpGroup<G>& wg, uint64_t (&s)[WarpGroup<G>::SPL],
                                          uint64_t* bucket, uint32_t k, uint64_t newkv,
-                                         bool valid, unsigned long long& ab) {
+                                         bool valid, uint32_t& ab) {
     constexpr int SPL = WarpGroup<G>::SPL;
     bool trying = valid, done = false;
     for (int iter = 0; iter <= SLOTS; ++iter) {
@@ -181,7 +181,7 @@ __device__ __forceinline__ bool wcme_cas(const WarpGroup<G>& wg, uint64_t (&s)[W
 template <int G>
 __device__ __forceinline__ bool wabc_claim(const WarpGroup<G>& wg, uint64_t (&s)[WarpGroup<G>::SPL],
                                            uint64_t* bucket, uint64_t kv, bool want,
-                                           unsigned long long& ab) {
+                                           uint32_t& ab) {
     constexpr int SPL = WarpGroup<G>::SPL;
     bool trying = want, placed = false;
     for (int iter = 0; iter <= SLOTS; ++iter) {
@@ -214,7 +214,7 @@ __device__ __forceinline__ bool wabc_claim(const WarpGroup<G>& wg, uint64_t (&s)
 template <int G>
 __device__ __forceinline__ bool wabc_claim_issue(const WarpGroup<G>& wg, int jf, uint64_t* bucket, uint64_t kv,
                                                  bool want, bool& pend, uint64_t& pend_prev,
-                                                 uint32_t& pend_item, uint32_t item, unsigned long long& ab) {
+                                                 uint32_t& pend_item, uint32_t item, uint32_t& ab) {
     constexpr int SPL = WarpGroup<G>::SPL;
     const uint32_t F = wg.ballot(want && jf < SPL);
     if (want && F && wg.gl == __ffs(F) - 1) {
@@ -254,7 +254,7 @@ k_find(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint
     WG wg;
     if (n_dev) n = *n_dev;
     const bool stash_on = sv.ctrl->stash_tail != 0;
-    unsigned long long ab = 0;
+    uint32_t ab = 0;                       // per-thread: < 2^32 bytes
     const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
     // software pipeline: next iteration's (op, key) loads while this one probes
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(BLOCK)
 k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
               const uint64_t* __restrict__ n_dev, DedupView dd, Ctrl* ctrl) {
     if (n_dev) n = *n_dev;
-    unsigned long long ab = 0;
+    uint32_t ab = 0;                       // per-thread: < 2^32 bytes
     const int lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
     for (uint64_t t0 = (uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u); t0 < n; t0 += stride) {
@@ -372,7 +372,7 @@ k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict
     const uint64_t base = part_info[MAX_PARTS + part];
     const int lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
-    unsigned long long ab = 0;
+    uint32_t ab = 0;                       // per-thread: < 2^32 bytes
     for (uint64_t t0 = (uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u); t0 < n; t0 += stride) {
         const uint64_t t = t0 + lane;
         const bool active = t < n;
@@ -511,7 +511,7 @@ __device__ __forceinline__ uint32_t dedup_owner(const DedupView& dd, uint32_t k,
 // Owner check of one group (all lanes call): only flagged ops probe the table.
 template <int G>
 __device__ __forceinline__ bool owns(const WarpGroup<G>& wg, const DedupView& dd, bool valid,
-                                     uint32_t k, uint32_t op, unsigned long long& ab) {
+                                     uint32_t k, uint32_t op, uint32_t& ab) {
     if (!dd.slots) return true;
     uint32_t owner = (uint32_t)op;
     if (valid && wg.gl == 0) {
@@ -550,7 +550,8 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     if (n_dev) n = *n_dev;
     const bool place_only = kvs != nullptr;
     const bool stash_on = !place_only && sv.ctrl->stash_tail != 0;
-    unsigned long long added = 0, ab = 0;
+    unsigned long long added = 0;
+    uint32_t ab = 0;                       // per-thread: < 2^32 bytes
     bool pend = false;                     // this lane issued a claim last iteration
     uint64_t pend_prev = EMPTY;            // ... and this is its CAS result
     uint32_t pend_item = 0;
@@ -701,7 +702,8 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     WG wg;
     const uint64_t n = sv.ctrl->n_left;
     if (!kvs && blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(&sv.ctrl->leftovers, (unsigned long long)n);
-    unsigned long long evict = 0, depth = 0, pushes = 0, lost = 0, ab = 0, st3 = 0;
+    unsigned long long evict = 0, depth = 0, pushes = 0, lost = 0, st3 = 0;
+    uint32_t ab = 0;                       // per-thread: < 2^32 bytes
     // Dynamic scheduling: every warp iteration advances each busy group by one
     // eviction round; a group whose entry is placed (or stashed) immediately
     // takes the next leftover, so a warp never idles behind its longest chain.
@@ -827,7 +829,8 @@ k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uin
     WG wg;
     if (n_dev) n = *n_dev;
     const bool stash_on = sv.ctrl->stash_tail != 0;
-    unsigned long long removed = 0, ab = 0;
+    unsigned long long removed = 0;
+    uint32_t ab = 0;                       // per-thread: < 2^32 bytes
     const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
     for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
