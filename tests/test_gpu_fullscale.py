@@ -41,3 +41,25 @@ def test_cfg3_full_scale_mixed_with_resize():
         p.erase(gen.keys_of(np.arange(lo, lo + bsz, dtype=np.uint32)))
     sg, so = p.check_state(trajectory=False)
     assert sg["count"] == 0 and (sg["merge_aborts"] > 0 or sg["n_buckets"] == 1024)
+
+
+def test_cfg4_full_scale_zipf():
+    """Config 4: 2^21 buckets (growth off) prefilled with 0.90 * 2^26 keys; Z1 =
+    one 2^26-op mixed batch of Zipf(0.99) draws over the present keys (50%
+    insert with value = op index, 50% find: 3.3 M copies of the hottest key);
+    Z2 = 2^22 Zipf inserts over an absent universe.  Every status / value and
+    the final key -> value set equal the oracle's."""
+    from gpu_util import Pair
+    from phased_model import OP_FIND, OP_INSERT
+    nb = 1 << 21
+    p = Pair(nb * 32, lf_grow=2.0, lf_shrink=0)
+    n_pre = int(0.90 * (1 << 26))
+    ids = np.arange(n_pre, dtype=np.uint32)
+    p.insert(gen.keys_of(ids), gen.vals_of(ids))
+    n1 = 1 << 26
+    r1 = gen.zipf_ranks(n1, n_pre, 0.99, seed=7)
+    ops = np.where(np.random.default_rng(8).random(n1) < 0.5, OP_INSERT, OP_FIND).astype(np.uint8)
+    p.mixed(ops, gen.keys_of((r1 - 1).astype(np.uint32)), np.arange(n1, dtype=np.uint32))
+    r2 = gen.zipf_ranks(1 << 22, int(0.05 * (1 << 26)), 0.99, seed=9)
+    p.insert(gen.keys_of((r2 - 1 + (1 << 31)).astype(np.uint32)), np.arange(1 << 22, dtype=np.uint32))
+    p.check_state()
