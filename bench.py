@@ -435,13 +435,33 @@ def secondary_measurements(table, keys, vals, queries, n, nb, dev, prof_main):
         torch.cuda.synchronize()
         times.append((ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])))
     res["unique_updates_gps"] = n / (statistics.mean(t[0] for t in times) * 1e-3) / 1e9
+    del tu
+
+    # hash pairs (§V-B, Fig. 8): the step's insert + find on the BitHash1/2 pair
+    # vs the constant-memory CRC-32 / CRC-64 pair, same batch and table size
+    pairs = {}
+    for hp in ("bithash", "crc"):
+        th = HiveTable(nb * 32, lf_grow=2.0, lf_shrink=0, hash=hp)
+        for _ in range(2):
+            th.clear(); th.insert(keys, vals); th.find(queries)
+        times = []
+        for _ in range(3):
+            th.clear()
+            ev[0].record(); th.insert(keys, vals); ev[1].record(); th.find(queries); ev[2].record()
+            torch.cuda.synchronize()
+            times.append((ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])))
+        ti, tf = statistics.mean(t[0] for t in times), statistics.mean(t[1] for t in times)
+        pairs[hp] = {"insert_gops": n / (ti * 1e-3) / 1e9, "find_gops": n / (tf * 1e-3) / 1e9,
+                     "step_gops": 2 * n / ((ti + tf) * 1e-3) / 1e9}
+        del th
+    pairs["crc_vs_bithash_insert"] = pairs["crc"]["insert_gops"] / pairs["bithash"]["insert_gops"]
+    res["hash_pairs"] = pairs
     # erase half of the keys from the full table (dedup on)
     half = keys[: n // 2]
     table.clear(); table.insert(keys, vals)
     ev[0].record(); table.erase(half); ev[1].record()
     torch.cuda.synchronize()
     res["erase_gps"] = (n // 2) / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9
-    del tu
 
     # config 3: 64 batches x 2^20 mixed ops (40/20/40) over U = 2^26, 1K buckets
     # start, growth + shrink, then the id-order drain tail.

@@ -63,6 +63,13 @@ typedef enum {
                                  insert or erase batch -> the owner-election
                                  pass is skipped.  Results
                                  are undefined if the assertion is false. */
+#define HIVE_HASH_CRC    2u   /* use the lookup-based hash pair of §V-B
+                                 (PAPER:569-574): h1 = CRC-32/IEEE, h2 = low 32
+                                 bits of CRC-64/XZ, over the 4 little-endian key
+                                 bytes, byte-wise tables in constant memory
+                                 (reading A-26).  Default (flag clear):
+                                 BitHash1 / BitHash2 (Listing 1).  Any other
+                                 flag bit -> HIVE_EINVAL. */
 
 typedef struct {
     uint64_t capacity;       /* initial slots; rounded up to 32-slot buckets
@@ -76,7 +83,7 @@ typedef struct {
                                 (value A-8)                        */
     float    stash_fraction; /* stash capacity / slots, 0.02,
                                 floor 1024 entries                           */
-    uint32_t flags;          /* HIVE_KEYS_UNIQUE                              */
+    uint32_t flags;          /* HIVE_KEYS_UNIQUE | HIVE_HASH_CRC              */
 } hive_config;
 
 /* Stats snapshot (sync). */
@@ -216,6 +223,25 @@ hive_status hive_route_keys(uint32_t n_shards, uint32_t seed, const uint32_t* d_
 hive_status hive_unroute(const uint32_t* d_pos, uint64_t n, const uint8_t* d_in8,
                          uint8_t* d_out8, const uint32_t* d_in32, uint32_t* d_out32,
                          void* stream);
+
+/* ---- hash study (§III-C Listing 1 / Theorem 1 / CSR, §V-B pairs) -------------
+ * Hash functions by id: BitHash1 / BitHash2 (Listing 1), CRC-32
+ * (IEEE) and the low 32 bits of CRC-64 (XZ), both over the 4 little-endian key
+ * bytes from constant-memory tables (reading A-26). */
+#define HIVE_FN_BITHASH1 0u
+#define HIVE_FN_BITHASH2 1u
+#define HIVE_FN_CRC32    2u
+#define HIVE_FN_CRC64    3u
+/* d_out[i] = fn(d_keys[i]) for i < n (device arrays, caller-owned; async on
+ * `stream`).  HIVE_EINVAL for an unknown fn or null pointers with n > 0. */
+hive_status hive_hash(uint32_t fn, const uint32_t* d_keys, uint64_t n, uint32_t* d_out,
+                      void* stream);
+/* Observed collisions Y = sum_b (L_b - 1)_+ of the n device keys over m
+ * single-slot bins, bin = fn(k) mod m (Theorem 1; CSR =
+ * E[Y] / Y).  Synchronous; *y_out is a host word.  Uses a
+ * temporary m-bit device bitmap.  1 <= m <= 2^32, else HIVE_EINVAL. */
+hive_status hive_collisions(uint32_t fn, const uint32_t* d_keys, uint64_t n, uint64_t m,
+                            uint64_t* y_out, void* stream);
 
 /* Split packed records (value << 32 | key) into key / value arrays. */
 hive_status hive_unpack_kv(const uint64_t* d_kv, uint64_t n, uint32_t* d_keys,

@@ -93,6 +93,19 @@ def lib():
         L.oracle_prefix_rank.restype = u32
         L.oracle_select_nth_one.argtypes = [u32, u32]
         L.oracle_select_nth_one.restype = ctypes.c_int
+        L.oracle_crc32_bytes.argtypes = [vp, u64]
+        L.oracle_crc32_bytes.restype = u32
+        L.oracle_crc64_bytes.argtypes = [vp, u64]
+        L.oracle_crc64_bytes.restype = u64
+        for n in ("oracle_crc32", "oracle_crc64_lo"):
+            getattr(L, n).argtypes = [u32]
+            getattr(L, n).restype = u32
+        L.oracle_set_hash.argtypes = [vp, u32]
+        L.oracle_set_hash.restype = ctypes.c_int
+        L.oracle_uniform_expected_collisions.argtypes = [u64, u64]
+        L.oracle_uniform_expected_collisions.restype = ctypes.c_double
+        L.oracle_observed_collisions.argtypes = [u32, vp, u64, u64]
+        L.oracle_observed_collisions.restype = u64
         L.oracle_shard.argtypes = [u32, u32, u32]
         L.oracle_shard.restype = u32
         _lib = L
@@ -112,10 +125,12 @@ class OracleTable:
 
     def __init__(self, capacity: int, max_capacity: int = 0, lf_grow: float = 0.9,
                  lf_shrink: float = 0.25, max_evictions: int = 16, resize_k: int = 1024,
-                 stash_fraction: float = 0.02):
+                 stash_fraction: float = 0.02, hash: str = "bithash"):
         self._L = lib()
         self._h = self._L.oracle_create(capacity, max_capacity, lf_grow, lf_shrink,
                                         max_evictions, resize_k, stash_fraction)
+        if self._L.oracle_set_hash(self._h, HASH_KINDS.get(hash, 99)) != 0:
+            raise ValueError(hash)
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
@@ -185,6 +200,40 @@ class OracleTable:
 # --- primitives (for pins) ------------------------------------------------------
 def pack(k, v): return lib().oracle_pack(k, v)
 def unpack(p): return lib().oracle_unpack_key(p), lib().oracle_unpack_value(p)
+HASH_KINDS = {"bithash": 0, "crc": 1}
+HASH_FNS = {"bithash1": 0, "bithash2": 1, "crc32": 2, "crc64": 3}
+
+
+def crc32_bytes(b: bytes) -> int:
+    a = np.frombuffer(b, np.uint8).copy()
+    return lib().oracle_crc32_bytes(_ptr(a), len(a))
+
+
+def crc64_bytes(b: bytes) -> int:
+    a = np.frombuffer(b, np.uint8).copy()
+    return lib().oracle_crc64_bytes(_ptr(a), len(a))
+
+
+def crc32(k): return lib().oracle_crc32(k)
+def crc64_lo(k): return lib().oracle_crc64_lo(k)
+
+
+def uniform_expected_collisions(n: int, m: int) -> float:
+    """Theorem 1: E[Y] = n - m(1 - (1 - 1/m)^n)."""
+    return lib().oracle_uniform_expected_collisions(n, m)
+
+
+def observed_collisions(fn: str, keys, m: int) -> int:
+    """Y = sum_b (L_b - 1)_+ with bin = hash(k) mod m."""
+    k = _u32(keys)
+    return lib().oracle_observed_collisions(HASH_FNS[fn], _ptr(k), len(k), m)
+
+
+def csr(fn: str, keys, m: int) -> float:
+    """Collision Speedup Ratio E[Y] / Y_observed."""
+    return uniform_expected_collisions(len(keys), m) / observed_collisions(fn, keys, m)
+
+
 def bithash1(k): return lib().oracle_bithash1(k)
 def bithash2(k): return lib().oracle_bithash2(k)
 def addr(h, mask, split): return lib().oracle_addr(h, mask, split)

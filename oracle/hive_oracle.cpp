@@ -62,6 +62,44 @@ uint32_t BitHash2(uint32_t key) {
     return key;                               /* PAPER:248 */
 }
 
+/* ---- §III-C / §V-B lookup-based hashes (PAPER:254, 569-574; reading A-26):
+ * CRC-32/IEEE and CRC-64/XZ over the 4 little-endian key bytes, written
+ * here as the bit-serial definition of a reflected CRC (shift register, one
+ * polynomial reduction per input bit) rather than the byte-wise table the
+ * paper puts in constant memory -- same function, independent arithmetic. -- */
+uint32_t Crc32Bytes(const uint8_t* p, uint64_t n) {
+    uint32_t c = 0xFFFFFFFFu;                         /* init all ones */
+    for (uint64_t i = 0; i < n; ++i) {
+        c ^= p[i];
+        for (int bit = 0; bit < 8; ++bit)
+            c = (c & 1u) ? (c >> 1) ^ 0xEDB88320u : (c >> 1);   /* reflected 0x04C11DB7 */
+    }
+    return ~c;                                        /* xorout all ones */
+}
+uint64_t Crc64Bytes(const uint8_t* p, uint64_t n) {
+    uint64_t c = ~0ull;
+    for (uint64_t i = 0; i < n; ++i) {
+        c ^= p[i];
+        for (int bit = 0; bit < 8; ++bit)
+            c = (c & 1ull) ? (c >> 1) ^ 0xC96C5795D7870F42ull : (c >> 1);   /* reflected ECMA-182 */
+    }
+    return ~c;
+}
+uint32_t Crc32Key(uint32_t key) {
+    uint8_t b[4] = {(uint8_t)key, (uint8_t)(key >> 8), (uint8_t)(key >> 16), (uint8_t)(key >> 24)};
+    return Crc32Bytes(b, 4);
+}
+uint32_t Crc64Key(uint32_t key) {   /* low 32 bits of CRC-64 (reading A-26) */
+    uint8_t b[4] = {(uint8_t)key, (uint8_t)(key >> 8), (uint8_t)(key >> 16), (uint8_t)(key >> 24)};
+    return (uint32_t)Crc64Bytes(b, 4);
+}
+/* The table's hash pair: 0 = (BitHash1, BitHash2) (the paper's default,
+ * §V-B), 1 = (CRC-32, CRC-64) (the lookup-based pair of Fig. 8). */
+uint32_t HashPair(uint32_t kind, int which, uint32_t key) {
+    if (kind == 1) return which == 1 ? Crc32Key(key) : Crc64Key(key);
+    return which == 1 ? BitHash1(key) : BitHash2(key);
+}
+
 /* ---- §IV-C addressing: index_mask = 2^m - 1, split pointer (PAPER:485-488);
  * the address rule under a split pointer is Litwin's (reading A-2). -------- */
 uint32_t Addr(uint32_t h, uint32_t index_mask, uint32_t split) {
@@ -151,8 +189,11 @@ struct Table {
     uint32_t Mask() const { return (uint32_t)((1ull << m) - 1); }
     uint64_t* Slot(uint64_t b, int lane) { return &buckets[b * S + lane]; }
 
-    uint32_t B1(uint32_t k) const { return Addr(BitHash1(k), Mask(), split); }
-    uint32_t B2(uint32_t k) const { return Addr(BitHash2(k), Mask(), split); }
+    uint32_t hash_kind = 0;          /* HashPair kind */
+    uint32_t H1(uint32_t k) const { return HashPair(hash_kind, 1, k); }
+    uint32_t H2(uint32_t k) const { return HashPair(hash_kind, 2, k); }
+    uint32_t B1(uint32_t k) const { return Addr(H1(k), Mask(), split); }
+    uint32_t B2(uint32_t k) const { return Addr(H2(k), Mask(), split); }
 
     /* AltBucket (Alg. 3 line 31): the other candidate; equal candidates ->
      * cur; neither -> first candidate. */
@@ -381,7 +422,7 @@ struct Table {
             if (kv[l] == EMPTY) continue;
             uint32_t k = UnpackKey(kv[l]);
             /* reading A-3: the hash that addressed the entry to b_src */
-            uint32_t h = ((BitHash1(k) & index_mask) == b_src) ? BitHash1(k) : BitHash2(k);
+            uint32_t h = ((H1(k) & index_mask) == b_src) ? H1(k) : H2(k);
             should_move[l] = ((h & next_mask) == b_dst);
         }
         uint32_t move_mask = Ballot(should_move);
@@ -722,6 +763,34 @@ uint32_t oracle_unpack_key(uint64_t pair) { return UnpackKey(pair); }
 uint32_t oracle_unpack_value(uint64_t pair) { return UnpackValue(pair); }
 uint32_t oracle_bithash1(uint32_t key) { return BitHash1(key); }
 uint32_t oracle_bithash2(uint32_t key) { return BitHash2(key); }
+uint32_t oracle_crc32_bytes(const uint8_t* p, uint64_t n) { return Crc32Bytes(p, n); }
+uint64_t oracle_crc64_bytes(const uint8_t* p, uint64_t n) { return Crc64Bytes(p, n); }
+uint32_t oracle_crc32(uint32_t key) { return Crc32Key(key); }
+uint32_t oracle_crc64_lo(uint32_t key) { return Crc64Key(key); }
+int oracle_set_hash(oracle_t o, uint32_t kind) {
+    if (kind > 1 || o->t.count != 0) return 1;   /* only on an empty table */
+    o->t.hash_kind = kind;
+    return 0;
+}
+/* Theorem 1: E[Y] = n - m(1 - (1 - 1/m)^n). */
+double oracle_uniform_expected_collisions(uint64_t n, uint64_t m) {
+    return (double)n - (double)m * (1.0 - std::pow(1.0 - 1.0 / (double)m, (double)n));
+}
+/* Y = sum_b (L_b - 1)_+ over m single-slot bins, bin = h mod m (
+ * SPEC:187 reading), h = hash `fn` (0 BitHash1, 1 BitHash2, 2 CRC-32,
+ * 3 CRC-64 low word) of each key. */
+uint64_t oracle_observed_collisions(uint32_t fn, const uint32_t* keys, uint64_t n, uint64_t m) {
+    std::vector<uint64_t> load(m, 0);
+    for (uint64_t i = 0; i < n; ++i) {
+        uint32_t h = fn == 0 ? BitHash1(keys[i]) : fn == 1 ? BitHash2(keys[i])
+                   : fn == 2 ? Crc32Key(keys[i]) : Crc64Key(keys[i]);
+        ++load[h % m];
+    }
+    uint64_t y = 0;
+    for (uint64_t b = 0; b < m; ++b)
+        if (load[b] > 1) y += load[b] - 1;
+    return y;
+}
 uint32_t oracle_addr(uint32_t h, uint32_t index_mask, uint32_t split) { return Addr(h, index_mask, split); }
 uint32_t oracle_alt(uint32_t key, uint32_t cur, uint32_t index_mask, uint32_t split) {
     uint32_t c1 = Addr(BitHash1(key), index_mask, split), c2 = Addr(BitHash2(key), index_mask, split);

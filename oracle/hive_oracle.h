@@ -79,6 +79,17 @@ uint32_t oracle_unpack_key(uint64_t pair);
 uint32_t oracle_unpack_value(uint64_t pair);
 uint32_t oracle_bithash1(uint32_t key);
 uint32_t oracle_bithash2(uint32_t key);
+/* Lookup-based hashes of §V-B (reading A-26). */
+uint32_t oracle_crc32_bytes(const uint8_t* p, uint64_t n);   /* CRC-32/IEEE */
+uint64_t oracle_crc64_bytes(const uint8_t* p, uint64_t n);   /* CRC-64/XZ   */
+uint32_t oracle_crc32(uint32_t key);      /* over the 4 LE key bytes        */
+uint32_t oracle_crc64_lo(uint32_t key);   /* low 32 bits, 4 LE key bytes    */
+/* Select the table's hash pair (0 BitHash1/2, 1 CRC-32/CRC-64) on an empty
+ * table; nonzero return = refused. */
+int oracle_set_hash(oracle_t t, uint32_t kind);
+/* Theorem 1 and CSR. */
+double   oracle_uniform_expected_collisions(uint64_t n, uint64_t m);
+uint64_t oracle_observed_collisions(uint32_t fn, const uint32_t* keys, uint64_t n, uint64_t m);
 uint32_t oracle_addr(uint32_t h, uint32_t index_mask, uint32_t split);
 uint32_t oracle_alt(uint32_t key, uint32_t cur, uint32_t index_mask, uint32_t split);
 uint32_t oracle_ballot(const uint8_t* preds32);

@@ -50,6 +50,29 @@ __device__ __forceinline__ uint32_t bithash2(uint32_t key) {
     key = (key ^ 0xb55a4f09u) ^ (key >> 16);
     return key;
 }
+// ---- lookup-based pair, §V-B (reading A-26) ----------------------
+// "precomputed lookup tables stored in GPU constant memory": CRC-32/IEEE
+// (reflected polynomial 0xEDB88320) and CRC-64/XZ (reflected ECMA-182,
+// 0xC96C5795D7870F42), both init/xorout all-ones, over the 4 little-endian key
+// bytes; the CRC-64 result is reduced to its low 32 bits.  The tables are
+// filled by init_hash_tables() (hive_kernels.cu) — only that translation unit's
+// copy is ever read.
+static __constant__ uint32_t c_crc32_tab[256];
+static __constant__ uint64_t c_crc64_tab[256];
+__device__ __forceinline__ uint32_t crc32_key(uint32_t key) {
+    uint32_t c = 0xFFFFFFFFu;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c = c_crc32_tab[(c ^ (key >> (8 * i))) & 0xFFu] ^ (c >> 8);
+    return ~c;
+}
+__device__ __forceinline__ uint32_t crc64_key(uint32_t key) {
+    uint64_t c = ~0ull;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c = c_crc64_tab[(c ^ (key >> (8 * i))) & 0xFFu] ^ (c >> 8);
+    return (uint32_t)~c;
+}
+enum HashKind : uint32_t { HASH_BITHASH = 0, HASH_CRC = 1 };
+
 // MurmurHash3 finaliser: shard routing and the per-batch owner-election table
 // (independent of BitHash1/2).
 __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
@@ -103,6 +126,15 @@ struct TableView {
     // only ever added (erase leaves them; split copies, merge ORs), so a word
     // missing any of k's bits proves k is in no place but b1.
     uint64_t* spill;
+    uint32_t hkind;      // HashKind: the (h1, h2) pair of this table
+    // The two hash functions: BitHash1/2 (Listing 1, default) or the lookup-
+    // based CRC-32 / CRC-64 pair (§V-B).  The branch is warp-uniform.
+    __device__ __forceinline__ uint32_t h1(uint32_t k) const {
+        return hkind == HASH_CRC ? crc32_key(k) : bithash1(k);
+    }
+    __device__ __forceinline__ uint32_t h2(uint32_t k) const {
+        return hkind == HASH_CRC ? crc64_key(k) : bithash2(k);
+    }
     __device__ __forceinline__ uint32_t addr(uint32_t h) const {
         uint32_t b = h & mask;
         if (b < split) b = h & ((mask << 1) | 1u);
@@ -111,7 +143,7 @@ struct TableView {
     // AltBucket (Alg. 3 line 34): the other candidate, equal -> cur,
     // neither -> first.
     __device__ __forceinline__ uint32_t alt(uint32_t k, uint32_t cur) const {
-        uint32_t c1 = addr(bithash1(k)), c2 = addr(bithash2(k));
+        uint32_t c1 = addr(h1(k)), c2 = addr(h2(k));
         return cur == c1 ? c2 : (cur == c2 ? c1 : c1);
     }
     __device__ __forceinline__ uint64_t* bucket(uint32_t b) const {

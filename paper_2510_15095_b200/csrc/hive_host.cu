@@ -187,10 +187,11 @@ struct hive_table_s {
 
     uint64_t nb() const { return (1ull << m) + split; }
     TableView tv() const {
-        return TableView{(uint64_t*)va, (uint32_t)((1ull << m) - 1), split, (uint64_t*)sp.va};
+        return TableView{(uint64_t*)va, (uint32_t)((1ull << m) - 1), split, (uint64_t*)sp.va, hkind()};
     }
     StashView sv() const { return StashView{ring, sidx, stash_cap, idx_cap - 1, ctrl}; }
     bool dedup_on() const { return !(cfg.flags & HIVE_KEYS_UNIQUE); }
+    uint32_t hkind() const { return (cfg.flags & HIVE_HASH_CRC) ? HASH_CRC : HASH_BITHASH; }
     uint64_t stash_cap_for(uint64_t n_b) const {
         uint64_t c = (uint64_t)llround((double)cfg.stash_fraction * (double)n_b * SLOTS);
         return std::max<uint64_t>(1024, c);
@@ -526,7 +527,8 @@ hive_status shrink_after(hive_table_s* h, cudaStream_t s) {
     for (size_t i = 0; i < segs.size(); ++i) h->stage_h[8 + i] = segs[i].pairs;
     CK(cudaMemcpyAsync(h->aborts, h->stage_h + 8, segs.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
     for (size_t i = 0; i < segs.size(); ++i) {
-        TableView tv{(uint64_t*)h->va, (uint32_t)((1ull << segs[i].m) - 1), segs[i].split0, (uint64_t*)h->sp.va};
+        TableView tv{(uint64_t*)h->va, (uint32_t)((1ull << segs[i].m) - 1), segs[i].split0, (uint64_t*)h->sp.va,
+                     h->hkind()};
         Prof p(h, "k_merge", s);
         CK(launch_merge(s, tv, (uint32_t)segs[i].pairs, h->aborts + i, i ? h->aborts + i - 1 : nullptr,
                         i ? segs[i - 1].pairs : 0));
@@ -565,6 +567,18 @@ hive_status erase_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* i
 
 // ---- host-buffer pipeline -----------------------------------------------------------
 namespace {
+// CRC constant tables are per device (module constant memory): fill them once.
+bool ensure_hash_tables() {
+    static std::mutex mu;
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) { set_err(e, "cudaGetDevice", __LINE__); return false; }
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 64 && done[dev]) return true;
+    if (cudaError_t e = init_hash_tables(); e != cudaSuccess) { set_err(e, "init_hash_tables", __LINE__); return false; }
+    if (dev < 64) done[dev] = true;
+    return true;
+}
 constexpr uint64_t HOST_CHUNK = 1ull << 22;   // ops per transfer / launch chunk
 
 hive_status pipe_init(hive_table_s* h, size_t n_events) {
@@ -621,6 +635,7 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     if (!cfg || !out || cfg->capacity == 0 || cfg->stash_fraction < 0.0f) return HIVE_EINVAL;
     if (cfg->lf_grow < 1.0f && cfg->lf_shrink > 0.0f && cfg->lf_shrink >= cfg->lf_grow) return HIVE_EINVAL;
     if (cfg->lf_grow <= 0.0f) return HIVE_EINVAL;
+    if (cfg->flags & ~(HIVE_KEYS_UNIQUE | HIVE_HASH_CRC)) return HIVE_EINVAL;
     *out = nullptr;
     if (!load_vmm(g_vmm)) return HIVE_ECUDA;
     cudaStream_t s = (cudaStream_t)stream;
@@ -632,6 +647,7 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     if (cudaGetDevice(&h->dev) != cudaSuccess) return fail(HIVE_ECUDA);
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev);
     h->grids = query_grids(h->num_sms);
+    if (!ensure_hash_tables()) return fail(HIVE_ECUDA);
 
     // A-20: any n_b >= 2, held as (m = floor(log2 n_b), split = n_b - 2^m)
     const uint64_t nb = std::max<uint64_t>(2, (cfg->capacity + SLOTS - 1) / SLOTS);
@@ -1000,6 +1016,39 @@ hive_status hive_unroute(const uint32_t* d_pos, uint64_t n, const uint8_t* d_in8
     if (!d_pos || ((d_out8 != nullptr) != (d_in8 != nullptr)) || ((d_out32 != nullptr) != (d_in32 != nullptr)))
         return HIVE_EINVAL;
     CK(launch_unroute((cudaStream_t)stream, d_pos, n, d_in8, d_out8, d_in32, d_out32));
+    return HIVE_OK;
+}
+
+hive_status hive_hash(uint32_t fn, const uint32_t* d_keys, uint64_t n, uint32_t* d_out, void* stream) {
+    if (fn > HIVE_FN_CRC64) return HIVE_EINVAL;
+    if (n == 0) return HIVE_OK;
+    if (!d_keys || !d_out) return HIVE_EINVAL;
+    if (!ensure_hash_tables()) return HIVE_ECUDA;
+    CK(launch_hash((cudaStream_t)stream, fn, d_keys, n, d_out, nullptr, 1));
+    return HIVE_OK;
+}
+
+hive_status hive_collisions(uint32_t fn, const uint32_t* d_keys, uint64_t n, uint64_t m,
+                            uint64_t* y_out, void* stream) {
+    if (fn > HIVE_FN_CRC64 || m == 0 || m > (1ull << 32) || !y_out) return HIVE_EINVAL;
+    if (n && !d_keys) return HIVE_EINVAL;
+    if (!ensure_hash_tables()) return HIVE_ECUDA;
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint64_t words = (m + 31) / 32;
+    void* buf = nullptr;
+    CK(cudaMallocAsync(&buf, words * 4 + 8, s));
+    uint32_t* bins = (uint32_t*)((char*)buf + 8);
+    unsigned long long* total = (unsigned long long*)buf;
+    unsigned long long nonempty = 0;
+    cudaError_t e = cudaMemsetAsync(buf, 0, words * 4 + 8, s);
+    if (e == cudaSuccess && n) e = launch_hash(s, fn, d_keys, n, nullptr, bins, m);
+    if (e == cudaSuccess) e = launch_popc(s, bins, words, total);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&nonempty, total, 8, cudaMemcpyDeviceToHost, s);
+    cudaError_t e2 = cudaFreeAsync(buf, s);
+    if (e == cudaSuccess) e = e2;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) { set_err(e, "hive_collisions", __LINE__); return HIVE_ECUDA; }
+    *y_out = n - nonempty;      // sum_b (L_b - 1)_+ = n - #non-empty bins
     return HIVE_OK;
 }
 

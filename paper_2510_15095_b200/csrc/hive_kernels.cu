@@ -279,8 +279,8 @@ k_find(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint
         const bool valid = k != INVALID_KEY;
         uint32_t b1 = 0, b2 = 0;
         if (valid) {
-            b1 = tv.addr(bithash1(k));
-            b2 = tv.addr(bithash2(k));
+            b1 = tv.addr(tv.h1(k));
+            b2 = tv.addr(tv.h2(k));
         }
         uint64_t s[SPL];
         uint64_t spill_w = 0;
@@ -585,8 +585,8 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         bool valid = active && k != INVALID_KEY;
         uint32_t b1 = 0, b2 = 0;
         if (valid) {
-            b1 = tv.addr(bithash1(k));
-            b2 = tv.addr(bithash2(k));
+            b1 = tv.addr(tv.h1(k));
+            b2 = tv.addr(tv.h2(k));
         }
         bool two = valid && b2 != b1;
         const uint64_t fp = spill_fp(k);
@@ -739,8 +739,8 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             if (start) {
                 item = leftover[pos];
                 kv = kvs ? kvs[item] : pack(keys[item], vals[item]);
-                b = tv.addr(bithash1(key_of(kv)));               // start at b1
-                seed = bithash2(key_of(kv));
+                b = tv.addr(tv.h1(key_of(kv)));               // start at b1
+                seed = tv.h2(key_of(kv));
                 r = 0;
                 busy = true;
                 if (wg.gl == 0) ab += 4 + 8;
@@ -754,7 +754,7 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         if (busy && wg.gl == 0) ab += 256;
         const bool placed = wabc_claim<G>(wg, s, tv.bucket(b), kv, busy, ab);   // line 3
         if (placed) {
-            const uint32_t hb = tv.addr(bithash1(key_of(kv)));
+            const uint32_t hb = tv.addr(tv.h1(key_of(kv)));
             if (wg.gl == 0 && hb != b) {
                 atomicOr((unsigned long long*)&tv.spill[hb], (unsigned long long)spill_fp(key_of(kv)));
                 ab += 8;
@@ -775,7 +775,7 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         }
         ok = wg.bcast(ok, vl);
         if (evicting && ok) {
-            const uint32_t hb = tv.addr(bithash1(key_of(kv)));          // kv now lives in b
+            const uint32_t hb = tv.addr(tv.h1(key_of(kv)));          // kv now lives in b
             if (wg.gl == 0 && hb != b) {
                 atomicOr((unsigned long long*)&tv.spill[hb], (unsigned long long)spill_fp(key_of(kv)));
                 ab += 8;
@@ -792,7 +792,7 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             if (!placed) {                                   // Step 4: stash the in-hand entry
                 const unsigned long long pos = atomicAdd(&sv.ctrl->stash_tail, 1ull);
                 if (pos < sv.cap) {
-                    atomicOr((unsigned long long*)&tv.spill[tv.addr(bithash1(key_of(kv)))],
+                    atomicOr((unsigned long long*)&tv.spill[tv.addr(tv.h1(key_of(kv)))],
                              (unsigned long long)spill_fp(key_of(kv)));
                     sv.ring[pos] = kv;
                     stash_index_put(sv, key_of(kv), pos);
@@ -841,8 +841,8 @@ k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uin
         bool valid = k != INVALID_KEY;
         uint32_t b1 = 0, b2 = 0;
         if (valid) {
-            b1 = tv.addr(bithash1(k));
-            b2 = tv.addr(bithash2(k));
+            b1 = tv.addr(tv.h1(k));
+            b2 = tv.addr(tv.h2(k));
         }
         uint64_t s[SPL];
         uint64_t spill_w = 0;
@@ -941,8 +941,8 @@ k_split(TableView tv, uint32_t n_pairs, Ctrl* ctrl) {
     bool should_move = false;
     if (kv != EMPTY) {
         const uint32_t k = key_of(kv);
-        const uint32_t h1 = bithash1(k);
-        const uint32_t h = ((h1 & tv.mask) == b_src) ? h1 : bithash2(k);
+        const uint32_t h1 = tv.h1(k);
+        const uint32_t h = ((h1 & tv.mask) == b_src) ? h1 : tv.h2(k);
         should_move = (h & next_mask) == b_dst;
     }
     const uint32_t move_mask = __ballot_sync(FULL, should_move);
@@ -1040,7 +1040,7 @@ k_count_b1(TableView tv, uint64_t n_slots, Ctrl* ctrl) {
     for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < n_slots;
          i += (uint64_t)gridDim.x * BLOCK) {
         const uint64_t w = tv.buckets[i];
-        if (w != EMPTY && tv.addr(bithash1(key_of(w))) == (uint32_t)(i / SLOTS)) ++c;
+        if (w != EMPTY && tv.addr(tv.h1(key_of(w))) == (uint32_t)(i / SLOTS)) ++c;
     }
     block_add(&ctrl->in_b1, c);
 }
@@ -1265,6 +1265,26 @@ static int env_g(const char* name, int dflt) {
         }                                     \
     }
 
+// Byte-wise CRC tables of the §V-B lookup-based pair (reading A-26), written
+// to this module's constant memory on the current device.
+cudaError_t init_hash_tables() {
+    uint32_t t32[256];
+    uint64_t t64[256];
+    for (uint32_t b = 0; b < 256; ++b) {
+        uint32_t c = b;
+        uint64_t d = b;
+        for (int i = 0; i < 8; ++i) {
+            c = (c & 1u) ? (c >> 1) ^ 0xEDB88320u : (c >> 1);
+            d = (d & 1ull) ? (d >> 1) ^ 0xC96C5795D7870F42ull : (d >> 1);
+        }
+        t32[b] = c;
+        t64[b] = d;
+    }
+    cudaError_t e = cudaMemcpyToSymbol(c_crc32_tab, t32, sizeof(t32));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_crc64_tab, t64, sizeof(t64));
+    return e;
+}
+
 Grids query_grids(int num_sms) {
     Grids g;
     g.g_find = env_g("HIVE_G_FIND", G_FIND);
@@ -1402,6 +1422,47 @@ cudaError_t launch_unroute(cudaStream_t s, const uint32_t* pos, uint64_t n, cons
                            uint8_t* out8, const uint32_t* in32, uint32_t* out32) {
     const int grid = clamp_grid(1184, n, BLOCK);
     k_unroute<<<grid, BLOCK, 0, s>>>(pos, n, in8, out8, in32, out32);
+    return cudaGetLastError();
+}
+
+// ---- hash study (§III-C, Theorem 1 / CSR; §V-B pairs) -------------------------
+__device__ __forceinline__ uint32_t hash_fn(uint32_t fn, uint32_t k) {
+    switch (fn) {
+        case 0: return bithash1(k);
+        case 1: return bithash2(k);
+        case 2: return crc32_key(k);
+        default: return crc64_key(k);
+    }
+}
+__global__ void __launch_bounds__(BLOCK)
+k_hash(uint32_t fn, const uint32_t* __restrict__ keys, uint64_t n, uint32_t* __restrict__ out,
+       uint32_t* __restrict__ bins, uint64_t m) {
+    for (uint64_t i = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; i < n; i += (uint64_t)gridDim.x * BLOCK) {
+        const uint32_t h = hash_fn(fn, keys[i]);
+        if (out) out[i] = h;
+        if (bins) {                       // occupancy bitmap of bin = h mod m
+            const uint64_t b = h % m;
+            atomicOr(&bins[b >> 5], 1u << (b & 31));
+        }
+    }
+}
+__global__ void __launch_bounds__(BLOCK)
+k_popc(const uint32_t* __restrict__ bins, uint64_t words, unsigned long long* __restrict__ total) {
+    unsigned long long c = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; i < words; i += (uint64_t)gridDim.x * BLOCK)
+        c += __popc(bins[i]);
+    c = __reduce_add_sync(0xFFFFFFFFu, (unsigned)c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(total, c);
+}
+cudaError_t launch_hash(cudaStream_t s, uint32_t fn, const uint32_t* keys, uint64_t n, uint32_t* out,
+                        uint32_t* bins, uint64_t m) {
+    const int grid = (int)std::min<uint64_t>((n + BLOCK - 1) / BLOCK, 148ull * 16);
+    k_hash<<<grid, BLOCK, 0, s>>>(fn, keys, n, out, bins, m);
+    return cudaGetLastError();
+}
+cudaError_t launch_popc(cudaStream_t s, const uint32_t* bins, uint64_t words, unsigned long long* total) {
+    const int grid = (int)std::min<uint64_t>((words + BLOCK - 1) / BLOCK, 148ull * 16);
+    k_popc<<<grid > 0 ? grid : 1, BLOCK, 0, s>>>(bins, words, total);
     return cudaGetLastError();
 }
 

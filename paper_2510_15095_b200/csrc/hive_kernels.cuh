@@ -30,6 +30,9 @@ struct Grids {                           // persistent grid sizes (blocks)
 // Occupancy-derived persistent grid sizes for this device.
 Grids query_grids(int num_sms);
 
+// Fill the CRC-32 / CRC-64 constant tables (HASH_CRC) on the current device.
+cudaError_t init_hash_tables();
+
 cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                         uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
                         uint32_t* vals_out, uint8_t* found);
@@ -86,5 +89,11 @@ cudaError_t launch_unroute(cudaStream_t s, const uint32_t* pos, uint64_t n, cons
                            uint8_t* out8, const uint32_t* in32, uint32_t* out32);
 cudaError_t launch_unpack(cudaStream_t s, const uint64_t* kv, uint64_t n, uint32_t* keys,
                           uint32_t* vals);
+
+// Hash study: out[i] = fn(keys[i]) (fn 0 BitHash1, 1 BitHash2, 2 CRC-32,
+// 3 CRC-64 low word) and/or set bit (h mod m) of the `bins` bitmap.
+cudaError_t launch_hash(cudaStream_t s, uint32_t fn, const uint32_t* keys, uint64_t n, uint32_t* out,
+                        uint32_t* bins, uint64_t m);
+cudaError_t launch_popc(cudaStream_t s, const uint32_t* bins, uint64_t words, unsigned long long* total);
 
 }  // namespace hive

@@ -16,6 +16,9 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libhive.so")
 
 HIVE_KEYS_UNIQUE = 1
+HIVE_HASH_CRC = 2
+HASH_PAIRS = {"bithash": 0, "crc": HIVE_HASH_CRC}      # (BitHash1, BitHash2) / (CRC-32, CRC-64)
+HASH_FNS = {"bithash1": 0, "bithash2": 1, "crc32": 2, "crc64": 3}
 OP_FIND, OP_INSERT, OP_ERASE = 0, 1, 2
 INVALID_KEY = 0xFFFFFFFF
 
@@ -66,6 +69,8 @@ SIGNATURES = {
     "hive_route_keys": (_int, [_u32, _u32, _vp, _u64, _vp, _vp, _vp, _vp]),
     "hive_unroute": (_int, [_vp, _u64, _vp, _vp, _vp, _vp, _vp]),
     "hive_unpack_kv": (_int, [_vp, _u64, _vp, _vp, _vp]),
+    "hive_hash": (_int, [_u32, _vp, _u64, _vp, _vp]),
+    "hive_collisions": (_int, [_u32, _vp, _u64, _u64, ctypes.POINTER(_u64), _vp]),
     "hive_status_string": (ctypes.c_char_p, [_int]),
     "hive_last_error": (ctypes.c_char_p, []),
 }
@@ -135,7 +140,8 @@ class HiveTable:
 
     def __init__(self, capacity: int, max_capacity: int = 0, lf_grow: float = 0.9,
                  lf_shrink: float = 0.25, max_evictions: int = 16, resize_k: int = 1024,
-                 stash_fraction: float = 0.02, keys_unique: bool = False, stream=None):
+                 stash_fraction: float = 0.02, keys_unique: bool = False, hash: str = "bithash",
+                 stream=None):
         L = lib()
         if not torch.cuda.is_available():
             raise HiveError("no CUDA device: the Hive table runs only on the GPU")
@@ -144,7 +150,7 @@ class HiveTable:
         cfg.capacity, cfg.max_capacity = capacity, max_capacity
         cfg.lf_grow, cfg.lf_shrink = lf_grow, lf_shrink
         cfg.max_evictions, cfg.resize_k, cfg.stash_fraction = max_evictions, resize_k, stash_fraction
-        cfg.flags = HIVE_KEYS_UNIQUE if keys_unique else 0
+        cfg.flags = (HIVE_KEYS_UNIQUE if keys_unique else 0) | HASH_PAIRS[hash]
         self.cfg = cfg
         h = ctypes.c_void_p()
         _check(L.hive_create(ctypes.byref(cfg), ctypes.c_void_p(_stream(stream)), ctypes.byref(h)), "hive_create")
@@ -317,3 +323,19 @@ def unpack_kv(kv: torch.Tensor, stream=None):
     v = torch.empty(n, dtype=torch.uint32, device=kv.device)
     _check(lib().hive_unpack_kv(_p(kv), n, _p(k), _p(v), _stream(stream)), "hive_unpack_kv")
     return k, v
+
+
+def hash_keys(fn: str, keys: torch.Tensor, stream=None) -> torch.Tensor:
+    """hive_hash: fn(keys) on the device (fn in HASH_FNS)."""
+    n = keys.numel()
+    out = torch.empty(n, dtype=torch.uint32, device=keys.device)
+    _check(lib().hive_hash(HASH_FNS[fn], _p(keys), n, _p(out), _stream(stream)), "hive_hash")
+    return out
+
+
+def collisions(fn: str, keys: torch.Tensor, m: int, stream=None) -> int:
+    """hive_collisions: Y = sum_b (L_b - 1)_+ over m bins (Theorem 1)."""
+    y = _u64(0)
+    _check(lib().hive_collisions(HASH_FNS[fn], _p(keys), keys.numel(), m, ctypes.byref(y),
+                                 _stream(stream)), "hive_collisions")
+    return int(y.value)

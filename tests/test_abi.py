@@ -45,6 +45,15 @@ def test_status_strings_without_gpu():
     # argument validation happens before any CUDA call
     assert L.hive_insert(None, None, None, 0, None, None) == 1      # NULL handle -> EINVAL
     assert L.hive_route(0, 0, None, None, None, 0, None, None, None, None, None) == 1
+    assert L.hive_hash(7, None, 0, None, None) == 1                 # unknown hash fn
+    y = hive._u64(0)
+    assert L.hive_collisions(2, None, 0, 0, hive.ctypes.byref(y), None) == 1   # m = 0
+    cfg = hive.HiveConfig()
+    L.hive_config_default(hive.ctypes.byref(cfg))
+    assert cfg.flags == 0                                           # default pair: BitHash1/2
+    cfg.flags = 4                                                   # undefined flag bit
+    h = hive.ctypes.c_void_p()
+    assert L.hive_create(hive.ctypes.byref(cfg), None, hive.ctypes.byref(h)) == 1
 
 
 def test_product_never_imports_the_oracle():
