@@ -283,7 +283,7 @@ def main():
     p_h1 = st["in_b1"] / bucket_keys
     hbm_peak, peak_kind = peaks()
 
-    kern = {k: v[0] / v[1] for k, v in prof.items()}           # avg ms per launch
+    kern = {k: v[0] / v[1] for k, v in prof.items() if v[1]}   # avg ms per launch (memsets: 0 launches)
     launches = {k: v[1] for k, v in prof.items()}
     fam = {"k_find": "find", "k_insert_fast": "insert", "k_insert_slow": "evict", "k_erase": "erase",
            "k_dedup_elect": "elect"}

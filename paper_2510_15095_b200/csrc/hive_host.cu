@@ -151,6 +151,13 @@ struct hive_table_s {
     uint32_t* owner = nullptr; uint64_t owner_cap = 0;
     uint8_t* flag = nullptr;  uint64_t flag_cap = 0;
     uint64_t* erec = nullptr; uint64_t erec_cap = 0;     // election records (op << 32 | key)
+    uint32_t* dups = nullptr; uint64_t dups_cap = 0;     // election duplicate lists
+    unsigned long long* ndups = nullptr;                 // their lengths (MAX_PARTS)
+    const uint64_t* elect_tab = nullptr;                 // table the epochs below refer to
+    uint64_t elect_tab_words = 0;                        // its cleared extent
+    uint32_t elect_opbits = 0;
+    uint64_t elect_epoch = 0;                            // next free epoch
+    int coop_grid = 0;                                   // persistent election grid
     unsigned long long* ecount = nullptr;                // per-part counts + cursors
     uint64_t* einfo = nullptr;                           // per-part totals / bases
     uint32_t* left = nullptr; uint64_t left_cap = 0;
@@ -175,7 +182,7 @@ struct hive_table_s {
     unsigned long long* aborts = nullptr;   // per-segment first aborting merge pair
 
     // profiling
-    struct Rec { const char* name; cudaEvent_t a, b; };
+    struct Rec { const char* name; cudaEvent_t a, b; uint32_t launches; };
     bool prof = false;
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
@@ -224,7 +231,8 @@ struct Prof {
     const char* name;
     cudaStream_t s;
     cudaEvent_t a = nullptr;
-    Prof(hive_table_s* t, const char* nm, cudaStream_t st) : h(t), name(nm), s(st) {
+    uint32_t launches;                   // kernel launches inside the scope
+    Prof(hive_table_s* t, const char* nm, cudaStream_t st, uint32_t nl = 1) : h(t), name(nm), s(st), launches(nl) {
         if (h->prof) {
             a = get_event(h);
             cudaEventRecord(a, s);
@@ -234,7 +242,7 @@ struct Prof {
         if (h->prof) {
             cudaEvent_t b = get_event(h);
             cudaEventRecord(b, s);
-            h->recs.push_back({name, a, b});
+            h->recs.push_back({name, a, b, launches});
         }
     }
 };
@@ -366,30 +374,86 @@ hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* 
     // with a 1 GiB table vs 49 G/s L2-resident).
     static const uint64_t sub_bytes = getenv("HIVE_ELECT_MB") ? (uint64_t)atoi(getenv("HIVE_ELECT_MB")) << 20
                                                               : (32ull << 20);
+    // table entries per expected part record (HIVE_ELECT_F, experiments)
+    static const double fill = getenv("HIVE_ELECT_F") ? atof(getenv("HIVE_ELECT_F")) : 2.5;
     uint32_t parts = 1;
     while (parts < MAX_PARTS && 2 * n_upper * sizeof(uint64_t) / parts > sub_bytes) parts *= 2;
-    const uint64_t sub = pow2_at_least(std::max<uint64_t>(1024, parts == 1 ? 2 * n_upper
-                                                                          : (5 * n_upper / parts) / 2));
-    CKS(ensure(h->dd, h->dd_cap, sub * parts));
+    const uint64_t sub = pow2_at_least(std::max<uint64_t>(
+        1024, parts == 1 ? 2 * n_upper : (uint64_t)(fill * (double)n_upper / parts)));
+    CKS(ensure(h->dd, h->dd_cap, sub));
     CKS(ensure(h->owner, h->owner_cap, n_batch));
     CKS(ensure(h->flag, h->flag_cap, n_batch));
-    *dd = DedupView{h->dd, sub - 1, h->flag, h->owner, parts};
-    CK(cudaMemsetAsync(h->dd, 0xFF, sub * parts * sizeof(uint64_t), s));
+    CKS(ensure(h->dups, h->dups_cap, 2 * n_upper));
+    *dd = DedupView{h->dd, sub - 1, h->flag, h->owner, h->dups, h->ndups};
+    CK(cudaMemsetAsync(h->ndups, 0, MAX_PARTS * sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(h->flag, 0, n_batch, s));
+    const int rgrid = 2 * h->num_sms;
     if (parts == 1) {
-        Prof p(h, "k_dedup_elect", s);
+        Prof p(h, "k_dedup_elect", s, 2);
+        h->elect_tab = nullptr;                              // plain words: epochs invalid
+        CK(cudaMemsetAsync(h->dd, 0xFF, sub * sizeof(uint64_t), s));
         CK(launch_dedup_elect(h->grids.dedup, s, keys, idx, n_upper, n_dev, *dd, h->ctrl));
+        CK(launch_dedup_resolve(rgrid, s, keys, nullptr, 0, *dd));
         return HIVE_OK;
     }
     CKS(ensure(h->erec, h->erec_cap, n_upper));
+    // Persistent cooperative variant (epoch-tagged table, no per-part clears or
+    // launches): cfg2 step 11.64 ms vs 11.56 ms for the per-part launches below
+    // (its stale-entry reclaims miss L2, the per-part memsets pull the table into
+    // L2).  Kept behind HIVE_ELECT_COOP=1 and covered by the parity tests.
+    static const bool coop = getenv("HIVE_ELECT_COOP") ? atoi(getenv("HIVE_ELECT_COOP")) != 0 : false;
     {
-        Prof p(h, "k_elect_partition", s);
+        Prof p(h, "k_elect_partition", s, 3);
         CK(launch_elect_partition(s, keys, idx, n_upper, n_dev, parts, h->ecount, h->ecount + MAX_PARTS,
                                   h->einfo, h->erec, h->num_sms));
     }
-    Prof p(h, "k_dedup_elect", s);
-    for (uint32_t q = 0; q < parts; ++q)
-        CK(launch_dedup_elect_part(h->grids.dedup, s, h->erec, h->einfo, q, *dd, h->ctrl));
+    if (coop) {
+        // One persistent launch for all parts; table words carry the part's
+        // epoch, so the table is cleared only when the epochs run out.
+        uint32_t op_bits = 1;
+        while (op_bits < 32 && (1ull << op_bits) < n_batch) ++op_bits;
+        static const uint32_t min_bits = getenv("HIVE_ELECT_OPBITS") ? atoi(getenv("HIVE_ELECT_OPBITS")) : 1;
+        op_bits = std::max(op_bits, min_bits);             // tests: force few epochs / none
+        if (op_bits > 30) op_bits = 32;                    // no room for an epoch: clear per part
+        const uint64_t n_epochs = op_bits >= 32 ? 0 : (1ull << (32 - op_bits));
+        if (op_bits < 32) {
+            if (h->dd != h->elect_tab || op_bits != h->elect_opbits || h->elect_epoch + parts > n_epochs) {
+                Prof p(h, "elect_clear", s, 0);
+                CK(cudaMemsetAsync(h->dd, 0xFF, sub * sizeof(uint64_t), s));
+                h->elect_tab = h->dd;
+                h->elect_opbits = op_bits;
+                h->elect_epoch = 0;
+                h->elect_tab_words = sub;
+            } else if (sub > h->elect_tab_words) {
+                // words beyond the last cleared extent hold garbage: clear them
+                CK(cudaMemsetAsync(h->dd + h->elect_tab_words, 0xFF,
+                                   (sub - h->elect_tab_words) * sizeof(uint64_t), s));
+                h->elect_tab_words = sub;
+            }
+        } else {
+            h->elect_tab = nullptr;                          // in-kernel clears leave no epochs
+        }
+        Prof p(h, "k_dedup_elect", s);
+        CK(launch_elect_coop(h->coop_grid, s, h->erec, h->einfo, parts, keys, *dd, (uint32_t)h->elect_epoch,
+                             op_bits, h->ctrl));
+        h->elect_epoch += parts;
+        return HIVE_OK;
+    }
+    // One table for all parts, cleared right before each part: its lines stay
+    // in L2 (no DRAM fetch for the atomics, no write-back between parts).
+    h->elect_tab = nullptr;
+    for (uint32_t q = 0; q < parts; ++q) {
+        {
+            Prof p(h, "elect_clear", s, 0);
+            CK(cudaMemsetAsync(h->dd, 0xFF, sub * sizeof(uint64_t), s));
+        }
+        {
+            Prof p(h, "k_dedup_elect", s);
+            CK(launch_dedup_elect_part(h->grids.dedup, s, h->erec, h->einfo, q, *dd, h->ctrl));
+        }
+        Prof p(h, "k_dedup_resolve", s);
+        CK(launch_dedup_resolve(rgrid, s, keys, h->einfo, q, *dd));
+    }
     return HIVE_OK;
 }
 
@@ -406,7 +470,7 @@ hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* 
                          const uint64_t* n_dev, uint64_t n_batch, uint8_t* status,
                          uint32_t* vals_zero, cudaStream_t s, const InsertChunks* chunks = nullptr) {
     const bool dedup = !kvs && h->dedup_on();
-    DedupView dd{nullptr, 0, nullptr, nullptr};
+    DedupView dd{nullptr, 0, nullptr, nullptr, nullptr, nullptr};
     if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
     CKS(ensure(h->left, h->left_cap, std::max<uint64_t>(n_upper, 1)));
     CK(cudaMemsetAsync(&h->ctrl->n_left, 0, sizeof(uint64_t), s));
@@ -529,7 +593,7 @@ hive_status shrink_after(hive_table_s* h, cudaStream_t s) {
     for (size_t i = 0; i < segs.size(); ++i) {
         TableView tv{(uint64_t*)h->va, (uint32_t)((1ull << segs[i].m) - 1), segs[i].split0, (uint64_t*)h->sp.va,
                      h->hkind()};
-        Prof p(h, "k_merge", s);
+        Prof p(h, "k_merge", s, 2);
         CK(launch_merge(s, tv, (uint32_t)segs[i].pairs, h->aborts + i, i ? h->aborts + i - 1 : nullptr,
                         i ? segs[i - 1].pairs : 0));
     }
@@ -549,7 +613,7 @@ hive_status erase_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* i
                         const uint64_t* n_dev, uint64_t n_batch, uint8_t* out, uint32_t* vals_zero,
                         cudaStream_t s) {
     const bool dedup = h->dedup_on();
-    DedupView dd{nullptr, 0, nullptr, nullptr};
+    DedupView dd{nullptr, 0, nullptr, nullptr, nullptr, nullptr};
     if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
     {
         Prof p(h, "k_erase", s);
@@ -647,6 +711,7 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     if (cudaGetDevice(&h->dev) != cudaSuccess) return fail(HIVE_ECUDA);
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev);
     h->grids = query_grids(h->num_sms);
+    h->coop_grid = elect_coop_grid(h->num_sms);
     if (!ensure_hash_tables()) return fail(HIVE_ECUDA);
 
     // A-20: any n_b >= 2, held as (m = floor(log2 n_b), split = n_b - 2^m)
@@ -691,6 +756,8 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     if (cudaMalloc((void**)&h->einfo, 2 * MAX_PARTS * sizeof(uint64_t)) != cudaSuccess) return fail(HIVE_ENOMEM);
     if (cudaMalloc((void**)&h->ecount, 2 * MAX_PARTS * sizeof(unsigned long long)) != cudaSuccess)
         return fail(HIVE_ENOMEM);
+    if (cudaMalloc((void**)&h->ndups, MAX_PARTS * sizeof(unsigned long long)) != cudaSuccess)
+        return fail(HIVE_ENOMEM);
     if (cudaMalloc((void**)&h->aborts, MAX_SEGMENTS * sizeof(unsigned long long)) != cudaSuccess)
         return fail(HIVE_ENOMEM);
     memset(h->ctrl_h, 0, sizeof(Ctrl));
@@ -725,7 +792,7 @@ hive_status hive_destroy(hive_t h) {
     vrange_free(h->dr);
     vrange_free(h->sp);
     void* bufs[] = {h->ctrl, h->dd, h->owner, h->flag, h->left, h->cls, h->cnt, h->pinfo, h->aborts,
-                    h->erec, h->ecount, h->einfo, h->hk, h->hv, h->hst, h->fq, h->fv, h->ff};
+                    h->erec, h->ecount, h->einfo, h->dups, h->ndups, h->hk, h->hv, h->hst, h->fq, h->fv, h->ff};
     for (auto e : h->pipe_ev) cudaEventDestroy(e);
     if (h->ins_free) cudaEventDestroy(h->ins_free);
     if (h->find_free) cudaEventDestroy(h->find_free);
@@ -793,7 +860,7 @@ hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
     CKS(ensure(h->cls, h->cls_cap, 3 * n));
     CKS(ensure(h->cnt, h->cnt_cap, 3 * part_warps(n) + 1));
     {
-        Prof p(h, "k_classify", s);
+        Prof p(h, "k_classify", s, 3);
         CK(launch_partition(s, PART_CLASSIFY, 3, 0, d_keys, d_vals, d_op, n, h->cnt, h->pinfo, h->cls, n,
                             nullptr, nullptr, nullptr, d_result, d_vals_out));
     }
@@ -952,8 +1019,8 @@ int hive_profile_read(hive_t h, const char** names, double* ms, uint64_t* launch
         cudaEventElapsedTime(&t, r.a, r.b);
         bool hit = false;
         for (auto& a : h->agg)
-            if (strcmp(a.name, r.name) == 0) { a.ms += t; a.n++; hit = true; break; }
-        if (!hit) h->agg.push_back({r.name, (double)t, 1});
+            if (strcmp(a.name, r.name) == 0) { a.ms += t; a.n += r.launches; hit = true; break; }
+        if (!hit) h->agg.push_back({r.name, (double)t, r.launches});
         h->pool.push_back(r.a);
         h->pool.push_back(r.b);
     }
