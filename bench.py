@@ -342,6 +342,7 @@ def main():
         e2e = {"value": total_ops / (e_ms * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": 3 * 4 * n, "d2h_bytes_per_step": (1 + 4 + 1) * n,
                "ms_per_step": e_ms}
+        e2e.update(link_bound(keys_h, vals_h, q_h, st_h, vo_h, fo_h, e_ms))
 
     if sharded:
         # sharded public API with host buffers: H2D inputs, collective insert +
@@ -412,6 +413,46 @@ def main():
         print(json.dumps(line), flush=True)
     if sharded:
         dist.destroy_process_group()
+
+
+def link_bound(keys_h, vals_h, q_h, st_h, vo_h, fo_h, e_ms):
+    """Host link bound of the e2e step: the same pinned buffers copied alone
+    (H2D of the inputs, D2H of the results, each direction timed separately and
+    then both at once on two streams); bound = the concurrent copy time."""
+    import torch
+    dev = torch.device("cuda")
+    d_in = [torch.empty_like(x, device=dev) for x in (keys_h, vals_h, q_h)]
+    d_out = [torch.empty_like(x, device=dev) for x in (st_h, vo_h, fo_h)]
+    s_up, s_dn = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def run(up, down):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        torch.cuda.synchronize()
+        ev[0].record()
+        if up:
+            s_up.wait_event(ev[0])
+            with torch.cuda.stream(s_up):
+                for d, h in zip(d_in, (keys_h, vals_h, q_h)):
+                    d.copy_(h, non_blocking=True)
+        if down:
+            s_dn.wait_event(ev[0])
+            with torch.cuda.stream(s_dn):
+                for h, d in zip((st_h, vo_h, fo_h), d_out):
+                    h.copy_(d, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s_up)
+        torch.cuda.current_stream().wait_stream(s_dn)
+        ev[1].record()
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1])
+
+    run(True, True)
+    up_ms = min(run(True, False) for _ in range(2))
+    dn_ms = min(run(False, True) for _ in range(2))
+    both_ms = min(run(True, True) for _ in range(2))
+    h2d = sum(x.numel() * x.element_size() for x in (keys_h, vals_h, q_h))
+    d2h = sum(x.numel() * x.element_size() for x in (st_h, vo_h, fo_h))
+    return {"h2d_GBps": h2d / (up_ms * 1e-3) / 1e9, "d2h_GBps": d2h / (dn_ms * 1e-3) / 1e9,
+            "link_bound_ms": both_ms, "frac_of_link_bound": both_ms / e_ms}
 
 
 def secondary_measurements(table, keys, vals, queries, n, nb, dev, prof_main):

@@ -151,13 +151,6 @@ struct hive_table_s {
     uint32_t* owner = nullptr; uint64_t owner_cap = 0;
     uint8_t* flag = nullptr;  uint64_t flag_cap = 0;
     uint64_t* erec = nullptr; uint64_t erec_cap = 0;     // election records (op << 32 | key)
-    uint32_t* dups = nullptr; uint64_t dups_cap = 0;     // election duplicate lists
-    unsigned long long* ndups = nullptr;                 // their lengths (MAX_PARTS)
-    const uint64_t* elect_tab = nullptr;                 // table the epochs below refer to
-    uint64_t elect_tab_words = 0;                        // its cleared extent
-    uint32_t elect_opbits = 0;
-    uint64_t elect_epoch = 0;                            // next free epoch
-    int coop_grid = 0;                                   // persistent election grid
     unsigned long long* ecount = nullptr;                // per-part counts + cursors
     uint64_t* einfo = nullptr;                           // per-part totals / bases
     uint32_t* left = nullptr; uint64_t left_cap = 0;
@@ -374,85 +367,38 @@ hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* 
     // with a 1 GiB table vs 49 G/s L2-resident).
     static const uint64_t sub_bytes = getenv("HIVE_ELECT_MB") ? (uint64_t)atoi(getenv("HIVE_ELECT_MB")) << 20
                                                               : (32ull << 20);
-    // table entries per expected part record (HIVE_ELECT_F, experiments)
+    // sub-table entries per expected part record (HIVE_ELECT_F, experiments)
     static const double fill = getenv("HIVE_ELECT_F") ? atof(getenv("HIVE_ELECT_F")) : 2.5;
+    // HIVE_ELECT_JIT=0: clear all sub-tables up front (measured slower)
+    static const bool jit = getenv("HIVE_ELECT_JIT") ? atoi(getenv("HIVE_ELECT_JIT")) != 0 : true;
     uint32_t parts = 1;
     while (parts < MAX_PARTS && 2 * n_upper * sizeof(uint64_t) / parts > sub_bytes) parts *= 2;
     const uint64_t sub = pow2_at_least(std::max<uint64_t>(
         1024, parts == 1 ? 2 * n_upper : (uint64_t)(fill * (double)n_upper / parts)));
-    CKS(ensure(h->dd, h->dd_cap, sub));
+    CKS(ensure(h->dd, h->dd_cap, sub * parts));
     CKS(ensure(h->owner, h->owner_cap, n_batch));
     CKS(ensure(h->flag, h->flag_cap, n_batch));
-    CKS(ensure(h->dups, h->dups_cap, 2 * n_upper));
-    *dd = DedupView{h->dd, sub - 1, h->flag, h->owner, h->dups, h->ndups};
-    CK(cudaMemsetAsync(h->ndups, 0, MAX_PARTS * sizeof(unsigned long long), s));
+    *dd = DedupView{h->dd, sub - 1, h->flag, h->owner, parts};
     CK(cudaMemsetAsync(h->flag, 0, n_batch, s));
-    const int rgrid = 2 * h->num_sms;
+    if (parts == 1 || !jit) CK(cudaMemsetAsync(h->dd, 0xFF, sub * parts * sizeof(uint64_t), s));
     if (parts == 1) {
-        Prof p(h, "k_dedup_elect", s, 2);
-        h->elect_tab = nullptr;                              // plain words: epochs invalid
-        CK(cudaMemsetAsync(h->dd, 0xFF, sub * sizeof(uint64_t), s));
+        Prof p(h, "k_dedup_elect", s);
         CK(launch_dedup_elect(h->grids.dedup, s, keys, idx, n_upper, n_dev, *dd, h->ctrl));
-        CK(launch_dedup_resolve(rgrid, s, keys, nullptr, 0, *dd));
         return HIVE_OK;
     }
     CKS(ensure(h->erec, h->erec_cap, n_upper));
-    // Persistent cooperative variant (epoch-tagged table, no per-part clears or
-    // launches): cfg2 step 11.64 ms vs 11.56 ms for the per-part launches below
-    // (its stale-entry reclaims miss L2, the per-part memsets pull the table into
-    // L2).  Kept behind HIVE_ELECT_COOP=1 and covered by the parity tests.
-    static const bool coop = getenv("HIVE_ELECT_COOP") ? atoi(getenv("HIVE_ELECT_COOP")) != 0 : false;
     {
         Prof p(h, "k_elect_partition", s, 3);
         CK(launch_elect_partition(s, keys, idx, n_upper, n_dev, parts, h->ecount, h->ecount + MAX_PARTS,
                                   h->einfo, h->erec, h->num_sms));
     }
-    if (coop) {
-        // One persistent launch for all parts; table words carry the part's
-        // epoch, so the table is cleared only when the epochs run out.
-        uint32_t op_bits = 1;
-        while (op_bits < 32 && (1ull << op_bits) < n_batch) ++op_bits;
-        static const uint32_t min_bits = getenv("HIVE_ELECT_OPBITS") ? atoi(getenv("HIVE_ELECT_OPBITS")) : 1;
-        op_bits = std::max(op_bits, min_bits);             // tests: force few epochs / none
-        if (op_bits > 30) op_bits = 32;                    // no room for an epoch: clear per part
-        const uint64_t n_epochs = op_bits >= 32 ? 0 : (1ull << (32 - op_bits));
-        if (op_bits < 32) {
-            if (h->dd != h->elect_tab || op_bits != h->elect_opbits || h->elect_epoch + parts > n_epochs) {
-                Prof p(h, "elect_clear", s, 0);
-                CK(cudaMemsetAsync(h->dd, 0xFF, sub * sizeof(uint64_t), s));
-                h->elect_tab = h->dd;
-                h->elect_opbits = op_bits;
-                h->elect_epoch = 0;
-                h->elect_tab_words = sub;
-            } else if (sub > h->elect_tab_words) {
-                // words beyond the last cleared extent hold garbage: clear them
-                CK(cudaMemsetAsync(h->dd + h->elect_tab_words, 0xFF,
-                                   (sub - h->elect_tab_words) * sizeof(uint64_t), s));
-                h->elect_tab_words = sub;
-            }
-        } else {
-            h->elect_tab = nullptr;                          // in-kernel clears leave no epochs
-        }
-        Prof p(h, "k_dedup_elect", s);
-        CK(launch_elect_coop(h->coop_grid, s, h->erec, h->einfo, parts, keys, *dd, (uint32_t)h->elect_epoch,
-                             op_bits, h->ctrl));
-        h->elect_epoch += parts;
-        return HIVE_OK;
-    }
-    // One table for all parts, cleared right before each part: its lines stay
-    // in L2 (no DRAM fetch for the atomics, no write-back between parts).
-    h->elect_tab = nullptr;
+    // Each part's sub-table is cleared right before its launch: the memset
+    // leaves its lines in L2, where the election's CASes then hit.  The
+    // sub-tables stay intact for the probe kernels' owner lookups.
+    Prof p(h, "k_dedup_elect", s, parts);
     for (uint32_t q = 0; q < parts; ++q) {
-        {
-            Prof p(h, "elect_clear", s, 0);
-            CK(cudaMemsetAsync(h->dd, 0xFF, sub * sizeof(uint64_t), s));
-        }
-        {
-            Prof p(h, "k_dedup_elect", s);
-            CK(launch_dedup_elect_part(h->grids.dedup, s, h->erec, h->einfo, q, *dd, h->ctrl));
-        }
-        Prof p(h, "k_dedup_resolve", s);
-        CK(launch_dedup_resolve(rgrid, s, keys, h->einfo, q, *dd));
+        if (jit) CK(cudaMemsetAsync(h->dd + (uint64_t)q * sub, 0xFF, sub * sizeof(uint64_t), s));
+        CK(launch_dedup_elect_part(h->grids.dedup, s, h->erec, h->einfo, q, *dd, h->ctrl));
     }
     return HIVE_OK;
 }
@@ -470,7 +416,7 @@ hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* 
                          const uint64_t* n_dev, uint64_t n_batch, uint8_t* status,
                          uint32_t* vals_zero, cudaStream_t s, const InsertChunks* chunks = nullptr) {
     const bool dedup = !kvs && h->dedup_on();
-    DedupView dd{nullptr, 0, nullptr, nullptr, nullptr, nullptr};
+    DedupView dd{nullptr, 0, nullptr, nullptr};
     if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
     CKS(ensure(h->left, h->left_cap, std::max<uint64_t>(n_upper, 1)));
     CK(cudaMemsetAsync(&h->ctrl->n_left, 0, sizeof(uint64_t), s));
@@ -566,8 +512,12 @@ hive_status grow_before(hive_table_s* h, uint64_t n_ins, cudaStream_t s) {
 // LIFO pairs; each segment is one check+apply launch pair that stops at its
 // first aborting pair (and merges nothing if an earlier segment aborted);
 // one synchronising read returns how far the merges got.
-hive_status shrink_after(hive_table_s* h, cudaStream_t s) {
+// count_lb: a host-known lower bound on the live count (count at the phase
+// start minus the erase ops); when even it is above the contraction threshold
+// the device read -- a stream sync -- is skipped.
+hive_status shrink_after(hive_table_s* h, cudaStream_t s, int64_t count_lb = -1) {
     if (h->cfg.lf_shrink <= 0.0f || h->nb() <= h->nb_min) return HIVE_OK;
+    if (count_lb >= 0 && (double)count_lb >= (double)h->cfg.lf_shrink * (double)h->nb() * SLOTS) return HIVE_OK;
     CKS(read_ctrl(h, s));
     const uint64_t count = h->ctrl_h->count;
     struct Seg { uint32_t m, split0; uint64_t pairs; };
@@ -613,7 +563,7 @@ hive_status erase_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* i
                         const uint64_t* n_dev, uint64_t n_batch, uint8_t* out, uint32_t* vals_zero,
                         cudaStream_t s) {
     const bool dedup = h->dedup_on();
-    DedupView dd{nullptr, 0, nullptr, nullptr, nullptr, nullptr};
+    DedupView dd{nullptr, 0, nullptr, nullptr};
     if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
     {
         Prof p(h, "k_erase", s);
@@ -711,7 +661,6 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     if (cudaGetDevice(&h->dev) != cudaSuccess) return fail(HIVE_ECUDA);
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev);
     h->grids = query_grids(h->num_sms);
-    h->coop_grid = elect_coop_grid(h->num_sms);
     if (!ensure_hash_tables()) return fail(HIVE_ECUDA);
 
     // A-20: any n_b >= 2, held as (m = floor(log2 n_b), split = n_b - 2^m)
@@ -756,8 +705,6 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     if (cudaMalloc((void**)&h->einfo, 2 * MAX_PARTS * sizeof(uint64_t)) != cudaSuccess) return fail(HIVE_ENOMEM);
     if (cudaMalloc((void**)&h->ecount, 2 * MAX_PARTS * sizeof(unsigned long long)) != cudaSuccess)
         return fail(HIVE_ENOMEM);
-    if (cudaMalloc((void**)&h->ndups, MAX_PARTS * sizeof(unsigned long long)) != cudaSuccess)
-        return fail(HIVE_ENOMEM);
     if (cudaMalloc((void**)&h->aborts, MAX_SEGMENTS * sizeof(unsigned long long)) != cudaSuccess)
         return fail(HIVE_ENOMEM);
     memset(h->ctrl_h, 0, sizeof(Ctrl));
@@ -792,7 +739,7 @@ hive_status hive_destroy(hive_t h) {
     vrange_free(h->dr);
     vrange_free(h->sp);
     void* bufs[] = {h->ctrl, h->dd, h->owner, h->flag, h->left, h->cls, h->cnt, h->pinfo, h->aborts,
-                    h->erec, h->ecount, h->einfo, h->dups, h->ndups, h->hk, h->hv, h->hst, h->fq, h->fv, h->ff};
+                    h->erec, h->ecount, h->einfo, h->hk, h->hv, h->hst, h->fq, h->fv, h->ff};
     for (auto e : h->pipe_ev) cudaEventDestroy(e);
     if (h->ins_free) cudaEventDestroy(h->ins_free);
     if (h->find_free) cudaEventDestroy(h->find_free);
@@ -867,14 +814,17 @@ hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
     const uint64_t* n_find = h->pinfo + 0;
     const uint64_t* n_ins = h->pinfo + 1;
     const uint64_t* n_era = h->pinfo + 2;
+    int64_t count_lb = -1;
     if (h->cfg.lf_grow < 1.0f) {           // one sync: phase sizes + counters
         CK(cudaMemcpyAsync(h->stage_h, h->pinfo, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
         CKS(read_ctrl(h, s));
-        if (h->stage_h[1]) CKS(grow_known(h, h->ctrl_h->count, h->stage_h[1], s));
+        const uint64_t count0 = h->ctrl_h->count, n_erase = h->stage_h[2];
+        count_lb = count0 > n_erase ? (int64_t)(count0 - n_erase) : 0;
+        if (h->stage_h[1]) CKS(grow_known(h, count0, h->stage_h[1], s));
     }
     CKS(insert_phase(h, d_keys, d_vals, nullptr, h->cls + n, n, n_ins, n, d_result, d_vals_out, s));
     CKS(erase_phase(h, d_keys, h->cls + 2 * n, n, n_era, n, d_result, d_vals_out, s));
-    CKS(shrink_after(h, s));
+    CKS(shrink_after(h, s, count_lb));
     Prof p(h, "k_find", s);
     CK(launch_find(h->grids, s, d_keys, h->cls, n, n_find, h->tv(), h->sv(), d_vals_out, d_result));
     return HIVE_OK;

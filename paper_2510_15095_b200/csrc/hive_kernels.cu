@@ -5,7 +5,6 @@
 // 256 B bucket is touched once per probe).  Persistent grid-stride kernels of
 // 256 threads; one operation per 8-lane group (4 slots = one 256-bit load per
 // lane), so each warp keeps four independent bucket probes in flight.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -327,274 +326,87 @@ k_find(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint
 // once gets flag[op] = 1 (the first conflicting arrival flags the creator), so
 // the phase kernels consult the table only for those ops.
 // --------------------------------------------------------------------------------
-// Append op to a part's duplicate list (each record appends at most twice:
-// itself once, and the entry it displaced or matched).
-__device__ __forceinline__ void dup_push(const DedupView& dd, uint32_t* list, uint32_t part, uint32_t op) {
-    list[atomicAdd(&dd.n_dups[part], 1ull)] = op;
-}
-
-// Finish one election after its first-probe CAS returned `pv` at slot hh:
-// linear probing on collisions; on a match, flag and list the op and the
-// current owner, and raise the owner to max(op).
-__device__ __forceinline__ void elect_finish(const DedupView& dd, uint32_t* list, uint32_t part,
-                                             uint64_t word, uint64_t pv, uint64_t hh, bool listed,
-                                             uint32_t& ab) {
-    const uint32_t k = (uint32_t)(word >> 32), op = (uint32_t)word;
-    ab += 32;
-    for (uint64_t probe = 1; pv != EMPTY && probe <= dd.mask; ++probe) {
-        if ((uint32_t)(pv >> 32) == k) {
-            dd.flag[op] = 1;
-            dd.flag[(uint32_t)pv] = 1;
-            if (!listed) dup_push(dd, list, part, op);
-            dup_push(dd, list, part, (uint32_t)pv);
-            if (word > pv) atomicMax((unsigned long long*)&dd.slots[hh], (unsigned long long)word);
-            return;
+__global__ void __launch_bounds__(BLOCK)
+k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
+              const uint64_t* __restrict__ n_dev, DedupView dd, Ctrl* ctrl) {
+    if (n_dev) n = *n_dev;
+    uint32_t ab = 0;                       // per-thread: < 2^32 bytes
+    const int lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u); t0 < n; t0 += stride) {
+        const uint64_t t = t0 + lane;
+        const bool active = t < n;
+        const uint64_t op = active ? (idx ? (uint64_t)idx[t] : t) : 0;
+        const uint32_t k = active ? keys[op] : INVALID_KEY;
+        const uint32_t grp = __match_any_sync(FULL, k);
+        if (active) ab += 4 + (idx ? 4 : 0);
+        if (k == INVALID_KEY) continue;
+        if (__popc(grp) > 1) dd.flag[op] = 1;
+        if ((31 - __clz(grp)) != lane) continue;
+        const uint64_t word = ((uint64_t)k << 32) | op;
+        const uint32_t hk = fmix32(k ^ DEDUP_SEED);
+        uint64_t* tab = dd.sub(hk);
+        uint64_t h = hk & dd.mask;
+        for (uint64_t probe = 0; probe <= dd.mask; ++probe) {
+            const uint64_t prev = cas64(&tab[h], EMPTY, word);
+            ab += 32;
+            if (prev == EMPTY) break;
+            if ((uint32_t)(prev >> 32) == k) {
+                dd.flag[op] = 1;
+                dd.flag[(uint32_t)prev] = 1;
+                if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
+                break;
+            }
+            h = (h + 1) & dd.mask;
         }
-        hh = (hh + 1) & dd.mask;
-        pv = cas64(&dd.slots[hh], EMPTY, word);
-        ab += 32;
     }
+    block_add(&ctrl->abytes[AB_ELECT], ab);
 }
 
-// One part of a partitioned election: records (op << 32 | key) of part `part`.
-// Latency-bound (a load, then a dependent CAS): each warp takes EPR records per
-// lane per iteration and issues all of their loads, then all of their first-
-// probe CASes, before waiting on any result.
-template <bool MATCH, int EPR>
+// Election over one part of a hash-partitioned phase: input = the part's
+// (op << 32 | key) records in op order (stable partition), sub-table L2-resident.
 __global__ void __launch_bounds__(BLOCK)
 k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict__ part_info, uint32_t part,
                    DedupView dd, Ctrl* ctrl) {
     const uint64_t n = part_info[part];
     const uint64_t base = part_info[MAX_PARTS + part];
-    uint32_t* list = dd.dups + 2 * base;
     const int lane = threadIdx.x & 31;
-    const uint64_t wstride = (uint64_t)gridDim.x * BLOCK * EPR;
+    const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
     uint32_t ab = 0;                       // per-thread: < 2^32 bytes
-    for (uint64_t t0 = ((uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u)) * EPR; t0 < n; t0 += wstride) {
-        uint64_t w[EPR];
-#pragma unroll
-        for (int r = 0; r < EPR; ++r) {
-            const uint64_t t = t0 + r * 32 + lane;
-            w[r] = t < n ? recs[base + t] : EMPTY;
-        }
-        uint64_t word[EPR], prev[EPR], h[EPR];
-        bool lead[EPR], dup[EPR];
-#pragma unroll
-        for (int r = 0; r < EPR; ++r) {
-            const uint32_t k = (uint32_t)w[r], op = (uint32_t)(w[r] >> 32);
-            const bool active = w[r] != EMPTY;
-            uint32_t mx = op;
-            dup[r] = false;
-            if (MATCH) {
-                // input order inside a warp is arbitrary: elect the max op of
-                // the lanes holding the same key
-                const uint32_t grp = __match_any_sync(FULL, k);
-                dup[r] = active && __popc(grp) > 1;
-                if (dup[r]) {
-                    dd.flag[op] = 1;
-                    dup_push(dd, list, part, op);
-                    mx = __reduce_max_sync(grp, op);
-                }
-            }
-            lead[r] = active && op == mx;
-            word[r] = ((uint64_t)k << 32) | op;
-            h[r] = fmix32(k ^ DEDUP_SEED) & dd.mask;
-            if (active) ab += 8;
-        }
-#pragma unroll
-        for (int r = 0; r < EPR; ++r)
-            if (lead[r]) prev[r] = cas64(&dd.slots[h[r]], EMPTY, word[r]);
-#pragma unroll
-        for (int r = 0; r < EPR; ++r)
-            if (lead[r]) elect_finish(dd, list, part, word[r], prev[r], h[r], dup[r], ab);
-    }
-    block_add(&ctrl->abytes[AB_ELECT], ab);
-}
-
-// Single-table election (phases small enough for one L2-sized table): ops
-// are read in index order (idx: the classify list of the phase).
-template <bool MATCH, int EPR>
-__global__ void __launch_bounds__(BLOCK)
-k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
-              const uint64_t* __restrict__ n_dev, DedupView dd, Ctrl* ctrl) {
-    if (n_dev) n = *n_dev;
-    const int lane = threadIdx.x & 31;
-    const uint64_t wstride = (uint64_t)gridDim.x * BLOCK * EPR;
-    uint32_t ab = 0;                       // per-thread: < 2^32 bytes
-    for (uint64_t t0 = ((uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u)) * EPR; t0 < n; t0 += wstride) {
-        uint32_t opv[EPR], kv[EPR];
-#pragma unroll
-        for (int r = 0; r < EPR; ++r) {
-            const uint64_t t = t0 + r * 32 + lane;
-            opv[r] = t < n ? (idx ? idx[t] : (uint32_t)t) : 0xFFFFFFFFu;
-        }
-#pragma unroll
-        for (int r = 0; r < EPR; ++r) kv[r] = opv[r] != 0xFFFFFFFFu ? keys[opv[r]] : INVALID_KEY;
-        uint64_t word[EPR], prev[EPR], h[EPR];
-        bool lead[EPR], dup[EPR];
-#pragma unroll
-        for (int r = 0; r < EPR; ++r) {
-            const uint32_t k = kv[r], op = opv[r];
-            const bool active = k != INVALID_KEY;
-            if (op != 0xFFFFFFFFu) ab += 4 + (idx ? 4 : 0);
-            uint32_t mx = op;
-            dup[r] = false;
-            if (MATCH) {
-                const uint32_t grp = __match_any_sync(FULL, k);
-                dup[r] = active && __popc(grp) > 1;
-                if (dup[r]) {
-                    dd.flag[op] = 1;
-                    dup_push(dd, dd.dups, 0, op);
-                    mx = __reduce_max_sync(grp, op);
-                }
-            }
-            lead[r] = active && op == mx;
-            word[r] = ((uint64_t)k << 32) | op;
-            h[r] = fmix32(k ^ DEDUP_SEED) & dd.mask;
-        }
-#pragma unroll
-        for (int r = 0; r < EPR; ++r)
-            if (lead[r]) prev[r] = cas64(&dd.slots[h[r]], EMPTY, word[r]);
-#pragma unroll
-        for (int r = 0; r < EPR; ++r)
-            if (lead[r]) elect_finish(dd, dd.dups, 0, word[r], prev[r], h[r], dup[r], ab);
-    }
-    block_add(&ctrl->abytes[AB_ELECT], ab);
-}
-
-// ---- persistent election over all parts (one cooperative launch) ------------------
-// Table words are (key << 32) | (epoch << op_bits) | op: part q of a phase uses
-// epoch epoch0 + q, so an entry of another epoch counts as free and the table
-// is cleared only when the epochs run out (host side), not before every part.
-// Per part: elect (CAS, stale entries reclaimed by CAS), grid barrier, resolve
-// the part's duplicate list into owner_of, grid barrier.  clear_each (batches
-// too large for an epoch field) clears the table in-kernel before each part.
-struct EpochCode {
-    uint32_t op_bits;
-    uint32_t epoch;
-    __device__ __forceinline__ uint64_t word(uint32_t k, uint32_t op) const {
-        return ((uint64_t)k << 32) | ((uint64_t)epoch << op_bits) | op;
-    }
-    __device__ __forceinline__ bool live(uint64_t e) const {    // not EMPTY, this epoch
-        return e != EMPTY && (op_bits >= 32 || ((uint32_t)e >> op_bits) == epoch);
-    }
-    __device__ __forceinline__ uint32_t op_of(uint64_t e) const {
-        return op_bits >= 32 ? (uint32_t)e : ((uint32_t)e & ((1u << op_bits) - 1u));
-    }
-};
-
-__device__ __forceinline__ void elect_epoch(const DedupView& dd, uint32_t* list, uint32_t part,
-                                            const EpochCode& ec, uint32_t k, uint32_t op, bool listed,
-                                            uint32_t& ab) {
-    const uint64_t word = ec.word(k, op);
-    uint64_t h = fmix32(k ^ DEDUP_SEED) & dd.mask;
-    uint64_t pv = cas64(&dd.slots[h], EMPTY, word);
-    ab += 32;
-    for (uint64_t probe = 0; probe <= dd.mask;) {
-        if (pv == EMPTY) return;                               // claimed
-        if (!ec.live(pv)) {                                    // stale: reclaim
-            const uint64_t r = cas64(&dd.slots[h], pv, word);
-            ab += 32;
-            if (r == pv) return;
-            pv = r;
-            continue;
-        }
-        if ((uint32_t)(pv >> 32) == k) {                       // same key, this phase
-            const uint32_t o = ec.op_of(pv);
+    for (uint64_t t0 = (uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u); t0 < n; t0 += stride) {
+        const uint64_t t = t0 + lane;
+        const bool active = t < n;
+        const uint64_t w = active ? recs[base + t] : EMPTY;
+        const uint32_t k = (uint32_t)w, op = (uint32_t)(w >> 32);
+        const uint32_t grp = __match_any_sync(FULL, k);
+        if (active) ab += 8;
+        if (!active) continue;
+        // input order inside a warp is arbitrary here: elect the max op of the
+        // lanes holding the same key
+        uint32_t mx = op;
+        if (__popc(grp) > 1) {
             dd.flag[op] = 1;
-            dd.flag[o] = 1;
-            if (!listed) dup_push(dd, list, part, op);
-            dup_push(dd, list, part, o);
-            if (word > pv) atomicMax((unsigned long long*)&dd.slots[h], (unsigned long long)word);
-            return;
+            mx = __reduce_max_sync(grp, op);
         }
-        h = (h + 1) & dd.mask;
-        ++probe;
-        pv = cas64(&dd.slots[h], EMPTY, word);
-        ab += 32;
-    }
-}
-
-template <bool MATCH>
-__global__ void __launch_bounds__(BLOCK)
-k_elect_coop(const uint64_t* __restrict__ recs, const uint64_t* __restrict__ part_info, uint32_t n_parts,
-             const uint32_t* __restrict__ keys, DedupView dd, uint32_t epoch0, uint32_t op_bits,
-             Ctrl* ctrl) {
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
-    const int lane = threadIdx.x & 31;
-    const uint64_t gtid = (uint64_t)blockIdx.x * BLOCK + threadIdx.x;
-    const uint64_t gthreads = (uint64_t)gridDim.x * BLOCK;
-    uint32_t ab = 0;
-    for (uint32_t q = 0; q < n_parts; ++q) {
-        EpochCode ec{op_bits, op_bits >= 32 ? 0u : epoch0 + q};
-        if (op_bits >= 32) {                                   // no epoch field: clear
-            for (uint64_t i = gtid; i <= dd.mask; i += gthreads) dd.slots[i] = EMPTY;
-            grid.sync();
-        }
-        const uint64_t n = part_info[q];
-        const uint64_t base = part_info[MAX_PARTS + q];
-        uint32_t* list = dd.dups + 2 * base;
-        for (uint64_t t0 = gtid & ~31ull; t0 < n; t0 += gthreads) {
-            const uint64_t t = t0 + lane;
-            const bool active = t < n;
-            const uint64_t w = active ? recs[base + t] : EMPTY;
-            const uint32_t k = (uint32_t)w, op = (uint32_t)(w >> 32);
-            if (active) ab += 8;
-            uint32_t mx = op;
-            bool dup = false;
-            if (MATCH) {
-                const uint32_t grp = __match_any_sync(FULL, k);
-                dup = active && __popc(grp) > 1;
-                if (dup) {
-                    dd.flag[op] = 1;
-                    dup_push(dd, list, q, op);
-                    mx = __reduce_max_sync(grp, op);
-                }
-            }
-            if (active && op == mx) elect_epoch(dd, list, q, ec, k, op, dup, ab);
-        }
-        grid.sync();
-        const uint64_t nd = dd.n_dups[q];
-        for (uint64_t i = gtid; i < nd; i += gthreads) {
-            const uint32_t op = list[i];
-            const uint32_t k = keys[op];
-            uint64_t h = fmix32(k ^ DEDUP_SEED) & dd.mask;
-            uint32_t owner = op;
-            for (uint64_t probe = 0; probe <= dd.mask; ++probe) {
-                const uint64_t e = dd.slots[h];
-                if (!ec.live(e)) break;
-                if ((uint32_t)(e >> 32) == k) { owner = ec.op_of(e); break; }
-                h = (h + 1) & dd.mask;
-            }
-            dd.owner_of[op] = owner;
-        }
-        if (q + 1 < n_parts) grid.sync();
-    }
-    block_add(&ctrl->abytes[AB_ELECT], ab);
-}
-
-// Resolve: owner_of[op] for every listed op of part `part` (part_info null =
-// the single-table election), read from the table before it is reused.
-__global__ void __launch_bounds__(BLOCK)
-k_dedup_resolve(const uint32_t* __restrict__ keys, const uint64_t* __restrict__ part_info, uint32_t part,
-                DedupView dd) {
-    const uint64_t n = dd.n_dups[part];
-    const uint32_t* list = dd.dups + (part_info ? 2 * part_info[MAX_PARTS + part] : 0);
-    for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (uint64_t)gridDim.x * BLOCK) {
-        const uint32_t op = list[i];
-        const uint32_t k = keys[op];
+        if (op != mx) continue;
+        const uint64_t word = ((uint64_t)k << 32) | op;
         const uint32_t hk = fmix32(k ^ DEDUP_SEED);
+        uint64_t* tab = dd.sub(hk);
         uint64_t h = hk & dd.mask;
-        uint32_t owner = op;
         for (uint64_t probe = 0; probe <= dd.mask; ++probe) {
-            const uint64_t e = dd.slots[h];
-            if (e == EMPTY) break;
-            if ((uint32_t)(e >> 32) == k) { owner = (uint32_t)e; break; }
+            const uint64_t prev = cas64(&tab[h], EMPTY, word);
+            ab += 32;
+            if (prev == EMPTY) break;
+            if ((uint32_t)(prev >> 32) == k) {
+                dd.flag[op] = 1;
+                dd.flag[(uint32_t)prev] = 1;
+                if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
+                break;
+            }
             h = (h + 1) & dd.mask;
         }
-        dd.owner_of[op] = owner;
     }
+    block_add(&ctrl->abytes[AB_ELECT], ab);
 }
 
 // Hash partition of one phase's ops for the election (order inside a part is
@@ -751,6 +563,19 @@ cudaError_t launch_elect_partition(cudaStream_t s, const uint32_t* keys, const u
     return cudaGetLastError();
 }
 
+__device__ __forceinline__ uint32_t dedup_owner(const DedupView& dd, uint32_t k, uint32_t self) {
+    const uint32_t hk = fmix32(k ^ DEDUP_SEED);
+    const uint64_t* tab = dd.sub(hk);
+    uint64_t h = hk & dd.mask;
+    for (uint64_t probe = 0; probe <= dd.mask; ++probe) {
+        uint64_t e = tab[h];
+        if (e == EMPTY) return self;
+        if ((uint32_t)(e >> 32) == k) return (uint32_t)e;
+        h = (h + 1) & dd.mask;
+    }
+    return self;
+}
+
 // Owner check of one group (all lanes call): only flagged ops probe the table.
 template <int G>
 __device__ __forceinline__ bool owns(const WarpGroup<G>& wg, const DedupView& dd, bool valid,
@@ -760,8 +585,9 @@ __device__ __forceinline__ bool owns(const WarpGroup<G>& wg, const DedupView& dd
     if (valid && wg.gl == 0) {
         ab += 1;
         if (dd.flag[op]) {
-            owner = dd.owner_of[op];
-            ab += 4;
+            owner = dedup_owner(dd, k, op);
+            dd.owner_of[op] = owner;
+            ab += 8 + 4;
         }
     }
     return wg.bcast(owner, 0) == op;
@@ -1543,7 +1369,7 @@ Grids query_grids(int num_sms) {
     HIVE_DISPATCH_GM(g.g_insert, g.minb, OCC_INS)
     HIVE_DISPATCH_GM(g.g_slow, g.minb, OCC_SLOW)
     HIVE_DISPATCH_GM(g.g_erase, g.minb, OCC_ERA)
-    g.dedup = occ((const void*)k_dedup_elect<true, ELECT_EPR>) * num_sms;
+    g.dedup = occ((const void*)k_dedup_elect) * num_sms;
     g.stream = 4 * num_sms;
     return g;
 }
@@ -1565,44 +1391,14 @@ cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, c
 
 cudaError_t launch_dedup_elect_part(int grid, cudaStream_t s, const uint64_t* recs, const uint64_t* part_info,
                                     uint32_t part, DedupView dd, Ctrl* ctrl) {
-    static const bool match = getenv("HIVE_ELECT_MATCH") ? atoi(getenv("HIVE_ELECT_MATCH")) != 0 : true;
-    static const int epr = getenv("HIVE_ELECT_EPR") ? atoi(getenv("HIVE_ELECT_EPR")) : ELECT_EPR;
-#define L_EP(M, R) k_dedup_elect_part<M, R><<<grid, BLOCK, 0, s>>>(recs, part_info, part, dd, ctrl)
-    if (match) { if (epr == 1) L_EP(true, 1); else if (epr == 2) L_EP(true, 2); else L_EP(true, 4); }
-    else { if (epr == 1) L_EP(false, 1); else if (epr == 2) L_EP(false, 2); else L_EP(false, 4); }
-#undef L_EP
-    return cudaGetLastError();
-}
-
-int elect_coop_grid(int num_sms) {
-    return occ((const void*)k_elect_coop<true>) * num_sms;
-}
-
-cudaError_t launch_elect_coop(int grid, cudaStream_t s, const uint64_t* recs, const uint64_t* part_info,
-                              uint32_t n_parts, const uint32_t* keys, DedupView dd, uint32_t epoch0,
-                              uint32_t op_bits, Ctrl* ctrl) {
-    static const bool match = getenv("HIVE_ELECT_MATCH") ? atoi(getenv("HIVE_ELECT_MATCH")) != 0 : true;
-    void* args[] = {(void*)&recs, (void*)&part_info, (void*)&n_parts, (void*)&keys, (void*)&dd,
-                    (void*)&epoch0, (void*)&op_bits, (void*)&ctrl};
-    const void* fn = match ? (const void*)k_elect_coop<true> : (const void*)k_elect_coop<false>;
-    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BLOCK), args, 0, s);
-}
-
-cudaError_t launch_dedup_resolve(int grid, cudaStream_t s, const uint32_t* keys, const uint64_t* part_info,
-                                 uint32_t part, DedupView dd) {
-    k_dedup_resolve<<<grid, BLOCK, 0, s>>>(keys, part_info, part, dd);
+    k_dedup_elect_part<<<grid, BLOCK, 0, s>>>(recs, part_info, part, dd, ctrl);
     return cudaGetLastError();
 }
 
 cudaError_t launch_dedup_elect(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                                uint64_t n, const uint64_t* n_dev, DedupView dd, Ctrl* ctrl) {
     if (!n_dev) grid = clamp_grid(grid, n, BLOCK);
-    static const bool match = getenv("HIVE_ELECT_MATCH") ? atoi(getenv("HIVE_ELECT_MATCH")) != 0 : true;
-    static const int epr = getenv("HIVE_ELECT_EPR") ? atoi(getenv("HIVE_ELECT_EPR")) : ELECT_EPR;
-#define L_E(M, R) k_dedup_elect<M, R><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, dd, ctrl)
-    if (match) { if (epr == 1) L_E(true, 1); else if (epr == 2) L_E(true, 2); else L_E(true, 4); }
-    else { if (epr == 1) L_E(false, 1); else if (epr == 2) L_E(false, 2); else L_E(false, 4); }
-#undef L_E
+    k_dedup_elect<<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, dd, ctrl);
     return cudaGetLastError();
 }
 

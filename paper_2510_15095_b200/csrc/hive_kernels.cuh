@@ -15,7 +15,6 @@ constexpr int WARPS_PER_BLOCK = BLOCK / 32;
 constexpr int G_FIND = 4, G_INSERT = 4, G_ERASE = 2, G_SLOW = 2;
 constexpr int MINB_FIND_DEFAULT = 6;           // 40 regs: 3.60 ms vs 3.79 (48 regs) vs 4.60 (32, spills)
 constexpr int MINB_DEFAULT = 4;          // 4 blocks/SM => <= 64 registers (ncu: 74-80 regs left 36% warps active)
-constexpr int ELECT_EPR = 1;              // election records per lane per iteration
 constexpr int PART_CHUNK = 2048;         // elements per warp in the stable partition
 constexpr int MAX_PARTS = 64;
 
@@ -83,15 +82,6 @@ cudaError_t launch_elect_partition(cudaStream_t s, const uint32_t* keys, const u
                                    const uint64_t* n_dev, uint32_t n_parts, unsigned long long* gcount,
                                    unsigned long long* cursor, uint64_t* part_info, uint64_t* recs,
                                    int num_sms);
-// Persistent cooperative election of all parts of a partitioned phase
-// (epoch-tagged table words; op_bits >= 32: clear the table before each part).
-int elect_coop_grid(int num_sms);
-cudaError_t launch_elect_coop(int grid, cudaStream_t s, const uint64_t* recs, const uint64_t* part_info,
-                              uint32_t n_parts, const uint32_t* keys, DedupView dd, uint32_t epoch0,
-                              uint32_t op_bits, Ctrl* ctrl);
-// owner_of[] for the duplicate list of one part (part_info null: single table).
-cudaError_t launch_dedup_resolve(int grid, cudaStream_t s, const uint32_t* keys, const uint64_t* part_info,
-                                 uint32_t part, DedupView dd);
 cudaError_t launch_dedup_elect_part(int grid, cudaStream_t s, const uint64_t* recs, const uint64_t* part_info,
                                     uint32_t part, DedupView dd, Ctrl* ctrl);
 

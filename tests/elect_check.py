@@ -1,4 +1,4 @@
-"""Run by test_gpu_parity.test_election_epochs_and_modes in a subprocess (the
+"""Run by test_gpu_parity.test_election_modes_over_many_phases in a subprocess (the
 election knobs are read once per process): several partitioned-election
 batches with heavy duplicates, element-by-element against the oracle."""
 import os

@@ -213,21 +213,16 @@ def test_partitioned_owner_election_large_batches():
     p.find(rng.integers(0, 1 << 22, 1 << 20, dtype=np.uint64).astype(np.uint32))
 
 
-@pytest.mark.parametrize("env", [{}, {"HIVE_ELECT_COOP": "1"},
-                                 {"HIVE_ELECT_COOP": "1", "HIVE_ELECT_OPBITS": "30"},
-                                 {"HIVE_ELECT_COOP": "1", "HIVE_ELECT_OPBITS": "31"},
-                                 {"HIVE_ELECT_MATCH": "0"}])
-def test_election_epochs_and_modes(env):
+@pytest.mark.parametrize("env", [{}, {"HIVE_ELECT_JIT": "0"}, {"HIVE_ELECT_F": "1.2"}])
+def test_election_modes_over_many_phases(env):
     """Five rounds of duplicate-heavy 2^22-op partitioned phases (plus small
-    single-table phases in between) against the oracle, for the default
-    per-part election, the persistent cooperative variant with its epoch-
-    tagged table (default epochs, 2 epoch bits = a wrap every other phase, no
-    epoch field = in-kernel clears), and without in-warp pre-aggregation."""
+    single-table phases in between) against the oracle: sub-tables cleared just
+    in time (default) or up front, and a denser sub-table (longer probes)."""
     import os
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
-    r = subprocess.run([sys.executable, os.path.join(here, "elect_epoch_check.py")],
+    r = subprocess.run([sys.executable, os.path.join(here, "elect_check.py")],
                        env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-3000:]
 
