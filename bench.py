@@ -310,6 +310,8 @@ def main():
                 "kernel_ms": kern[dominant], "per_kernel": per_kernel,
                 "alg_bytes_rule": "counted in-kernel: 256 B per bucket probe, 32 B per CAS sector, "
                                   "8 B per spill/stash word, exact key/value/result streams"}
+    if not sharded:
+        roofline["ceilings"] = gather_ceiling(queries, nb, dev, per_kernel, hbm_peak)
 
     # ---- e2e through the public API with host buffers (pinned) ---------------------------
     e2e = None
@@ -413,6 +415,35 @@ def main():
         print(json.dumps(line), flush=True)
     if sharded:
         dist.destroy_process_group()
+
+
+def gather_ceiling(keys, nb, dev, per_kernel, hbm_peak, reps=5):
+    """SURVEY §8(d) calibration ceiling: hive_gather_ceiling reads one random
+    256 B block per key from an array the size of the cfg2 bucket array, with
+    k_find's lane groups and loads; its GB/s (256 B block + 4 B key + 4 B out per
+    op) is ceiling (iii), beside (i) nominal 8 TB/s and (ii) the measured copy."""
+    import torch
+    from paper_2510_15095_b200 import hive
+    blocks = torch.zeros(nb * 32, dtype=torch.int64, device=dev)
+    out = torch.empty(keys.numel(), dtype=torch.uint32, device=dev)
+    s = torch.cuda.current_stream()
+    for _ in range(2):
+        hive.gather_ceiling(blocks, keys, out, stream=s)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
+    for r in range(reps):
+        ev[2 * r].record(s)
+        hive.gather_ceiling(blocks, keys, out, stream=s)
+        ev[2 * r + 1].record(s)
+    torch.cuda.synchronize()
+    ms = statistics.mean(ev[2 * r].elapsed_time(ev[2 * r + 1]) for r in range(reps))
+    gbps = keys.numel() * (256 + 8) / (ms * 1e-3) / 1e9
+    del blocks, out
+    res = {"random_256B_gather_GBps": gbps, "gather_ms": ms, "gather_ops": keys.numel(),
+           "gather_array_bytes": nb * 256, "measured_copy_GBps": hbm_peak, "nominal_GBps": 8000.0}
+    for k, v in per_kernel.items():
+        res[k] = {"of_nominal": v["achieved_GBps"] / 8000.0, "of_copy": v["achieved_GBps"] / hbm_peak,
+                  "of_gather": v["achieved_GBps"] / gbps}
+    return res
 
 
 def link_bound(keys_h, vals_h, q_h, st_h, vo_h, fo_h, e_ms):

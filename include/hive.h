@@ -243,6 +243,17 @@ hive_status hive_hash(uint32_t fn, const uint32_t* d_keys, uint64_t n, uint32_t*
 hive_status hive_collisions(uint32_t fn, const uint32_t* d_keys, uint64_t n, uint64_t m,
                             uint64_t* y_out, void* stream);
 
+/* ---- calibration ceiling ------------------------------------
+ * The pure gather a probe reduces to, timed beside the probe kernels: for
+ * i < n, d_out[i] = xor of the 64 32-bit words of 256 B block
+ * b = (fmix32(d_keys[i]) * n_blocks) >> 32 of d_blocks, read with the same
+ * lane groups and 256-bit loads as the lookup kernel.  d_blocks: device,
+ * 256 B aligned, n_blocks * 256 B; d_keys uint32[n], d_out uint32[n] device,
+ * caller-owned.  Async on `stream`.  HIVE_EINVAL for null pointers with n > 0,
+ * misalignment, or n_blocks outside [1, 2^32]. */
+hive_status hive_gather_ceiling(const uint64_t* d_blocks, uint64_t n_blocks, const uint32_t* d_keys,
+                                uint64_t n, uint32_t* d_out, void* stream);
+
 /* Split packed records (value << 32 | key) into key / value arrays. */
 hive_status hive_unpack_kv(const uint64_t* d_kv, uint64_t n, uint32_t* d_keys,
                            uint32_t* d_vals, void* stream);

@@ -1045,6 +1045,24 @@ hive_status hive_hash(uint32_t fn, const uint32_t* d_keys, uint64_t n, uint32_t*
     return HIVE_OK;
 }
 
+hive_status hive_gather_ceiling(const uint64_t* d_blocks, uint64_t n_blocks, const uint32_t* d_keys,
+                                uint64_t n, uint32_t* d_out, void* stream) {
+    if (n == 0) return HIVE_OK;
+    if (!d_blocks || !d_keys || !d_out || n_blocks == 0 || n_blocks > (1ull << 32)) return HIVE_EINVAL;
+    if ((uintptr_t)d_blocks % 256) return HIVE_EINVAL;
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    static thread_local int grid_dev = -1;
+    static thread_local Grids gr{};
+    if (grid_dev != dev) {
+        gr = query_grids(sms);
+        grid_dev = dev;
+    }
+    CK(launch_gather(gr, (cudaStream_t)stream, d_keys, n, d_blocks, n_blocks, d_out));
+    return HIVE_OK;
+}
+
 hive_status hive_collisions(uint32_t fn, const uint32_t* d_keys, uint64_t n, uint64_t m,
                             uint64_t* y_out, void* stream) {
     if (fn > HIVE_FN_CRC64 || m == 0 || m > (1ull << 32) || !y_out) return HIVE_EINVAL;

@@ -1276,6 +1276,41 @@ k_unpack(const uint64_t* __restrict__ kv, uint64_t n, uint32_t* __restrict__ key
     }
 }
 
+// Calibration ceiling (SURVEY §8(d) "Calibration ceiling"): the pure gather a
+// probe reduces to.  Per op: read a 4 B key, pick a 256 B block by the
+// multiply-high reduction of fmix32(key), load it with the same group loads as
+// k_find (G lanes, 256-bit vectors), write one 4 B word (xor of the block).  No
+// compares, no second probe: random 256 B reads at the find kernel's access
+// count, against which the probe kernels' GB/s is judged.
+template <int G, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
+k_gather(const uint32_t* __restrict__ keys, uint64_t n, const uint64_t* __restrict__ blocks,
+         uint64_t n_blocks, uint32_t* __restrict__ out) {
+    using WG = WarpGroup<G>;
+    constexpr int SPL = WG::SPL;
+    WG wg;
+    const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
+    const uint64_t stride = (((uint64_t)gridDim.x * BLOCK) >> 5) * WG::GPW;
+    uint64_t t = warp * WG::GPW + wg.gi;
+    uint32_t k_n = t < n ? keys[t] : 0u;
+    for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += stride) {
+        t = t0 + wg.gi;
+        const uint32_t k = k_n;
+        if (t + stride < n) k_n = keys[t + stride];
+        uint64_t s[SPL];
+        uint32_t x = 0;
+        if (t < n) {
+            const uint64_t b = ((uint64_t)fmix32(k) * n_blocks) >> 32;
+            load_slots_ro<SPL>(blocks + b * SLOTS + wg.gl * SPL, s);
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) x ^= (uint32_t)s[j] ^ (uint32_t)(s[j] >> 32);
+        }
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) x ^= __shfl_xor_sync(FULL, x, o);
+        if (t < n && wg.gl == 0) out[t] = x;
+    }
+}
+
 // --------------------------------------------------------------------------------
 // launchers
 // --------------------------------------------------------------------------------
@@ -1369,6 +1404,8 @@ Grids query_grids(int num_sms) {
     HIVE_DISPATCH_GM(g.g_insert, g.minb, OCC_INS)
     HIVE_DISPATCH_GM(g.g_slow, g.minb, OCC_SLOW)
     HIVE_DISPATCH_GM(g.g_erase, g.minb, OCC_ERA)
+#define OCC_GATHER(G, MB) g.gather = occ((const void*)k_gather<G, MB>) * num_sms
+    HIVE_DISPATCH_GM8(g.g_find, g.minb_find, OCC_GATHER)
     g.dedup = occ((const void*)k_dedup_elect) * num_sms;
     g.stream = 4 * num_sms;
     return g;
@@ -1531,6 +1568,14 @@ cudaError_t launch_hash(cudaStream_t s, uint32_t fn, const uint32_t* keys, uint6
 cudaError_t launch_popc(cudaStream_t s, const uint32_t* bins, uint64_t words, unsigned long long* total) {
     const int grid = (int)std::min<uint64_t>((words + BLOCK - 1) / BLOCK, 148ull * 16);
     k_popc<<<grid > 0 ? grid : 1, BLOCK, 0, s>>>(bins, words, total);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const Grids& gr, cudaStream_t s, const uint32_t* keys, uint64_t n,
+                          const uint64_t* blocks, uint64_t n_blocks, uint32_t* out) {
+    const int grid = clamp_grid(gr.gather, n, BLOCK / gr.g_find);
+#define L_GATHER(G, MB) k_gather<G, MB><<<grid, BLOCK, 0, s>>>(keys, n, blocks, n_blocks, out)
+    HIVE_DISPATCH_GM8(gr.g_find, gr.minb_find, L_GATHER)
     return cudaGetLastError();
 }
 

@@ -21,7 +21,7 @@ constexpr int MAX_PARTS = 64;
 enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1, PART_ELECT = 2, PART_ROUTE_KEYS = 3 };
 
 struct Grids {                           // persistent grid sizes (blocks)
-    int find, insert_fast, insert_slow, erase, dedup, stream;
+    int find, insert_fast, insert_slow, erase, dedup, stream, gather;
     int g_find, g_insert, g_slow, g_erase;   // lanes per operation
     int minb;                                // min resident blocks/SM for the mutating kernels
     int minb_find;                           // ... and for k_find
@@ -32,6 +32,11 @@ Grids query_grids(int num_sms);
 
 // Fill the CRC-32 / CRC-64 constant tables (HASH_CRC) on the current device.
 cudaError_t init_hash_tables();
+
+// Calibration gather: random 256 B block reads at k_find's
+// access pattern; out[i] = xor of block (fmix32(keys[i]) * n_blocks) >> 32.
+cudaError_t launch_gather(const Grids& gr, cudaStream_t s, const uint32_t* keys, uint64_t n,
+                          const uint64_t* blocks, uint64_t n_blocks, uint32_t* out);
 
 cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                         uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,

@@ -70,6 +70,7 @@ SIGNATURES = {
     "hive_unroute": (_int, [_vp, _u64, _vp, _vp, _vp, _vp, _vp]),
     "hive_unpack_kv": (_int, [_vp, _u64, _vp, _vp, _vp]),
     "hive_hash": (_int, [_u32, _vp, _u64, _vp, _vp]),
+    "hive_gather_ceiling": (_int, [_vp, _u64, _vp, _u64, _vp, _vp]),
     "hive_collisions": (_int, [_u32, _vp, _u64, _u64, ctypes.POINTER(_u64), _vp]),
     "hive_status_string": (ctypes.c_char_p, [_int]),
     "hive_last_error": (ctypes.c_char_p, []),
@@ -330,6 +331,19 @@ def hash_keys(fn: str, keys: torch.Tensor, stream=None) -> torch.Tensor:
     n = keys.numel()
     out = torch.empty(n, dtype=torch.uint32, device=keys.device)
     _check(lib().hive_hash(HASH_FNS[fn], _p(keys), n, _p(out), _stream(stream)), "hive_hash")
+    return out
+
+
+def gather_ceiling(blocks: torch.Tensor, keys: torch.Tensor, out: torch.Tensor | None = None,
+                   stream=None) -> torch.Tensor:
+    """hive_gather_ceiling: random 256 B block reads at the lookup kernel's access
+    pattern (SURVEY §8(d) calibration ceiling); blocks is a uint64 tensor of
+    n_blocks * 32 words."""
+    n = keys.numel()
+    if out is None:
+        out = torch.empty(n, dtype=torch.uint32, device=keys.device)
+    _check(lib().hive_gather_ceiling(_p(blocks), blocks.numel() // 32, _p(keys), n, _p(out),
+                                     _stream(stream)), "hive_gather_ceiling")
     return out
 
 

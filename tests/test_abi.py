@@ -48,6 +48,7 @@ def test_status_strings_without_gpu():
     assert L.hive_hash(7, None, 0, None, None) == 1                 # unknown hash fn
     y = hive._u64(0)
     assert L.hive_collisions(2, None, 0, 0, hive.ctypes.byref(y), None) == 1   # m = 0
+    assert L.hive_gather_ceiling(None, 0, None, 1, None, None) == 1  # NULL blocks, n > 0
     cfg = hive.HiveConfig()
     L.hive_config_default(hive.ctypes.byref(cfg))
     assert cfg.flags == 0                                           # default pair: BitHash1/2

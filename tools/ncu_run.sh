@@ -16,3 +16,8 @@ python tools/erase_once.py > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_erase" -c 1 \
     -o gpurun_out/prof_erase python tools/erase_once.py > gpurun_out/prof_erase.log 2>&1
 ls -la gpurun_out
+# config-3 mixed run: per-launch durations of every kernel of the 64 batches
+ncu --metrics gpu__time_duration.sum --clock-control none --csv -c 4000 \
+    --log-file gpurun_out/launches_cfg3.csv python tools/prof_cfg3.py > gpurun_out/launches_cfg3.log 2>&1
+python tools/prof_cfg3.py > gpurun_out/prof_cfg3.json 2>&1
+ls -la gpurun_out
