@@ -168,6 +168,7 @@ struct hive_table_s {
     uint8_t* ff = nullptr; uint64_t ff_cap = 0;
     cudaStream_t up = nullptr, down = nullptr;
     cudaEvent_t ins_free = nullptr, find_free = nullptr;
+    cudaEvent_t ctrl_ev = nullptr;     // hive_mixed: control-block read completed
     std::vector<cudaEvent_t> pipe_ev;
 
     uint64_t grows = 0, shrinks = 0, merge_aborts = 0;
@@ -414,10 +415,12 @@ struct InsertChunks {
 hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* vals,
                          const uint64_t* kvs, const uint32_t* idx, uint64_t n_upper,
                          const uint64_t* n_dev, uint64_t n_batch, uint8_t* status,
-                         uint32_t* vals_zero, cudaStream_t s, const InsertChunks* chunks = nullptr) {
+                         uint32_t* vals_zero, cudaStream_t s, const InsertChunks* chunks = nullptr,
+                         const DedupView* pre = nullptr) {
     const bool dedup = !kvs && h->dedup_on();
     DedupView dd{nullptr, 0, nullptr, nullptr};
-    if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
+    if (dedup && pre) dd = *pre;                 // election already enqueued by the caller
+    else if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
     CKS(ensure(h->left, h->left_cap, std::max<uint64_t>(n_upper, 1)));
     CK(cudaMemsetAsync(&h->ctrl->n_left, 0, sizeof(uint64_t), s));
     CK(cudaMemsetAsync(&h->ctrl->slow_next, 0, sizeof(uint64_t), s));
@@ -743,6 +746,7 @@ hive_status hive_destroy(hive_t h) {
     for (auto e : h->pipe_ev) cudaEventDestroy(e);
     if (h->ins_free) cudaEventDestroy(h->ins_free);
     if (h->find_free) cudaEventDestroy(h->find_free);
+    if (h->ctrl_ev) cudaEventDestroy(h->ctrl_ev);
     if (h->up) cudaStreamDestroy(h->up);
     if (h->down) cudaStreamDestroy(h->down);
     for (void* b : bufs)
@@ -815,14 +819,31 @@ hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
     const uint64_t* n_ins = h->pinfo + 1;
     const uint64_t* n_era = h->pinfo + 2;
     int64_t count_lb = -1;
-    if (h->cfg.lf_grow < 1.0f) {           // one sync: phase sizes + counters
+    DedupView dd_ins{nullptr, 0, nullptr, nullptr};
+    bool pre = false;
+    if (h->cfg.lf_grow < 1.0f) {           // one wait: phase sizes + counters
+        if (!h->ctrl_ev) CK(cudaEventCreateWithFlags(&h->ctrl_ev, cudaEventDisableTiming));
         CK(cudaMemcpyAsync(h->stage_h, h->pinfo, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-        CKS(read_ctrl(h, s));
+        CK(cudaMemcpyAsync(h->ctrl_h, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(h->ctrl_ev, s));
+        // The insert phase's owner election does not depend on the table
+        // geometry: enqueue it before waiting, so the GPU has work while the
+        // host plans the resize from the count it just read.
+        if (h->dedup_on()) {
+            CKS(elect_owners(h, d_keys, h->cls + n, n, n_ins, n, &dd_ins, s));
+            pre = true;
+        }
+        {
+            Trace tr("read_ctrl", 0);
+            CK(cudaEventSynchronize(h->ctrl_ev));
+        }
+        h->tail_known = h->ctrl_h->stash_tail;
         const uint64_t count0 = h->ctrl_h->count, n_erase = h->stage_h[2];
         count_lb = count0 > n_erase ? (int64_t)(count0 - n_erase) : 0;
         if (h->stage_h[1]) CKS(grow_known(h, count0, h->stage_h[1], s));
     }
-    CKS(insert_phase(h, d_keys, d_vals, nullptr, h->cls + n, n, n_ins, n, d_result, d_vals_out, s));
+    CKS(insert_phase(h, d_keys, d_vals, nullptr, h->cls + n, n, n_ins, n, d_result, d_vals_out, s, nullptr,
+                     pre ? &dd_ins : nullptr));
     CKS(erase_phase(h, d_keys, h->cls + 2 * n, n, n_era, n, d_result, d_vals_out, s));
     CKS(shrink_after(h, s, count_lb));
     Prof p(h, "k_find", s);

@@ -780,6 +780,8 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     uint64_t kv = EMPTY;
     uint64_t qa = 0, qb = 0;                 // warp-uniform claimed range of leftover positions
     bool drained = n == 0;
+    bool have = false;                       // s already holds bucket b (prefetched)
+    uint64_t s[SPL];
     const uint32_t leaders = __ballot_sync(FULL, wg.gl == 0);
     while (true) {
         // ---- hand out work to idle groups ----
@@ -811,15 +813,19 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
                 seed = tv.h2(key_of(kv));
                 r = 0;
                 busy = true;
+                have = false;
                 if (wg.gl == 0) ab += 4 + 8;
             }
         }
         if (!__any_sync(FULL, busy)) continue;
         // ---- one round of Alg. 3 for every busy group ----
-        uint64_t s[SPL];
-        if (busy) load_slots<SPL>(wg.slot_ptr(tv.bucket(b)), s);
-        else fill_empty<SPL>(s);
-        if (busy && wg.gl == 0) ab += 256;
+        if (busy && !have) {
+            load_slots<SPL>(wg.slot_ptr(tv.bucket(b)), s);
+            if (wg.gl == 0) ab += 256;
+        } else if (!busy) {
+            fill_empty<SPL>(s);
+        }
+        have = false;
         const bool placed = wabc_claim<G>(wg, s, tv.bucket(b), kv, busy, ab);   // line 3
         if (placed) {
             const uint32_t hb = tv.addr(tv.h1(key_of(kv)));
@@ -835,13 +841,22 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         const int vs = (int)((seed + r * 11u) & 31u);
         const int vl = vs / SPL;
         const uint64_t victim = wg.bcast(pick<SPL>(s, vs % SPL), vl);
-        bool ok = false;
-        if (evicting && wg.gl == vl && victim != EMPTY) {
-            const uint64_t prev = cas64(tv.bucket(b) + vs, victim, kv);
+        const bool can = evicting && victim != EMPTY;
+        // The victim's next bucket is known now: its load is issued right after
+        // the swap CAS, so a round costs max(load, CAS) latency, not the sum.
+        // A lost CAS discards the prefetched view (the round reloads b).
+        const uint32_t nb = can ? tv.alt(key_of(victim), b) : b;
+        uint64_t prev = victim;
+        if (can && wg.gl == vl) {
+            prev = cas64(tv.bucket(b) + vs, victim, kv);
             ab += 32;
-            ok = (prev == victim);
         }
-        ok = wg.bcast(ok, vl);
+        const bool pf = can && r + 1 < max_evictions;       // the last round stashes instead
+        if (pf) {
+            load_slots<SPL>(wg.slot_ptr(tv.bucket(nb)), s);
+            if (wg.gl == 0) ab += 256;
+        }
+        const bool ok = wg.bcast(can && wg.gl == vl && prev == victim, vl);
         if (evicting && ok) {
             const uint32_t hb = tv.addr(tv.h1(key_of(kv)));          // kv now lives in b
             if (wg.gl == 0 && hb != b) {
@@ -849,7 +864,8 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
                 ab += 8;
             }
             kv = victim;                                     // line 33
-            b = tv.alt(key_of(kv), b);                       // line 34
+            b = nb;                                          // line 34: AltBucket
+            have = pf;
             if (wg.gl == 0) ++evict;
         }
         if (busy) ++r;
@@ -1128,26 +1144,42 @@ __device__ __forceinline__ uint32_t part_of(int mode, uint32_t n_parts, uint32_t
     return (uint32_t)(((uint64_t)fmix32(keys[i] ^ seed) * (uint64_t)n_parts) >> 32);
 }
 
+// Lanes of the warp holding the same label q (all lanes call).  Labels below
+// 16 (classify: 3 opcodes + invalid, routing: <= 8 shards + invalid) take 4
+// ballots; larger label sets use __match_any_sync (measured ~3x slower).
+__device__ __forceinline__ uint32_t same_label(uint32_t q, bool small) {
+    if (!small) return __match_any_sync(FULL, q);
+    uint32_t g = FULL;
+#pragma unroll
+    for (int bit = 0; bit < 4; ++bit) {
+        const uint32_t b = __ballot_sync(FULL, (q >> bit) & 1u);
+        g &= ((q >> bit) & 1u) ? b : ~b;
+    }
+    return g;
+}
+
 // Stable partition pass 1: per-warp, per-part counts (part-major layout).
 __global__ void __launch_bounds__(BLOCK)
 k_part_count(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __restrict__ keys,
              const uint8_t* __restrict__ ops, uint64_t n, uint64_t n_warps,
              uint64_t* __restrict__ cnt, const uint32_t* __restrict__ idx,
-             const uint64_t* __restrict__ n_dev) {
+             const uint64_t* __restrict__ n_dev, uint32_t chunk) {
     if (n_dev) n = *n_dev;
     __shared__ uint32_t sc[WARPS_PER_BLOCK][MAX_PARTS + 1];
+    const bool small = n_parts < 16;
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t w = (uint64_t)blockIdx.x * WARPS_PER_BLOCK + wib;
     for (int p = lane; p <= MAX_PARTS; p += 32) sc[wib][p] = 0;
     __syncwarp();
     if (w < n_warps) {
-        const uint64_t lo = w * PART_CHUNK;
-        const uint64_t hi = lo + PART_CHUNK < n ? lo + PART_CHUNK : (lo < n ? n : lo);
+        const uint64_t lo = w * chunk;
+        const uint64_t hi = lo + chunk < n ? lo + chunk : (lo < n ? n : lo);
         for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
             const uint64_t i = i0 + lane;
             const uint64_t e = i < hi ? (idx ? (uint64_t)idx[i] : i) : 0;
-            const uint32_t p = i < hi ? part_of(mode, n_parts, seed, keys, ops, e) : MAX_PARTS;
-            const uint32_t grp = __match_any_sync(FULL, p);
+            uint32_t p = i < hi ? part_of(mode, n_parts, seed, keys, ops, e) : MAX_PARTS;
+            if (small && p >= n_parts) p = MAX_PARTS;
+            const uint32_t grp = same_label(small && p == MAX_PARTS ? 15u : p, small);
             if ((__ffs(grp) - 1) == lane) sc[wib][p] += __popc(grp);
             __syncwarp();
         }
@@ -1213,22 +1245,24 @@ k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __rest
                uint64_t idx_stride, uint64_t* __restrict__ send_kv, uint8_t* __restrict__ send_ops,
                uint32_t* __restrict__ pos_out, uint8_t* __restrict__ result_zero,
                uint32_t* __restrict__ vals_zero, const uint32_t* __restrict__ idx,
-               const uint64_t* __restrict__ n_dev) {
+               const uint64_t* __restrict__ n_dev, uint32_t chunk) {
     __shared__ uint64_t run[WARPS_PER_BLOCK][MAX_PARTS + 1];
+    const bool small = n_parts < 16;
     if (n_dev) n = *n_dev;
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t w = (uint64_t)blockIdx.x * WARPS_PER_BLOCK + wib;
     if (w >= n_warps) return;
     for (uint32_t p = lane; p < n_parts; p += 32) run[wib][p] = off[(uint64_t)p * n_warps + w];
     __syncwarp();
-    const uint64_t lo = w * PART_CHUNK;
-    const uint64_t hi = lo + PART_CHUNK < n ? lo + PART_CHUNK : (lo < n ? n : lo);
+    const uint64_t lo = w * chunk;
+    const uint64_t hi = lo + chunk < n ? lo + chunk : (lo < n ? n : lo);
     for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
         const uint64_t i = i0 + lane;
         const bool in = i < hi;
         const uint64_t e = in ? (idx ? (uint64_t)idx[i] : i) : 0;
-        const uint32_t p = in ? part_of(mode, n_parts, seed, keys, ops, e) : MAX_PARTS;
-        const uint32_t grp = __match_any_sync(FULL, p);
+        uint32_t p = in ? part_of(mode, n_parts, seed, keys, ops, e) : MAX_PARTS;
+        if (small && p >= n_parts) p = MAX_PARTS;
+        const uint32_t grp = same_label(small && p == MAX_PARTS ? 15u : p, small);
         const uint32_t rank = __popc(grp & lanemask_lt());
         uint64_t pos = 0;
         if (in && p < n_parts) pos = run[wib][p] + rank;
@@ -1504,7 +1538,15 @@ cudaError_t launch_count_b1(int grid, cudaStream_t s, TableView tv, uint64_t n_b
     return cudaGetLastError();
 }
 
-uint64_t part_warps(uint64_t n) { return (n + PART_CHUNK - 1) / PART_CHUNK; }
+// Elements per warp of the stable partition: enough warps to fill the GPU for
+// small batches (a 2^20-op classify ran on 512 warps at 2048 per warp),
+// PART_CHUNK for large ones (bounds the single-block scan).
+uint32_t part_chunk(uint64_t n) {
+    uint64_t c = 256;
+    while (c < (uint64_t)PART_CHUNK && c * 16384 < n) c *= 2;
+    return (uint32_t)c;
+}
+uint64_t part_warps(uint64_t n) { const uint64_t c = part_chunk(n); return (n + c - 1) / c; }
 
 cudaError_t launch_partition(cudaStream_t s, int mode, uint32_t n_parts, uint32_t seed,
                              const uint32_t* keys, const uint32_t* vals, const uint8_t* ops,
@@ -1513,13 +1555,14 @@ cudaError_t launch_partition(cudaStream_t s, int mode, uint32_t n_parts, uint32_
                              uint8_t* send_ops, uint32_t* pos, uint8_t* result_zero,
                              uint32_t* vals_zero, const uint32_t* idx, const uint64_t* n_dev) {
     const uint64_t nw = part_warps(n);
+    const uint32_t chunk = part_chunk(n);
     const int grid = (int)((nw + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK);
-    if (nw) k_part_count<<<grid, BLOCK, 0, s>>>(mode, n_parts, seed, keys, ops, n, nw, cnt, idx, n_dev);
+    if (nw) k_part_count<<<grid, BLOCK, 0, s>>>(mode, n_parts, seed, keys, ops, n, nw, cnt, idx, n_dev, chunk);
     k_part_scan<<<1, 1024, 0, s>>>(cnt, (uint64_t)n_parts * nw, n_parts, nw, part_info);
     if (nw)
         k_part_scatter<<<grid, BLOCK, 0, s>>>(mode, n_parts, seed, keys, vals, ops, n, nw, cnt, part_info,
                                               out_idx, idx_stride, send_kv, send_ops, pos, result_zero,
-                                              vals_zero, idx, n_dev);
+                                              vals_zero, idx, n_dev, chunk);
     return cudaGetLastError();
 }
 
