@@ -128,3 +128,18 @@ def test_crc_pair_decides_placement():
     t = HiveTable(nb * 32, lf_grow=2.0, lf_shrink=0, stash_fraction=0.5)
     t.insert(_dev(keys), _dev(gen.vals_of(np.arange(100))))
     assert t.stats()["stash_used"] == 0
+
+
+@pytest.mark.parametrize("n,n_blocks", [(1, 1), (1000, 3), (33333, 4097), (1 << 20, 1 << 16)])
+def test_gather_ceiling_reads_the_named_blocks(n, n_blocks):
+    """hive_gather_ceiling (SURVEY §8(d) calibration ceiling, not the method):
+    out[i] = xor of the 64 32-bit words of block (fmix32(k_i) * n_blocks) >> 32."""
+    from paper_2510_15095_b200 import hive
+    rng = np.random.default_rng(n + n_blocks)
+    blocks = rng.integers(0, 1 << 63, n_blocks * 32, dtype=np.int64)
+    keys = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    out = hive.gather_ceiling(torch.from_numpy(blocks).cuda(), _dev(keys)).cpu().numpy().astype(np.uint32)
+    b = (gen.fmix32(keys).astype(np.uint64) * np.uint64(n_blocks)) >> np.uint64(32)
+    words = blocks.view(np.uint32).reshape(n_blocks, 64)
+    exp = np.bitwise_xor.reduce(words[b.astype(np.int64)], axis=1)
+    assert (out == exp).all()
