@@ -130,7 +130,9 @@ hive_status hive_destroy(hive_t h);
 
 /* Four-step insert / replace.  d_keys, d_vals: uint32[n].
  * d_status (nullable): uint8[n]; 0 = absent at phase start (inserted),
- * 1 = present (value replaced), 2 = reserved key, 3 = failed (stash full).
+ * 1 = present (value replaced), 2 = reserved key, 3 = this op's eviction
+ * chain found the stash full and dropped its in-hand entry (this key or a key
+ * it displaced; hive_stats.failed counts dropped entries, reading A-28).
  * May grow the table first (one small D2H of the counters when growth is
  * enabled). */
 hive_status hive_insert(hive_t h, const uint32_t* d_keys, const uint32_t* d_vals,

@@ -766,7 +766,6 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
               TableView tv, StashView sv, uint32_t max_evictions, uint8_t* __restrict__ status) {
     using WG = WarpGroup<G>;
     constexpr int SPL = WG::SPL;
-    constexpr uint32_t BATCH = 2 * WG::GPW;          // leftover positions claimed per refill
     WG wg;
     const uint64_t n = sv.ctrl->n_left;
     if (!kvs && blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(&sv.ctrl->leftovers, (unsigned long long)n);
@@ -775,40 +774,54 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     // Dynamic scheduling: every warp iteration advances each busy group by one
     // eviction round; a group whose entry is placed (or stashed) immediately
     // takes the next leftover, so a warp never idles behind its longest chain.
+    // Jobs come from a warp buffer: lane l holds the item and entry of leftover
+    // position base + l, claimed 32 at a time with one atomic and loaded ahead
+    // (items at the claim, entries during the next round), so starting a job is
+    // a shuffle, not a dependent atomic -> item -> key/value load chain.
     bool busy = false;                       // group-uniform job state
     uint32_t item = 0, b = 0, seed = 0, r = 0;
     uint64_t kv = EMPTY;
-    uint64_t qa = 0, qb = 0;                 // warp-uniform claimed range of leftover positions
-    bool drained = n == 0;
+    const int lane = threadIdx.x & 31;
+    uint32_t q_item = 0;                     // this lane's buffered job
+    uint64_t q_kv = EMPTY;
+    uint32_t qa = 0, qn = 0;                 // warp-uniform: next buffered job, buffered jobs
+    bool kv_due = false;                     // warp-uniform: q_kv not loaded yet
+    bool drained = n == 0;                   // warp-uniform: no positions left to claim
+    auto refill = [&]() {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&sv.ctrl->slow_next, 32ull);
+        base = __shfl_sync(FULL, base, 0);
+        qa = 0;
+        qn = base >= n ? 0u : (uint32_t)(n - base < 32 ? n - base : 32);
+        if (base + 32 >= n) drained = true;
+        if ((uint32_t)lane < qn) q_item = leftover[base + lane];
+        kv_due = qn != 0;
+    };
+    auto load_kv = [&]() {
+        if (kv_due && (uint32_t)lane < qn) q_kv = kvs ? kvs[q_item] : pack(keys[q_item], vals[q_item]);
+        kv_due = false;
+    };
+    if (!drained) refill();
     bool have = false;                       // s already holds bucket b (prefetched)
     uint64_t s[SPL];
     const uint32_t leaders = __ballot_sync(FULL, wg.gl == 0);
     while (true) {
         // ---- hand out work to idle groups ----
         const uint32_t idle = __ballot_sync(FULL, !busy && wg.gl == 0);
-        if (drained && idle == leaders) break;
-        if (idle && !drained) {
+        if (drained && qa == qn && idle == leaders) break;
+        if (idle && qa < qn) {
+            load_kv();                                         // no-op unless the buffer is fresh
             const uint32_t need = __popc(idle);
             const uint32_t rank = wg.bcast((uint32_t)__popc(idle & lanemask_lt()), 0);
-            const uint64_t avail = qb - qa;
-            uint64_t pos = ~0ull;
-            if (rank < avail) pos = qa + rank;
-            if (need > avail) {
-                unsigned long long base = 0;
-                if ((threadIdx.x & 31) == 0) base = atomicAdd(&sv.ctrl->slow_next, (unsigned long long)BATCH);
-                base = __shfl_sync(FULL, base, 0);
-                if (rank >= avail) pos = base + (rank - avail);
-                qa = base + (need - avail);
-                qb = base + BATCH;
-                if (base + (need - avail) >= n) drained = true;
-            } else {
-                qa += need;
-            }
-            if (qa >= n) qa = qb = n;
-            const bool start = !busy && pos < n;
+            const uint32_t take = need < qn - qa ? need : qn - qa;
+            const bool start = !busy && rank < take;           // group-uniform
+            const int src = (int)(qa + (start ? rank : 0u));
+            const uint32_t it = __shfl_sync(FULL, q_item, src);
+            const uint64_t e = __shfl_sync(FULL, q_kv, src);
+            qa += take;
             if (start) {
-                item = leftover[pos];
-                kv = kvs ? kvs[item] : pack(keys[item], vals[item]);
+                item = it;
+                kv = e;
                 b = tv.addr(tv.h1(key_of(kv)));               // start at b1
                 seed = tv.h2(key_of(kv));
                 r = 0;
@@ -817,7 +830,11 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
                 if (wg.gl == 0) ab += 4 + 8;
             }
         }
-        if (!__any_sync(FULL, busy)) continue;
+        if (qa == qn && !drained) refill();
+        if (!__any_sync(FULL, busy)) {
+            load_kv();
+            continue;
+        }
         // ---- one round of Alg. 3 for every busy group ----
         if (busy && !have) {
             load_slots<SPL>(wg.slot_ptr(tv.bucket(b)), s);
@@ -826,6 +843,7 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             fill_empty<SPL>(s);
         }
         have = false;
+        load_kv();                                             // overlaps this round's bucket load
         const bool placed = wabc_claim<G>(wg, s, tv.bucket(b), kv, busy, ab);   // line 3
         if (placed) {
             const uint32_t hb = tv.addr(tv.h1(key_of(kv)));
