@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--n-log2", type=int, default=N_LOG2, help="keys per rank (debug only)")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", choices=("nccl", "p2p"), default="nccl",
+                    help="sharded path: NCCL all-to-all (default) or the peer-memory exchange (NEXT-1)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the hash-sharded (NCCL all-to-all) path even at world size 1 (testing)")
     return ap.parse_args()
@@ -204,8 +206,11 @@ def main():
     found = torch.empty(n, dtype=torch.uint8, device=dev)
 
     if sharded:
-        from paper_2510_15095_b200.sharded import ShardedHive
-        sh = ShardedHive(nb * 32, lf_grow=2.0, lf_shrink=0)
+        from paper_2510_15095_b200.sharded import P2PShardedHive, ShardedHive
+        if args.exchange == "p2p":
+            sh = P2PShardedHive(nb * 32, region=n, lf_grow=2.0, lf_shrink=0)
+        else:
+            sh = ShardedHive(nb * 32, lf_grow=2.0, lf_shrink=0)
         table = sh.table
 
         def step():
@@ -399,7 +404,8 @@ def main():
                                    "(LF 0.95, growth off) + 2^%d finds (50%% hits) per rank"
                                    % (args.n_log2, nb, args.n_log2),
                        "keys_per_rank": n, "buckets_per_rank": nb,
-                       "parallelism": "single GPU" if not sharded else f"hash-sharded x{world} (NCCL all-to-all)",
+                       "parallelism": "single GPU" if not sharded else
+                       f"hash-sharded x{world} ({'NCCL all-to-all' if args.exchange == 'nccl' else 'peer-memory exchange'})",
                        "l2": "inputs and table larger than L2 (no flush)", "owner_election": "on"},
             **out,
             "clocks": clk.summary(),

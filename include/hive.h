@@ -226,6 +226,65 @@ hive_status hive_unroute(const uint32_t* d_pos, uint64_t n, const uint8_t* d_in8
                          uint8_t* d_out8, const uint32_t* d_in32, uint32_t* d_out32,
                          void* stream);
 
+/* ---- peer-memory exchange -------------------------
+ * The sharded table's exchange without NCCL: source ranks store op records
+ * straight into the owners' inboxes and owners store results straight back,
+ * over NVLink peer mappings (CUDA IPC).  1 <= n_shards <= 8.  Every exchange
+ * buffer is laid out in `region`-sized regions, one per rank:
+ *   inbox_kv  uint64[n_shards * region]  owner side; source r writes
+ *             (value << 32 | key) records at [r * region, r * region + cnt[r])
+ *   inbox_ops uint8 [n_shards * region]  same layout, opcodes (mixed batches)
+ *   cnt       uint64[n_shards]           owner side; cnt[r] written by source r
+ *   res32/res8 [n_shards * region]       source side; owner o writes results at
+ *             [o * region, ...) in the order it received them
+ * Peer pointer arguments are HOST arrays of n_shards DEVICE pointers (entry
+ * p = shard p's buffer as mapped in this process; this rank's own entry is its
+ * local buffer).  The caller orders the phases: route on every rank, a
+ * cross-rank barrier (stream sync + process-group barrier), compact + the
+ * owner's batch op + return, a barrier, then hive_unroute(d_pos, ...) over
+ * res8 / res32 gives results in the caller's op order.  n_shards * region
+ * must be <= 2^32 (positions are 32-bit). */
+
+/* Stable route of this rank's batch into the owners' inboxes (shard(k) as in
+ * hive_route), then cnt[rank] on every owner.  d_pos uint32[n]: p * region +
+ * (position in this rank's region of owner p), the hive_unroute index into
+ * res8 / res32.  d_counts uint64[n_shards]: records sent per owner (device).
+ * d_ops / peer_ops nullable together.  n <= region. */
+hive_status hive_route_p2p(uint32_t n_shards, uint32_t rank, uint32_t seed, const uint32_t* d_keys,
+                           const uint32_t* d_vals, const uint8_t* d_ops, uint64_t n, uint64_t region,
+                           uint64_t* const* peer_kv, uint8_t* const* peer_ops, uint64_t* const* peer_cnt,
+                           uint32_t* d_pos, uint64_t* d_counts, void* stream);
+/* Owner: concatenate the n_src inbox regions (cnt[r] records each, rank order)
+ * into d_keys / d_vals / d_ops [n_total = sum cnt] (d_ops with d_inbox_ops). */
+hive_status hive_inbox_compact(uint32_t n_src, uint64_t region, const uint64_t* d_inbox_kv,
+                               const uint8_t* d_inbox_ops, const uint64_t* d_cnt, uint64_t n_total,
+                               uint32_t* d_keys, uint32_t* d_vals, uint8_t* d_ops, void* stream);
+/* Owner: result j of the compacted batch (source r = the region j came from)
+ * is stored at peer_res32[r][rank * region + (j - start_r)] (and res8). */
+hive_status hive_return_p2p(uint32_t n_src, uint32_t rank, uint64_t region, const uint64_t* d_cnt,
+                            uint64_t n_total, const uint32_t* d_res32, const uint8_t* d_res8,
+                            uint32_t* const* peer_res32, uint8_t* const* peer_res8, void* stream);
+/* Device-side phase barrier (replaces a host barrier between the phases).
+ * Signal words: uint64[17] per rank, zeroed at allocation: [phase * 8 + r] =
+ * the last epoch source r signalled for that phase, [16] = timeout marker.
+ * hive_p2p_signal: after this rank's earlier stream work, store `epoch` into
+ * every peer's word [phase * 8 + rank] (release, system scope).
+ * hive_p2p_wait: stream-ordered wait until d_sig[phase * 8 + r] >= epoch for
+ * all r < n (acquire); after timeout_ns it stops waiting and sets d_sig[16]
+ * = 1, which the caller checks at its next synchronisation.  phase in {0, 1}. */
+hive_status hive_p2p_signal(uint32_t n, uint32_t rank, uint32_t phase, uint64_t epoch,
+                            uint64_t* const* peer_sig, void* stream);
+hive_status hive_p2p_wait(uint32_t n, uint32_t phase, uint64_t epoch, uint64_t* d_sig, uint64_t timeout_ns,
+                          void* stream);
+/* Exchange buffers: plain cudaMalloc allocations (IPC-exportable base
+ * pointers); the handle is the 64-byte cudaIpcMemHandle_t.  hive_ipc_open
+ * maps a peer's buffer (peer access enabled lazily); hive_ipc_close unmaps. */
+hive_status hive_dev_alloc(uint64_t bytes, void** d_out);
+hive_status hive_dev_free(void* d_ptr);
+hive_status hive_ipc_handle(const void* d_ptr, uint8_t* handle_out);
+hive_status hive_ipc_open(const uint8_t* handle, void** d_out);
+hive_status hive_ipc_close(void* d_ptr);
+
 /* ---- hash study (§III-C Listing 1 / Theorem 1 / CSR, §V-B pairs) -------------
  * Hash functions by id: BitHash1 / BitHash2 (Listing 1), CRC-32
  * (IEEE) and the low 32 bits of CRC-64 (XZ), both over the 4 little-endian key

@@ -1057,6 +1057,123 @@ hive_status hive_unroute(const uint32_t* d_pos, uint64_t n, const uint8_t* d_in8
     return HIVE_OK;
 }
 
+// ---- NEXT-1 peer-memory exchange ------------------------------------------------------
+static bool fill_peers(PeerDest& pd, uint32_t n, uint64_t region, uint32_t rank) {
+    if (n == 0 || n > (uint32_t)MAX_PEERS || rank >= n || region == 0) return false;
+    if ((uint64_t)n * region > (1ull << 32)) return false;     // pos_out is 32-bit
+    pd = PeerDest{};
+    pd.region = region;
+    pd.rank = rank;
+    return true;
+}
+
+hive_status hive_route_p2p(uint32_t n_shards, uint32_t rank, uint32_t seed, const uint32_t* d_keys,
+                           const uint32_t* d_vals, const uint8_t* d_ops, uint64_t n, uint64_t region,
+                           uint64_t* const* peer_kv, uint8_t* const* peer_ops, uint64_t* const* peer_cnt,
+                           uint32_t* d_pos, uint64_t* d_counts, void* stream) {
+    PeerDest pd;
+    if (!fill_peers(pd, n_shards, region, rank) || !peer_kv || !peer_cnt || !d_counts) return HIVE_EINVAL;
+    if (n > region || (n && (!d_keys || !d_pos))) return HIVE_EINVAL;
+    for (uint32_t p = 0; p < n_shards; ++p) {
+        if (!peer_kv[p] || !peer_cnt[p] || (d_ops && (!peer_ops || !peer_ops[p]))) return HIVE_EINVAL;
+        pd.kv[p] = peer_kv[p];
+        pd.ops[p] = d_ops ? peer_ops[p] : nullptr;
+        pd.cnt[p] = (unsigned long long*)peer_cnt[p];
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    struct P2PScratch { uint64_t* cnt = nullptr; uint64_t cap = 0; uint64_t* info = nullptr; };
+    static std::mutex mu;
+    static P2PScratch scratch[64];
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    P2PScratch& rs = scratch[dev & 63];
+    CKS(ensure(rs.cnt, rs.cap, (uint64_t)n_shards * part_warps(n) + 1));
+    if (!rs.info) CK(cudaMalloc((void**)&rs.info, 2 * MAX_PARTS * sizeof(uint64_t)));
+    CK(launch_route_p2p(s, n_shards, seed, d_keys, d_vals, d_ops, n, rs.cnt, rs.info, d_pos, pd));
+    CK(cudaMemcpyAsync(d_counts, rs.info, n_shards * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    return HIVE_OK;
+}
+
+hive_status hive_inbox_compact(uint32_t n_src, uint64_t region, const uint64_t* d_inbox_kv,
+                               const uint8_t* d_inbox_ops, const uint64_t* d_cnt, uint64_t n_total,
+                               uint32_t* d_keys, uint32_t* d_vals, uint8_t* d_ops, void* stream) {
+    if (n_src == 0 || n_src > (uint32_t)MAX_PEERS || !d_cnt) return HIVE_EINVAL;
+    if (n_total && (!d_inbox_kv || !d_keys || !d_vals || ((d_ops != nullptr) != (d_inbox_ops != nullptr))))
+        return HIVE_EINVAL;
+    CK(launch_inbox_compact((cudaStream_t)stream, n_src, region, d_inbox_kv, d_inbox_ops, d_cnt, n_total, d_keys,
+                            d_vals, d_ops));
+    return HIVE_OK;
+}
+
+hive_status hive_return_p2p(uint32_t n_src, uint32_t rank, uint64_t region, const uint64_t* d_cnt,
+                            uint64_t n_total, const uint32_t* d_res32, const uint8_t* d_res8,
+                            uint32_t* const* peer_res32, uint8_t* const* peer_res8, void* stream) {
+    PeerDest pd;
+    if (!fill_peers(pd, n_src, region, rank) || !d_cnt) return HIVE_EINVAL;
+    for (uint32_t p = 0; p < n_src; ++p) {
+        if ((d_res32 && (!peer_res32 || !peer_res32[p])) || (d_res8 && (!peer_res8 || !peer_res8[p])))
+            return HIVE_EINVAL;
+        pd.res32[p] = d_res32 ? peer_res32[p] : nullptr;
+        pd.res8[p] = d_res8 ? peer_res8[p] : nullptr;
+    }
+    CK(launch_return_p2p((cudaStream_t)stream, n_src, d_cnt, n_total, d_res32, d_res8, pd));
+    return HIVE_OK;
+}
+
+hive_status hive_p2p_signal(uint32_t n, uint32_t rank, uint32_t phase, uint64_t epoch,
+                            uint64_t* const* peer_sig, void* stream) {
+    PeerDest pd;
+    if (!fill_peers(pd, n, 1, rank) || phase > 1 || !peer_sig) return HIVE_EINVAL;
+    for (uint32_t p = 0; p < n; ++p) {
+        if (!peer_sig[p]) return HIVE_EINVAL;
+        pd.sig[p] = (unsigned long long*)peer_sig[p];
+    }
+    CK(launch_p2p_signal((cudaStream_t)stream, n, phase, epoch, pd));
+    return HIVE_OK;
+}
+
+hive_status hive_p2p_wait(uint32_t n, uint32_t phase, uint64_t epoch, uint64_t* d_sig, uint64_t timeout_ns,
+                          void* stream) {
+    if (n == 0 || n > (uint32_t)MAX_PEERS || phase > 1 || !d_sig) return HIVE_EINVAL;
+    CK(launch_p2p_wait((cudaStream_t)stream, n, phase, epoch, (unsigned long long*)d_sig, timeout_ns));
+    return HIVE_OK;
+}
+
+hive_status hive_dev_alloc(uint64_t bytes, void** d_out) {
+    if (!d_out || bytes == 0) return HIVE_EINVAL;
+    *d_out = nullptr;
+    cudaError_t e = cudaMalloc(d_out, bytes);
+    if (e != cudaSuccess) { set_err(e, "cudaMalloc", __LINE__); return HIVE_ENOMEM; }
+    return HIVE_OK;
+}
+
+hive_status hive_dev_free(void* d_ptr) {
+    if (d_ptr) CK(cudaFree(d_ptr));
+    return HIVE_OK;
+}
+
+hive_status hive_ipc_handle(const void* d_ptr, uint8_t* handle_out) {
+    if (!d_ptr || !handle_out) return HIVE_EINVAL;
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+    memcpy(handle_out, &h, sizeof(h));
+    return HIVE_OK;
+}
+
+hive_status hive_ipc_open(const uint8_t* handle, void** d_out) {
+    if (!handle || !d_out) return HIVE_EINVAL;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    CK(cudaIpcOpenMemHandle(d_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return HIVE_OK;
+}
+
+hive_status hive_ipc_close(void* d_ptr) {
+    if (d_ptr) CK(cudaIpcCloseMemHandle(d_ptr));
+    return HIVE_OK;
+}
+
 hive_status hive_hash(uint32_t fn, const uint32_t* d_keys, uint64_t n, uint32_t* d_out, void* stream) {
     if (fn > HIVE_FN_CRC64) return HIVE_EINVAL;
     if (n == 0) return HIVE_OK;

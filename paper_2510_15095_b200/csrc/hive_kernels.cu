@@ -1263,7 +1263,7 @@ k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __rest
                uint64_t idx_stride, uint64_t* __restrict__ send_kv, uint8_t* __restrict__ send_ops,
                uint32_t* __restrict__ pos_out, uint8_t* __restrict__ result_zero,
                uint32_t* __restrict__ vals_zero, const uint32_t* __restrict__ idx,
-               const uint64_t* __restrict__ n_dev, uint32_t chunk) {
+               const uint64_t* __restrict__ n_dev, uint32_t chunk, PeerDest pd) {
     __shared__ uint64_t run[WARPS_PER_BLOCK][MAX_PARTS + 1];
     const bool small = n_parts < 16;
     if (n_dev) n = *n_dev;
@@ -1300,6 +1300,15 @@ k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __rest
         } else if (mode == PART_ROUTE_KEYS) {
             reinterpret_cast<uint32_t*>(send_kv)[pos] = keys[i];
             pos_out[i] = (uint32_t)pos;
+        } else if (mode == PART_ROUTE_P2P) {
+            // owner p's inbox, this rank's region: a remote store over NVLink
+            // (a local one when p is this rank); the stable rank keeps the
+            // (rank, index) order the owner's PHASED batch relies on
+            const uint64_t rel = pos - part_info[MAX_PARTS + p];
+            const uint64_t at = (uint64_t)pd.rank * pd.region + rel;
+            pd.kv[p][at] = ((uint64_t)(vals ? vals[i] : 0u) << 32) | keys[i];
+            if (pd.ops[p]) pd.ops[p][at] = ops[i];
+            pos_out[i] = (uint32_t)((uint64_t)p * pd.region + rel);
         } else {
             send_kv[pos] = ((uint64_t)(vals ? vals[i] : 0u) << 32) | keys[i];
             if (send_ops) send_ops[pos] = ops[i];
@@ -1566,12 +1575,31 @@ uint32_t part_chunk(uint64_t n) {
 }
 uint64_t part_warps(uint64_t n) { const uint64_t c = part_chunk(n); return (n + c - 1) / c; }
 
+cudaError_t launch_partition_pd(cudaStream_t s, int mode, uint32_t n_parts, uint32_t seed,
+                                const uint32_t* keys, const uint32_t* vals, const uint8_t* ops,
+                                uint64_t n, uint64_t* cnt, uint64_t* part_info,
+                                uint32_t* out_idx, uint64_t idx_stride, uint64_t* send_kv,
+                                uint8_t* send_ops, uint32_t* pos, uint8_t* result_zero,
+                                uint32_t* vals_zero, const uint32_t* idx, const uint64_t* n_dev,
+                                const PeerDest& pd);
+
 cudaError_t launch_partition(cudaStream_t s, int mode, uint32_t n_parts, uint32_t seed,
                              const uint32_t* keys, const uint32_t* vals, const uint8_t* ops,
                              uint64_t n, uint64_t* cnt, uint64_t* part_info,
                              uint32_t* out_idx, uint64_t idx_stride, uint64_t* send_kv,
                              uint8_t* send_ops, uint32_t* pos, uint8_t* result_zero,
                              uint32_t* vals_zero, const uint32_t* idx, const uint64_t* n_dev) {
+    return launch_partition_pd(s, mode, n_parts, seed, keys, vals, ops, n, cnt, part_info, out_idx, idx_stride,
+                               send_kv, send_ops, pos, result_zero, vals_zero, idx, n_dev, PeerDest{});
+}
+
+cudaError_t launch_partition_pd(cudaStream_t s, int mode, uint32_t n_parts, uint32_t seed,
+                                const uint32_t* keys, const uint32_t* vals, const uint8_t* ops,
+                                uint64_t n, uint64_t* cnt, uint64_t* part_info,
+                                uint32_t* out_idx, uint64_t idx_stride, uint64_t* send_kv,
+                                uint8_t* send_ops, uint32_t* pos, uint8_t* result_zero,
+                                uint32_t* vals_zero, const uint32_t* idx, const uint64_t* n_dev,
+                                const PeerDest& pd) {
     const uint64_t nw = part_warps(n);
     const uint32_t chunk = part_chunk(n);
     const int grid = (int)((nw + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK);
@@ -1580,7 +1608,7 @@ cudaError_t launch_partition(cudaStream_t s, int mode, uint32_t n_parts, uint32_
     if (nw)
         k_part_scatter<<<grid, BLOCK, 0, s>>>(mode, n_parts, seed, keys, vals, ops, n, nw, cnt, part_info,
                                               out_idx, idx_stride, send_kv, send_ops, pos, result_zero,
-                                              vals_zero, idx, n_dev, chunk);
+                                              vals_zero, idx, n_dev, chunk, pd);
     return cudaGetLastError();
 }
 
@@ -1651,6 +1679,134 @@ cudaError_t launch_stash_reset(cudaStream_t s, StashView sv) {
     cudaError_t e = cudaMemsetAsync(sv.ring, 0xFF, sv.cap * sizeof(uint64_t), s);
     if (e != cudaSuccess) return e;
     return cudaMemsetAsync(sv.index, 0xFF, (sv.idx_mask + 1) * sizeof(uint64_t), s);
+}
+
+// ---- NEXT-1 peer-memory exchange -------------------------------------
+// Per-source count of this rank's records, written into every owner's count
+// array (remote stores), after the scatter in stream order.
+__global__ void k_p2p_counts(const uint64_t* __restrict__ part_info, uint32_t n_shards, PeerDest pd) {
+    const uint32_t p = threadIdx.x;
+    if (p < n_shards) pd.cnt[p][pd.rank] = part_info[p];
+    __threadfence_system();
+}
+
+// Region prefix of the n_src per-source counts (n_src <= MAX_PEERS), per block.
+__device__ __forceinline__ void region_starts(const uint64_t* cnt, uint32_t n_src, uint64_t* start) {
+    if (threadIdx.x == 0) {
+        uint64_t a = 0;
+        for (uint32_t r = 0; r < n_src; ++r) {
+            start[r] = a;
+            a += cnt[r];
+        }
+        start[n_src] = a;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(BLOCK)
+k_inbox_compact(uint32_t n_src, uint64_t region, const uint64_t* __restrict__ inbox_kv,
+                const uint8_t* __restrict__ inbox_ops, const uint64_t* __restrict__ cnt, uint64_t n_total,
+                uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint8_t* __restrict__ ops) {
+    __shared__ uint64_t start[MAX_PEERS + 1];
+    region_starts(cnt, n_src, start);
+    for (uint64_t j = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; j < n_total; j += (uint64_t)gridDim.x * BLOCK) {
+        uint32_t r = 0;
+        while (r + 1 < n_src && start[r + 1] <= j) ++r;
+        const uint64_t at = (uint64_t)r * region + (j - start[r]);
+        const uint64_t w = inbox_kv[at];
+        keys[j] = key_of(w);
+        vals[j] = val_of(w);
+        if (ops) ops[j] = inbox_ops[at];
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK)
+k_return_p2p(uint32_t n_src, const uint64_t* __restrict__ cnt, uint64_t n_total,
+             const uint32_t* __restrict__ res32, const uint8_t* __restrict__ res8, PeerDest pd) {
+    __shared__ uint64_t start[MAX_PEERS + 1];
+    region_starts(cnt, n_src, start);
+    for (uint64_t j = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; j < n_total; j += (uint64_t)gridDim.x * BLOCK) {
+        uint32_t r = 0;
+        while (r + 1 < n_src && start[r + 1] <= j) ++r;
+        // source r's result region of this owner (remote store)
+        const uint64_t at = (uint64_t)pd.rank * pd.region + (j - start[r]);
+        if (res32) pd.res32[r][at] = res32[j];
+        if (res8) pd.res8[r][at] = res8[j];
+    }
+    __threadfence_system();
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void k_p2p_signal(uint32_t n, uint32_t phase, uint64_t epoch, PeerDest pd) {
+    const uint32_t p = threadIdx.x;
+    __threadfence_system();                       // this rank's earlier stores first
+    if (p < n) {
+        unsigned long long* w = pd.sig[p] + phase * MAX_PEERS + pd.rank;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(w), "l"((unsigned long long)epoch) : "memory");
+    }
+}
+
+__global__ void k_p2p_wait(uint32_t n, uint32_t phase, uint64_t epoch, unsigned long long* sig_own,
+                           uint64_t timeout_ns) {
+    const uint32_t r = threadIdx.x;
+    if (r < n) {
+        const unsigned long long* w = sig_own + phase * MAX_PEERS + r;
+        const uint64_t t0 = globaltimer();
+        while (true) {
+            unsigned long long v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(w) : "memory");
+            if (v >= epoch) break;
+            if (globaltimer() - t0 > timeout_ns) {          // a peer never arrived: flag, do not hang
+                atomicExch(sig_own + 2 * MAX_PEERS, 1ull);
+                break;
+            }
+            __nanosleep(200);
+        }
+    }
+    __threadfence_system();
+}
+
+cudaError_t launch_p2p_signal(cudaStream_t s, uint32_t n, uint32_t phase, uint64_t epoch, const PeerDest& pd) {
+    k_p2p_signal<<<1, 32, 0, s>>>(n, phase, epoch, pd);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_wait(cudaStream_t s, uint32_t n, uint32_t phase, uint64_t epoch,
+                            unsigned long long* sig_own, uint64_t timeout_ns) {
+    k_p2p_wait<<<1, 32, 0, s>>>(n, phase, epoch, sig_own, timeout_ns);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_route_p2p(cudaStream_t s, uint32_t n_shards, uint32_t seed, const uint32_t* keys,
+                             const uint32_t* vals, const uint8_t* ops, uint64_t n, uint64_t* cnt,
+                             uint64_t* part_info, uint32_t* pos, const PeerDest& pd) {
+    cudaError_t e = launch_partition_pd(s, PART_ROUTE_P2P, n_shards, seed, keys, vals, ops, n, cnt, part_info,
+                                        nullptr, 0, nullptr, nullptr, pos, nullptr, nullptr, nullptr, nullptr, pd);
+    if (e != cudaSuccess) return e;
+    k_p2p_counts<<<1, 32, 0, s>>>(part_info, n_shards, pd);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inbox_compact(cudaStream_t s, uint32_t n_src, uint64_t region, const uint64_t* inbox_kv,
+                                 const uint8_t* inbox_ops, const uint64_t* cnt, uint64_t n_total,
+                                 uint32_t* keys, uint32_t* vals, uint8_t* ops) {
+    if (!n_total) return cudaSuccess;
+    const int grid = clamp_grid(148 * 8, n_total, BLOCK);
+    k_inbox_compact<<<grid, BLOCK, 0, s>>>(n_src, region, inbox_kv, inbox_ops, cnt, n_total, keys, vals, ops);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_return_p2p(cudaStream_t s, uint32_t n_src, const uint64_t* cnt, uint64_t n_total,
+                              const uint32_t* res32, const uint8_t* res8, const PeerDest& pd) {
+    if (!n_total) return cudaSuccess;
+    const int grid = clamp_grid(148 * 8, n_total, BLOCK);
+    k_return_p2p<<<grid, BLOCK, 0, s>>>(n_src, cnt, n_total, res32, res8, pd);
+    return cudaGetLastError();
 }
 
 }  // namespace hive

@@ -18,7 +18,25 @@ constexpr int MINB_DEFAULT = 4;          // 4 blocks/SM => <= 64 registers (ncu:
 constexpr int PART_CHUNK = 2048;         // elements per warp in the stable partition
 constexpr int MAX_PARTS = 64;
 
-enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1, PART_ELECT = 2, PART_ROUTE_KEYS = 3 };
+enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1, PART_ELECT = 2, PART_ROUTE_KEYS = 3, PART_ROUTE_P2P = 4 };
+
+// Peer-memory exchange: the owners' inbox / count /
+// result buffers of up to MAX_PEERS shards, passed by value.  Every buffer is
+// laid out by region: source (or owner) r's records sit at [r * region, ...).
+constexpr int MAX_PEERS = 8;
+struct PeerDest {
+    uint64_t* kv[MAX_PEERS];                 // owner p's inbox records (value << 32 | key)
+    uint8_t* ops[MAX_PEERS];                 // owner p's inbox opcodes (nullable)
+    unsigned long long* cnt[MAX_PEERS];      // owner p's per-source record counts
+    uint32_t* res32[MAX_PEERS];              // source p's result words (return path)
+    uint8_t* res8[MAX_PEERS];                // source p's result bytes (return path)
+    unsigned long long* sig[MAX_PEERS];      // peer p's signal words [2 phases][MAX_PEERS]
+    uint64_t region;                         // records per region
+    uint32_t rank;                           // this rank
+};
+// Signal words per rank: [phase * MAX_PEERS + source] = epoch, then one
+// timeout marker.
+constexpr int SIG_WORDS = 2 * MAX_PEERS + 1;
 
 struct Grids {                           // persistent grid sizes (blocks)
     int find, insert_fast, insert_slow, erase, dedup, stream, gather;
@@ -76,6 +94,26 @@ cudaError_t launch_count_b1(int grid, cudaStream_t s, TableView tv, uint64_t n_b
 // Stable partition: count -> scan -> scatter.  cnt must hold n_parts * n_warps
 // words, part_info 2 * MAX_PARTS words (totals, bases).
 uint64_t part_warps(uint64_t n);
+// NEXT-1: stable route of this rank's batch straight into the owners' inboxes
+// (remote stores over NVLink), then each owner's per-source count.
+cudaError_t launch_route_p2p(cudaStream_t s, uint32_t n_shards, uint32_t seed, const uint32_t* keys,
+                             const uint32_t* vals, const uint8_t* ops, uint64_t n, uint64_t* cnt,
+                             uint64_t* part_info, uint32_t* pos, const PeerDest& pd);
+// Owner: gather the per-source inbox regions into contiguous key / value / op arrays.
+cudaError_t launch_inbox_compact(cudaStream_t s, uint32_t n_src, uint64_t region, const uint64_t* inbox_kv,
+                                 const uint8_t* inbox_ops, const uint64_t* cnt, uint64_t n_total,
+                                 uint32_t* keys, uint32_t* vals, uint8_t* ops);
+// Owner: write each record's results into its source's result region (remote stores).
+cudaError_t launch_return_p2p(cudaStream_t s, uint32_t n_src, const uint64_t* cnt, uint64_t n_total,
+                              const uint32_t* res32, const uint8_t* res8, const PeerDest& pd);
+
+// Device-side phase barrier of the peer exchange: every rank stores `epoch`
+// into each peer's signal word (release, system scope) after its stores; a
+// rank waits (acquire spin, bounded by timeout_ns) until all n sources have.
+cudaError_t launch_p2p_signal(cudaStream_t s, uint32_t n, uint32_t phase, uint64_t epoch, const PeerDest& pd);
+cudaError_t launch_p2p_wait(cudaStream_t s, uint32_t n, uint32_t phase, uint64_t epoch,
+                            unsigned long long* sig_own, uint64_t timeout_ns);
+
 cudaError_t launch_partition(cudaStream_t s, int mode, uint32_t n_parts, uint32_t seed,
                              const uint32_t* keys, const uint32_t* vals, const uint8_t* ops,
                              uint64_t n, uint64_t* cnt, uint64_t* part_info,

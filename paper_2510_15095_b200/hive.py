@@ -71,6 +71,16 @@ SIGNATURES = {
     "hive_unpack_kv": (_int, [_vp, _u64, _vp, _vp, _vp]),
     "hive_hash": (_int, [_u32, _vp, _u64, _vp, _vp]),
     "hive_gather_ceiling": (_int, [_vp, _u64, _vp, _u64, _vp, _vp]),
+    "hive_route_p2p": (_int, [_u32, _u32, _u32, _vp, _vp, _vp, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hive_inbox_compact": (_int, [_u32, _u64, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
+    "hive_return_p2p": (_int, [_u32, _u32, _u64, _vp, _u64, _vp, _vp, _vp, _vp, _vp]),
+    "hive_p2p_signal": (_int, [_u32, _u32, _u32, _u64, _vp, _vp]),
+    "hive_p2p_wait": (_int, [_u32, _u32, _u64, _vp, _u64, _vp]),
+    "hive_dev_alloc": (_int, [_u64, ctypes.POINTER(_vp)]),
+    "hive_dev_free": (_int, [_vp]),
+    "hive_ipc_handle": (_int, [_vp, _vp]),
+    "hive_ipc_open": (_int, [_vp, ctypes.POINTER(_vp)]),
+    "hive_ipc_close": (_int, [_vp]),
     "hive_collisions": (_int, [_u32, _vp, _u64, _u64, ctypes.POINTER(_u64), _vp]),
     "hive_status_string": (ctypes.c_char_p, [_int]),
     "hive_last_error": (ctypes.c_char_p, []),
@@ -353,3 +363,73 @@ def collisions(fn: str, keys: torch.Tensor, m: int, stream=None) -> int:
     _check(lib().hive_collisions(HASH_FNS[fn], _p(keys), keys.numel(), m, ctypes.byref(y),
                                  _stream(stream)), "hive_collisions")
     return int(y.value)
+
+
+# ---- peer-memory exchange ----------------------------------------
+def _ptrs(ptrs):
+    """Host array of device pointers (ints) for the C ABI (None stays NULL)."""
+    if ptrs is None:
+        return None
+    arr = (ctypes.c_void_p * len(ptrs))(*[ctypes.c_void_p(int(p)) if p else None for p in ptrs])
+    return arr
+
+
+def dev_alloc(nbytes: int) -> int:
+    out = _vp()
+    _check(lib().hive_dev_alloc(nbytes, ctypes.byref(out)), "hive_dev_alloc")
+    return int(out.value)
+
+
+def dev_free(ptr: int):
+    _check(lib().hive_dev_free(ctypes.c_void_p(ptr)), "hive_dev_free")
+
+
+def ipc_handle(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _check(lib().hive_ipc_handle(ctypes.c_void_p(ptr), buf), "hive_ipc_handle")
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    out = _vp()
+    buf = ctypes.create_string_buffer(handle, 64)
+    _check(lib().hive_ipc_open(buf, ctypes.byref(out)), "hive_ipc_open")
+    return int(out.value)
+
+
+def ipc_close(ptr: int):
+    _check(lib().hive_ipc_close(ctypes.c_void_p(ptr)), "hive_ipc_close")
+
+
+def route_p2p(n_shards, rank, seed, keys, vals, ops, region, peer_kv, peer_ops, peer_cnt, pos, counts,
+              stream=None):
+    n = keys.numel()
+    _check(lib().hive_route_p2p(n_shards, rank, seed, _p(keys), _p(vals), _p(ops), n, region, _ptrs(peer_kv),
+                                _ptrs(peer_ops), _ptrs(peer_cnt), _p(pos), _p(counts),
+                                _stream(stream)), "hive_route_p2p")
+
+
+def inbox_compact(n_src, region, inbox_kv: int, inbox_ops: int, cnt: int, n_total, keys, vals, ops,
+                  stream=None):
+    _check(lib().hive_inbox_compact(n_src, region, ctypes.c_void_p(inbox_kv),
+                                    ctypes.c_void_p(inbox_ops) if inbox_ops else None, ctypes.c_void_p(cnt),
+                                    n_total, _p(keys), _p(vals), _p(ops), _stream(stream)), "hive_inbox_compact")
+
+
+def return_p2p(n_src, rank, region, cnt: int, n_total, res32, res8, peer_res32, peer_res8, stream=None):
+    _check(lib().hive_return_p2p(n_src, rank, region, ctypes.c_void_p(cnt), n_total, _p(res32), _p(res8),
+                                 _ptrs(peer_res32), _ptrs(peer_res8), _stream(stream)), "hive_return_p2p")
+
+
+def unroute_raw(pos, n, in8: int, out8, in32: int, out32, stream=None):
+    """hive_unroute with raw device pointers for the inputs (exchange buffers)."""
+    _check(lib().hive_unroute(_p(pos), n, ctypes.c_void_p(in8) if in8 else None, _p(out8),
+                              ctypes.c_void_p(in32) if in32 else None, _p(out32), _stream(stream)), "hive_unroute")
+
+
+def p2p_signal(n, rank, phase, epoch, peer_sig, stream=None):
+    _check(lib().hive_p2p_signal(n, rank, phase, epoch, _ptrs(peer_sig), _stream(stream)), "hive_p2p_signal")
+
+
+def p2p_wait(n, phase, epoch, sig: int, timeout_ns=10_000_000_000, stream=None):
+    _check(lib().hive_p2p_wait(n, phase, epoch, ctypes.c_void_p(sig), timeout_ns, _stream(stream)), "hive_p2p_wait")

@@ -122,3 +122,184 @@ class ShardedHive:
         br = self._a2a_u8(result, sc, rc)
         r, vo = self.ops.unroute(pos, in8=br, in32=bv)
         return vo, r
+
+
+# ---- NEXT-1: exchange over NVLink peer memory (no NCCL on the data path) -------------
+class _DevView:
+    """Zero-copy torch view of a raw device allocation (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _view(ptr: int, n: int, dtype: torch.dtype) -> torch.Tensor:
+    ts = {torch.uint8: "|u1", torch.int32: "<i4", torch.int64: "<i8"}[dtype]
+    return torch.as_tensor(_DevView(ptr, n, ts), device="cuda")
+
+
+class PeerBuffers:
+    """One rank's exchange buffers (plain cudaMalloc: IPC-exportable), laid out
+    in `region`-sized per-rank regions (include/hive.h, NEXT-1)."""
+
+    FIELDS = (("kv", 8), ("ops", 1), ("cnt", 0), ("res32", 4), ("res8", 1), ("sig", 0))
+    SIG_WORDS = 17                           # [2 phases][8 sources] epochs + timeout marker
+
+    def __init__(self, world: int, region: int):
+        self.world, self.region = world, region
+        self.ptr = {}
+        for name, width in self.FIELDS:
+            nbytes = {"cnt": world * 8, "sig": self.SIG_WORDS * 8}.get(name, world * region * width)
+            self.ptr[name] = hive.dev_alloc(nbytes)
+        _view(self.ptr["sig"], self.SIG_WORDS, torch.int64).zero_()
+        torch.cuda.synchronize()
+        self.owned = True
+
+    @classmethod
+    def mapped(cls, world: int, region: int, ptrs: dict):
+        b = cls.__new__(cls)
+        b.world, b.region, b.ptr, b.owned = world, region, dict(ptrs), False
+        return b
+
+    def handles(self) -> dict:
+        return {k: hive.ipc_handle(v) for k, v in self.ptr.items()}
+
+    def close(self):
+        for v in self.ptr.values():
+            (hive.dev_free if self.owned else hive.ipc_close)(v)
+        self.ptr = {}
+
+
+class P2PShardedHive:
+    """Hash-partitioned table whose exchange is done by the kernels themselves:
+    hive_route_p2p stores each op record straight into its owner's inbox over
+    NVLink, the owner runs one PHASED batch on the compacted inbox, and
+    hive_return_p2p stores the results straight back; the source's
+    hive_unroute restores its op order.  The phases are ordered by device-side
+    signals (hive_p2p_signal / hive_p2p_wait: release stores into the peers'
+    signal words, acquire spins), not host barriers; the one host sync per call
+    is the owner's read of its inbox counts.  Same semantics as ShardedHive: a
+    shard sees the union batch in (rank, index) order.
+
+    `virtual_group` builds `world` ranks inside ONE process on one GPU (the
+    peers' buffers are then plain local pointers): the tests drive the phases
+    of all virtual ranks in lockstep to check the multi-rank logic."""
+
+    def __init__(self, capacity_per_shard: int, region: int, group=None, seed: int = SHARD_SEED,
+                 _virtual=None, **cfg):
+        self.seed, self.region, self.group = seed, region, group
+        self._virtual = _virtual is not None
+        if _virtual is None:
+            self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+            self.own = PeerBuffers(self.world, region)
+            hs = [None] * self.world
+            dist.all_gather_object(hs, self.own.handles(), group=group)
+            self.peers = [self.own if r == self.rank else
+                          PeerBuffers.mapped(self.world, region, {k: hive.ipc_open(h) for k, h in hs[r].items()})
+                          for r in range(self.world)]
+        else:
+            self.rank, self.world, self.peers = _virtual
+            self.own = self.peers[self.rank]
+        if self.world > 8:
+            raise hive.HiveError("peer-memory exchange supports at most 8 shards (one node)")
+        self.table = hive.HiveTable(capacity_per_shard, **cfg)
+        self._state = None
+        self._epoch = 0
+        if _virtual is None:
+            dist.barrier(group=group)       # every rank's signal words are zeroed
+
+    @classmethod
+    def virtual_group(cls, world: int, capacity_per_shard: int, region: int, **cfg):
+        bufs = [PeerBuffers(world, region) for _ in range(world)]
+        return [cls(capacity_per_shard, region, _virtual=(r, world, bufs), **cfg) for r in range(world)]
+
+    def close(self):
+        if self._virtual:                 # every virtual rank frees only its own buffers
+            self.own.close()
+        else:
+            for p in self.peers:
+                p.close()                 # peers: IPC unmap; own: free
+        self.table.close()
+
+    def _col(self, name):
+        return [p.ptr[name] for p in self.peers]
+
+    # ---- the three phases (every rank runs each phase before any runs the next) ----
+    def route_phase(self, kind: str, keys, vals=None, ops=None):
+        n = keys.numel()
+        if n > self.region:
+            raise hive.HiveError(f"batch of {n} ops exceeds the exchange region ({self.region})")
+        if vals is None:
+            vals = torch.zeros(n, dtype=torch.uint32, device=keys.device)
+        pos = torch.empty(n, dtype=torch.uint32, device=keys.device)
+        counts = torch.empty(self.world, dtype=torch.int64, device=keys.device)
+        self._epoch += 1
+        hive.route_p2p(self.world, self.rank, self.seed, keys, vals, ops, self.region, self._col("kv"),
+                       self._col("ops") if ops is not None else None, self._col("cnt"), pos, counts)
+        hive.p2p_signal(self.world, self.rank, 0, self._epoch, self._col("sig"))
+        self._state = (kind, n, pos)
+
+    def _check_timeout(self):
+        if int(_view(self.own.ptr["sig"], PeerBuffers.SIG_WORDS, torch.int64)[-1].item()):
+            raise hive.HiveError("peer exchange: a peer did not signal within the timeout")
+
+    def serve_phase(self):
+        kind = self._state[0]
+        hive.p2p_wait(self.world, 0, self._epoch, self.own.ptr["sig"])   # every source's records are in
+        cnt = _view(self.own.ptr["cnt"], self.world, torch.int64)
+        n_total = int(cnt.sum().item())
+        self._check_timeout()
+        dev = cnt.device
+        k = torch.empty(max(n_total, 1), dtype=torch.uint32, device=dev)
+        v = torch.empty(max(n_total, 1), dtype=torch.uint32, device=dev)
+        o = torch.empty(max(n_total, 1), dtype=torch.uint8, device=dev) if kind == "mixed" else None
+        hive.inbox_compact(self.world, self.region, self.own.ptr["kv"], self.own.ptr["ops"] if o is not None else 0,
+                           self.own.ptr["cnt"], n_total, k, v, o)
+        k, v = k[:n_total], v[:n_total]
+        r32 = r8 = None
+        if kind == "insert":
+            r8 = self.table.insert(k, v)
+        elif kind == "erase":
+            r8 = self.table.erase(k)
+        elif kind == "find":
+            r32, r8 = self.table.find(k)
+        else:
+            r32, r8 = self.table.mixed(o[:n_total], k, v)
+        hive.return_p2p(self.world, self.rank, self.region, self.own.ptr["cnt"], n_total, r32, r8,
+                        self._col("res32") if r32 is not None else None,
+                        self._col("res8") if r8 is not None else None)
+        hive.p2p_signal(self.world, self.rank, 1, self._epoch, self._col("sig"))
+
+    def finish_phase(self):
+        kind, n, pos = self._state
+        self._state = None
+        dev = pos.device
+        hive.p2p_wait(self.world, 1, self._epoch, self.own.ptr["sig"])   # every owner's results are back
+        out8 = torch.empty(n, dtype=torch.uint8, device=dev)
+        out32 = torch.empty(n, dtype=torch.uint32, device=dev) if kind in ("find", "mixed") else None
+        if n:
+            hive.unroute_raw(pos, n, self.own.ptr["res8"], out8,
+                             self.own.ptr["res32"] if out32 is not None else 0, out32)
+        return out8, out32
+
+    def _call(self, kind, keys, vals=None, ops=None):
+        # no host barrier: the phases are ordered by the device-side signals;
+        # the only host synchronisation is the owner's read of its inbox counts
+        self.route_phase(kind, keys, vals, ops)
+        self.serve_phase()
+        return self.finish_phase()
+
+    # ---- collective batch ops (every rank calls with its own local batch) -----------
+    def insert(self, keys, vals):
+        return self._call("insert", keys, vals)[0]
+
+    def erase(self, keys):
+        return self._call("erase", keys)[0]
+
+    def find(self, keys):
+        f, v = self._call("find", keys)
+        return v, f
+
+    def mixed(self, op_codes, keys, vals):
+        r, vo = self._call("mixed", keys, vals, op_codes)
+        return vo, r

@@ -49,6 +49,10 @@ def test_status_strings_without_gpu():
     y = hive._u64(0)
     assert L.hive_collisions(2, None, 0, 0, hive.ctypes.byref(y), None) == 1   # m = 0
     assert L.hive_gather_ceiling(None, 0, None, 1, None, None) == 1  # NULL blocks, n > 0
+    assert L.hive_route_p2p(0, 0, 0, None, None, None, 0, 1, None, None, None, None, None, None) == 1
+    assert L.hive_route_p2p(9, 0, 0, None, None, None, 0, 1, None, None, None, None, None, None) == 1
+    assert L.hive_inbox_compact(9, 1, None, None, None, 0, None, None, None, None) == 1
+    assert L.hive_return_p2p(2, 2, 1, None, 0, None, None, None, None, None) == 1   # rank >= n_src
     cfg = hive.HiveConfig()
     L.hive_config_default(hive.ctypes.byref(cfg))
     assert cfg.flags == 0                                           # default pair: BitHash1/2
