@@ -44,6 +44,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", choices=("nccl", "p2p"), default="nccl",
                     help="sharded path: NCCL all-to-all (default) or the peer-memory exchange (NEXT-1)")
+    ap.add_argument("--cfg5", action="store_true",
+                    help="BASELINE config 5: a hash-sharded table of 2^T keys over the ranks (strong scaling), "
+                         "inserted, looked up (50%% hits) and 2^(T-3) erased in 2^26-op batches")
+    ap.add_argument("--cfg5-log2", type=int, default=31, help="T of --cfg5 (total keys 2^T)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the hash-sharded (NCCL all-to-all) path even at world size 1 (testing)")
     return ap.parse_args()
@@ -166,6 +170,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.cfg5:
+        run_cfg5(args, rank, world, local)
         return
 
     import torch
@@ -421,6 +428,97 @@ def main():
         print(json.dumps(line), flush=True)
     if sharded:
         dist.destroy_process_group()
+
+
+def run_cfg5(args, rank: int, world: int, local: int):
+    """BASELINE config 5: 2^T keys hash-sharded over the
+    ranks.  Rank r inserts ids [r 2^T/G, (r+1) 2^T/G) in 2^26-op batches (routed
+    by hash, not by rank) into shards sized for LF 0.95 (growth off), then
+    looks up 2^T/G keys (half present ids of any rank, half absent ids from
+    2^31), then erases 2^(T-3)/G of its own ids.  A step is that whole pass
+    after hive_clear; value = all ranks' ops / the max-over-ranks step time."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_15095_b200 import u32
+    from paper_2510_15095_b200.build import build as build_lib
+    from paper_2510_15095_b200.sharded import P2PShardedHive, ShardedHive
+    if rank == 0:
+        build_lib()
+    torch.cuda.set_device(local)
+    if world == 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29518")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    total = 1 << args.cfg5_log2
+    per = total // world
+    B = min(1 << 26, per)
+    nb = -(-per * 100 // (95 * 32))
+    sh = (P2PShardedHive(nb * 32, region=B, lf_grow=2.0, lf_shrink=0) if args.exchange == "p2p"
+          else ShardedHive(nb * 32, lf_grow=2.0, lf_shrink=0))
+    rng = np.random.default_rng(505 + rank)
+    ins, fnd, era = [], [], []
+    for lo in range(rank * per, (rank + 1) * per, B):
+        ids = np.arange(lo, lo + B, dtype=np.uint64).astype(np.uint32)
+        ins.append((u32(gen.keys_of(ids), dev), u32(gen.vals_of(ids), dev)))
+    for b in range(per // B):
+        hit = rng.integers(0, total, B // 2, dtype=np.uint64)
+        miss = (1 << 31) + rank * per // 2 + b * (B // 2) + np.arange(B // 2, dtype=np.uint64)
+        q = np.concatenate([hit, miss])[rng.permutation(B)].astype(np.uint32)
+        fnd.append(u32(gen.keys_of(q), dev))
+    n_era = max(per // 8, 1)
+    for lo in range(rank * per, rank * per + n_era, B):
+        ids = np.arange(lo, min(lo + B, rank * per + n_era), dtype=np.uint64).astype(np.uint32)
+        era.append(u32(gen.keys_of(ids), dev))
+    ops_per_rank = per + per + n_era
+    last = {}
+
+    def step():
+        sh.table.clear()
+        for k, v in ins:
+            last["st"] = sh.insert(k, v)
+        last["found"] = [sh.find(q)[1] for q in fnd]
+        last["erased"] = [sh.erase(k) for k in era]
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record()
+        for _ in range(args.steps):
+            step()
+        end.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([start.elapsed_time(end) / args.steps], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    # correctness guard: every find batch is exactly half hits, every erase hits
+    hits = sum(int(f.sum().item()) for f in last["found"])
+    assert hits == len(fnd) * (B // 2), (hits, len(fnd) * (B // 2))
+    assert all(bool((e == 1).all().item()) for e in last["erased"])
+    cnt = torch.tensor([sh.table.stats()["count"]], device=dev, dtype=torch.int64)
+    dist.all_reduce(cnt)
+    assert int(cnt.item()) == total - n_era * world, int(cnt.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": world * ops_per_rank / (ms * 1e-3) / 1e9, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"cfg5: hash-sharded table of 2^{args.cfg5_log2} keys over {world} GPU(s): "
+                                   f"insert all, 2^{args.cfg5_log2} finds (50% hits), 2^{args.cfg5_log2 - 3} "
+                                   f"erases, in 2^26-op batches",
+                       "keys_total": total, "buckets_per_shard": nb, "batch": B,
+                       "parallelism": f"hash-sharded x{world} ("
+                                      f"{'NCCL all-to-all' if args.exchange == 'nccl' else 'peer-memory exchange'})",
+                       "l2": "inputs and tables larger than L2 (no flush)"},
+            "clocks": clk.summary(), "count_total": int(cnt.item())}), flush=True)
+    dist.destroy_process_group()
 
 
 def gather_ceiling(keys, nb, dev, per_kernel, hbm_peak, reps=5):
