@@ -97,6 +97,7 @@ struct Ctrl {
     unsigned long long count;          // live keys (buckets + stash), A-19
     unsigned long long stash_tail;     // ring slots used since the last drain
     unsigned long long n_left;         // Step-3 leftover list length (this phase)
+    unsigned long long slow_next;      // Step-3 work queue cursor (this phase; cleared with n_left)
     unsigned long long evictions;      // Step-3 victim swaps
     unsigned long long max_depth;      // deepest Step-3 round count
     unsigned long long stash_pushes;   // Step-4 pushes
@@ -105,7 +106,6 @@ struct Ctrl {
     unsigned long long first_abort;    // merge: first aborting pair (LIFO index)
     unsigned long long dump_n;         // dump cursor
     unsigned long long in_b1;          // stats: keys resident in addr(h1)
-    unsigned long long slow_next;      // Step-3 work queue cursor (this phase)
     unsigned long long step3;          // entries placed by the Step-3 loop (cumulative)
     unsigned long long pad[3];
     // Algorithmic bytes touched, per kernel family: 256 per

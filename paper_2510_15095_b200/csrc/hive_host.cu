@@ -13,6 +13,7 @@
 #include <mutex>
 #include <chrono>
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -150,6 +151,11 @@ struct hive_table_s {
     uint64_t* dd = nullptr;   uint64_t dd_cap = 0;
     uint32_t* owner = nullptr; uint64_t owner_cap = 0;
     uint8_t* flag = nullptr;  uint64_t flag_cap = 0;
+    // second set: hive_mixed elects its ERASE phase before the control wait
+    // (small batches only: one sub-table, no partition scratch)
+    uint64_t* dd2 = nullptr;   uint64_t dd2_cap = 0;
+    uint32_t* owner2 = nullptr; uint64_t owner2_cap = 0;
+    uint8_t* flag2 = nullptr;  uint64_t flag2_cap = 0;
     uint64_t* erec = nullptr; uint64_t erec_cap = 0;     // election records (op << 32 | key)
     unsigned long long* ecount = nullptr;                // per-part counts + cursors
     uint64_t* einfo = nullptr;                           // per-part totals / bases
@@ -404,6 +410,35 @@ hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* 
     return HIVE_OK;
 }
 
+// Owner election of a phase small enough for one sub-table, into the second
+// scratch set (hive_mixed's ERASE phase, elected before the control wait).
+// Returns false (nothing enqueued) when the phase would need partitioning.
+bool elect_owners_set2(hive_table_s* h, const uint32_t* keys, const uint32_t* idx, uint64_t n_upper,
+                       const uint64_t* n_dev, uint64_t n_batch, DedupView* dd, cudaStream_t s,
+                       hive_status* st) {
+    static const uint64_t sub_bytes = getenv("HIVE_ELECT_MB") ? (uint64_t)atoi(getenv("HIVE_ELECT_MB")) << 20
+                                                              : (32ull << 20);
+    *st = HIVE_OK;
+    if (2 * n_upper * sizeof(uint64_t) > sub_bytes) return false;
+    const uint64_t sub = pow2_at_least(std::max<uint64_t>(1024, 2 * n_upper));
+    auto fail = [&](hive_status e) { *st = e; return false; };
+    if (hive_status e = ensure(h->dd2, h->dd2_cap, sub); e != HIVE_OK) return fail(e);
+    if (hive_status e = ensure(h->owner2, h->owner2_cap, n_batch); e != HIVE_OK) return fail(e);
+    if (hive_status e = ensure(h->flag2, h->flag2_cap, n_batch); e != HIVE_OK) return fail(e);
+    *dd = DedupView{h->dd2, sub - 1, h->flag2, h->owner2, 1};
+    cudaError_t e = cudaMemsetAsync(h->flag2, 0, n_batch, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->dd2, 0xFF, sub * sizeof(uint64_t), s);
+    if (e == cudaSuccess) {
+        Prof p(h, "k_dedup_elect", s);
+        e = launch_dedup_elect(h->grids.dedup, s, keys, idx, n_upper, n_dev, *dd, h->ctrl);
+    }
+    if (e != cudaSuccess) {
+        set_err(e, "elect_owners_set2", __LINE__);
+        return fail(HIVE_ECUDA);
+    }
+    return true;
+}
+
 // ---- the INSERT phase (Steps 1-4, owner election, duplicate fix-up) ---------------
 // Chunked launch of the fast path for the host pipeline: chunk c covers ops
 // [c * chunk, ...) and waits for ready[c] (its values have been uploaded).
@@ -422,8 +457,8 @@ hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* 
     if (dedup && pre) dd = *pre;                 // election already enqueued by the caller
     else if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
     CKS(ensure(h->left, h->left_cap, std::max<uint64_t>(n_upper, 1)));
-    CK(cudaMemsetAsync(&h->ctrl->n_left, 0, sizeof(uint64_t), s));
-    CK(cudaMemsetAsync(&h->ctrl->slow_next, 0, sizeof(uint64_t), s));
+    static_assert(offsetof(Ctrl, slow_next) == offsetof(Ctrl, n_left) + sizeof(uint64_t), "adjacent");
+    CK(cudaMemsetAsync(&h->ctrl->n_left, 0, 2 * sizeof(uint64_t), s));     // n_left + slow_next
     if (chunks) {
         Prof p(h, "k_insert_fast", s);
         for (uint64_t off = 0, c = 0; off < n_upper; off += chunks->chunk, ++c) {
@@ -564,10 +599,11 @@ hive_status shrink_after(hive_table_s* h, cudaStream_t s, int64_t count_lb = -1)
 
 hive_status erase_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* idx, uint64_t n_upper,
                         const uint64_t* n_dev, uint64_t n_batch, uint8_t* out, uint32_t* vals_zero,
-                        cudaStream_t s) {
+                        cudaStream_t s, const DedupView* pre = nullptr) {
     const bool dedup = h->dedup_on();
     DedupView dd{nullptr, 0, nullptr, nullptr};
-    if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
+    if (dedup && pre) dd = *pre;                 // election already enqueued by the caller
+    else if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
     {
         Prof p(h, "k_erase", s);
         CK(launch_erase(h->grids, s, keys, idx, n_upper, n_dev, h->tv(), h->sv(), dd, out,
@@ -741,7 +777,7 @@ hive_status hive_destroy(hive_t h) {
     vrange_free(h->ix);
     vrange_free(h->dr);
     vrange_free(h->sp);
-    void* bufs[] = {h->ctrl, h->dd, h->owner, h->flag, h->left, h->cls, h->cnt, h->pinfo, h->aborts,
+    void* bufs[] = {h->ctrl, h->dd, h->owner, h->flag, h->dd2, h->owner2, h->flag2, h->left, h->cls, h->cnt, h->pinfo, h->aborts,
                     h->erec, h->ecount, h->einfo, h->hk, h->hv, h->hst, h->fq, h->fv, h->ff};
     for (auto e : h->pipe_ev) cudaEventDestroy(e);
     if (h->ins_free) cudaEventDestroy(h->ins_free);
@@ -819,8 +855,8 @@ hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
     const uint64_t* n_ins = h->pinfo + 1;
     const uint64_t* n_era = h->pinfo + 2;
     int64_t count_lb = -1;
-    DedupView dd_ins{nullptr, 0, nullptr, nullptr};
-    bool pre = false;
+    DedupView dd_ins{nullptr, 0, nullptr, nullptr}, dd_era{nullptr, 0, nullptr, nullptr};
+    bool pre = false, pre_era = false;
     if (h->cfg.lf_grow < 1.0f) {           // one wait: phase sizes + counters
         if (!h->ctrl_ev) CK(cudaEventCreateWithFlags(&h->ctrl_ev, cudaEventDisableTiming));
         CK(cudaMemcpyAsync(h->stage_h, h->pinfo, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
@@ -832,6 +868,9 @@ hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
         if (h->dedup_on()) {
             CKS(elect_owners(h, d_keys, h->cls + n, n, n_ins, n, &dd_ins, s));
             pre = true;
+            hive_status e2 = HIVE_OK;
+            pre_era = elect_owners_set2(h, d_keys, h->cls + 2 * n, n, n_era, n, &dd_era, s, &e2);
+            CKS(e2);
         }
         {
             Trace tr("read_ctrl", 0);
@@ -844,7 +883,7 @@ hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
     }
     CKS(insert_phase(h, d_keys, d_vals, nullptr, h->cls + n, n, n_ins, n, d_result, d_vals_out, s, nullptr,
                      pre ? &dd_ins : nullptr));
-    CKS(erase_phase(h, d_keys, h->cls + 2 * n, n, n_era, n, d_result, d_vals_out, s));
+    CKS(erase_phase(h, d_keys, h->cls + 2 * n, n, n_era, n, d_result, d_vals_out, s, pre_era ? &dd_era : nullptr));
     CKS(shrink_after(h, s, count_lb));
     Prof p(h, "k_find", s);
     CK(launch_find(h->grids, s, d_keys, h->cls, n, n_find, h->tv(), h->sv(), d_vals_out, d_result));

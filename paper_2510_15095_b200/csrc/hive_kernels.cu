@@ -1192,22 +1192,34 @@ k_part_count(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __restri
     if (w < n_warps) {
         const uint64_t lo = w * chunk;
         const uint64_t hi = lo + chunk < n ? lo + chunk : (lo < n ? n : lo);
-        for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
-            const uint64_t i = i0 + lane;
-            const uint64_t e = i < hi ? (idx ? (uint64_t)idx[i] : i) : 0;
-            uint32_t p = i < hi ? part_of(mode, n_parts, seed, keys, ops, e) : MAX_PARTS;
-            if (small && p >= n_parts) p = MAX_PARTS;
-            const uint32_t grp = same_label(small && p == MAX_PARTS ? 15u : p, small);
-            if ((__ffs(grp) - 1) == lane) sc[wib][p] += __popc(grp);
-            __syncwarp();
+        // PART_UNROLL rows of 32 elements per iteration: their loads are all
+        // issued before the first label is ranked
+        for (uint64_t i0 = lo; i0 < hi; i0 += 32 * PART_UNROLL) {
+            uint32_t pp[PART_UNROLL];
+#pragma unroll
+            for (int u = 0; u < PART_UNROLL; ++u) {
+                const uint64_t i = i0 + u * 32 + lane;
+                const uint64_t e = i < hi ? (idx ? (uint64_t)idx[i] : i) : 0;
+                pp[u] = i < hi ? part_of(mode, n_parts, seed, keys, ops, e) : MAX_PARTS;
+            }
+#pragma unroll
+            for (int u = 0; u < PART_UNROLL; ++u) {
+                uint32_t p = pp[u];
+                if (small && p >= n_parts) p = MAX_PARTS;
+                const uint32_t grp = same_label(small && p == MAX_PARTS ? 15u : p, small);
+                if ((__ffs(grp) - 1) == lane) sc[wib][p] += __popc(grp);
+                __syncwarp();
+            }
         }
         for (uint32_t p = lane; p < n_parts; p += 32) cnt[(uint64_t)p * n_warps + w] = sc[wib][p];
     }
 }
 
-// Pass 2: exclusive scan over cnt (single block, coalesced 1024-element tiles,
-// warp-shuffle scans); part_info[p] = total of part p,
-// part_info[MAX_PARTS + p] = global start of part p.
+// Pass 2: exclusive scan over cnt (single block).  Tiles of 1024 threads x
+// SCAN_ITEMS consecutive elements: each thread scans its items serially, the
+// thread totals are scanned with warp shuffles, the warp totals by warp 0.
+// part_info[p] = total of part p, part_info[MAX_PARTS + p] = start of part p.
+constexpr int SCAN_ITEMS = 8;
 __global__ void __launch_bounds__(1024)
 k_part_scan(uint64_t* __restrict__ cnt, uint64_t E, uint32_t n_parts, uint64_t n_warps,
             uint64_t* __restrict__ part_info) {
@@ -1216,10 +1228,17 @@ k_part_scan(uint64_t* __restrict__ cnt, uint64_t E, uint32_t n_parts, uint64_t n
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) carry = 0;
     __syncthreads();
-    for (uint64_t base = 0; base < E; base += 1024) {
-        const uint64_t i = base + tid;
-        const uint64_t v = i < E ? cnt[i] : 0;
-        uint64_t x = v;
+    constexpr uint64_t TILE = 1024ull * SCAN_ITEMS;
+    for (uint64_t base = 0; base < E; base += TILE) {
+        const uint64_t i0 = base + (uint64_t)tid * SCAN_ITEMS;
+        uint64_t v[SCAN_ITEMS];
+        uint64_t t = 0;
+#pragma unroll
+        for (int j = 0; j < SCAN_ITEMS; ++j) {
+            v[j] = i0 + j < E ? cnt[i0 + j] : 0;
+            t += v[j];
+        }
+        uint64_t x = t;                                   // inclusive warp scan of thread totals
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint64_t y = __shfl_up_sync(FULL, x, o);
@@ -1237,10 +1256,14 @@ k_part_scan(uint64_t* __restrict__ cnt, uint64_t E, uint32_t n_parts, uint64_t n
             wsum[lane] = w;
         }
         __syncthreads();
-        const uint64_t c = carry;
-        if (i < E) cnt[i] = c + (wid ? wsum[wid - 1] : 0) + x - v;
+        uint64_t run = carry + (wid ? wsum[wid - 1] : 0) + x - t;
+#pragma unroll
+        for (int j = 0; j < SCAN_ITEMS; ++j) {
+            if (i0 + j < E) cnt[i0 + j] = run;
+            run += v[j];
+        }
         __syncthreads();
-        if (tid == 0) carry = c + wsum[31];
+        if (tid == 0) carry += wsum[31];
         __syncthreads();
     }
     const uint64_t total = carry;
@@ -1274,45 +1297,57 @@ k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __rest
     __syncwarp();
     const uint64_t lo = w * chunk;
     const uint64_t hi = lo + chunk < n ? lo + chunk : (lo < n ? n : lo);
-    for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
-        const uint64_t i = i0 + lane;
-        const bool in = i < hi;
-        const uint64_t e = in ? (idx ? (uint64_t)idx[i] : i) : 0;
-        uint32_t p = in ? part_of(mode, n_parts, seed, keys, ops, e) : MAX_PARTS;
-        if (small && p >= n_parts) p = MAX_PARTS;
-        const uint32_t grp = same_label(small && p == MAX_PARTS ? 15u : p, small);
-        const uint32_t rank = __popc(grp & lanemask_lt());
-        uint64_t pos = 0;
-        if (in && p < n_parts) pos = run[wib][p] + rank;
-        __syncwarp();
-        if (in && p < n_parts && (__ffs(grp) - 1) == lane) run[wib][p] += __popc(grp);
-        __syncwarp();
-        if (!in) continue;
-        if (mode == PART_ELECT) {
-            if (p < n_parts) send_kv[pos] = (e << 32) | keys[e];
-        } else if (mode == PART_CLASSIFY) {
-            if (p < n_parts) {
-                out_idx[(uint64_t)p * idx_stride + (pos - part_info[MAX_PARTS + p])] = (uint32_t)i;
+    for (uint64_t r0 = lo; r0 < hi; r0 += 32 * PART_UNROLL) {
+        uint32_t pp[PART_UNROLL];
+        uint64_t ee[PART_UNROLL];
+#pragma unroll
+        for (int u = 0; u < PART_UNROLL; ++u) {                  // all rows' loads first
+            const uint64_t i = r0 + u * 32 + lane;
+            ee[u] = i < hi ? (idx ? (uint64_t)idx[i] : i) : 0;
+            pp[u] = i < hi ? part_of(mode, n_parts, seed, keys, ops, ee[u]) : MAX_PARTS;
+        }
+#pragma unroll
+        for (int u = 0; u < PART_UNROLL; ++u) {                  // then rank the rows in order
+            const uint64_t i0 = r0 + u * 32;
+            const uint64_t i = i0 + lane;
+            const bool in = i < hi;
+            const uint64_t e = ee[u];
+            uint32_t p = pp[u];
+            if (small && p >= n_parts) p = MAX_PARTS;
+            const uint32_t grp = same_label(small && p == MAX_PARTS ? 15u : p, small);
+            const uint32_t rank = __popc(grp & lanemask_lt());
+            uint64_t pos = 0;
+            if (in && p < n_parts) pos = run[wib][p] + rank;
+            __syncwarp();
+            if (in && p < n_parts && (__ffs(grp) - 1) == lane) run[wib][p] += __popc(grp);
+            __syncwarp();
+            if (!in) continue;
+            if (mode == PART_ELECT) {
+                if (p < n_parts) send_kv[pos] = (e << 32) | keys[e];
+            } else if (mode == PART_CLASSIFY) {
+                if (p < n_parts) {
+                    out_idx[(uint64_t)p * idx_stride + (pos - part_info[MAX_PARTS + p])] = (uint32_t)i;
+                } else {
+                    if (result_zero) result_zero[i] = 0;
+                    if (vals_zero) vals_zero[i] = 0;
+                }
+            } else if (mode == PART_ROUTE_KEYS) {
+                reinterpret_cast<uint32_t*>(send_kv)[pos] = keys[i];
+                pos_out[i] = (uint32_t)pos;
+            } else if (mode == PART_ROUTE_P2P) {
+                // owner p's inbox, this rank's region: a remote store over NVLink
+                // (a local one when p is this rank); the stable rank keeps the
+                // (rank, index) order the owner's PHASED batch relies on
+                const uint64_t rel = pos - part_info[MAX_PARTS + p];
+                const uint64_t at = (uint64_t)pd.rank * pd.region + rel;
+                pd.kv[p][at] = ((uint64_t)(vals ? vals[i] : 0u) << 32) | keys[i];
+                if (pd.ops[p]) pd.ops[p][at] = ops[i];
+                pos_out[i] = (uint32_t)((uint64_t)p * pd.region + rel);
             } else {
-                if (result_zero) result_zero[i] = 0;
-                if (vals_zero) vals_zero[i] = 0;
+                send_kv[pos] = ((uint64_t)(vals ? vals[i] : 0u) << 32) | keys[i];
+                if (send_ops) send_ops[pos] = ops[i];
+                pos_out[i] = (uint32_t)pos;
             }
-        } else if (mode == PART_ROUTE_KEYS) {
-            reinterpret_cast<uint32_t*>(send_kv)[pos] = keys[i];
-            pos_out[i] = (uint32_t)pos;
-        } else if (mode == PART_ROUTE_P2P) {
-            // owner p's inbox, this rank's region: a remote store over NVLink
-            // (a local one when p is this rank); the stable rank keeps the
-            // (rank, index) order the owner's PHASED batch relies on
-            const uint64_t rel = pos - part_info[MAX_PARTS + p];
-            const uint64_t at = (uint64_t)pd.rank * pd.region + rel;
-            pd.kv[p][at] = ((uint64_t)(vals ? vals[i] : 0u) << 32) | keys[i];
-            if (pd.ops[p]) pd.ops[p][at] = ops[i];
-            pos_out[i] = (uint32_t)((uint64_t)p * pd.region + rel);
-        } else {
-            send_kv[pos] = ((uint64_t)(vals ? vals[i] : 0u) << 32) | keys[i];
-            if (send_ops) send_ops[pos] = ops[i];
-            pos_out[i] = (uint32_t)pos;
         }
     }
 }

@@ -15,7 +15,8 @@ constexpr int WARPS_PER_BLOCK = BLOCK / 32;
 constexpr int G_FIND = 4, G_INSERT = 4, G_ERASE = 2, G_SLOW = 2;
 constexpr int MINB_FIND_DEFAULT = 6;           // 40 regs: 3.60 ms vs 3.79 (48 regs) vs 4.60 (32, spills)
 constexpr int MINB_DEFAULT = 4;          // 4 blocks/SM => <= 64 registers (ncu: 74-80 regs left 36% warps active)
-constexpr int PART_CHUNK = 2048;         // elements per warp in the stable partition
+constexpr int PART_CHUNK = 8192;         // max elements per warp in the stable partition
+constexpr int PART_UNROLL = 4;           // rows of 32 elements whose loads are in flight together
 constexpr int MAX_PARTS = 64;
 
 enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1, PART_ELECT = 2, PART_ROUTE_KEYS = 3, PART_ROUTE_P2P = 4 };

@@ -61,13 +61,28 @@ class ShardedHive:
 
     # ---- exchange ---------------------------------------------------------------
     def _counts(self, send_counts: torch.Tensor):
+        if self.world == 1:
+            sc = send_counts.cpu().tolist()                    # one small D2H per batch
+            return sc, sc
         recv_counts = torch.empty_like(send_counts)
         dist.all_to_all_single(recv_counts, send_counts, group=self.group)
         both = torch.stack([send_counts, recv_counts]).cpu()   # one small D2H per batch
         return both[0].tolist(), both[1].tolist()
 
     def _a2a(self, x: torch.Tensor, out_splits, in_splits) -> torch.Tensor:
+        """All-to-all of a routed buffer.  This rank's own block never goes
+        through the collective: a device copy (or, at world size 1, nothing)
+        places it, and NCCL moves only the off-diagonal blocks."""
+        if self.world == 1:
+            return x
         out = torch.empty(sum(out_splits), dtype=x.dtype, device=x.device)
+        if x.is_cuda and dist.get_backend(self.group) == "nccl":
+            outs, ins = list(out.split(out_splits)), list(x.split(in_splits))
+            me = self.rank
+            outs[me].copy_(ins[me])
+            dist.all_to_all([o if r != me else o[:0] for r, o in enumerate(outs)],
+                            [t if r != me else t[:0] for r, t in enumerate(ins)], group=self.group)
+            return out
         dist.all_to_all_single(out, x, out_splits, in_splits, group=self.group)
         return out
 
