@@ -135,6 +135,7 @@ struct hive_table_s {
     VRange sp;                         // spill filter: one u64 per bucket
     CUdeviceptr va = 0;                // == bk.va
     uint64_t max_buckets = 0, nb_min = 0;
+    uint64_t nb_at_drain = 0;          // bucket count when the stash was last drained (A-29)
     uint32_t m0 = 0, split0 = 0, m = 0, split = 0;
 
     // stash ring + index (A-10)
@@ -489,12 +490,23 @@ hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* 
 // stash tail of the synchronising read that preceded the resize.  The oracle
 // drains after every K-bucket batch; the GPU drains once per resize phase
 // (stash membership is not observable, count is unchanged either way).
-hive_status drain_reinsert(hive_table_s* h, cudaStream_t s) {
+// Expansion-time drains are batched (reading A-29): while the table has grown
+// by less than 1/8 since the last drain and the stash is under 1/4 of its
+// capacity -- with room for 1/16 of the coming inserts -- the drain waits for
+// a later expansion phase.  Contraction always drains (the capacity shrinks).
+// HIVE_DRAIN_EVERY=1 drains at every resize phase.
+hive_status drain_reinsert(hive_table_s* h, cudaStream_t s, bool growing = false, uint64_t n_ins = 0) {
+    static const bool every = getenv("HIVE_DRAIN_EVERY") && atoi(getenv("HIVE_DRAIN_EVERY")) != 0;
     const uint64_t new_cap = h->stash_cap_for(h->nb());
     if (h->tail_known == 0) {
         if (new_cap != h->stash_cap) CKS(stash_reset(h, new_cap, s));
+        h->nb_at_drain = h->nb();
         return HIVE_OK;
     }
+    if (growing && !every && h->tail_known != ~0ull && 8 * h->nb() < 9 * h->nb_at_drain &&
+        4 * h->tail_known < h->stash_cap && h->tail_known + n_ins / 16 < h->stash_cap)
+        return HIVE_OK;
+    h->nb_at_drain = h->nb();
     const uint64_t used = std::min<uint64_t>(h->tail_known, h->stash_cap);
     Trace tr("drain", used);
     CKS(vrange_map(h, h->dr, used * sizeof(uint64_t)));
@@ -536,7 +548,7 @@ hive_status grow_known(hive_table_s* h, uint64_t count, uint64_t n_ins, cudaStre
         if (h->split == round_end) { h->m += 1; h->split = 0; }
     }
     h->grows += batches;
-    return drain_reinsert(h, s);
+    return drain_reinsert(h, s, true, n_ins);
 }
 
 hive_status grow_before(hive_table_s* h, uint64_t n_ins, cudaStream_t s) {
@@ -709,6 +721,7 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     h->m = h->m0 = m;
     h->split = h->split0 = (uint32_t)(nb - (1ull << m));
     h->nb_min = nb;
+    h->nb_at_drain = nb;
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     uint64_t maxb = cfg->max_capacity ? (cfg->max_capacity + SLOTS - 1) / SLOTS
@@ -764,6 +777,7 @@ hive_status hive_clear(hive_t h, void* stream) {
     CK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), s));
     CKS(stash_reset(h, h->stash_cap_for(h->nb_min), s));
     h->grows = h->shrinks = h->merge_aborts = 0;
+    h->nb_at_drain = h->nb_min;
     h->last = s;
     return HIVE_OK;
 }
