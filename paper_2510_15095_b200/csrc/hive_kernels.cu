@@ -1350,6 +1350,9 @@ k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __rest
             }
         }
     }
+    // peer stores are made visible system-wide before the phase signal
+    // (k_p2p_signal runs after this kernel in stream order)
+    if (mode == PART_ROUTE_P2P) __threadfence_system();
 }
 
 __global__ void __launch_bounds__(BLOCK)
