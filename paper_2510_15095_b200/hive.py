@@ -431,5 +431,5 @@ def p2p_signal(n, rank, phase, epoch, peer_sig, stream=None):
     _check(lib().hive_p2p_signal(n, rank, phase, epoch, _ptrs(peer_sig), _stream(stream)), "hive_p2p_signal")
 
 
-def p2p_wait(n, phase, epoch, sig: int, timeout_ns=10_000_000_000, stream=None):
+def p2p_wait(n, phase, epoch, sig: int, timeout_ns=60_000_000_000, stream=None):
     _check(lib().hive_p2p_wait(n, phase, epoch, ctypes.c_void_p(sig), timeout_ns, _stream(stream)), "hive_p2p_wait")
