@@ -935,11 +935,26 @@ k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uin
     uint32_t ab = 0;                       // per-thread: < 2^32 bytes
     const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
-    for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += nw * WG::GPW) {
+    // software pipeline (as in k_find): the next iteration's (op, key) loads
+    // are in flight while this one probes
+    const uint64_t stride = nw * WG::GPW;
+    uint32_t op_n = 0, k_n = INVALID_KEY;
+    {
+        const uint64_t t = warp * WG::GPW + wg.gi;
+        if (t < n) {
+            op_n = idx ? idx[t] : (uint32_t)t;
+            k_n = keys[op_n];
+        }
+    }
+    for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += stride) {
         const uint64_t t = t0 + wg.gi;
         const bool active = t < n;
-        const uint32_t op = active ? (idx ? idx[t] : (uint32_t)t) : 0u;   // < 2^32 (API)
-        const uint32_t k = active ? keys[op] : INVALID_KEY;
+        const uint32_t op = active ? op_n : 0u;                // < 2^32 (API)
+        const uint32_t k = active ? k_n : INVALID_KEY;
+        if (t + stride < n) {
+            op_n = idx ? idx[t + stride] : (uint32_t)(t + stride);
+            k_n = keys[op_n];
+        }
         bool valid = k != INVALID_KEY;
         uint32_t b1 = 0, b2 = 0;
         if (valid) {
