@@ -58,6 +58,7 @@ class ShardedHive:
         self.seed = seed
         self.ops = ops if ops is not None else CudaOps(capacity_per_shard, **cfg)
         self.table = self.ops.table
+        self._single_a2a = False                    # fall back to all_to_all_single
 
     # ---- exchange ---------------------------------------------------------------
     def _counts(self, send_counts: torch.Tensor):
@@ -76,13 +77,16 @@ class ShardedHive:
         if self.world == 1:
             return x
         out = torch.empty(sum(out_splits), dtype=x.dtype, device=x.device)
-        if x.is_cuda and dist.get_backend(self.group) == "nccl":
+        if x.is_cuda and dist.get_backend(self.group) == "nccl" and not self._single_a2a:
             outs, ins = list(out.split(out_splits)), list(x.split(in_splits))
             me = self.rank
-            outs[me].copy_(ins[me])
-            dist.all_to_all([o if r != me else o[:0] for r, o in enumerate(outs)],
-                            [t if r != me else t[:0] for r, t in enumerate(ins)], group=self.group)
-            return out
+            try:
+                dist.all_to_all([o if r != me else o[:0] for r, o in enumerate(outs)],
+                                [t if r != me else t[:0] for r, t in enumerate(ins)], group=self.group)
+                outs[me].copy_(ins[me])
+                return out
+            except (RuntimeError, ValueError):      # argument rejected before any transfer
+                self._single_a2a = True
         dist.all_to_all_single(out, x, out_splits, in_splits, group=self.group)
         return out
 
