@@ -1152,7 +1152,8 @@ hive_status hive_inbox_compact(uint32_t n_src, uint64_t region, const uint64_t* 
                                const uint8_t* d_inbox_ops, const uint64_t* d_cnt, uint64_t n_total,
                                uint32_t* d_keys, uint32_t* d_vals, uint8_t* d_ops, void* stream) {
     if (n_src == 0 || n_src > (uint32_t)MAX_PEERS || !d_cnt) return HIVE_EINVAL;
-    if (n_total && (!d_inbox_kv || !d_keys || !d_vals || ((d_ops != nullptr) != (d_inbox_ops != nullptr))))
+    if (n_total && (!d_inbox_kv || !d_keys || !d_vals || region == 0 || n_total > (uint64_t)n_src * region ||
+                    ((d_ops != nullptr) != (d_inbox_ops != nullptr))))
         return HIVE_EINVAL;
     CK(launch_inbox_compact((cudaStream_t)stream, n_src, region, d_inbox_kv, d_inbox_ops, d_cnt, n_total, d_keys,
                             d_vals, d_ops));
@@ -1163,7 +1164,7 @@ hive_status hive_return_p2p(uint32_t n_src, uint32_t rank, uint64_t region, cons
                             uint64_t n_total, const uint32_t* d_res32, const uint8_t* d_res8,
                             uint32_t* const* peer_res32, uint8_t* const* peer_res8, void* stream) {
     PeerDest pd;
-    if (!fill_peers(pd, n_src, region, rank) || !d_cnt) return HIVE_EINVAL;
+    if (!fill_peers(pd, n_src, region, rank) || !d_cnt || n_total > (uint64_t)n_src * region) return HIVE_EINVAL;
     for (uint32_t p = 0; p < n_src; ++p) {
         if ((d_res32 && (!peer_res32 || !peer_res32[p])) || (d_res8 && (!peer_res8 || !peer_res8[p])))
             return HIVE_EINVAL;
