@@ -541,12 +541,27 @@ def gather_ceiling(keys, nb, dev, per_kernel, hbm_peak, reps=5):
     torch.cuda.synchronize()
     ms = statistics.mean(ev[2 * r].elapsed_time(ev[2 * r + 1]) for r in range(reps))
     gbps = keys.numel() * (256 + 8) / (ms * 1e-3) / 1e9
+    # the read/write mix of an insert probe: + one 32 B sector dirtied per op
+    # by a plain store (mode 1) or a CAS (mode 2)
+    rw = {}
+    for mode, name in ((1, "store"), (2, "cas")):
+        hive.gather_ceiling_rw(blocks, keys, mode, out, stream=s)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            hive.gather_ceiling_rw(blocks, keys, mode, out, stream=s)
+        e1.record(s)
+        torch.cuda.synchronize()
+        m = e0.elapsed_time(e1) / reps
+        rw[name] = {"ms": m, "GBps": keys.numel() * (256 + 32 + 8) / (m * 1e-3) / 1e9}
     del blocks, out
     res = {"random_256B_gather_GBps": gbps, "gather_ms": ms, "gather_ops": keys.numel(),
-           "gather_array_bytes": nb * 256, "measured_copy_GBps": hbm_peak, "nominal_GBps": 8000.0}
+           "gather_array_bytes": nb * 256, "measured_copy_GBps": hbm_peak, "nominal_GBps": 8000.0,
+           "gather_plus_store": rw["store"], "gather_plus_cas": rw["cas"]}
     for k, v in per_kernel.items():
         res[k] = {"of_nominal": v["achieved_GBps"] / 8000.0, "of_copy": v["achieved_GBps"] / hbm_peak,
-                  "of_gather": v["achieved_GBps"] / gbps}
+                  "of_gather": v["achieved_GBps"] / gbps,
+                  "of_gather_plus_cas": v["achieved_GBps"] / rw["cas"]["GBps"]}
     return res
 
 

@@ -314,6 +314,14 @@ hive_status hive_collisions(uint32_t fn, const uint32_t* d_keys, uint64_t n, uin
  * misalignment, or n_blocks outside [1, 2^32]. */
 hive_status hive_gather_ceiling(const uint64_t* d_blocks, uint64_t n_blocks, const uint32_t* d_keys,
                                 uint64_t n, uint32_t* d_out, void* stream);
+/* The same gather with the read/write mix of an insert probe: mode 0 = read
+ * only (as above); mode 1 = the group's leader then stores 8 B (s0 ^ 1) into
+ * slot (key & 31) of the block; mode 2 = that slot is updated by a 64-bit CAS
+ * (expected = the block's first word as read, new = that ^ 1; the CAS result
+ * is folded into d_out).  d_blocks is written in modes 1-2.  HIVE_EINVAL for
+ * mode > 2 or the conditions above. */
+hive_status hive_gather_ceiling_rw(uint64_t* d_blocks, uint64_t n_blocks, const uint32_t* d_keys, uint64_t n,
+                                   uint32_t* d_out, uint32_t mode, void* stream);
 
 /* Split packed records (value << 32 | key) into key / value arrays. */
 hive_status hive_unpack_kv(const uint64_t* d_kv, uint64_t n, uint32_t* d_keys,

@@ -1239,6 +1239,12 @@ hive_status hive_hash(uint32_t fn, const uint32_t* d_keys, uint64_t n, uint32_t*
 
 hive_status hive_gather_ceiling(const uint64_t* d_blocks, uint64_t n_blocks, const uint32_t* d_keys,
                                 uint64_t n, uint32_t* d_out, void* stream) {
+    return hive_gather_ceiling_rw((uint64_t*)d_blocks, n_blocks, d_keys, n, d_out, 0, stream);
+}
+
+hive_status hive_gather_ceiling_rw(uint64_t* d_blocks, uint64_t n_blocks, const uint32_t* d_keys, uint64_t n,
+                                   uint32_t* d_out, uint32_t mode, void* stream) {
+    if (mode > 2) return HIVE_EINVAL;
     if (n == 0) return HIVE_OK;
     if (!d_blocks || !d_keys || !d_out || n_blocks == 0 || n_blocks > (1ull << 32)) return HIVE_EINVAL;
     if ((uintptr_t)d_blocks % 256) return HIVE_EINVAL;
@@ -1251,7 +1257,7 @@ hive_status hive_gather_ceiling(const uint64_t* d_blocks, uint64_t n_blocks, con
         gr = query_grids(sms);
         grid_dev = dev;
     }
-    CK(launch_gather(gr, (cudaStream_t)stream, d_keys, n, d_blocks, n_blocks, d_out));
+    CK(launch_gather(gr, (cudaStream_t)stream, d_keys, n, d_blocks, n_blocks, d_out, mode));
     return HIVE_OK;
 }
 

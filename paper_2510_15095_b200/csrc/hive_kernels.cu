@@ -1396,10 +1396,12 @@ k_unpack(const uint64_t* __restrict__ kv, uint64_t n, uint32_t* __restrict__ key
 // k_find (G lanes, 256-bit vectors), write one 4 B word (xor of the block).  No
 // compares, no second probe: random 256 B reads at the find kernel's access
 // count, against which the probe kernels' GB/s is judged.
+// mode 1 adds a plain 8 B store and mode 2 a 64-bit CAS (with return) into
+// one slot of each gathered block: the read/write mix of an insert probe.
 template <int G, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB)
 k_gather(const uint32_t* __restrict__ keys, uint64_t n, const uint64_t* __restrict__ blocks,
-         uint64_t n_blocks, uint32_t* __restrict__ out) {
+         uint64_t n_blocks, uint32_t* __restrict__ out, uint32_t mode) {
     using WG = WarpGroup<G>;
     constexpr int SPL = WG::SPL;
     WG wg;
@@ -1415,9 +1417,16 @@ k_gather(const uint32_t* __restrict__ keys, uint64_t n, const uint64_t* __restri
         uint32_t x = 0;
         if (t < n) {
             const uint64_t b = ((uint64_t)fmix32(k) * n_blocks) >> 32;
-            load_slots_ro<SPL>(blocks + b * SLOTS + wg.gl * SPL, s);
+            uint64_t* blk = const_cast<uint64_t*>(blocks) + b * SLOTS;
+            if (mode) load_slots<SPL>(blk + wg.gl * SPL, s);
+            else load_slots_ro<SPL>(blk + wg.gl * SPL, s);
 #pragma unroll
             for (int j = 0; j < SPL; ++j) x ^= (uint32_t)s[j] ^ (uint32_t)(s[j] >> 32);
+            if (mode && wg.gl == 0) {
+                const int j = (int)(k & 31u);              // one slot, one dirty sector
+                if (mode == 1) blk[j] = s[0] ^ 1ull;
+                else x ^= (uint32_t)cas64(blk + j, s[0], s[0] ^ 1ull);
+            }
         }
 #pragma unroll
         for (int o = 1; o < G; o <<= 1) x ^= __shfl_xor_sync(FULL, x, o);
@@ -1714,9 +1723,9 @@ cudaError_t launch_popc(cudaStream_t s, const uint32_t* bins, uint64_t words, un
 }
 
 cudaError_t launch_gather(const Grids& gr, cudaStream_t s, const uint32_t* keys, uint64_t n,
-                          const uint64_t* blocks, uint64_t n_blocks, uint32_t* out) {
+                          const uint64_t* blocks, uint64_t n_blocks, uint32_t* out, uint32_t mode) {
     const int grid = clamp_grid(gr.gather, n, BLOCK / gr.g_find);
-#define L_GATHER(G, MB) k_gather<G, MB><<<grid, BLOCK, 0, s>>>(keys, n, blocks, n_blocks, out)
+#define L_GATHER(G, MB) k_gather<G, MB><<<grid, BLOCK, 0, s>>>(keys, n, blocks, n_blocks, out, mode)
     HIVE_DISPATCH_GM8(gr.g_find, gr.minb_find, L_GATHER)
     return cudaGetLastError();
 }

@@ -55,7 +55,7 @@ cudaError_t init_hash_tables();
 // Calibration gather: random 256 B block reads at k_find's
 // access pattern; out[i] = xor of block (fmix32(keys[i]) * n_blocks) >> 32.
 cudaError_t launch_gather(const Grids& gr, cudaStream_t s, const uint32_t* keys, uint64_t n,
-                          const uint64_t* blocks, uint64_t n_blocks, uint32_t* out);
+                          const uint64_t* blocks, uint64_t n_blocks, uint32_t* out, uint32_t mode);
 
 cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                         uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,

@@ -71,6 +71,7 @@ SIGNATURES = {
     "hive_unpack_kv": (_int, [_vp, _u64, _vp, _vp, _vp]),
     "hive_hash": (_int, [_u32, _vp, _u64, _vp, _vp]),
     "hive_gather_ceiling": (_int, [_vp, _u64, _vp, _u64, _vp, _vp]),
+    "hive_gather_ceiling_rw": (_int, [_vp, _u64, _vp, _u64, _vp, _u32, _vp]),
     "hive_route_p2p": (_int, [_u32, _u32, _u32, _vp, _vp, _vp, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hive_inbox_compact": (_int, [_u32, _u64, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
     "hive_return_p2p": (_int, [_u32, _u32, _u64, _vp, _u64, _vp, _vp, _vp, _vp, _vp]),
@@ -354,6 +355,18 @@ def gather_ceiling(blocks: torch.Tensor, keys: torch.Tensor, out: torch.Tensor |
         out = torch.empty(n, dtype=torch.uint32, device=keys.device)
     _check(lib().hive_gather_ceiling(_p(blocks), blocks.numel() // 32, _p(keys), n, _p(out),
                                      _stream(stream)), "hive_gather_ceiling")
+    return out
+
+
+def gather_ceiling_rw(blocks: torch.Tensor, keys: torch.Tensor, mode: int, out: torch.Tensor | None = None,
+                      stream=None) -> torch.Tensor:
+    """hive_gather_ceiling_rw: the gather plus an 8 B store (mode 1) or a CAS
+    (mode 2) into one slot per block -- an insert probe's read/write mix."""
+    n = keys.numel()
+    if out is None:
+        out = torch.empty(n, dtype=torch.uint32, device=keys.device)
+    _check(lib().hive_gather_ceiling_rw(_p(blocks), blocks.numel() // 32, _p(keys), n, _p(out), mode,
+                                        _stream(stream)), "hive_gather_ceiling_rw")
     return out
 
 

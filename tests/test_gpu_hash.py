@@ -143,3 +143,29 @@ def test_gather_ceiling_reads_the_named_blocks(n, n_blocks):
     words = blocks.view(np.uint32).reshape(n_blocks, 64)
     exp = np.bitwise_xor.reduce(words[b.astype(np.int64)], axis=1)
     assert (out == exp).all()
+
+
+def test_gather_ceiling_rw_store_and_cas():
+    """hive_gather_ceiling_rw: mode 1 stores word0 ^ 1 into slot (k & 31) of
+    the key's block; mode 2 CASes that slot from word0 to word0 ^ 1 (so only
+    slot 0, or a slot equal to word0, changes).  Keys here hit distinct blocks."""
+    from paper_2510_15095_b200 import hive
+    rng = np.random.default_rng(11)
+    n_blocks = 1 << 16
+    keys = rng.integers(0, 1 << 32, 3000, dtype=np.uint64).astype(np.uint32)
+    b = ((gen.fmix32(keys).astype(np.uint64) * np.uint64(n_blocks)) >> np.uint64(32)).astype(np.int64)
+    _, first = np.unique(b, return_index=True)
+    keys, b = keys[np.sort(first)], b[np.sort(first)]            # one key per block
+    orig = rng.integers(0, 1 << 63, n_blocks * 32, dtype=np.int64)
+    for mode in (1, 2):
+        dev = torch.from_numpy(orig.copy()).cuda()
+        hive.gather_ceiling_rw(dev, _dev(keys), mode)
+        got = dev.cpu().numpy().reshape(n_blocks, 32)
+        exp = orig.copy().reshape(n_blocks, 32)
+        j = (keys & 31).astype(np.int64)
+        if mode == 1:
+            exp[b, j] = exp[b, 0] ^ 1
+        else:
+            hit = exp[b, j] == exp[b, 0]
+            exp[b[hit], j[hit]] = exp[b[hit], 0] ^ 1
+        assert (got == exp).all(), mode
