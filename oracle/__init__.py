@@ -106,6 +106,8 @@ def lib():
         L.oracle_uniform_expected_collisions.restype = ctypes.c_double
         L.oracle_observed_collisions.argtypes = [u32, vp, u64, u64]
         L.oracle_observed_collisions.restype = u64
+        L.oracle_fmix32.argtypes = [u32]
+        L.oracle_fmix32.restype = u32
         L.oracle_shard.argtypes = [u32, u32, u32]
         L.oracle_shard.restype = u32
         _lib = L
@@ -242,6 +244,7 @@ def first_set(m): return lib().oracle_first_set(m)
 def prefix_rank(m, lane): return lib().oracle_prefix_rank(m, lane)
 def select_nth_one(m, r): return lib().oracle_select_nth_one(m, r)
 def shard(key, seed, g): return lib().oracle_shard(key, seed, g)
+def fmix32(h): return lib().oracle_fmix32(h)
 
 
 def ballot(preds) -> int:

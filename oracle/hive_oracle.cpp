@@ -507,6 +507,15 @@ struct Table {
             buckets.resize(NB() * S);           /* the partner bucket is released */
             freeMask.resize(NB());
         }
+        /* Reading A-30: a regressed round whose first merge aborted is left at
+         * split == 2^m, which is the state (m+1, 0) re-expressed (A-7).  It is
+         * written back as (m+1, 0): ExpandBatch's round arithmetic
+         * (2^m - split buckets left in the round) needs split < 2^m, and with
+         * split == 2^m the table could never grow again. */
+        if (split == (uint32_t)(1ull << m)) {
+            m++;
+            split = 0;
+        }
         st.shrinks++;
         DrainAndReinsert();
         return aborted;
@@ -806,6 +815,7 @@ uint32_t oracle_ballot(const uint8_t* preds32) {
 int oracle_first_set(uint32_t mask) { return FirstSet(mask); }
 uint32_t oracle_prefix_rank(uint32_t mask, uint32_t lane) { return PrefixRank(mask, lane); }
 int oracle_select_nth_one(uint32_t mask, uint32_t r) { return SelectNthOne(mask, r); }
+uint32_t oracle_fmix32(uint32_t h) { return Fmix32(h); }
 /* shard(k) = (uint64(fmix32(k ^ seed)) * G) >> 32 */
 uint32_t oracle_shard(uint32_t key, uint32_t seed, uint32_t n_shards) {
     return (uint32_t)(((uint64_t)Fmix32(key ^ seed) * (uint64_t)n_shards) >> 32);

@@ -605,6 +605,13 @@ hive_status shrink_after(hive_table_s* h, cudaStream_t s, int64_t count_lb = -1)
         h->split = segs[i].split0 - (uint32_t)merged;
         if (merged < segs[i].pairs) { h->merge_aborts++; break; }
     }
+    // Reading A-30: a regressed round that merged nothing leaves split == 2^m,
+    // the state (m+1, 0) re-expressed (A-7); write it back as (m+1, 0) so that
+    // grow_known's round arithmetic (2^m - split buckets left) holds.
+    if (h->split == (1u << h->m)) {
+        h->m += 1;
+        h->split = 0;
+    }
     h->shrinks += batches;
     return drain_reinsert(h, s);
 }
@@ -826,7 +833,8 @@ hive_status hive_find(hive_t h, const uint32_t* d_keys, uint64_t n, uint32_t* d_
                       uint8_t* d_found, void* stream) {
     if (!h) return HIVE_EINVAL;
     if (n == 0) return HIVE_OK;
-    if (!d_keys || !d_vals_out) return HIVE_EINVAL;
+    // op indices are 32-bit inside the kernels (as for insert / erase / mixed)
+    if (!d_keys || !d_vals_out || n >= (1ull << 32)) return HIVE_EINVAL;
     BusyGuard g(h);
     if (!g.ok) return HIVE_EBUSY;
     cudaStream_t s = (cudaStream_t)stream;
@@ -946,7 +954,7 @@ hive_status hive_find_host(hive_t h, const uint32_t* h_keys, uint64_t n, uint32_
                            uint8_t* h_found, void* stream) {
     if (!h) return HIVE_EINVAL;
     if (n == 0) return HIVE_OK;
-    if (!h_keys || !h_vals_out) return HIVE_EINVAL;
+    if (!h_keys || !h_vals_out || n >= (1ull << 32)) return HIVE_EINVAL;
     BusyGuard g(h);
     if (!g.ok) return HIVE_EBUSY;
     cudaStream_t s = (cudaStream_t)stream;
@@ -1062,6 +1070,26 @@ int hive_profile_read(hive_t h, const char** names, double* ms, uint64_t* launch
     return k;
 }
 
+// Scratch of the stateless routing calls, kept per (device, stream) for the
+// life of the process: allocator calls cost 5-95 ms on this system, and two
+// streams of one device must not share the count / info words (their launches
+// may run concurrently).  The map is guarded by a mutex; a stream's scratch is
+// only ever used by launches on that stream, which execute in order.
+struct RouteScratch { uint64_t* cnt = nullptr; uint64_t cap = 0; uint64_t* info = nullptr; };
+static hive_status route_scratch(cudaStream_t s, RouteScratch** out) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<int, cudaStream_t>, RouteScratch*>> tab;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& e : tab)
+        if (e.first.first == dev && e.first.second == s) { *out = e.second; return HIVE_OK; }
+    auto* rs = new RouteScratch();
+    tab.push_back({{dev, s}, rs});
+    *out = rs;
+    return HIVE_OK;
+}
+
 static hive_status route_impl(int mode, uint32_t n_shards, uint32_t seed, const uint32_t* d_keys,
                               const uint32_t* d_vals, const uint8_t* d_ops, uint64_t n, uint64_t* d_send_kv,
                               uint8_t* d_send_ops, uint32_t* d_pos, uint64_t* d_counts, void* stream) {
@@ -1069,16 +1097,9 @@ static hive_status route_impl(int mode, uint32_t n_shards, uint32_t seed, const 
     if (n >= (1ull << 32)) return HIVE_EINVAL;
     if (n && (!d_keys || !d_send_kv || !d_pos || (d_send_ops && !d_ops))) return HIVE_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
-    // Per-device scratch kept for the life of the process: allocator calls cost
-    // 5-95 ms on this system and a stream-ordered pool releases its memory at
-    // every synchronisation.  Calls on one device are serialised by the lock.
-    struct RouteScratch { uint64_t* cnt = nullptr; uint64_t cap = 0; uint64_t* info = nullptr; };
-    static std::mutex mu;
-    static RouteScratch scratch[64];
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lock(mu);
-    RouteScratch& rs = scratch[dev & 63];
+    RouteScratch* rsp = nullptr;
+    CKS(route_scratch(s, &rsp));
+    RouteScratch& rs = *rsp;
     const uint64_t E = (uint64_t)n_shards * part_warps(n) + 1;
     CKS(ensure(rs.cnt, rs.cap, E));
     if (!rs.info) CK(cudaMalloc((void**)&rs.info, 2 * MAX_PARTS * sizeof(uint64_t)));
@@ -1134,13 +1155,9 @@ hive_status hive_route_p2p(uint32_t n_shards, uint32_t rank, uint32_t seed, cons
         pd.cnt[p] = (unsigned long long*)peer_cnt[p];
     }
     cudaStream_t s = (cudaStream_t)stream;
-    struct P2PScratch { uint64_t* cnt = nullptr; uint64_t cap = 0; uint64_t* info = nullptr; };
-    static std::mutex mu;
-    static P2PScratch scratch[64];
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lock(mu);
-    P2PScratch& rs = scratch[dev & 63];
+    RouteScratch* rsp = nullptr;
+    CKS(route_scratch(s, &rsp));
+    RouteScratch& rs = *rsp;
     CKS(ensure(rs.cnt, rs.cap, (uint64_t)n_shards * part_warps(n) + 1));
     if (!rs.info) CK(cudaMalloc((void**)&rs.info, 2 * MAX_PARTS * sizeof(uint64_t)));
     CK(launch_route_p2p(s, n_shards, seed, d_keys, d_vals, d_ops, n, rs.cnt, rs.info, d_pos, pd));

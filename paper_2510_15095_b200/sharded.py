@@ -58,7 +58,9 @@ class ShardedHive:
         self.seed = seed
         self.ops = ops if ops is not None else CudaOps(capacity_per_shard, **cfg)
         self.table = self.ops.table
-        self._single_a2a = False                    # fall back to all_to_all_single
+        # The exchange form is fixed at construction from the backend, which is
+        # the same on every rank, so all ranks always issue the same collective.
+        self._list_a2a = dist.get_backend(group) == "nccl"
 
     # ---- exchange ---------------------------------------------------------------
     def _counts(self, send_counts: torch.Tensor):
@@ -77,16 +79,13 @@ class ShardedHive:
         if self.world == 1:
             return x
         out = torch.empty(sum(out_splits), dtype=x.dtype, device=x.device)
-        if x.is_cuda and dist.get_backend(self.group) == "nccl" and not self._single_a2a:
+        if self._list_a2a:
             outs, ins = list(out.split(out_splits)), list(x.split(in_splits))
             me = self.rank
-            try:
-                dist.all_to_all([o if r != me else o[:0] for r, o in enumerate(outs)],
-                                [t if r != me else t[:0] for r, t in enumerate(ins)], group=self.group)
-                outs[me].copy_(ins[me])
-                return out
-            except (RuntimeError, ValueError):      # argument rejected before any transfer
-                self._single_a2a = True
+            dist.all_to_all([o if r != me else o[:0] for r, o in enumerate(outs)],
+                            [t if r != me else t[:0] for r, t in enumerate(ins)], group=self.group)
+            outs[me].copy_(ins[me])
+            return out
         dist.all_to_all_single(out, x, out_splits, in_splits, group=self.group)
         return out
 
@@ -259,7 +258,10 @@ class P2PShardedHive:
         self._state = (kind, n, pos)
 
     def _check_timeout(self):
-        if int(_view(self.own.ptr["sig"], PeerBuffers.SIG_WORDS, torch.int64)[-1].item()):
+        sig = _view(self.own.ptr["sig"], PeerBuffers.SIG_WORDS, torch.int64)
+        if int(sig[-1].item()):
+            sig[-1].zero_()                     # reset the marker: the handle stays usable
+            self._state = None
             raise hive.HiveError("peer exchange: a peer did not signal within the timeout")
 
     def serve_phase(self):
@@ -294,6 +296,7 @@ class P2PShardedHive:
         self._state = None
         dev = pos.device
         hive.p2p_wait(self.world, 1, self._epoch, self.own.ptr["sig"])   # every owner's results are back
+        self._check_timeout()                   # never unroute stale results of a lost owner
         out8 = torch.empty(n, dtype=torch.uint8, device=dev)
         out32 = torch.empty(n, dtype=torch.uint32, device=dev) if kind in ("find", "mixed") else None
         if n:

@@ -27,9 +27,12 @@ def gpu_dump(t: HiveTable) -> dict:
 class Pair:
     """A CUDA table and an oracle table with the same configuration."""
 
-    def __init__(self, capacity, **cfg):
+    def __init__(self, capacity, oracle_cfg=None, **cfg):
+        """oracle_cfg: settings that differ on the oracle side only (e.g. a larger
+        stash, which changes no result unless it overflows)."""
         self.g = HiveTable(capacity, **cfg)
         ocfg = {k: v for k, v in cfg.items() if k != "keys_unique"}
+        ocfg.update(oracle_cfg or {})
         self.o = oracle.OracleTable(capacity, **ocfg)
 
     def insert(self, keys, vals):

@@ -24,9 +24,11 @@ def test_cfg3_full_scale_mixed_with_resize():
     first-choice keys; the oracle's paper-literal lowest-slot victim rule then
     overflows a 2% stash within the first batches (the GPU's rotating victim
     does not).  Stash capacity does not change any result unless it overflows,
-    so both sides run with a 30% stash here."""
+    so the ORACLE runs with a 30% stash while the GPU runs exactly as bench.py
+    times it (default 2% stash, batched drains A-29); Pair checks that the GPU
+    never dropped an entry (stats.failed == 0)."""
     from gpu_util import Pair
-    p = Pair(1024 * 32, stash_fraction=0.30)
+    p = Pair(1024 * 32, oracle_cfg={"stash_fraction": 0.30})
     nbat, bsz, U = 64, 1 << 20, 1 << 26
     for b in range(nbat):
         ops = gen.bernoulli_ops(bsz, 0.4, 0.2, seed=1000 + b)
@@ -34,7 +36,7 @@ def test_cfg3_full_scale_mixed_with_resize():
         p.mixed(ops, gen.keys_of(ids), gen.vals_of(ids))
         sg, so = p.g.stats(), p.o.stats()
         assert (sg["n_buckets"], sg["m"], sg["split"]) == (so["n_buckets"], so["m"], so["split"]), b
-        assert sg["count"] == so["count"]
+        assert sg["count"] == so["count"] and sg["failed"] == 0
     p.check_state()
     assert p.g.stats()["n_buckets"] > 600_000
     for lo in range(0, U, bsz):
@@ -63,3 +65,28 @@ def test_cfg4_full_scale_zipf():
     r2 = gen.zipf_ranks(1 << 22, int(0.05 * (1 << 26)), 0.99, seed=9)
     p.insert(gen.keys_of((r2 - 1 + (1 << 31)).astype(np.uint32)), np.arange(1 << 22, dtype=np.uint32))
     p.check_state()
+
+
+def test_cfg4_zipf_insert_to_lf_095():
+    """Config 4's "90-95% load ... stressing stash fallback" end: 2^21 buckets
+    prefilled to LF 0.93, then one batch of 2^23 Zipf(0.99) inserts over an
+    absent universe of 0.06 * 2^26 keys (1.39 M distinct, in-batch duplicates
+    up to ~4% of the batch per key) lifts the table to LF >= 0.95,
+    through Steps 3-4.  Statuses, the final key -> value set and the stash
+    contents (seen through finds) equal the oracle's."""
+    from gpu_util import Pair
+    nb = 1 << 21
+    p = Pair(nb * 32, lf_grow=2.0, lf_shrink=0)
+    n_pre = int(0.93 * (1 << 26))
+    ids = np.arange(n_pre, dtype=np.uint32)
+    p.insert(gen.keys_of(ids), gen.vals_of(ids))
+    r2 = gen.zipf_ranks(1 << 23, int(0.06 * (1 << 26)), 0.99, seed=9)
+    k2 = gen.keys_of((r2 - 1 + (1 << 31)).astype(np.uint32))
+    p.insert(k2, np.arange(1 << 23, dtype=np.uint32))
+    sg, so = p.check_state()
+    assert sg["count"] >= 0.95 * nb * 32, sg["count"] / (nb * 32)
+    assert sg["leftovers"] > 0 and sg["evictions"] > 0          # Step 3 ran
+    assert sg["stash_pushes"] > 0                               # Step 4 ran
+    # every key, including the stashed ones, is found with the oracle's value
+    allk = np.concatenate([gen.keys_of(ids[::7]), np.unique(k2)])
+    p.find(allk)

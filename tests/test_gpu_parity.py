@@ -281,3 +281,31 @@ def test_overflow_beyond_capacity_and_stash():
     dk, dv = dk.cpu().numpy().astype(np.uint32), dv.cpu().numpy().astype(np.uint32)
     assert len(dk) == n - n_bad and len(set(dk.tolist())) == len(dk)
     assert set(dk.tolist()) == set(keys[f].tolist())
+
+
+def test_grow_after_regressed_merge_abort():
+    """ADVICE r1 (high), reading A-30: a contraction that regresses (m, 0) ->
+    (m-1, 2^(m-1)) (A-7) and aborts its first merge leaves the GPU table at
+    (m, 0) again; later inserts must still grow it.  Merge aborts depend on the
+    slot layout, so seeds are searched until the GPU table hits that case; every
+    result and the final key set still equal the oracle's."""
+    hit = 0
+    for seed in range(400):
+        rng = np.random.default_rng(seed)
+        p = _pair(64, lf_shrink=0.5, resize_k=2)
+        keys = rng.choice(1 << 20, 200, replace=False).astype(np.uint32)
+        p.insert(keys[:110], keys[:110])
+        er = keys[:110][rng.permutation(110)[: int(rng.integers(50, 100))]]
+        p.erase(er)
+        sg = p.g.stats()
+        if not (sg["merge_aborts"] == 1 and sg["n_buckets"] == 4):
+            continue
+        assert (sg["m"], sg["split"]) == (2, 0)
+        hit += 1
+        p.insert(keys[110:], keys[110:])
+        sg, so = p.check_state(trajectory=False)
+        assert sg["n_buckets"] > 4 and sg["count"] <= 0.9 * sg["n_buckets"] * 32
+        p.find(keys)
+        if hit >= 3:
+            break
+    assert hit >= 1

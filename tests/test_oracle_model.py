@@ -144,3 +144,49 @@ def test_phased_duplicates_example():
     assert r.tolist() == [0, 1, 0, 1, 0]
     v, f = t.find([9])
     assert v.tolist() == [91]
+
+
+def test_cfg1_expansion_trajectory_closed_form():
+    """SURVEY §8(d) cfg1 (BASELINE configs[0]): 1024 buckets, lf 0.9 / 0.25, K = 1024.
+    Growing before the 2^16-key insert phase while (count + n_ins) > 0.9 * n_b * 32
+    (reading A-19) in K-bucket batches: 29,491 < 65,536 ->
+    1024 -> 2048 buckets (one whole round: m = 11, split = 0), 58,982 < 65,536 ->
+    3072 (m = 11, split = 1024), 88,474 >= 65,536 stop; LF 2/3.  2^15 erases
+    (half present) leave 49,152 keys = LF 0.5 > 0.25: no contraction."""
+    t = oracle.OracleTable(1024 * 32, lf_grow=0.9, lf_shrink=0.25, resize_k=1024)
+    n = 1 << 16
+    ids = np.arange(n, dtype=np.uint32)
+    st = t.insert(gen.keys_of(ids), gen.vals_of(ids))
+    assert (st == 0).all()
+    s = t.stats()
+    assert (s["n_buckets"], s["m"], s["split"], s["grows"], s["count"]) == (3072, 11, 1024, 2, n)
+    qids, hit = gen.mixed_queries(n // 2, n // 2, n, seed=101)
+    vals, found = t.find(gen.keys_of(qids))
+    assert (found == hit).all() and (vals[hit == 1] == gen.vals_of(qids[hit == 1])).all()
+    eids = np.concatenate([np.arange(n // 4, dtype=np.uint32), qids[hit == 0][: n // 4]])
+    er = t.erase(gen.keys_of(eids))
+    assert er.sum() == n // 4
+    s = t.stats()
+    assert (s["n_buckets"], s["count"], s["shrinks"]) == (3072, 49_152, 0)
+    assert t.check() == ""
+
+
+def test_grow_after_regressed_merge_abort():
+    """ADVICE r1 (high) regression, reading A-30: a contraction that regresses
+    (m, 0) -> (m-1, 2^(m-1)) (A-7) and then aborts its first merge must leave a
+    state the expansion can continue from.  Before the fix the table stayed at
+    4 buckets with 141 keys (LF 1.1) because ExpandBatch saw split == 2^m."""
+    rng = np.random.default_rng(64)
+    t = oracle.OracleTable(64, lf_grow=0.9, lf_shrink=0.5, resize_k=2)
+    keys = rng.choice(1 << 20, 200, replace=False).astype(np.uint32)
+    t.insert(keys[:110], keys[:110])
+    assert (t.stats()["n_buckets"], t.stats()["m"], t.stats()["split"]) == (4, 2, 0)
+    er = keys[:110][rng.permutation(110)[: int(rng.integers(50, 100))]]
+    t.erase(er)
+    s = t.stats()
+    assert s["merge_aborts"] == 1 and s["n_buckets"] == 4      # the first merge aborted
+    assert s["split"] < (1 << s["m"])                          # normalised state (A-30)
+    t.insert(keys[110:], keys[110:])
+    s = t.stats()
+    assert s["count"] <= 0.9 * s["n_buckets"] * 32 and s["n_buckets"] > 4
+    assert t.check() == ""
