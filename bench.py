@@ -217,13 +217,19 @@ def main():
         if args.exchange == "p2p":
             sh = P2PShardedHive(nb * 32, region=n, lf_grow=2.0, lf_shrink=0)
         else:
-            sh = ShardedHive(nb * 32, lf_grow=2.0, lf_shrink=0)
+            sh = ShardedHive(nb * 32, batch_max=n, lf_grow=2.0, lf_shrink=0)
         table = sh.table
 
         def step():
             table.clear()
-            sh.insert(keys, vals)
-            sh.find(queries)
+            if args.exchange == "p2p":
+                status.copy_(sh.insert(keys, vals))
+                v, f = sh.find(queries)
+                vals_out.copy_(v)
+                found.copy_(f)
+            else:
+                sh.insert(keys, vals, status)
+                sh.find(queries, vals_out, found)
     else:
         table = HiveTable(nb * 32, lf_grow=2.0, lf_shrink=0)
         sh = None
@@ -267,12 +273,11 @@ def main():
     total_ops = 2 * n * world
     value = total_ops / (ms_per_step * 1e-3) / 1e9
 
-    # correctness guard on the last step (no outputs are trusted blindly)
-    if not sharded:
-        hit = np.zeros(1)
-        st_bad = int((status != 0).sum().item())
-        fnd = int(found.sum().item())
-        assert st_bad == 0 and fnd == n // 2, (st_bad, fnd)
+    # correctness guard on the last step (no outputs are trusted blindly): all
+    # inserted keys are new and exactly half of each rank's queries hit
+    st_bad = int((status != 0).sum().item())
+    fnd = int(found.sum().item())
+    assert st_bad == 0 and fnd == n // 2, (st_bad, fnd)
 
     out = {}
     if not sharded:
@@ -367,12 +372,18 @@ def main():
         fo_h = torch.empty(n, dtype=torch.uint8).pin_memory()
 
         def e2e_step_sh():
+            # the collective calls with host buffers: hive_insert_host /
+            # hive_find_host on the sharded handle (H2D, exchange, D2H inside)
             table.clear()
-            st = sh.insert(keys_h.to(dev, non_blocking=True), vals_h.to(dev, non_blocking=True))
-            st_h.copy_(st, non_blocking=True)
-            v, f = sh.find(q_h.to(dev, non_blocking=True))
-            vo_h.copy_(v, non_blocking=True)
-            fo_h.copy_(f, non_blocking=True)
+            if args.exchange == "p2p":
+                st = sh.insert(keys_h.to(dev, non_blocking=True), vals_h.to(dev, non_blocking=True))
+                st_h.copy_(st, non_blocking=True)
+                v, f = sh.find(q_h.to(dev, non_blocking=True))
+                vo_h.copy_(v, non_blocking=True)
+                fo_h.copy_(f, non_blocking=True)
+            else:
+                sh.insert_host(keys_h, vals_h, st_h)
+                sh.find_host(q_h, vo_h, fo_h)
 
         e2e_step_sh()
         torch.cuda.synchronize()
@@ -458,7 +469,7 @@ def run_cfg5(args, rank: int, world: int, local: int):
     B = min(1 << 26, per)
     nb = -(-per * 100 // (95 * 32))
     sh = (P2PShardedHive(nb * 32, region=B, lf_grow=2.0, lf_shrink=0) if args.exchange == "p2p"
-          else ShardedHive(nb * 32, lf_grow=2.0, lf_shrink=0))
+          else ShardedHive(nb * 32, batch_max=B, lf_grow=2.0, lf_shrink=0))
     rng = np.random.default_rng(505 + rank)
     ins, fnd, era = [], [], []
     for lo in range(rank * per, (rank + 1) * per, B):

@@ -53,9 +53,11 @@ typedef enum {
     HIVE_EINVAL = 1,      /* bad argument / config                          */
     HIVE_ENOMEM = 2,      /* device or VA allocation failed                 */
     HIVE_ECUDA = 3,       /* CUDA runtime / driver error                    */
-    HIVE_ENCCL = 4,       /* reserved (collectives run in the binding)      */
+    HIVE_ENCCL = 4,       /* NCCL error (sharded tables)                    */
     HIVE_ESTASHFULL = 5,  /* sticky: an entry could not be stored           */
-    HIVE_EBUSY = 6        /* handle already in use by a concurrent call     */
+    HIVE_EBUSY = 6,       /* handle already in use by a concurrent call     */
+    HIVE_EXCHANGE = 7     /* sticky (sharded): an op did not fit its padded
+                             exchange region and was not processed          */
 } hive_status;
 
 /* Flags for hive_config.flags */
@@ -84,6 +86,18 @@ typedef struct {
     float    stash_fraction; /* stash capacity / slots, 0.02,
                                 floor 1024 entries                           */
     uint32_t flags;          /* HIVE_KEYS_UNIQUE | HIVE_HASH_CRC              */
+    /* ---- sharded tables ---- */
+    void*    nccl_comm;      /* NULL: single-GPU table.  Else an ncclComm_t
+                                (e.g. from hive_nccl_comm_init): this handle is
+                                rank `rank` of a hash-partitioned table of
+                                `nranks` shards (rank and size from the comm);
+                                capacity etc. are PER SHARD.  Owned by the
+                                caller; must outlive the handle.              */
+    uint64_t shard_batch_max;/* sharded: the largest local batch any rank
+                                passes to one call (required, > 0)            */
+    float    shard_slack;    /* sharded: padded exchange capacity per peer =
+                                ceil(shard_batch_max / nranks * (1 + slack))
+                                + 1024 records; default 0.0625              */
 } hive_config;
 
 /* Stats snapshot (sync). */
@@ -114,7 +128,47 @@ typedef struct {
     uint64_t step3;          /* entries placed by the Step-3 loop (new keys,
                                 reinserted stash entries, lost fast claims);
                                 Step-2 placements = new keys - leftovers      */
+    uint64_t xfail;          /* sharded: ops of this rank not processed
+                                because their exchange region was full        */
 } hive_stats_t;
+
+/* ---- Sharded tables (BASELINE configs[4]) ---------------
+ * A handle created with cfg.nccl_comm != NULL is one shard of a table
+ * hash-partitioned over the comm's ranks: key k is owned by rank
+ * shard(k) = (fmix32(k ^ HIVE_SHARD_SEED) * nranks) >> 32 (MurmurHash3's
+ * finaliser, independent of BitHash1/2 so every shard uses all its buckets).
+ * Every op call (hive_insert / find / erase / mixed and their _host forms) is
+ * COLLECTIVE: all ranks call it in the same order, each with its own local
+ * batch (n may differ per rank, 0 allowed, n <= shard_batch_max), and each
+ * gets the results for its own ops in its own order.  Semantics are those of
+ * ONE single-GPU call on the union batch in (rank, index) order: e.g. among
+ * in-batch duplicates the op of the highest (rank, index) wins.
+ * Exchange: a stable route kernel packs each op record into a padded send
+ * buffer of nranks regions of C = shard_slack-padded capacity, then one
+ * ncclAlltoAll moves the per-region counts and one the records (plus one
+ * for opcodes in mixed calls); each owner compacts the received records by
+ * device-side counts and runs the PHASED batch; results return by the inverse
+ * ncclAlltoAll and an unpermute kernel.  No host synchronisation happens when
+ * growth and contraction are off (lf_grow >= 1, lf_shrink <= 0), so the whole
+ * call can be captured in a CUDA graph.  An op that does not fit its region
+ * (more than C ops of one rank's batch owned by one shard -- a ~30-sigma
+ * event for hashed keys at the default slack) is not processed: insert /
+ * erase / mixed result 4, find found = 2, and the handle's sticky
+ * HIVE_EXCHANGE flag is reported by hive_stats / hive_size.
+ * hive_clear / size / stats / dump / profile act on the local shard only. */
+#define HIVE_SHARD_SEED 0x5BD1E995u
+
+/* NCCL bootstrap without NCCL headers in the caller (libnccl.so.2 is loaded
+ * at run time; ncclAlltoAll needs NCCL >= 2.28, older versions use grouped
+ * send / recv).  hive_nccl_unique_id (rank 0) fills 128 bytes that the caller
+ * broadcasts to every rank (e.g. through torch.distributed); every rank then
+ * calls hive_nccl_comm_init with the current CUDA device set (collective).
+ * hive_nccl_comm_destroy frees a comm made here.  HIVE_ENCCL on failure. */
+hive_status hive_nccl_unique_id(uint8_t* id_out);
+hive_status hive_nccl_comm_init(int nranks, int rank, const uint8_t* id, void** comm_out);
+hive_status hive_nccl_comm_destroy(void* comm);
+/* Shard geometry of a handle: *nranks = 1, *rank = 0 for a single-GPU table. */
+hive_status hive_shard_info(hive_t h, int* nranks, int* rank, uint64_t* cap_per_peer);
 
 /* Fill *cfg with the defaults above. */
 void hive_config_default(hive_config* cfg);
@@ -122,7 +176,11 @@ void hive_config_default(hive_config* cfg);
 /* Create a table (sync).  Reserves virtual address space for max_capacity
  * and maps physical 2 MiB chunks for the initial buckets (EMPTY-filled).
  * Returns HIVE_EINVAL for cfg == NULL, out == NULL, capacity == 0,
- * lf_shrink >= lf_grow (when both are enabled), stash_fraction < 0. */
+ * lf_shrink >= lf_grow (when both are enabled), stash_fraction < 0, or a
+ * sharded config with shard_batch_max == 0, more than 32 ranks or a padded
+ * exchange of 2^32 records or more; HIVE_ENCCL if the comm cannot be queried.
+ * Sharded: collective (no communication, but every rank must create its
+ * shard before the first op call). */
 hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out);
 
 /* Destroy (sync on the table's last stream); frees everything it owns. */
@@ -132,7 +190,8 @@ hive_status hive_destroy(hive_t h);
  * d_status (nullable): uint8[n]; 0 = absent at phase start (inserted),
  * 1 = present (value replaced), 2 = reserved key, 3 = this op's eviction
  * chain found the stash full and dropped its in-hand entry (this key or a key
- * it displaced; hive_stats.failed counts dropped entries, reading A-28).
+ * it displaced; hive_stats.failed counts dropped entries, reading A-28),
+ * 4 = not processed (sharded handles only: exchange region full).
  * May grow the table first (one small D2H of the counters when growth is
  * enabled). */
 hive_status hive_insert(hive_t h, const uint32_t* d_keys, const uint32_t* d_vals,

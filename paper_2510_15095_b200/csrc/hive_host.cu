@@ -7,6 +7,7 @@
 // ("allocates K new buckets").
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <atomic>
@@ -104,6 +105,77 @@ bool load_vmm(Vmm& v) {
 }
 Vmm g_vmm;
 
+// ---- NCCL, loaded at run time (sharded tables) ------------------------------------
+// The library does not link NCCL: libnccl.so.2 is dlopen'ed on first use.  If
+// the process has already loaded one (torch's), RTLD_NOLOAD picks that copy,
+// so comms made by hive_nccl_comm_init and the calls below share one NCCL.
+// ncclComm_t is a pointer and ncclDataType_t / ncclResult_t are int enums; the
+// 128-byte ncclUniqueId is passed by value as in nccl.h.
+struct NcclUniqueId { char internal[128]; };
+enum { NCCL_U8 = 1, NCCL_U32 = 3, NCCL_U64 = 5 };   // ncclUint8 / ncclUint32 / ncclUint64
+struct Nccl {
+    int (*get_version)(int*) = nullptr;
+    int (*get_unique_id)(NcclUniqueId*) = nullptr;
+    int (*comm_init_rank)(void**, int, NcclUniqueId, int) = nullptr;
+    int (*comm_destroy)(void*) = nullptr;
+    int (*comm_count)(void*, int*) = nullptr;
+    int (*comm_user_rank)(void*, int*) = nullptr;
+    int (*alltoall)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;   // NCCL >= 2.28
+    int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*group_start)() = nullptr;
+    int (*group_end)() = nullptr;
+    const char* (*error_string)(int) = nullptr;
+    int version = 0;
+    bool ok = false;
+};
+Nccl g_nccl;
+std::mutex g_nccl_mu;
+
+bool load_nccl() {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.ok) return true;
+    void* so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!so) so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!so) { g_err = std::string("dlopen(libnccl.so.2) failed: ") + dlerror(); return false; }
+    struct { const char* name; void** fn; bool need; } tab[] = {
+        {"ncclGetVersion", (void**)&g_nccl.get_version, true},
+        {"ncclGetUniqueId", (void**)&g_nccl.get_unique_id, true},
+        {"ncclCommInitRank", (void**)&g_nccl.comm_init_rank, true},
+        {"ncclCommDestroy", (void**)&g_nccl.comm_destroy, true},
+        {"ncclCommCount", (void**)&g_nccl.comm_count, true},
+        {"ncclCommUserRank", (void**)&g_nccl.comm_user_rank, true},
+        {"ncclAlltoAll", (void**)&g_nccl.alltoall, false},
+        {"ncclSend", (void**)&g_nccl.send, true},
+        {"ncclRecv", (void**)&g_nccl.recv, true},
+        {"ncclGroupStart", (void**)&g_nccl.group_start, true},
+        {"ncclGroupEnd", (void**)&g_nccl.group_end, true},
+        {"ncclGetErrorString", (void**)&g_nccl.error_string, true},
+    };
+    for (auto& e : tab) {
+        *e.fn = dlsym(so, e.name);
+        if (!*e.fn && e.need) { g_err = std::string("NCCL symbol missing: ") + e.name; return false; }
+    }
+    g_nccl.get_version(&g_nccl.version);
+    g_nccl.ok = true;
+    return true;
+}
+
+void set_err_nccl(int r, const char* what, int line) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s at hive_host.cu:%d: NCCL %d (%s)", what, line, r,
+             g_nccl.error_string ? g_nccl.error_string(r) : "?");
+    g_err = buf;
+}
+#define CKN(x)                                        \
+    do {                                              \
+        int _r = (x);                                 \
+        if (_r != 0) {                                \
+            set_err_nccl(_r, #x, __LINE__);           \
+            return HIVE_ENCCL;                        \
+        }                                             \
+    } while (0)
+
 uint64_t pow2_at_least(uint64_t x) {
     uint64_t p = 1;
     while (p < x) p <<= 1;
@@ -192,6 +264,25 @@ struct hive_table_s {
 
     std::atomic<int> busy{0};
     cudaStream_t last = nullptr;
+
+    // ---- sharded table (cfg.nccl_comm != NULL): padded exchange buffers ----
+    // Carved from one allocation; tot = nranks * cap records.
+    struct Shard {
+        void* comm = nullptr;
+        int nranks = 1, rank = 0;
+        uint64_t cap = 0, tot = 0, batch_max = 0;
+        void* base = nullptr;
+        uint64_t *send_kv = nullptr, *recv_kv = nullptr, *cnt_send = nullptr, *cnt_recv = nullptr;
+        uint64_t *n_dev = nullptr, *pcnt = nullptr, *pinfo = nullptr;
+        uint8_t *send_op = nullptr, *recv_op = nullptr, *oc = nullptr;
+        uint8_t *r8c = nullptr, *ret8 = nullptr, *rr8 = nullptr;
+        uint32_t *pos = nullptr, *kc = nullptr, *vc = nullptr, *back = nullptr;
+        uint32_t *r32c = nullptr, *ret32 = nullptr, *rr32 = nullptr;
+        // host-buffer calls: device staging of the local batch
+        uint32_t *hk = nullptr, *hv = nullptr, *ho32 = nullptr;
+        uint8_t *ho8 = nullptr, *hop = nullptr;
+    } sh;
+    bool sharded() const { return sh.comm != nullptr; }
 
     uint64_t nb() const { return (1ull << m) + split; }
     TableView tv() const {
@@ -671,6 +762,193 @@ hive_status pipe_init(hive_table_s* h, size_t n_events) {
 }
 }  // namespace
 
+namespace {
+// The PHASED mixed batch: classify, INSERT, ERASE, FIND.  n is
+// an upper bound of the batch when n_dev (device word) holds its length.
+hive_status mixed_impl(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, const uint32_t* d_vals,
+                       uint64_t n, const uint64_t* n_dev, uint32_t* d_vals_out, uint8_t* d_result,
+                       cudaStream_t s) {
+    // classify: stable partition of op indices by opcode (3 regions of n)
+    CKS(ensure(h->cls, h->cls_cap, 3 * n));
+    CKS(ensure(h->cnt, h->cnt_cap, 3 * part_warps(n) + 1));
+    {
+        Prof p(h, "k_classify", s, 3);
+        CK(launch_partition(s, PART_CLASSIFY, 3, 0, d_keys, d_vals, d_op, n, h->cnt, h->pinfo, h->cls, n,
+                            nullptr, nullptr, nullptr, d_result, d_vals_out, nullptr, n_dev));
+    }
+    const uint64_t* n_find = h->pinfo + 0;
+    const uint64_t* n_ins = h->pinfo + 1;
+    const uint64_t* n_era = h->pinfo + 2;
+    int64_t count_lb = -1;
+    DedupView dd_ins{nullptr, 0, nullptr, nullptr}, dd_era{nullptr, 0, nullptr, nullptr};
+    bool pre = false, pre_era = false;
+    if (h->cfg.lf_grow < 1.0f) {           // one wait: phase sizes + counters
+        if (!h->ctrl_ev) CK(cudaEventCreateWithFlags(&h->ctrl_ev, cudaEventDisableTiming));
+        CK(cudaMemcpyAsync(h->stage_h, h->pinfo, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(h->ctrl_h, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(h->ctrl_ev, s));
+        // The insert phase's owner election does not depend on the table
+        // geometry: enqueue it before waiting, so the GPU has work while the
+        // host plans the resize from the count it just read.
+        if (h->dedup_on()) {
+            CKS(elect_owners(h, d_keys, h->cls + n, n, n_ins, n, &dd_ins, s));
+            pre = true;
+            hive_status e2 = HIVE_OK;
+            pre_era = elect_owners_set2(h, d_keys, h->cls + 2 * n, n, n_era, n, &dd_era, s, &e2);
+            CKS(e2);
+        }
+        {
+            Trace tr("read_ctrl", 0);
+            CK(cudaEventSynchronize(h->ctrl_ev));
+        }
+        h->tail_known = h->ctrl_h->stash_tail;
+        const uint64_t count0 = h->ctrl_h->count, n_erase = h->stage_h[2];
+        count_lb = count0 > n_erase ? (int64_t)(count0 - n_erase) : 0;
+        if (h->stage_h[1]) CKS(grow_known(h, count0, h->stage_h[1], s));
+    }
+    CKS(insert_phase(h, d_keys, d_vals, nullptr, h->cls + n, n, n_ins, n, d_result, d_vals_out, s, nullptr,
+                     pre ? &dd_ins : nullptr));
+    CKS(erase_phase(h, d_keys, h->cls + 2 * n, n, n_era, n, d_result, d_vals_out, s, pre_era ? &dd_era : nullptr));
+    CKS(shrink_after(h, s, count_lb));
+    Prof p(h, "k_find", s);
+    CK(launch_find(h->grids, s, d_keys, h->cls, n, n_find, h->tv(), h->sv(), d_vals_out, d_result));
+    return HIVE_OK;
+}
+
+// ---- sharded table: padded NCCL exchange (include/hive.h "Sharded tables") -------
+enum ShardKind { SK_INSERT = 0, SK_FIND = 1, SK_ERASE = 2, SK_MIXED = 3 };
+
+// Buffers of the padded exchange, carved from one cudaMalloc (allocator calls
+// cost 5-95 ms each on this system).
+hive_status shard_alloc(hive_table_s* h) {
+    auto& S = h->sh;
+    const uint64_t tot = S.tot, bm = std::max<uint64_t>(S.batch_max, 1), G = (uint64_t)S.nranks;
+    const uint64_t pc = G * part_warps(bm) + 1;
+    struct Part { void** p; uint64_t bytes; } parts[] = {
+        {(void**)&S.send_kv, tot * 8}, {(void**)&S.recv_kv, tot * 8}, {(void**)&S.cnt_send, G * 8},
+        {(void**)&S.cnt_recv, G * 8}, {(void**)&S.n_dev, 8}, {(void**)&S.pcnt, pc * 8},
+        {(void**)&S.pinfo, 2 * MAX_PARTS * 8}, {(void**)&S.pos, bm * 4}, {(void**)&S.kc, tot * 4},
+        {(void**)&S.vc, tot * 4}, {(void**)&S.back, tot * 4}, {(void**)&S.r32c, tot * 4},
+        {(void**)&S.ret32, tot * 4}, {(void**)&S.rr32, tot * 4}, {(void**)&S.hk, bm * 4},
+        {(void**)&S.hv, bm * 4}, {(void**)&S.ho32, bm * 4}, {(void**)&S.send_op, tot},
+        {(void**)&S.recv_op, tot}, {(void**)&S.oc, tot}, {(void**)&S.r8c, tot}, {(void**)&S.ret8, tot},
+        {(void**)&S.rr8, tot}, {(void**)&S.ho8, bm}, {(void**)&S.hop, bm},
+    };
+    uint64_t total = 0;
+    for (auto& q : parts) total += (q.bytes + 255) / 256 * 256;
+    Trace tr("shard_alloc", total);
+    cudaError_t e = cudaMalloc(&S.base, total);
+    if (e != cudaSuccess) { set_err(e, "cudaMalloc(shard buffers)", __LINE__); return HIVE_ENOMEM; }
+    uint64_t off = 0;
+    for (auto& q : parts) {
+        *q.p = (char*)S.base + off;
+        off += (q.bytes + 255) / 256 * 256;
+    }
+    // results of padding positions are never read, but keep them defined
+    CK(cudaMemset(S.base, 0, total));
+    return HIVE_OK;
+}
+
+// One all-to-all of `count` elements per peer: ncclAlltoAll (NCCL >= 2.28) or
+// a group of send / recv pairs.
+hive_status a2a(hive_table_s* h, const void* send, void* recv, size_t count, int dtype, size_t esize,
+                cudaStream_t s) {
+    auto& S = h->sh;
+    if (g_nccl.alltoall) {
+        CKN(g_nccl.alltoall(send, recv, count, dtype, S.comm, s));
+        return HIVE_OK;
+    }
+    CKN(g_nccl.group_start());
+    for (int p = 0; p < S.nranks; ++p) {
+        CKN(g_nccl.send((const char*)send + p * count * esize, count, dtype, p, S.comm, s));
+        CKN(g_nccl.recv((char*)recv + p * count * esize, count, dtype, p, S.comm, s));
+    }
+    CKN(g_nccl.group_end());
+    return HIVE_OK;
+}
+
+// One collective op of a sharded handle: route -> all-to-all -> owner phase on
+// the union batch (rank order) -> all-to-all back -> unpermute.  Stream-
+// ordered; the host waits only where the local phase itself needs a count
+// (growth / contraction enabled).
+hive_status shard_call(hive_table_s* h, int kind, const uint8_t* d_op, const uint32_t* d_keys,
+                       const uint32_t* d_vals, uint64_t n, uint32_t* out32, uint8_t* out8, cudaStream_t s) {
+    auto& S = h->sh;
+    if (n > S.batch_max) {
+        g_err = "sharded call: n exceeds shard_batch_max";
+        return HIVE_EINVAL;
+    }
+    const uint32_t G = (uint32_t)S.nranks;
+    const uint64_t cap = S.cap, tot = S.tot;
+    const bool mixed = kind == SK_MIXED, vals32 = kind == SK_FIND || kind == SK_MIXED;
+    {
+        Prof p(h, "k_route_pad", s, 3);
+        if (n) {
+            CK(launch_route_pad(s, G, HIVE_SHARD_SEED, d_keys, kind == SK_INSERT || mixed ? d_vals : nullptr,
+                                mixed ? d_op : nullptr, n, cap, S.pcnt, S.pinfo, S.send_kv,
+                                mixed ? S.send_op : nullptr, S.pos, S.cnt_send, h->ctrl));
+        } else {
+            CK(cudaMemsetAsync(S.cnt_send, 0, G * sizeof(uint64_t), s));
+        }
+    }
+    {
+        Prof p(h, "nccl_alltoall(fwd)", s, 0);
+        CKN(g_nccl.group_start());
+        hive_status st = a2a(h, S.cnt_send, S.cnt_recv, 1, NCCL_U64, 8, s);
+        if (st == HIVE_OK) st = a2a(h, S.send_kv, S.recv_kv, cap, NCCL_U64, 8, s);
+        if (st == HIVE_OK && mixed) st = a2a(h, S.send_op, S.recv_op, cap, NCCL_U8, 1, s);
+        CKN(g_nccl.group_end());
+        CKS(st);
+    }
+    {
+        Prof p(h, "k_owner_compact", s);
+        CK(launch_owner_compact(s, G, cap, S.recv_kv, mixed ? S.recv_op : nullptr, S.cnt_recv, S.kc, S.vc,
+                                mixed ? S.oc : nullptr, S.back, S.n_dev));
+    }
+    switch (kind) {
+        case SK_INSERT:
+            if (h->cfg.lf_grow < 1.0f) {             // growth needs the union batch size on the host
+                CK(cudaMemcpyAsync(h->stage_h, S.n_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+                CKS(read_ctrl(h, s));
+                if (h->stage_h[0]) CKS(grow_known(h, h->ctrl_h->count, h->stage_h[0], s));
+            }
+            CKS(insert_phase(h, S.kc, S.vc, nullptr, nullptr, tot, S.n_dev, tot, S.r8c, nullptr, s));
+            break;
+        case SK_FIND: {
+            Prof p(h, "k_find", s);
+            CK(launch_find(h->grids, s, S.kc, nullptr, tot, S.n_dev, h->tv(), h->sv(), S.r32c, S.r8c));
+            break;
+        }
+        case SK_ERASE:
+            CKS(erase_phase(h, S.kc, nullptr, tot, S.n_dev, tot, S.r8c, nullptr, s));
+            CKS(shrink_after(h, s));
+            break;
+        default:
+            CKS(mixed_impl(h, S.oc, S.kc, S.vc, tot, S.n_dev, S.r32c, S.r8c, s));
+    }
+    {
+        Prof p(h, "k_owner_return", s);
+        CK(launch_owner_return(s, tot, S.n_dev, S.back, S.r8c, vals32 ? S.r32c : nullptr, S.ret8,
+                               vals32 ? S.ret32 : nullptr));
+    }
+    {
+        Prof p(h, "nccl_alltoall(back)", s, 0);
+        CKN(g_nccl.group_start());
+        hive_status st = a2a(h, S.ret8, S.rr8, cap, NCCL_U8, 1, s);
+        if (st == HIVE_OK && vals32) st = a2a(h, S.ret32, S.rr32, cap, NCCL_U32, 4, s);
+        CKN(g_nccl.group_end());
+        CKS(st);
+    }
+    if (n && (out8 || out32)) {
+        Prof p(h, "k_unroute_pad", s);
+        CK(launch_unroute_pad(s, S.pos, n, S.rr8, out8, out32 ? S.rr32 : nullptr, out32,
+                              kind == SK_FIND ? 2 : 4));
+    }
+    return HIVE_OK;
+}
+
+}  // namespace
+
 // =====================================================================================
 // C ABI
 // =====================================================================================
@@ -686,6 +964,9 @@ void hive_config_default(hive_config* c) {
     c->resize_k = 1024;
     c->stash_fraction = 0.02f;
     c->flags = 0;
+    c->nccl_comm = nullptr;
+    c->shard_batch_max = 0;
+    c->shard_slack = 0.0625f;
 }
 
 const char* hive_status_string(hive_status s) {
@@ -697,6 +978,7 @@ const char* hive_status_string(hive_status s) {
         case HIVE_ENCCL: return "NCCL error";
         case HIVE_ESTASHFULL: return "stash full (entries lost)";
         case HIVE_EBUSY: return "handle busy";
+        case HIVE_EXCHANGE: return "sharded exchange region full (ops not processed)";
     }
     return "unknown";
 }
@@ -708,6 +990,7 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     if (cfg->lf_grow < 1.0f && cfg->lf_shrink > 0.0f && cfg->lf_shrink >= cfg->lf_grow) return HIVE_EINVAL;
     if (cfg->lf_grow <= 0.0f) return HIVE_EINVAL;
     if (cfg->flags & ~(HIVE_KEYS_UNIQUE | HIVE_HASH_CRC)) return HIVE_EINVAL;
+    if (cfg->nccl_comm && (cfg->shard_batch_max == 0 || cfg->shard_slack < 0.0f)) return HIVE_EINVAL;
     *out = nullptr;
     if (!load_vmm(g_vmm)) return HIVE_ECUDA;
     cudaStream_t s = (cudaStream_t)stream;
@@ -767,6 +1050,22 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     if (cudaMalloc((void**)&h->aborts, MAX_SEGMENTS * sizeof(unsigned long long)) != cudaSuccess)
         return fail(HIVE_ENOMEM);
     memset(h->ctrl_h, 0, sizeof(Ctrl));
+    if (cfg->nccl_comm) {                     // one shard of a hash-partitioned table
+        if (!load_nccl()) return fail(HIVE_ENCCL);
+        auto& S = h->sh;
+        S.comm = cfg->nccl_comm;
+        int r = g_nccl.comm_count(S.comm, &S.nranks);
+        if (r == 0) r = g_nccl.comm_user_rank(S.comm, &S.rank);
+        if (r != 0) { set_err_nccl(r, "ncclCommCount/UserRank", __LINE__); return fail(HIVE_ENCCL); }
+        if (S.nranks < 1 || S.nranks > 32) return fail(HIVE_EINVAL);
+        S.batch_max = cfg->shard_batch_max;
+        const double per = std::ceil((double)S.batch_max / S.nranks * (1.0 + (double)cfg->shard_slack));
+        S.cap = std::min<uint64_t>((uint64_t)per + 1024, S.batch_max);
+        S.tot = S.cap * (uint64_t)S.nranks;
+        if (S.tot >= (1ull << 32) || S.batch_max >= (1ull << 32)) return fail(HIVE_EINVAL);
+        st = shard_alloc(h);
+        if (st != HIVE_OK) return fail(st);
+    }
     st = hive_clear(h, stream);
     if (st != HIVE_OK) return fail(st);
     if (cudaStreamSynchronize(s) != cudaSuccess) return fail(HIVE_ECUDA);
@@ -808,6 +1107,7 @@ hive_status hive_destroy(hive_t h) {
     if (h->down) cudaStreamDestroy(h->down);
     for (void* b : bufs)
         if (b) cudaFree(b);
+    if (h->sh.base) cudaFree(h->sh.base);
     if (h->ctrl_h) cudaFreeHost(h->ctrl_h);
     if (h->stage_h) cudaFreeHost(h->stage_h);
     for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -819,12 +1119,13 @@ hive_status hive_destroy(hive_t h) {
 hive_status hive_insert(hive_t h, const uint32_t* d_keys, const uint32_t* d_vals, uint64_t n,
                         uint8_t* d_status, void* stream) {
     if (!h) return HIVE_EINVAL;
-    if (n == 0) return HIVE_OK;
-    if (!d_keys || !d_vals || n >= (1ull << 32)) return HIVE_EINVAL;
+    if (n == 0 && !h->sharded()) return HIVE_OK;      // sharded calls are collective even when empty
+    if ((n && (!d_keys || !d_vals)) || n >= (1ull << 32)) return HIVE_EINVAL;
     BusyGuard g(h);
     if (!g.ok) return HIVE_EBUSY;
     cudaStream_t s = (cudaStream_t)stream;
     h->last = s;
+    if (h->sharded()) return shard_call(h, SK_INSERT, nullptr, d_keys, d_vals, n, nullptr, d_status, s);
     CKS(grow_before(h, n, s));
     return insert_phase(h, d_keys, d_vals, nullptr, nullptr, n, nullptr, n, d_status, nullptr, s);
 }
@@ -832,13 +1133,14 @@ hive_status hive_insert(hive_t h, const uint32_t* d_keys, const uint32_t* d_vals
 hive_status hive_find(hive_t h, const uint32_t* d_keys, uint64_t n, uint32_t* d_vals_out,
                       uint8_t* d_found, void* stream) {
     if (!h) return HIVE_EINVAL;
-    if (n == 0) return HIVE_OK;
+    if (n == 0 && !h->sharded()) return HIVE_OK;
     // op indices are 32-bit inside the kernels (as for insert / erase / mixed)
-    if (!d_keys || !d_vals_out || n >= (1ull << 32)) return HIVE_EINVAL;
+    if ((n && (!d_keys || !d_vals_out)) || n >= (1ull << 32)) return HIVE_EINVAL;
     BusyGuard g(h);
     if (!g.ok) return HIVE_EBUSY;
     cudaStream_t s = (cudaStream_t)stream;
     h->last = s;
+    if (h->sharded()) return shard_call(h, SK_FIND, nullptr, d_keys, nullptr, n, d_vals_out, d_found, s);
     Prof p(h, "k_find", s);
     CK(launch_find(h->grids, s, d_keys, nullptr, n, nullptr, h->tv(), h->sv(), d_vals_out, d_found));
     return HIVE_OK;
@@ -846,12 +1148,13 @@ hive_status hive_find(hive_t h, const uint32_t* d_keys, uint64_t n, uint32_t* d_
 
 hive_status hive_erase(hive_t h, const uint32_t* d_keys, uint64_t n, uint8_t* d_erased, void* stream) {
     if (!h) return HIVE_EINVAL;
-    if (n == 0) return HIVE_OK;
-    if (!d_keys || n >= (1ull << 32)) return HIVE_EINVAL;
+    if (n == 0 && !h->sharded()) return HIVE_OK;
+    if ((n && !d_keys) || n >= (1ull << 32)) return HIVE_EINVAL;
     BusyGuard g(h);
     if (!g.ok) return HIVE_EBUSY;
     cudaStream_t s = (cudaStream_t)stream;
     h->last = s;
+    if (h->sharded()) return shard_call(h, SK_ERASE, nullptr, d_keys, nullptr, n, nullptr, d_erased, s);
     CKS(erase_phase(h, d_keys, nullptr, n, nullptr, n, d_erased, nullptr, s));
     return shrink_after(h, s);
 }
@@ -859,68 +1162,37 @@ hive_status hive_erase(hive_t h, const uint32_t* d_keys, uint64_t n, uint8_t* d_
 hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, const uint32_t* d_vals,
                        uint64_t n, uint32_t* d_vals_out, uint8_t* d_result, void* stream) {
     if (!h) return HIVE_EINVAL;
-    if (n == 0) return HIVE_OK;
-    if (!d_op || !d_keys || !d_vals || !d_vals_out || !d_result || n >= (1ull << 32)) return HIVE_EINVAL;
+    if (n == 0 && !h->sharded()) return HIVE_OK;
+    if (n && (!d_op || !d_keys || !d_vals || !d_vals_out || !d_result)) return HIVE_EINVAL;
+    if (n >= (1ull << 32)) return HIVE_EINVAL;
     BusyGuard g(h);
     if (!g.ok) return HIVE_EBUSY;
     cudaStream_t s = (cudaStream_t)stream;
     h->last = s;
-    // classify: stable partition of op indices by opcode (3 regions of n)
-    CKS(ensure(h->cls, h->cls_cap, 3 * n));
-    CKS(ensure(h->cnt, h->cnt_cap, 3 * part_warps(n) + 1));
-    {
-        Prof p(h, "k_classify", s, 3);
-        CK(launch_partition(s, PART_CLASSIFY, 3, 0, d_keys, d_vals, d_op, n, h->cnt, h->pinfo, h->cls, n,
-                            nullptr, nullptr, nullptr, d_result, d_vals_out));
-    }
-    const uint64_t* n_find = h->pinfo + 0;
-    const uint64_t* n_ins = h->pinfo + 1;
-    const uint64_t* n_era = h->pinfo + 2;
-    int64_t count_lb = -1;
-    DedupView dd_ins{nullptr, 0, nullptr, nullptr}, dd_era{nullptr, 0, nullptr, nullptr};
-    bool pre = false, pre_era = false;
-    if (h->cfg.lf_grow < 1.0f) {           // one wait: phase sizes + counters
-        if (!h->ctrl_ev) CK(cudaEventCreateWithFlags(&h->ctrl_ev, cudaEventDisableTiming));
-        CK(cudaMemcpyAsync(h->stage_h, h->pinfo, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(h->ctrl_h, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
-        CK(cudaEventRecord(h->ctrl_ev, s));
-        // The insert phase's owner election does not depend on the table
-        // geometry: enqueue it before waiting, so the GPU has work while the
-        // host plans the resize from the count it just read.
-        if (h->dedup_on()) {
-            CKS(elect_owners(h, d_keys, h->cls + n, n, n_ins, n, &dd_ins, s));
-            pre = true;
-            hive_status e2 = HIVE_OK;
-            pre_era = elect_owners_set2(h, d_keys, h->cls + 2 * n, n, n_era, n, &dd_era, s, &e2);
-            CKS(e2);
-        }
-        {
-            Trace tr("read_ctrl", 0);
-            CK(cudaEventSynchronize(h->ctrl_ev));
-        }
-        h->tail_known = h->ctrl_h->stash_tail;
-        const uint64_t count0 = h->ctrl_h->count, n_erase = h->stage_h[2];
-        count_lb = count0 > n_erase ? (int64_t)(count0 - n_erase) : 0;
-        if (h->stage_h[1]) CKS(grow_known(h, count0, h->stage_h[1], s));
-    }
-    CKS(insert_phase(h, d_keys, d_vals, nullptr, h->cls + n, n, n_ins, n, d_result, d_vals_out, s, nullptr,
-                     pre ? &dd_ins : nullptr));
-    CKS(erase_phase(h, d_keys, h->cls + 2 * n, n, n_era, n, d_result, d_vals_out, s, pre_era ? &dd_era : nullptr));
-    CKS(shrink_after(h, s, count_lb));
-    Prof p(h, "k_find", s);
-    CK(launch_find(h->grids, s, d_keys, h->cls, n, n_find, h->tv(), h->sv(), d_vals_out, d_result));
-    return HIVE_OK;
+    if (h->sharded()) return shard_call(h, SK_MIXED, d_op, d_keys, d_vals, n, d_vals_out, d_result, s);
+    return mixed_impl(h, d_op, d_keys, d_vals, n, nullptr, d_vals_out, d_result, s);
 }
 
 hive_status hive_insert_host(hive_t h, const uint32_t* h_keys, const uint32_t* h_vals, uint64_t n,
                              uint8_t* h_status, void* stream) {
     if (!h) return HIVE_EINVAL;
-    if (n == 0) return HIVE_OK;
-    if (!h_keys || !h_vals || n >= (1ull << 32)) return HIVE_EINVAL;
+    if (n == 0 && !h->sharded()) return HIVE_OK;
+    if ((n && (!h_keys || !h_vals)) || n >= (1ull << 32)) return HIVE_EINVAL;
     BusyGuard g(h);
     if (!g.ok) return HIVE_EBUSY;
     cudaStream_t s = (cudaStream_t)stream;
     h->last = s;
+    if (h->sharded()) {                      // stage the local batch, then the collective call
+        auto& S = h->sh;
+        if (n > S.batch_max) return HIVE_EINVAL;
+        if (n) {
+            CK(cudaMemcpyAsync(S.hk, h_keys, n * 4, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(S.hv, h_vals, n * 4, cudaMemcpyHostToDevice, s));
+        }
+        CKS(shard_call(h, SK_INSERT, nullptr, S.hk, S.hv, n, nullptr, h_status ? S.ho8 : nullptr, s));
+        if (n && h_status) CK(cudaMemcpyAsync(h_status, S.ho8, n, cudaMemcpyDeviceToHost, s));
+        return HIVE_OK;
+    }
     const uint64_t nch = (n + HOST_CHUNK - 1) / HOST_CHUNK;
     CKS(pipe_init(h, nch + 3));
     CKS(ensure(h->hk, h->hk_cap, n));
@@ -953,12 +1225,21 @@ hive_status hive_insert_host(hive_t h, const uint32_t* h_keys, const uint32_t* h
 hive_status hive_find_host(hive_t h, const uint32_t* h_keys, uint64_t n, uint32_t* h_vals_out,
                            uint8_t* h_found, void* stream) {
     if (!h) return HIVE_EINVAL;
-    if (n == 0) return HIVE_OK;
-    if (!h_keys || !h_vals_out || n >= (1ull << 32)) return HIVE_EINVAL;
+    if (n == 0 && !h->sharded()) return HIVE_OK;
+    if ((n && (!h_keys || !h_vals_out)) || n >= (1ull << 32)) return HIVE_EINVAL;
     BusyGuard g(h);
     if (!g.ok) return HIVE_EBUSY;
     cudaStream_t s = (cudaStream_t)stream;
     h->last = s;
+    if (h->sharded()) {
+        auto& S = h->sh;
+        if (n > S.batch_max) return HIVE_EINVAL;
+        if (n) CK(cudaMemcpyAsync(S.hk, h_keys, n * 4, cudaMemcpyHostToDevice, s));
+        CKS(shard_call(h, SK_FIND, nullptr, S.hk, nullptr, n, S.ho32, h_found ? S.ho8 : nullptr, s));
+        if (n) CK(cudaMemcpyAsync(h_vals_out, S.ho32, n * 4, cudaMemcpyDeviceToHost, s));
+        if (n && h_found) CK(cudaMemcpyAsync(h_found, S.ho8, n, cudaMemcpyDeviceToHost, s));
+        return HIVE_OK;
+    }
     const uint64_t nch = (n + HOST_CHUNK - 1) / HOST_CHUNK;
     CKS(pipe_init(h, 2 * nch + 1));
     CKS(ensure(h->fq, h->fq_cap, n));
@@ -994,7 +1275,7 @@ hive_status hive_size(hive_t h, uint64_t* out) {
     if (!h || !out) return HIVE_EINVAL;
     CKS(read_ctrl(h, h->last));
     *out = h->ctrl_h->count;
-    return h->ctrl_h->failed ? HIVE_ESTASHFULL : HIVE_OK;
+    return h->ctrl_h->failed ? HIVE_ESTASHFULL : h->ctrl_h->xfail ? HIVE_EXCHANGE : HIVE_OK;
 }
 
 hive_status hive_stats(hive_t h, hive_stats_t* o) {
@@ -1023,7 +1304,8 @@ hive_status hive_stats(hive_t h, hive_stats_t* o) {
     o->mapped_bytes = h->bk.mapped;
     for (int i = 0; i < 8; ++i) o->alg_bytes[i] = c.abytes[i];
     o->step3 = c.step3;
-    return c.failed ? HIVE_ESTASHFULL : HIVE_OK;
+    o->xfail = c.xfail;
+    return c.failed ? HIVE_ESTASHFULL : c.xfail ? HIVE_EXCHANGE : HIVE_OK;
 }
 
 hive_status hive_dump(hive_t h, uint32_t* d_keys, uint32_t* d_vals, uint64_t cap, uint64_t* n_out,
@@ -1299,6 +1581,40 @@ hive_status hive_collisions(uint32_t fn, const uint32_t* d_keys, uint64_t n, uin
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) { set_err(e, "hive_collisions", __LINE__); return HIVE_ECUDA; }
     *y_out = n - nonempty;      // sum_b (L_b - 1)_+ = n - #non-empty bins
+    return HIVE_OK;
+}
+
+hive_status hive_nccl_unique_id(uint8_t* id_out) {
+    if (!id_out) return HIVE_EINVAL;
+    if (!load_nccl()) return HIVE_ENCCL;
+    NcclUniqueId id;
+    CKN(g_nccl.get_unique_id(&id));
+    memcpy(id_out, id.internal, sizeof id.internal);
+    return HIVE_OK;
+}
+
+hive_status hive_nccl_comm_init(int nranks, int rank, const uint8_t* id, void** comm_out) {
+    if (!id || !comm_out || nranks < 1 || rank < 0 || rank >= nranks) return HIVE_EINVAL;
+    if (!load_nccl()) return HIVE_ENCCL;
+    NcclUniqueId uid;
+    memcpy(uid.internal, id, sizeof uid.internal);
+    *comm_out = nullptr;
+    CKN(g_nccl.comm_init_rank(comm_out, nranks, uid, rank));
+    return HIVE_OK;
+}
+
+hive_status hive_nccl_comm_destroy(void* comm) {
+    if (!comm) return HIVE_OK;
+    if (!load_nccl()) return HIVE_ENCCL;
+    CKN(g_nccl.comm_destroy(comm));
+    return HIVE_OK;
+}
+
+hive_status hive_shard_info(hive_t h, int* nranks, int* rank, uint64_t* cap_per_peer) {
+    if (!h) return HIVE_EINVAL;
+    if (nranks) *nranks = h->sh.nranks;
+    if (rank) *rank = h->sh.rank;
+    if (cap_per_peer) *cap_per_peer = h->sh.cap;
     return HIVE_OK;
 }
 

@@ -1349,6 +1349,18 @@ k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __rest
             } else if (mode == PART_ROUTE_KEYS) {
                 reinterpret_cast<uint32_t*>(send_kv)[pos] = keys[i];
                 pos_out[i] = (uint32_t)pos;
+            } else if (mode == PART_ROUTE_PAD) {
+                // region p of the padded NCCL send buffer (pd.region = cap
+                // records); an op past the region's capacity is not sent
+                const uint64_t rel = pos - part_info[MAX_PARTS + p];
+                if (rel < pd.region) {
+                    const uint64_t at = (uint64_t)p * pd.region + rel;
+                    send_kv[at] = ((uint64_t)(vals ? vals[i] : 0u) << 32) | keys[i];
+                    if (send_ops) send_ops[at] = ops[i];
+                    pos_out[i] = (uint32_t)at;
+                } else {
+                    pos_out[i] = NO_POS;
+                }
             } else if (mode == PART_ROUTE_P2P) {
                 // owner p's inbox, this rank's region: a remote store over NVLink
                 // (a local one when p is this rank); the stable rank keeps the
@@ -1678,6 +1690,115 @@ cudaError_t launch_unroute(cudaStream_t s, const uint32_t* pos, uint64_t n, cons
                            uint8_t* out8, const uint32_t* in32, uint32_t* out32) {
     const int grid = clamp_grid(1184, n, BLOCK);
     k_unroute<<<grid, BLOCK, 0, s>>>(pos, n, in8, out8, in32, out32);
+    return cudaGetLastError();
+}
+
+// ---- sharded table over NCCL: padded exchange ------------------------------------
+__global__ void k_pad_counts(const uint64_t* __restrict__ part_info, uint32_t n_shards, uint64_t cap,
+                             uint64_t* __restrict__ cnt_send, Ctrl* ctrl) {
+    const uint32_t p = threadIdx.x;
+    unsigned long long over = 0;
+    if (p < n_shards) {
+        const uint64_t c = part_info[p];
+        cnt_send[p] = c < cap ? c : cap;
+        over = c > cap ? c - cap : 0;
+    }
+    over = warp_sum(over);                      // n_shards <= 32 (one warp)
+    if (p == 0 && over) atomicAdd(&ctrl->xfail, over);
+}
+
+// Region prefix of the n_src clipped counts, per block (n_src <= MAX_PARTS).
+__device__ __forceinline__ void pad_starts(const uint64_t* cnt, uint32_t n_src, uint64_t cap, uint64_t* start) {
+    if (threadIdx.x == 0) {
+        uint64_t a = 0;
+        for (uint32_t r = 0; r < n_src; ++r) {
+            start[r] = a;
+            a += cnt[r] < cap ? cnt[r] : cap;
+        }
+        start[n_src] = a;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(BLOCK)
+k_owner_compact(uint32_t n_src, uint64_t cap, const uint64_t* __restrict__ recv_kv,
+                const uint8_t* __restrict__ recv_ops, const uint64_t* __restrict__ cnt,
+                uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint8_t* __restrict__ ops,
+                uint32_t* __restrict__ back, uint64_t* __restrict__ n_dev) {
+    __shared__ uint64_t start[MAX_PARTS + 1];
+    pad_starts(cnt, n_src, cap, start);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = start[n_src];
+    const uint64_t total = (uint64_t)n_src * cap;
+    for (uint64_t j = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; j < total; j += (uint64_t)gridDim.x * BLOCK) {
+        const uint32_t r = (uint32_t)(j / cap);
+        const uint64_t o = j - (uint64_t)r * cap;
+        if (start[r] + o >= start[r + 1]) continue;          // padding
+        const uint64_t li = start[r] + o;
+        const uint64_t w = recv_kv[j];
+        keys[li] = key_of(w);
+        vals[li] = val_of(w);
+        if (ops) ops[li] = recv_ops[j];
+        back[li] = (uint32_t)j;
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK)
+k_owner_return(uint64_t n, const uint64_t* __restrict__ n_dev, const uint32_t* __restrict__ back,
+               const uint8_t* __restrict__ r8, const uint32_t* __restrict__ r32, uint8_t* __restrict__ ret8,
+               uint32_t* __restrict__ ret32) {
+    if (n_dev) n = *n_dev;
+    for (uint64_t j = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; j < n; j += (uint64_t)gridDim.x * BLOCK) {
+        const uint32_t at = back[j];
+        if (r8) ret8[at] = r8[j];
+        if (r32) ret32[at] = r32[j];
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK)
+k_unroute_pad(const uint32_t* __restrict__ pos, uint64_t n, const uint8_t* __restrict__ in8,
+              uint8_t* __restrict__ out8, const uint32_t* __restrict__ in32, uint32_t* __restrict__ out32,
+              uint8_t miss8) {
+    for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (uint64_t)gridDim.x * BLOCK) {
+        const uint32_t p = pos[i];
+        const bool ok = p != NO_POS;
+        if (out8) out8[i] = ok ? in8[p] : miss8;
+        if (out32) out32[i] = ok ? in32[p] : 0u;
+    }
+}
+
+cudaError_t launch_route_pad(cudaStream_t s, uint32_t n_shards, uint32_t seed, const uint32_t* keys,
+                             const uint32_t* vals, const uint8_t* ops, uint64_t n, uint64_t cap, uint64_t* cnt,
+                             uint64_t* part_info, uint64_t* send_kv, uint8_t* send_ops, uint32_t* pos,
+                             uint64_t* cnt_send, Ctrl* ctrl) {
+    PeerDest pd{};
+    pd.region = cap;
+    cudaError_t e = launch_partition_pd(s, PART_ROUTE_PAD, n_shards, seed, keys, vals, ops, n, cnt, part_info,
+                                        nullptr, 0, send_kv, send_ops, pos, nullptr, nullptr, nullptr, nullptr, pd);
+    if (e != cudaSuccess) return e;
+    k_pad_counts<<<1, 32, 0, s>>>(part_info, n_shards, cap, cnt_send, ctrl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_owner_compact(cudaStream_t s, uint32_t n_src, uint64_t cap, const uint64_t* recv_kv,
+                                 const uint8_t* recv_ops, const uint64_t* cnt_recv, uint32_t* keys, uint32_t* vals,
+                                 uint8_t* ops, uint32_t* back, uint64_t* n_dev) {
+    const int grid = clamp_grid(148 * 8, (uint64_t)n_src * cap, BLOCK);
+    k_owner_compact<<<grid, BLOCK, 0, s>>>(n_src, cap, recv_kv, recv_ops, cnt_recv, keys, vals, ops, back, n_dev);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_owner_return(cudaStream_t s, uint64_t n_upper, const uint64_t* n_dev, const uint32_t* back,
+                                const uint8_t* r8, const uint32_t* r32, uint8_t* ret8, uint32_t* ret32) {
+    const int grid = clamp_grid(148 * 8, n_upper, BLOCK);
+    k_owner_return<<<grid, BLOCK, 0, s>>>(n_upper, n_dev, back, r8, r32, ret8, ret32);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unroute_pad(cudaStream_t s, const uint32_t* pos, uint64_t n, const uint8_t* in8, uint8_t* out8,
+                               const uint32_t* in32, uint32_t* out32, uint8_t miss8) {
+    if (n == 0) return cudaSuccess;
+    const int grid = clamp_grid(148 * 8, n, BLOCK);
+    k_unroute_pad<<<grid, BLOCK, 0, s>>>(pos, n, in8, out8, in32, out32, miss8);
     return cudaGetLastError();
 }
 

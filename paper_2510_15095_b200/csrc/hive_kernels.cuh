@@ -19,7 +19,8 @@ constexpr int PART_CHUNK = 8192;         // max elements per warp in the stable 
 constexpr int PART_UNROLL = 4;           // rows of 32 elements whose loads are in flight together
 constexpr int MAX_PARTS = 64;
 
-enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1, PART_ELECT = 2, PART_ROUTE_KEYS = 3, PART_ROUTE_P2P = 4 };
+enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1, PART_ELECT = 2, PART_ROUTE_KEYS = 3, PART_ROUTE_P2P = 4,
+                PART_ROUTE_PAD = 5 };
 
 // Peer-memory exchange: the owners' inbox / count /
 // result buffers of up to MAX_PEERS shards, passed by value.  Every buffer is
@@ -128,6 +129,30 @@ cudaError_t launch_elect_partition(cudaStream_t s, const uint32_t* keys, const u
                                    int num_sms);
 cudaError_t launch_dedup_elect_part(int grid, cudaStream_t s, const uint64_t* recs, const uint64_t* part_info,
                                     uint32_t part, DedupView dd, Ctrl* ctrl);
+
+// ---- sharded table over NCCL (include/hive.h "Sharded tables") ------
+// Stable route into a padded send buffer of G regions of `cap` records
+// (region p = ops owned by shard p, in op order); ops past `cap` of their
+// region are not sent (pos = NO_POS, ctrl->xfail counts them).  cnt_send[p] =
+// records placed in region p.
+constexpr uint32_t NO_POS = 0xFFFFFFFFu;
+cudaError_t launch_route_pad(cudaStream_t s, uint32_t n_shards, uint32_t seed, const uint32_t* keys,
+                             const uint32_t* vals, const uint8_t* ops, uint64_t n, uint64_t cap, uint64_t* cnt,
+                             uint64_t* part_info, uint64_t* send_kv, uint8_t* send_ops, uint32_t* pos,
+                             uint64_t* cnt_send, Ctrl* ctrl);
+// Owner: the records of the G received regions (cnt_recv[r] valid in region
+// r), in source-rank order, as contiguous keys / values / opcodes; back[j] =
+// the padded position record j came from; *n_dev = the total.
+cudaError_t launch_owner_compact(cudaStream_t s, uint32_t n_src, uint64_t cap, const uint64_t* recv_kv,
+                                 const uint8_t* recv_ops, const uint64_t* cnt_recv, uint32_t* keys, uint32_t* vals,
+                                 uint8_t* ops, uint32_t* back, uint64_t* n_dev);
+// Owner: results of the compacted batch back into the padded layout
+// (ret8[back[j]] = r8[j], ret32 likewise; either pair may be null).
+cudaError_t launch_owner_return(cudaStream_t s, uint64_t n_upper, const uint64_t* n_dev, const uint32_t* back,
+                                const uint8_t* r8, const uint32_t* r32, uint8_t* ret8, uint32_t* ret32);
+// Source: out8[i] = in8[pos[i]] (pos == NO_POS: out8 = miss8, out32 = 0).
+cudaError_t launch_unroute_pad(cudaStream_t s, const uint32_t* pos, uint64_t n, const uint8_t* in8, uint8_t* out8,
+                               const uint32_t* in32, uint32_t* out32, uint8_t miss8);
 
 cudaError_t launch_unroute(cudaStream_t s, const uint32_t* pos, uint64_t n, const uint8_t* in8,
                            uint8_t* out8, const uint32_t* in32, uint32_t* out32);

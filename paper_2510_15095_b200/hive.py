@@ -23,7 +23,8 @@ OP_FIND, OP_INSERT, OP_ERASE = 0, 1, 2
 INVALID_KEY = 0xFFFFFFFF
 
 _STATUS = {0: "ok", 1: "invalid argument", 2: "out of memory", 3: "CUDA error", 4: "NCCL error",
-           5: "stash full", 6: "handle busy"}
+           5: "stash full", 6: "handle busy", 7: "sharded exchange region full"}
+SHARD_SEED = 0x5BD1E995                       # HIVE_SHARD_SEED
 
 
 class HiveError(RuntimeError):
@@ -34,7 +35,9 @@ class HiveConfig(ctypes.Structure):
     _fields_ = [("capacity", ctypes.c_uint64), ("max_capacity", ctypes.c_uint64),
                 ("lf_grow", ctypes.c_float), ("lf_shrink", ctypes.c_float),
                 ("max_evictions", ctypes.c_uint32), ("resize_k", ctypes.c_uint32),
-                ("stash_fraction", ctypes.c_float), ("flags", ctypes.c_uint32)]
+                ("stash_fraction", ctypes.c_float), ("flags", ctypes.c_uint32),
+                ("nccl_comm", ctypes.c_void_p), ("shard_batch_max", ctypes.c_uint64),
+                ("shard_slack", ctypes.c_float)]
 
 
 class HiveStats(ctypes.Structure):
@@ -43,7 +46,7 @@ class HiveStats(ctypes.Structure):
             "count", "stash_used", "stash_cap", "evictions", "max_depth", "stash_pushes", "leftovers",
             "grows", "shrinks", "merge_aborts", "failed", "in_b1", "mapped_bytes")] + [
         ("alg_bytes", ctypes.c_uint64 * 8)] + [
-        ("step3", ctypes.c_uint64)]
+        ("step3", ctypes.c_uint64), ("xfail", ctypes.c_uint64)]
 
 
 # every exported symbol of include/hive.h, with its ctypes signature
@@ -83,6 +86,10 @@ SIGNATURES = {
     "hive_ipc_open": (_int, [_vp, ctypes.POINTER(_vp)]),
     "hive_ipc_close": (_int, [_vp]),
     "hive_collisions": (_int, [_u32, _vp, _u64, _u64, ctypes.POINTER(_u64), _vp]),
+    "hive_nccl_unique_id": (_int, [_vp]),
+    "hive_nccl_comm_init": (_int, [_int, _int, _vp, ctypes.POINTER(_vp)]),
+    "hive_nccl_comm_destroy": (_int, [_vp]),
+    "hive_shard_info": (_int, [_vp, ctypes.POINTER(_int), ctypes.POINTER(_int), ctypes.POINTER(_u64)]),
     "hive_status_string": (ctypes.c_char_p, [_int]),
     "hive_last_error": (ctypes.c_char_p, []),
 }
@@ -153,7 +160,11 @@ class HiveTable:
     def __init__(self, capacity: int, max_capacity: int = 0, lf_grow: float = 0.9,
                  lf_shrink: float = 0.25, max_evictions: int = 16, resize_k: int = 1024,
                  stash_fraction: float = 0.02, keys_unique: bool = False, hash: str = "bithash",
-                 stream=None):
+                 stream=None, nccl_comm: int | None = None, shard_batch_max: int = 0,
+                 shard_slack: float = 0.0625):
+        """nccl_comm (an ncclComm_t from nccl_comm_init): create one shard of a
+        hash-partitioned table; every op call is then collective over the comm
+        (include/hive.h "Sharded tables")."""
         L = lib()
         if not torch.cuda.is_available():
             raise HiveError("no CUDA device: the Hive table runs only on the GPU")
@@ -163,6 +174,8 @@ class HiveTable:
         cfg.lf_grow, cfg.lf_shrink = lf_grow, lf_shrink
         cfg.max_evictions, cfg.resize_k, cfg.stash_fraction = max_evictions, resize_k, stash_fraction
         cfg.flags = (HIVE_KEYS_UNIQUE if keys_unique else 0) | HASH_PAIRS[hash]
+        cfg.nccl_comm = nccl_comm
+        cfg.shard_batch_max, cfg.shard_slack = shard_batch_max, shard_slack
         self.cfg = cfg
         h = ctypes.c_void_p()
         _check(L.hive_create(ctypes.byref(cfg), ctypes.c_void_p(_stream(stream)), ctypes.byref(h)), "hive_create")
@@ -263,7 +276,7 @@ class HiveTable:
     def stats(self, allow_failed: bool = False) -> dict:
         s = HiveStats()
         rc = self._L.hive_stats(self._h, ctypes.byref(s))
-        if not (allow_failed and rc == 5):
+        if not (allow_failed and rc in (5, 7)):
             _check(rc, "hive_stats")
         d = {n: getattr(s, n) for n, _ in HiveStats._fields_}
         d["alg_bytes"] = dict(zip(("find", "insert", "evict", "erase", "elect"), list(s.alg_bytes)[:5]))
@@ -276,6 +289,13 @@ class HiveTable:
         v = torch.empty(max(n.value, 1), dtype=torch.uint32, device="cuda")
         _check(self._L.hive_dump(self._h, _p(k), _p(v), n.value, ctypes.byref(n), _stream()), "hive_dump")
         return k[:n.value], v[:n.value]
+
+    def shard_info(self) -> tuple[int, int, int]:
+        """(nranks, rank, padded exchange capacity per peer); (1, 0, 0) unsharded."""
+        g, r, c = _int(), _int(), _u64()
+        _check(self._L.hive_shard_info(self._h, ctypes.byref(g), ctypes.byref(r), ctypes.byref(c)),
+               "hive_shard_info")
+        return g.value, r.value, c.value
 
     def profile(self, enable: bool = True):
         _check(self._L.hive_profile(self._h, 1 if enable else 0), "hive_profile")
@@ -446,3 +466,21 @@ def p2p_signal(n, rank, phase, epoch, peer_sig, stream=None):
 
 def p2p_wait(n, phase, epoch, sig: int, timeout_ns=60_000_000_000, stream=None):
     _check(lib().hive_p2p_wait(n, phase, epoch, ctypes.c_void_p(sig), timeout_ns, _stream(stream)), "hive_p2p_wait")
+
+
+# ---- NCCL bootstrap for sharded tables ----------------------------------------------
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().hive_nccl_unique_id(buf), "hive_nccl_unique_id")
+    return buf.raw
+
+
+def nccl_comm_init(nranks: int, rank: int, uid: bytes) -> int:
+    out = _vp()
+    buf = ctypes.create_string_buffer(uid, 128)
+    _check(lib().hive_nccl_comm_init(nranks, rank, buf, ctypes.byref(out)), "hive_nccl_comm_init")
+    return int(out.value)
+
+
+def nccl_comm_destroy(comm: int):
+    _check(lib().hive_nccl_comm_destroy(ctypes.c_void_p(comm)), "hive_nccl_comm_destroy")

@@ -1,20 +1,16 @@
 """Hash-partitioned Hive table: one shard per GPU.
 
 Each rank owns an independent Hive table (its own resize, stash and
-counters).  A batch is routed by shard(k) = (fmix32(k ^ seed) * G) >> 32
-with the stable partition kernel (hive_route), exchanged with an all-to-all
-(NCCL over NVLink/NVSwitch on GPUs; any torch.distributed backend works),
-processed by the owner shard, and the per-op results come back through the
-inverse all-to-all and the unpermute kernel (hive_unroute).
+counters).  Key k belongs to rank shard(k) = (fmix32(k ^ seed) * G) >> 32.
 
-Ordering: the receive buffer concatenates source ranks in rank order and the
-route is stable, so a shard sees the union batch in (rank, local index) order;
-in-batch duplicates across ranks therefore resolve to the op with the largest
+`ShardedHive` is the C-ABI sharded handle (NCCL inside the library, padded
+all-to-all, no host synchronisation with growth off).  `P2PShardedHive`
+ moves records and results with the kernels' own stores
+over NVLink peer mappings instead of NCCL.
+
+Ordering: a shard sees the union batch in (rank, local index) order; in-batch
+duplicates across ranks therefore resolve to the op with the largest
 (rank, index) — the "last write" of the rank-major global order.
-
-`ops` is the device-side primitive set.  `CudaOps` (the product) calls the
-C ABI; tests on CPU (gloo) substitute an equivalent test implementation to
-exercise the exchange logic without a GPU.
 """
 from __future__ import annotations
 
@@ -23,123 +19,53 @@ import torch.distributed as dist
 
 from . import hive
 
-SHARD_SEED = 0x5BD1E995
-
-
-class CudaOps:
-    """Routing primitives and a local table, all on the GPU via libhive.so."""
-
-    def __init__(self, capacity: int, **cfg):
-        self.table = hive.HiveTable(capacity, **cfg)
-
-    @staticmethod
-    def route(keys, vals, ops, n_shards, seed):
-        return hive.route(keys, vals, ops, n_shards, seed)
-
-    @staticmethod
-    def route_keys(keys, n_shards, seed):
-        return hive.route_keys(keys, n_shards, seed)
-
-    @staticmethod
-    def unroute(pos, in8=None, in32=None):
-        return hive.unroute(pos, in8=in8, in32=in32)
-
-    @staticmethod
-    def unpack(kv):
-        return hive.unpack_kv(kv)
+SHARD_SEED = hive.SHARD_SEED
 
 
 class ShardedHive:
-    def __init__(self, capacity_per_shard: int = 0, group=None, seed: int = SHARD_SEED,
-                 ops=None, **cfg):
+    """One rank's shard of a hash-partitioned Hive table behind the C ABI
+    (include/hive.h "Sharded tables"): argument marshalling only.  The NCCL
+    comm is made by the library (hive_nccl_unique_id on rank 0, broadcast over
+    the torch.distributed group, hive_nccl_comm_init on every rank); routing,
+    the padded ncclAlltoAll exchange, the owner's PHASED batch and the inverse
+    exchange all run inside the library on the current stream.  Every op is
+    collective: each rank passes its own local batch (<= batch_max ops)."""
+
+    def __init__(self, capacity_per_shard: int, batch_max: int, group=None, slack: float = 0.0625, **cfg):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        self.seed = seed
-        self.ops = ops if ops is not None else CudaOps(capacity_per_shard, **cfg)
-        self.table = self.ops.table
-        # The exchange form is fixed at construction from the backend, which is
-        # the same on every rank, so all ranks always issue the same collective.
-        self._list_a2a = dist.get_backend(group) == "nccl"
+        obj = [hive.nccl_unique_id() if self.rank == 0 else None]
+        src = 0 if group is None else dist.get_global_rank(group, 0)
+        dist.broadcast_object_list(obj, src=src, group=group)
+        self.comm = hive.nccl_comm_init(self.world, self.rank, obj[0])
+        self.table = hive.HiveTable(capacity_per_shard, nccl_comm=self.comm, shard_batch_max=batch_max,
+                                    shard_slack=slack, **cfg)
+        self.seed = SHARD_SEED
 
-    # ---- exchange ---------------------------------------------------------------
-    def _counts(self, send_counts: torch.Tensor):
-        if self.world == 1:
-            sc = send_counts.cpu().tolist()                    # one small D2H per batch
-            return sc, sc
-        recv_counts = torch.empty_like(send_counts)
-        dist.all_to_all_single(recv_counts, send_counts, group=self.group)
-        both = torch.stack([send_counts, recv_counts]).cpu()   # one small D2H per batch
-        return both[0].tolist(), both[1].tolist()
+    def close(self):
+        if getattr(self, "table", None) is not None:
+            self.table.close()
+            self.table = None
+            hive.nccl_comm_destroy(self.comm)
 
-    def _a2a(self, x: torch.Tensor, out_splits, in_splits) -> torch.Tensor:
-        """All-to-all of a routed buffer.  This rank's own block never goes
-        through the collective: a device copy (or, at world size 1, nothing)
-        places it, and NCCL moves only the off-diagonal blocks."""
-        if self.world == 1:
-            return x
-        out = torch.empty(sum(out_splits), dtype=x.dtype, device=x.device)
-        if self._list_a2a:
-            outs, ins = list(out.split(out_splits)), list(x.split(in_splits))
-            me = self.rank
-            dist.all_to_all([o if r != me else o[:0] for r, o in enumerate(outs)],
-                            [t if r != me else t[:0] for r, t in enumerate(ins)], group=self.group)
-            outs[me].copy_(ins[me])
-            return out
-        dist.all_to_all_single(out, x, out_splits, in_splits, group=self.group)
-        return out
+    def insert(self, keys, vals, status=None):
+        return self.table.insert(keys, vals, status)
 
-    def _a2a_u8(self, x, out_splits, in_splits):
-        return self._a2a(x, out_splits, in_splits)
+    def find(self, keys, vals_out=None, found=None):
+        return self.table.find(keys, vals_out, found)
 
-    def _a2a_u32(self, x, out_splits, in_splits):
-        # int32 view: every backend supports it
-        y = self._a2a(x.view(torch.int32), out_splits, in_splits)
-        return y.view(torch.uint32)
+    def erase(self, keys, erased=None):
+        return self.table.erase(keys, erased)
 
-    def _forward(self, keys, vals, ops_codes):
-        send_kv, send_ops, pos, counts = self.ops.route(keys, vals, ops_codes, self.world, self.seed)
-        sc, rc = self._counts(counts)
-        recv_kv = self._a2a(send_kv, rc, sc)
-        recv_ops = self._a2a_u8(send_ops, rc, sc) if send_ops is not None else None
-        k, v = self.ops.unpack(recv_kv)
-        return k, v, recv_ops, pos, sc, rc
+    def mixed(self, op_codes, keys, vals, vals_out=None, result=None):
+        return self.table.mixed(op_codes, keys, vals, vals_out, result)
 
-    # ---- collective batch ops (every rank calls with its own local batch) -----------
-    def insert(self, keys, vals):
-        k, v, _, pos, sc, rc = self._forward(keys, vals, None)
-        st = self.table.insert(k, v)
-        back = self._a2a_u8(st, sc, rc)
-        out8, _ = self.ops.unroute(pos, in8=back)
-        return out8
+    def insert_host(self, keys_h, vals_h, status_h=None):
+        return self.table.insert_host(keys_h, vals_h, status_h)
 
-    def _forward_keys(self, keys):
-        send, pos, counts = self.ops.route_keys(keys, self.world, self.seed)
-        sc, rc = self._counts(counts)
-        return self._a2a_u32(send, rc, sc), pos, sc, rc
-
-    def find(self, keys):
-        k, pos, sc, rc = self._forward_keys(keys)
-        vals, found = self.table.find(k)
-        bv = self._a2a_u32(vals, sc, rc)
-        bf = self._a2a_u8(found, sc, rc)
-        f, v = self.ops.unroute(pos, in8=bf, in32=bv)
-        return v, f
-
-    def erase(self, keys):
-        k, pos, sc, rc = self._forward_keys(keys)
-        er = self.table.erase(k)
-        back = self._a2a_u8(er, sc, rc)
-        out8, _ = self.ops.unroute(pos, in8=back)
-        return out8
-
-    def mixed(self, op_codes, keys, vals):
-        k, v, o, pos, sc, rc = self._forward(keys, vals, op_codes)
-        vals_out, result = self.table.mixed(o, k, v)
-        bv = self._a2a_u32(vals_out, sc, rc)
-        br = self._a2a_u8(result, sc, rc)
-        r, vo = self.ops.unroute(pos, in8=br, in32=bv)
-        return vo, r
+    def find_host(self, keys_h, vals_h=None, found_h=None):
+        return self.table.find_host(keys_h, vals_h, found_h)
 
 
 # ---- NEXT-1: exchange over NVLink peer memory (no NCCL on the data path) -------------

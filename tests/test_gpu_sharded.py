@@ -1,5 +1,7 @@
-"""The sharded path on one GPU: route kernel -> NCCL all-to-all (world size 1)
--> local phases -> inverse all-to-all -> unroute, against a plain table."""
+"""The sharded handle (include/hive.h "Sharded tables") on one GPU: the C-ABI
+collective calls (route -> padded ncclAlltoAll -> owner PHASED batch -> inverse
+ncclAlltoAll -> unpermute) at world size 1, element by element against the CPU
+oracle; graph capture of the host-sync-free form (growth off)."""
 import os
 import socket
 
@@ -13,37 +15,114 @@ import gen
 pytestmark = pytest.mark.gpu
 
 
-def test_sharded_world1_nccl_matches_plain_table():
+@pytest.fixture(scope="module")
+def pg():
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
-    from paper_2510_15095_b200 import HiveTable, u8, u32
-    from paper_2510_15095_b200.sharded import ShardedHive
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
-    try:
-        sh = ShardedHive(256 * 32, resize_k=16)
-        ref = HiveTable(256 * 32, resize_k=16)
-        rng = np.random.default_rng(9)
-        for b in range(5):
-            n = 20000
-            keys = u32(rng.integers(0, 30000, n, dtype=np.uint64).astype(np.uint32))
-            vals = u32(rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32))
-            ops = u8(gen.bernoulli_ops(n, 0.5, 0.2, seed=b))
-            vo1, r1 = sh.mixed(ops, keys, vals)
-            vo2, r2 = ref.mixed(ops, keys, vals)
-            assert torch.equal(r1.cpu(), r2.cpu()) and torch.equal(vo1.cpu(), vo2.cpu())
-        q = u32(rng.integers(0, 40000, 50000, dtype=np.uint64).astype(np.uint32))
-        v1, f1 = sh.find(q)
-        v2, f2 = ref.find(q)
-        assert torch.equal(f1.cpu(), f2.cpu()) and torch.equal(v1.cpu(), v2.cpu())
-        e1 = sh.erase(q[:1000])
-        e2 = ref.erase(q[:1000])
-        assert torch.equal(e1.cpu(), e2.cpu())
-        st1 = sh.insert(q[:5000], q[:5000])
-        st2 = ref.insert(q[:5000], q[:5000])
-        assert torch.equal(st1.cpu(), st2.cpu())
-    finally:
-        dist.destroy_process_group()
+    yield
+    dist.destroy_process_group()
+
+
+def _np(t):
+    return t.cpu().numpy()
+
+
+@pytest.mark.parametrize("grow", [True, False])
+def test_sharded_handle_world1_vs_oracle(pg, grow):
+    import oracle
+    from paper_2510_15095_b200 import u8, u32
+    from paper_2510_15095_b200.sharded import ShardedHive
+    cfg = dict(resize_k=16) if grow else dict(lf_grow=2.0, lf_shrink=0)
+    sh = ShardedHive(256 * 32 if grow else 2048 * 32, batch_max=40000, **cfg)
+    o = oracle.OracleTable(256 * 32 if grow else 2048 * 32, **cfg)
+    assert sh.table.shard_info()[:2] == (1, 0)
+    rng = np.random.default_rng(9)
+    for b in range(6):
+        n = int(rng.integers(0, 30000)) if b else 0                      # empty batch too
+        keys = rng.integers(0, 30000, n, dtype=np.uint64).astype(np.uint32)
+        keys[rng.random(n) < 0.01] = 0xFFFFFFFF
+        vals = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+        ops = gen.bernoulli_ops(n, 0.5, 0.2, seed=b)
+        vo, r = sh.mixed(u8(ops), u32(keys), u32(vals))
+        vo_o, r_o = o.mixed(ops, keys, vals)
+        assert (_np(r) == r_o).all() and (_np(vo).astype(np.uint32) == vo_o).all(), b
+    q = rng.integers(0, 40000, 50000, dtype=np.uint64).astype(np.uint32)
+    v, f = sh.find(u32(q))
+    v_o, f_o = o.find(q)
+    assert (_np(f) == f_o).all() and (_np(v).astype(np.uint32) == v_o).all()
+    e = sh.erase(u32(q[:20000]))
+    assert (_np(e) == o.erase(q[:20000])).all()
+    st = sh.insert(u32(q[:5000]), u32(q[:5000]))
+    assert (_np(st) == o.insert(q[:5000], q[:5000])).all()
+    # host-buffer forms of the collective calls
+    kh = torch.from_numpy(q[5000:9000].view(np.int32)).view(torch.uint32).pin_memory()
+    st_h = sh.insert_host(kh, kh)
+    vh, fh = sh.find_host(kh)
+    torch.cuda.synchronize()
+    assert (st_h.numpy() == o.insert(q[5000:9000], q[5000:9000])).all()
+    v_o, f_o = o.find(q[5000:9000])
+    assert (fh.numpy() == f_o).all() and (vh.numpy().view(np.uint32) == v_o).all()
+    k, v = sh.table.dump()
+    assert dict(zip(_np(k).astype(np.uint32).tolist(), _np(v).astype(np.uint32).tolist())) == o.dump_dict()
+    s = sh.table.stats()
+    assert s["xfail"] == 0 and s["failed"] == 0
+    if not grow:
+        assert s["n_buckets"] == 2048
+    sh.close()
+
+
+def test_sharded_batch_max_enforced(pg):
+    from paper_2510_15095_b200 import HiveError, u32
+    from paper_2510_15095_b200.sharded import ShardedHive
+    sh = ShardedHive(64 * 32, batch_max=100, lf_grow=2.0, lf_shrink=0)
+    with pytest.raises(HiveError):
+        sh.insert(u32(np.arange(101, dtype=np.uint32)), u32(np.arange(101, dtype=np.uint32)))
+    sh.close()
+
+
+def test_sharded_calls_capture_in_a_cuda_graph(pg):
+    """With growth and contraction off the collective calls never wait on the
+    host, so an insert + find + erase sequence captures into one CUDA graph
+    whose replays give the oracle's results."""
+    import oracle
+    from paper_2510_15095_b200 import u32
+    from paper_2510_15095_b200.sharded import ShardedHive
+    n = 1 << 16
+    sh = ShardedHive(4096 * 32, batch_max=n, lf_grow=2.0, lf_shrink=0)
+    ids = np.arange(n, dtype=np.uint32)
+    keys, vals = u32(gen.keys_of(ids)), u32(gen.vals_of(ids))
+    qids, hit = gen.mixed_queries(n // 2, n // 2, n, seed=5)
+    q = u32(gen.keys_of(qids))
+    st = torch.empty(n, dtype=torch.uint8, device="cuda")
+    vo = torch.empty(n, dtype=torch.uint32, device="cuda")
+    fo = torch.empty(n, dtype=torch.uint8, device="cuda")
+    er = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):                 # warm-up: sizes every scratch buffer
+        sh.insert(keys, vals, st)
+        sh.find(q, vo, fo)
+        sh.erase(keys[: n // 4], er)
+        sh.table.clear()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        sh.insert(keys, vals, st)
+        sh.find(q, vo, fo)
+        sh.erase(keys[: n // 4], er)
+    for rep in range(2):
+        sh.table.clear()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        o = oracle.OracleTable(4096 * 32, lf_grow=2.0, lf_shrink=0)
+        assert (_np(st) == o.insert(gen.keys_of(ids), gen.vals_of(ids))).all()
+        v_o, f_o = o.find(gen.keys_of(qids))
+        assert (_np(fo) == f_o).all() and (_np(vo).astype(np.uint32) == v_o).all()
+        assert (_np(er) == o.erase(gen.keys_of(ids[: n // 4]))).all()
+    del g
+    sh.close()

@@ -1,11 +1,12 @@
 """Hash-partitioned table, N > 1 path, on CPU: world size 2 over gloo.
 
-`ShardedHive` (the product's exchange logic: route -> all-to-all of counts and
-records -> local phases -> inverse all-to-all -> unpermute) runs unchanged;
-only the device primitives are replaced by an oracle-backed stand-in (routing
-by the oracle's shard function, a stable sort, and an OracleTable per rank).
-Expected results are computed independently in the parent: shard s processes
-the rank-major concatenation of the ops routed to it."""
+The sharded handle's padded exchange protocol (route into G regions of `cap`
+records -> all-to-all of counts and records -> owner compaction in rank order
+-> PHASED batch -> inverse all-to-all -> unpermute; hive_host.cu shard_call)
+is re-stated over torch.distributed with an oracle table per rank and run by
+two processes.  Expected results are computed independently in the parent:
+shard s processes the rank-major concatenation of the ops routed to it (the
+first `cap` per source)."""
 import os
 import socket
 
@@ -43,53 +44,74 @@ class OracleTableAdapter:
         return torch.from_numpy(vo.view(np.int32)).view(torch.uint32), torch.from_numpy(r)
 
 
-class OracleOps:
-    """CPU stand-in for hive_route / hive_unroute / hive_unpack_kv."""
+NO_POS = 0xFFFFFFFF
 
-    def __init__(self, capacity, **cfg):
+
+class PaddedExchangeModel:
+    """The sharded handle's exchange protocol (hive_host.cu shard_call,
+    include/hive.h "Sharded tables") re-stated over torch.distributed with an
+    oracle table per rank: stable route into G regions of `cap` records (ops
+    past a region's capacity are not sent: pos = NO_POS), one all-to-all of
+    the clipped counts and one of the padded records (+ opcodes), owner
+    compaction in source-rank order, the PHASED batch, results back into the
+    padded layout, the inverse all-to-all, unpermute with miss codes (4, find
+    found = 2)."""
+
+    def __init__(self, capacity, cap, seed, **cfg):
         self.table = OracleTableAdapter(capacity, **cfg)
+        self.cap, self.seed = cap, seed
+        self.G, self.rank = dist.get_world_size(), dist.get_rank()
 
-    @staticmethod
-    def route(keys, vals, ops, n_shards, seed):
+    def _a2a(self, x):
+        out = torch.empty_like(x)
+        dist.all_to_all_single(out, x)
+        return out
+
+    def call(self, kind, keys, vals=None, ops=None):
         import oracle
+        G, cap = self.G, self.cap
         k = keys.numpy().view(np.uint32)
-        sh = oracle.shard_array(k, seed, n_shards)
-        order = np.argsort(sh, kind="stable")
-        v = vals.numpy().view(np.uint32) if vals is not None else np.zeros_like(k)
-        kv = (v[order].astype(np.uint64) << np.uint64(32)) | k[order].astype(np.uint64)
-        pos = np.empty(len(k), np.int32)
-        pos[order] = np.arange(len(k), dtype=np.int32)
-        send_ops = torch.from_numpy(ops.numpy()[order].copy()) if ops is not None else None
-        counts = torch.from_numpy(np.bincount(sh, minlength=n_shards).astype(np.int64))
-        return torch.from_numpy(kv.view(np.int64)), send_ops, torch.from_numpy(pos), counts
-
-    @staticmethod
-    def route_keys(keys, n_shards, seed):
-        import oracle
-        k = keys.numpy().view(np.uint32)
-        sh = oracle.shard_array(k, seed, n_shards)
-        order = np.argsort(sh, kind="stable")
-        pos = np.empty(len(k), np.int32)
-        pos[order] = np.arange(len(k), dtype=np.int32)
-        counts = torch.from_numpy(np.bincount(sh, minlength=n_shards).astype(np.int64))
-        return _t32(k[order]), torch.from_numpy(pos), counts
-
-    @staticmethod
-    def unroute(pos, in8=None, in32=None):
-        p = pos.numpy()
-        o8 = torch.from_numpy(in8.numpy()[p].copy()) if in8 is not None else None
-        o32 = None
-        if in32 is not None:
-            o32 = torch.from_numpy(in32.numpy().view(np.int32)[p].copy()).view(torch.uint32)
-        return o8, o32
-
-    @staticmethod
-    def unpack(kv):
-        w = kv.numpy().view(np.uint64)
-        k = (w & np.uint64(0xFFFFFFFF)).astype(np.uint32)
-        v = (w >> np.uint64(32)).astype(np.uint32)
-        return (torch.from_numpy(k.view(np.int32)).view(torch.uint32),
-                torch.from_numpy(v.view(np.int32)).view(torch.uint32))
+        n = len(k)
+        sh = oracle.shard_array(k, self.seed, G)
+        send_kv = np.zeros(G * cap, np.int64)
+        send_op = np.zeros(G * cap, np.int32)
+        pos = np.full(n, NO_POS, np.uint64)
+        cnt = np.zeros(G, np.int64)
+        for i in range(n):                                   # stable, op order
+            p = int(sh[i])
+            if cnt[p] < cap:
+                at = p * cap + cnt[p]
+                v = int(vals.numpy().view(np.uint32)[i]) if vals is not None else 0
+                send_kv[at] = np.int64(np.uint64((v << 32) | int(k[i])).view(np.int64))
+                send_op[at] = int(ops[i]) if ops is not None else 0
+                pos[i] = at
+                cnt[p] += 1
+        rcnt = self._a2a(torch.from_numpy(cnt)).numpy()
+        rkv = self._a2a(torch.from_numpy(send_kv)).numpy().view(np.uint64)
+        rop = self._a2a(torch.from_numpy(send_op)).numpy()
+        idx = np.concatenate([np.arange(r * cap, r * cap + rcnt[r]) for r in range(G)]).astype(np.int64)
+        kc = (rkv[idx] & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+        vc = (rkv[idx] >> np.uint64(32)).astype(np.uint32)
+        oc = rop[idx].astype(np.uint8)
+        ret8 = np.zeros(G * cap, np.int32)
+        ret32 = np.zeros(G * cap, np.int64)
+        if kind == "insert":
+            ret8[idx] = self.table.insert(_t32(kc), _t32(vc)).numpy()
+        elif kind == "erase":
+            ret8[idx] = self.table.erase(_t32(kc)).numpy()
+        elif kind == "find":
+            v, f = self.table.find(_t32(kc))
+            ret8[idx], ret32[idx] = f.numpy(), v.numpy().view(np.uint32)
+        else:
+            v, r = self.table.mixed(torch.from_numpy(oc), _t32(kc), _t32(vc))
+            ret8[idx], ret32[idx] = r.numpy(), v.numpy().view(np.uint32)
+        rr8 = self._a2a(torch.from_numpy(ret8)).numpy()
+        rr32 = self._a2a(torch.from_numpy(ret32)).numpy()
+        sent = pos != NO_POS
+        p = np.where(sent, pos, 0).astype(np.int64)
+        out8 = np.where(sent, rr8[p], 2 if kind == "find" else 4).astype(np.uint8)
+        out32 = np.where(sent, rr32[p], 0).astype(np.uint32)
+        return out8, out32
 
 
 def _batches(rank):
@@ -110,32 +132,24 @@ def _t32(a):
     return torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).view(torch.uint32)
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, cap):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
-    from paper_2510_15095_b200.sharded import ShardedHive
-    sh = ShardedHive(ops=OracleOps(64 * 32, resize_k=16), seed=SEED)
+    sh = PaddedExchangeModel(64 * 32, cap, SEED, resize_k=16)
     res = []
     for kind, ops, keys, vals in _batches(rank):
-        if kind == "insert":
-            r = sh.insert(_t32(keys), _t32(vals))
-            res.append((r.numpy().copy(),))
-        elif kind == "mixed":
-            vo, r = sh.mixed(torch.from_numpy(ops), _t32(keys), _t32(vals))
-            res.append((r.numpy().copy(), vo.numpy().view(np.uint32).copy()))
-        elif kind == "find":
-            v, f = sh.find(_t32(keys))
-            res.append((f.numpy().copy(), v.numpy().view(np.uint32).copy()))
-        else:
-            r = sh.erase(_t32(keys))
-            res.append((r.numpy().copy(),))
+        o8, o32 = sh.call(kind, _t32(keys), _t32(vals) if vals is not None else None,
+                          ops if kind == "mixed" else None)
+        res.append((o8,) if kind in ("insert", "erase") else (o8, o32))
     q.put((rank, res))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def _expected():
-    """Independent expectation: per-shard oracles over rank-major sequences."""
+def _expected(cap):
+    """Independent expectation: per-shard oracles over rank-major sequences of
+    the ops each source could send (the first `cap` of its ops owned by that
+    shard, in op order); the others report 4 (find: found 2, value 0)."""
     import oracle
     shards = [oracle.OracleTable(64 * 32, resize_k=16) for _ in range(WORLD)]
     per_rank = [_batches(r) for r in range(WORLD)]
@@ -148,7 +162,7 @@ def _expected():
             for r in range(WORLD):
                 _, ops, keys, vals = per_rank[r][b]
                 sh = oracle.shard_array(keys, SEED, WORLD)
-                idx = np.flatnonzero(sh == s)
+                idx = np.flatnonzero(sh == s)[:cap]
                 cat_keys.append(keys[idx])
                 cat_vals.append(vals[idx] if vals is not None else np.zeros(len(idx), np.uint32))
                 cat_ops.append(ops[idx] if ops is not None else np.zeros(len(idx), np.uint8))
@@ -166,29 +180,39 @@ def _expected():
                 res = (shards[s].erase(k),)
             for j, (r, i) in enumerate(owners):
                 outs[r][i] = tuple(x[j] for x in res)
+        ncol = 1 if kind in ("insert", "erase") else 2
+        miss = (2, 0) if kind == "find" else (4, 0)
         for r in range(WORLD):
             n = len(per_rank[r][b][2])
-            exp[r].append(tuple(np.array([outs[r][i][c] for i in range(n)]) for c in range(len(outs[r][0]))))
+            exp[r].append(tuple(np.array([outs[r].get(i, miss)[c] for i in range(n)]) for c in range(ncol)))
     return exp
 
 
 @pytest.mark.timeout(300)
-def test_sharded_exchange_world2_gloo():
+@pytest.mark.parametrize("cap", [4000, 600])
+def test_padded_exchange_world2_gloo(cap):
+    """World size 2 over gloo: the padded exchange protocol against per-shard
+    oracles.  cap = 4000 never overflows (every batch < 4000 ops); cap = 600
+    makes the larger batches overflow their regions, exercising the not-sent
+    path (result 4 / found 2) while every sent op keeps exact semantics."""
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, cap)) for r in range(WORLD)]
     for p in procs:
         p.start()
     got = dict(q.get(timeout=240) for _ in range(WORLD))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    exp = _expected()
+    exp = _expected(cap)
+    overflowed = 0
     for r in range(WORLD):
         assert len(got[r]) == len(exp[r])
         for b, (g, e) in enumerate(zip(got[r], exp[r])):
             for gc, ec in zip(g, e):
                 assert (np.asarray(gc).astype(np.int64) == np.asarray(ec).astype(np.int64)).all(), (r, b)
+            overflowed += int((np.asarray(g[0]) == 4).sum())
+    assert (overflowed > 0) == (cap == 600)
