@@ -130,6 +130,13 @@ typedef struct {
                                 Step-2 placements = new keys - leftovers      */
     uint64_t xfail;          /* sharded: ops of this rank not processed
                                 because their exchange region was full        */
+    uint64_t step_cycles[4]; /* insertion step breakdown,
+                                collected while hive_profile level 2 is on:
+                                warp clock64() cycles in Step 1 (replace),
+                                Step 2 (claim-and-commit), Step 3 (bounded
+                                eviction), Step 4 (stash fallback); per warp
+                                region max-over-lanes end minus min-over-lanes
+                                start, summed over warps and regions          */
 } hive_stats_t;
 
 /* ---- Sharded tables (BASELINE configs[4]) ---------------
@@ -249,7 +256,9 @@ hive_status hive_dump(hive_t h, uint32_t* d_keys, uint32_t* d_vals, uint64_t cap
                       uint64_t* n_out, void* stream);
 
 /* Per-kernel device timing (CUDA events around every launch on the call's
- * stream).  Enabled by hive_profile(h, 1); hive_profile_read fills up to
+ * stream).  Enabled by hive_profile(h, 1); hive_profile(h, 2) additionally
+ * runs the insert kernels' clock64-instrumented variants (default lane
+ * geometry) that fill hive_stats.step_cycles.  hive_profile_read fills up to
  * max entries of names (pointers to static strings), total milliseconds and
  * launch counts, returns the number of kernels seen, and resets when
  * reset != 0.  Sync. */

@@ -113,6 +113,11 @@ struct Ctrl {
     // bucket probe, 32 per CAS / atomic sector, 8 per spill word or stash word,
     // exact bytes of the key / value / result streams.
     unsigned long long abytes[8];
+    // Insertion step breakdown (hive_profile level 2): warp
+    // cycles spent in Step 1 (replace), Step 2 (claim-and-commit), Step 3
+    // (bounded eviction) and Step 4 (stash fallback); per warp region,
+    // max-over-lanes end minus min-over-lanes start of clock64().
+    unsigned long long cyc[4];
 };
 enum AlgBytes { AB_FIND = 0, AB_INSERT = 1, AB_EVICT = 2, AB_ERASE = 3, AB_ELECT = 4, AB_RESIZE = 5 };
 
@@ -284,6 +289,37 @@ __device__ __forceinline__ void scan_slots(const uint64_t (&s)[SPL], uint32_t k,
         jf = (key == INVALID_KEY) ? j : jf;
     }
 }
+// As scan_slots, but jf = the first EMPTY slot in cyclic order from `rot`
+// (0 <= rot < SPL): concurrent claimers of one bucket start their free-slot
+// search at different slots (placement is not observable).
+template <int SPL>
+__device__ __forceinline__ void scan_slots_rot(const uint64_t (&s)[SPL], uint32_t k, uint32_t rot, int& jm,
+                                               int& jf) {
+    jm = SPL;
+    uint32_t fm = 0;
+#pragma unroll
+    for (int j = SPL - 1; j >= 0; --j) {
+        const uint32_t key = key_of(s[j]);
+        jm = (key == k) ? j : jm;
+        fm |= (key == INVALID_KEY ? 1u : 0u) << j;
+    }
+    if (SPL == 1) {
+        jf = fm ? 0 : SPL;
+        return;
+    }
+    const uint32_t all = (1u << SPL) - 1u;
+    const uint32_t r = ((fm >> rot) | (fm << (SPL - rot))) & all;
+    jf = r ? (int)((__ffs(r) - 1 + rot) % SPL) : SPL;
+}
+// Lane `rot`-rotated first set bit of a G-bit group mask (-1 if none).
+template <int G>
+__device__ __forceinline__ int first_rot(uint32_t m, uint32_t rot) {
+    if (G == 1) return m ? 0 : -1;
+    constexpr uint32_t all = (G == 32) ? 0xFFFFFFFFu : ((1u << G) - 1u);
+    const uint32_t r = rot ? (((m >> rot) | (m << (G - rot))) & all) : m;
+    return r ? (int)((__ffs(r) - 1 + rot) % G) : -1;
+}
+
 // First slot holding k and its value (find path).
 template <int SPL>
 __device__ __forceinline__ int scan_value(const uint64_t (&s)[SPL], uint32_t k, uint32_t& v) {

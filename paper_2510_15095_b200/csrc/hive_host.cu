@@ -257,6 +257,7 @@ struct hive_table_s {
     // profiling
     struct Rec { const char* name; cudaEvent_t a, b; uint32_t launches; };
     bool prof = false;
+    bool step_prof = false;            // hive_profile level 2: clock64 step breakdown
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
     struct Agg { const char* name; double ms; uint64_t n; };
@@ -557,17 +558,17 @@ hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* 
             CK(cudaStreamWaitEvent(s, chunks->ready[c], 0));
             CK(launch_insert_fast(h->grids, s, keys, vals, nullptr, nullptr,
                                   std::min<uint64_t>(chunks->chunk, n_upper - off), nullptr, h->tv(), h->sv(),
-                                  dd, status, nullptr, h->left, (uint32_t)off));
+                                  dd, status, nullptr, h->left, (uint32_t)off, h->step_prof));
         }
     } else {
         Prof p(h, kvs ? "k_insert_fast(reinsert)" : "k_insert_fast", s);
         CK(launch_insert_fast(h->grids, s, keys, vals, kvs, idx, n_upper, n_dev, h->tv(),
-                              h->sv(), dd, status, vals_zero, h->left));
+                              h->sv(), dd, status, vals_zero, h->left, 0, h->step_prof));
     }
     {
         Prof p(h, kvs ? "k_insert_slow(reinsert)" : "k_insert_slow", s);
         CK(launch_insert_slow(h->grids, s, keys, vals, kvs, h->left, h->tv(), h->sv(),
-                              h->cfg.max_evictions, status));
+                              h->cfg.max_evictions, status, h->step_prof));
     }
     if (dedup && status) {
         Prof p(h, "k_dup_copy", s);
@@ -1305,6 +1306,7 @@ hive_status hive_stats(hive_t h, hive_stats_t* o) {
     for (int i = 0; i < 8; ++i) o->alg_bytes[i] = c.abytes[i];
     o->step3 = c.step3;
     o->xfail = c.xfail;
+    for (int i = 0; i < 4; ++i) o->step_cycles[i] = c.cyc[i];
     return c.failed ? HIVE_ESTASHFULL : c.xfail ? HIVE_EXCHANGE : HIVE_OK;
 }
 
@@ -1322,6 +1324,7 @@ hive_status hive_dump(hive_t h, uint32_t* d_keys, uint32_t* d_vals, uint64_t cap
 hive_status hive_profile(hive_t h, int enable) {
     if (!h) return HIVE_EINVAL;
     h->prof = enable != 0;
+    h->step_prof = enable >= 2;
     return HIVE_OK;
 }
 

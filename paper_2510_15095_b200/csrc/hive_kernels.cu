@@ -39,6 +39,28 @@ __device__ __forceinline__ unsigned long long warp_max(unsigned long long v) {
     }
     return v;
 }
+__device__ __forceinline__ long long warp_min_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long u = __shfl_xor_sync(FULL, v, o);
+        v = u < v ? u : v;
+    }
+    return v;
+}
+__device__ __forceinline__ long long warp_max_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long u = __shfl_xor_sync(FULL, v, o);
+        v = u > v ? u : v;
+    }
+    return v;
+}
+// Warp-granularity region time: max over lanes of the end clock
+// minus min over lanes of the start clock.
+__device__ __forceinline__ unsigned long long warp_span(long long t_start, long long t_end) {
+    return (unsigned long long)(warp_max_ll(t_end) - warp_min_ll(t_start));
+}
+
 // One global atomic per block for a per-thread counter.  Every thread of the
 // block must call it (kernel epilogue, after the grid-stride loop).
 __device__ __forceinline__ void block_add(unsigned long long* dst, unsigned long long v) {
@@ -214,10 +236,14 @@ __device__ __forceinline__ bool wabc_claim(const WarpGroup<G>& wg, uint64_t (&s)
 template <int G>
 __device__ __forceinline__ bool wabc_claim_issue(const WarpGroup<G>& wg, int jf, uint64_t* bucket, uint64_t kv,
                                                  bool want, bool& pend, uint64_t& pend_prev,
-                                                 uint32_t& pend_item, uint32_t item, uint32_t& ab) {
+                                                 uint32_t& pend_item, uint32_t item, uint32_t& ab,
+                                                 uint32_t lrot) {
     constexpr int SPL = WarpGroup<G>::SPL;
     const uint32_t F = wg.ballot(want && jf < SPL);
-    if (want && F && wg.gl == __ffs(F) - 1) {
+    // the claiming lane is the first lane with a free slot in cyclic order
+    // from a per-key rotation, so concurrent claimers of one bucket rarely
+    // race for the same slot (a lost claim costs a Step-3 round)
+    if (want && F && wg.gl == first_rot<G>(F, lrot)) {
         pend_prev = cas64(wg.slot_ptr(bucket) + jf, EMPTY, kv);
         pend = true;
         pend_item = item;
@@ -603,7 +629,7 @@ __device__ __forceinline__ bool owns(const WarpGroup<G>& wg, const DedupView& dd
 // after a resize: Step 1 is skipped (those keys are in no bucket)
 // and nothing is counted.
 // --------------------------------------------------------------------------------
-template <int G, int MINB>
+template <int G, int MINB, bool PROF = false>
 __global__ void __launch_bounds__(BLOCK, MINB)
 k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
               const uint64_t* __restrict__ kvs, const uint32_t* __restrict__ idx, uint64_t n,
@@ -642,8 +668,11 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             v_n = vals[op_n];
         }
     };
+    unsigned long long cyc1 = 0, cyc2 = 0;   // PROF: this warp's Step-1 / Step-2 cycles
     fetch(warp * WG::GPW + wg.gi);
     for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += stride) {
+        long long c0 = 0;
+        if constexpr (PROF) c0 = clock64();
         const uint64_t t = t0 + wg.gi;
         const bool active = t < n;
         const uint32_t op = op_n;                    // op indices < 2^32 (API contract)
@@ -651,11 +680,14 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         const uint32_t v = v_n;
         fetch(t + stride);
         bool valid = active && k != INVALID_KEY;
-        uint32_t b1 = 0, b2 = 0;
+        uint32_t b1 = 0, b2 = 0, h2 = 0;
         if (valid) {
             b1 = tv.addr(tv.h1(k));
-            b2 = tv.addr(tv.h2(k));
+            h2 = tv.h2(k);
+            b2 = tv.addr(h2);
         }
+        // per-key start of the free-slot search (lane, slot): independent of b1
+        const uint32_t lrot = (h2 >> 24) % G, srot = (h2 >> 27) % WG::SPL;
         bool two = valid && b2 != b1;
         const uint64_t fp = spill_fp(k);
         // one bucket view: b1, later overwritten by b2 (b1's scan results are
@@ -688,7 +720,7 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             // Step 1: b1 (one scan gives the match and the first free slot); then
             // -- only if b1's spill word allows k to live elsewhere -- b2 and the
             // stash.
-            if (valid) scan_slots<SPL>(sv_, k, jm1, jf1);
+            if (valid) scan_slots_rot<SPL>(sv_, k, srot, jm1, jf1);
             if (__any_sync(FULL, wg.ballot(jm1 < SPL) != 0))
                 done = wcme_cas<G>(wg, sv_, tv.bucket(b1), k, kv, valid, ab);
             const bool maybe = valid && !done && (spill_w & fp) == fp;
@@ -714,23 +746,27 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
                 done |= wg.bcast(sdone, 0);
             }
         }
+        long long c1 = 0;
+        if constexpr (PROF) {
+            c1 = clock64();
+        }
         // resolve the claim issued in the previous iteration (its CAS has had
         // this iteration's loads to come back); a lost claim goes to Step 3
         wl.push(pend && pend_prev != EMPTY, pend_item, leftover, &sv.ctrl->n_left);
         pend = false;
         // Step 2: optimistic WABC claim in b1, then b2 (first-fit, A-21); b2 is
         // read only if b1 is full.
-        if (place_only && valid) scan_slots<SPL>(sv_, INVALID_KEY, jm1, jf1);
+        if (place_only && valid) scan_slots_rot<SPL>(sv_, INVALID_KEY, srot, jm1, jf1);
         bool placed = wabc_claim_issue<G>(wg, jf1, tv.bucket(b1), kv, valid && !done, pend, pend_prev,
-                                          pend_item, op, ab);
+                                          pend_item, op, ab, lrot);
         const bool want2 = two && !done && !placed;
         if (__any_sync(FULL, want2)) {
             if (want2 && !have2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), sv_);
             if (want2 && !have2 && wg.gl == 0) ab += 256;
             int jm2, jf2 = SPL;
-            if (want2) scan_slots<SPL>(sv_, INVALID_KEY, jm2, jf2);
+            if (want2) scan_slots_rot<SPL>(sv_, INVALID_KEY, srot, jm2, jf2);
             const bool p2 = wabc_claim_issue<G>(wg, jf2, tv.bucket(b2), kv, want2, pend, pend_prev,
-                                                pend_item, op, ab);
+                                                pend_item, op, ab, lrot);
             if (p2 && wg.gl == 0) {
                 atomicOr((unsigned long long*)&tv.spill[b1], (unsigned long long)fp);
                 ab += 8;
@@ -743,11 +779,23 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             if (!done) ++added;
         }
         wl.push(left && wg.gl == 0, op, leftover, &sv.ctrl->n_left);
+        if constexpr (PROF) {
+            const long long c2 = clock64();
+            const unsigned long long s1 = warp_span(c0, c1), s2 = warp_span(c1, c2);
+            if (wg.lane == 0) {
+                cyc1 += s1;
+                cyc2 += s2;
+            }
+        }
     }
     wl.push(pend && pend_prev != EMPTY, pend_item, leftover, &sv.ctrl->n_left);
     wl.flush(leftover, &sv.ctrl->n_left);
     block_add(&sv.ctrl->count, added);
     block_add(&sv.ctrl->abytes[AB_INSERT], ab);
+    if constexpr (PROF) {
+        block_add(&sv.ctrl->cyc[0], cyc1);
+        block_add(&sv.ctrl->cyc[1], cyc2);
+    }
 
 }
 
@@ -759,7 +807,7 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
 // rotates with the round (reading A-6 allows any victim rule; placement is not
 // observable).
 // --------------------------------------------------------------------------------
-template <int G, int MINB>
+template <int G, int MINB, bool PROF = false>
 __global__ void __launch_bounds__(BLOCK, MINB)
 k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
               const uint64_t* __restrict__ kvs, const uint32_t* __restrict__ leftover,
@@ -805,7 +853,10 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     bool have = false;                       // s already holds bucket b (prefetched)
     uint64_t s[SPL];
     const uint32_t leaders = __ballot_sync(FULL, wg.gl == 0);
+    unsigned long long cyc3 = 0, cyc4 = 0;    // PROF: this warp's Step-3 / Step-4 cycles
     while (true) {
+        long long c0 = 0;
+        if constexpr (PROF) c0 = clock64();
         // ---- hand out work to idle groups ----
         const uint32_t idle = __ballot_sync(FULL, !busy && wg.gl == 0);
         if (drained && qa == qn && idle == leaders) break;
@@ -833,6 +884,10 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         if (qa == qn && !drained) refill();
         if (!__any_sync(FULL, busy)) {
             load_kv();
+            if constexpr (PROF) {
+                const unsigned long long sp = warp_span(c0, clock64());
+                if (lane == 0) cyc3 += sp;
+            }
             continue;
         }
         // ---- one round of Alg. 3 for every busy group ----
@@ -888,6 +943,8 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         }
         if (busy) ++r;
         const bool finish = busy && (placed || r >= max_evictions);
+        long long c1 = 0;
+        if constexpr (PROF) c1 = clock64();
         if (finish && wg.gl == 0) {
             depth = r > depth ? r : depth;
             if (placed) ++st3;
@@ -907,6 +964,21 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             }
         }
         if (finish) busy = false;
+        if constexpr (PROF) {
+            // the round is Step 3; the finish block is Step 4 when a group of
+            // this warp pushed its in-hand entry to the stash
+            const long long c2 = clock64();
+            const bool pushed = __any_sync(FULL, finish && !placed);
+            const unsigned long long s3 = warp_span(c0, c1), s4 = warp_span(c1, c2);
+            if (lane == 0) {
+                cyc3 += s3 + (pushed ? 0 : s4);
+                cyc4 += pushed ? s4 : 0;
+            }
+        }
+    }
+    if constexpr (PROF) {
+        block_add(&sv.ctrl->cyc[2], cyc3);
+        block_add(&sv.ctrl->cyc[3], cyc4);
     }
     block_add(&sv.ctrl->evictions, evict);
     block_add(&sv.ctrl->stash_pushes, pushes);
@@ -1578,8 +1650,13 @@ cudaError_t launch_insert_fast(const Grids& gr, cudaStream_t s, const uint32_t* 
                                const uint64_t* kvs, const uint32_t* idx, uint64_t n,
                                const uint64_t* n_dev, TableView tv, StashView sv, DedupView dd,
                                uint8_t* status, uint32_t* vals_zero, uint32_t* leftover,
-                               uint32_t op_base) {
+                               uint32_t op_base, bool prof) {
     const int grid = n_dev ? gr.insert_fast : clamp_grid(gr.insert_fast, n, BLOCK / gr.g_insert);
+    if (prof) {                               // step timing: the default geometry only
+        k_insert_fast<G_INSERT, MINB_DEFAULT, true><<<grid, BLOCK, 0, s>>>(keys, vals, kvs, idx, n, n_dev, tv, sv,
+                                                                           dd, status, vals_zero, leftover, op_base);
+        return cudaGetLastError();
+    }
 #define L_INS(G, MB) k_insert_fast<G, MB><<<grid, BLOCK, 0, s>>>(keys, vals, kvs, idx, n, n_dev, tv, sv, dd, \
                                                          status, vals_zero, leftover, op_base)
     HIVE_DISPATCH_GM(gr.g_insert, gr.minb, L_INS)
@@ -1588,7 +1665,12 @@ cudaError_t launch_insert_fast(const Grids& gr, cudaStream_t s, const uint32_t* 
 
 cudaError_t launch_insert_slow(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
                                const uint64_t* kvs, const uint32_t* leftover, TableView tv,
-                               StashView sv, uint32_t max_evictions, uint8_t* status) {
+                               StashView sv, uint32_t max_evictions, uint8_t* status, bool prof) {
+    if (prof) {
+        k_insert_slow<G_SLOW, MINB_DEFAULT, true><<<gr.insert_slow, BLOCK, 0, s>>>(keys, vals, kvs, leftover, tv, sv,
+                                                                                 max_evictions, status);
+        return cudaGetLastError();
+    }
 #define L_SLOW(G, MB) k_insert_slow<G, MB><<<gr.insert_slow, BLOCK, 0, s>>>(keys, vals, kvs, leftover, tv, sv, \
                                                                     max_evictions, status)
     HIVE_DISPATCH_GM(gr.g_slow, gr.minb, L_SLOW)

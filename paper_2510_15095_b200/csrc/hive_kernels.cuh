@@ -69,11 +69,11 @@ cudaError_t launch_insert_fast(const Grids& gr, cudaStream_t s, const uint32_t* 
                                const uint64_t* kvs, const uint32_t* idx, uint64_t n,
                                const uint64_t* n_dev, TableView tv, StashView sv, DedupView dd,
                                uint8_t* status, uint32_t* vals_zero, uint32_t* leftover,
-                               uint32_t op_base = 0);
+                               uint32_t op_base = 0, bool prof = false);
 
 cudaError_t launch_insert_slow(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
                                const uint64_t* kvs, const uint32_t* leftover, TableView tv,
-                               StashView sv, uint32_t max_evictions, uint8_t* status);
+                               StashView sv, uint32_t max_evictions, uint8_t* status, bool prof = false);
 
 cudaError_t launch_erase(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                          uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,

@@ -46,7 +46,7 @@ class HiveStats(ctypes.Structure):
             "count", "stash_used", "stash_cap", "evictions", "max_depth", "stash_pushes", "leftovers",
             "grows", "shrinks", "merge_aborts", "failed", "in_b1", "mapped_bytes")] + [
         ("alg_bytes", ctypes.c_uint64 * 8)] + [
-        ("step3", ctypes.c_uint64), ("xfail", ctypes.c_uint64)]
+        ("step3", ctypes.c_uint64), ("xfail", ctypes.c_uint64), ("step_cycles", ctypes.c_uint64 * 4)]
 
 
 # every exported symbol of include/hive.h, with its ctypes signature
@@ -280,6 +280,7 @@ class HiveTable:
             _check(rc, "hive_stats")
         d = {n: getattr(s, n) for n, _ in HiveStats._fields_}
         d["alg_bytes"] = dict(zip(("find", "insert", "evict", "erase", "elect"), list(s.alg_bytes)[:5]))
+        d["step_cycles"] = list(s.step_cycles)
         return d
 
     def dump(self):
@@ -297,8 +298,10 @@ class HiveTable:
                "hive_shard_info")
         return g.value, r.value, c.value
 
-    def profile(self, enable: bool = True):
-        _check(self._L.hive_profile(self._h, 1 if enable else 0), "hive_profile")
+    def profile(self, enable: bool | int = True):
+        """True / 1: per-kernel CUDA-event timing; 2: also the clock64 insertion
+        step breakdown (stats()["step_cycles"])."""
+        _check(self._L.hive_profile(self._h, int(enable)), "hive_profile")
 
     def profile_read(self, reset: bool = True) -> dict:
         m = 64

@@ -309,3 +309,29 @@ def test_grow_after_regressed_merge_abort():
         if hit >= 3:
             break
     assert hit >= 1
+
+
+def test_step_breakdown_tool():
+    """NEXT-2: the clock64 step breakdown of tools/step_breakdown.py
+    on a 2^14-bucket table.  Shares partition the total; Step 4 time appears only
+    in batches that stashed; Steps 1-2 dominate at low load; the instrumented
+    kernels give the same table as the plain ones (checked against the oracle)."""
+    import sys
+    sys.path.insert(0, "tools")
+    from step_breakdown import breakdown
+    rows = breakdown(1 << 14)
+    for r in rows:
+        assert abs(sum(r["share"]) - 1.0) < 1e-9 and all(c >= 0 for c in r["cycles"])
+        assert (r["cycles"][3] > 0) == (r["stashed"] > 0)
+        if r["leftovers"] == 0:
+            assert r["cycles"][2] == 0
+    low = [r for r in rows if r["lf_to"] <= 0.75]
+    assert all(r["share"][0] + r["share"][1] > 0.8 for r in low)
+    # instrumented insert == plain insert, against the oracle
+    p = _pair(1024 * 32, lf_grow=2.0, lf_shrink=0)
+    p.g.profile(2)
+    keys = gen.present_keys(int(0.96 * 1024 * 32))
+    p.insert(keys, gen.vals_of(np.arange(len(keys))))
+    p.g.profile(False)
+    sg, _ = p.check_state()
+    assert sum(sg["step_cycles"]) > 0
