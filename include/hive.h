@@ -223,6 +223,27 @@ hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys,
                        const uint32_t* d_vals, uint64_t n, uint32_t* d_vals_out,
                        uint8_t* d_result, void* stream);
 
+/* Monolithic concurrent mixed batch (the paper's
+ * single-kernel model): the whole batch runs in ONE
+ * cooperative kernel launch, finds, erases and inserts interleaved in the same
+ * pass (no opcode classification, no phases).  Arguments and result codes are
+ * those of hive_mixed.  Contract (differs from hive_mixed's PHASED order):
+ * per key, all insert ops of the batch form one insert group and all erase
+ * ops one erase group; each group takes effect as one atomic step (its owner,
+ * the highest op index, applies it; an insert group stores its owner's
+ * value) and every member reports the key's presence before that step; each
+ * find is its own atomic read.  The results are LINEARIZABLE per key: some
+ * order of {insert group, erase group, finds} explains every result and the
+ * final table.  Single-type batches therefore give exactly hive_insert /
+ * hive_erase / hive_find's results.  Evictions (Step 3) run at the tail of
+ * the same launch, after every find and erase, so no lookup observes an
+ * entry held by an eviction chain (reading A-16).  Growth before the batch
+ * and contraction after it follow hive_mixed's rule (one wait when growth or
+ * contraction is enabled).  n < 2^31.  HIVE_EINVAL on sharded handles. */
+hive_status hive_mixed_concurrent(hive_t h, const uint8_t* d_op, const uint32_t* d_keys,
+                                  const uint32_t* d_vals, uint64_t n, uint32_t* d_vals_out,
+                                  uint8_t* d_result, void* stream);
+
 /* Host-buffer variants (the end-to-end public path).  h_* are HOST pointers
  * (page-locked memory recommended; pageable works but serialises copies).
  * Stream-ordered like the device calls: the results are in the host buffers

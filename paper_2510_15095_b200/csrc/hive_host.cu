@@ -231,6 +231,7 @@ struct hive_table_s {
     uint8_t* flag2 = nullptr;  uint64_t flag2_cap = 0;
     uint64_t* erec = nullptr; uint64_t erec_cap = 0;     // election records (op << 32 | key)
     unsigned long long* ecount = nullptr;                // per-part counts + cursors
+    int mono_grid = 0;                                   // co-resident grid of k_mixed_mono
     uint64_t* einfo = nullptr;                           // per-part totals / bases
     uint32_t* left = nullptr; uint64_t left_cap = 0;
     uint32_t* cls = nullptr;  uint64_t cls_cap = 0;
@@ -1172,6 +1173,37 @@ hive_status hive_mixed(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
     h->last = s;
     if (h->sharded()) return shard_call(h, SK_MIXED, d_op, d_keys, d_vals, n, d_vals_out, d_result, s);
     return mixed_impl(h, d_op, d_keys, d_vals, n, nullptr, d_vals_out, d_result, s);
+}
+
+hive_status hive_mixed_concurrent(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, const uint32_t* d_vals,
+                                  uint64_t n, uint32_t* d_vals_out, uint8_t* d_result, void* stream) {
+    if (!h) return HIVE_EINVAL;
+    if (h->sharded()) return HIVE_EINVAL;
+    if (n == 0) return HIVE_OK;
+    if (!d_op || !d_keys || !d_vals || !d_vals_out || !d_result || n >= (1ull << 31)) return HIVE_EINVAL;
+    BusyGuard g(h);
+    if (!g.ok) return HIVE_EBUSY;
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last = s;
+    if (h->mono_grid == 0) h->mono_grid = mono_grid(h->num_sms);
+    if (h->cfg.lf_grow < 1.0f) {             // grow for the batch's inserts (one wait, as hive_mixed)
+        CK(launch_count_ops(s, d_op, n, 1, h->ecount));
+        CK(cudaMemcpyAsync(h->stage_h, h->ecount, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CKS(read_ctrl(h, s));
+        if (h->stage_h[0]) CKS(grow_known(h, h->ctrl_h->count, h->stage_h[0], s));
+    }
+    const uint64_t tab = pow2_at_least(std::max<uint64_t>(1024, 2 * n));
+    CKS(ensure(h->dd, h->dd_cap, tab));
+    CKS(ensure(h->flag, h->flag_cap, n));
+    CKS(ensure(h->owner, h->owner_cap, n));
+    CKS(ensure(h->left, h->left_cap, n));
+    CK(cudaMemsetAsync(&h->ctrl->n_left, 0, 2 * sizeof(uint64_t), s));     // n_left + slow_next
+    {
+        Prof p(h, "k_mixed_mono", s);
+        CK(launch_mixed_mono(h->mono_grid, s, d_op, d_keys, d_vals, n, h->tv(), h->sv(), h->dd, tab - 1, h->flag,
+                             h->owner, h->left, h->cfg.max_evictions, d_result, d_vals_out));
+    }
+    return shrink_after(h, s);
 }
 
 hive_status hive_insert_host(hive_t h, const uint32_t* h_keys, const uint32_t* h_vals, uint64_t n,

@@ -5,6 +5,7 @@
 // 256 B bucket is touched once per probe).  Persistent grid-stride kernels of
 // 256 threads; one operation per 8-lane group (4 slots = one 256-bit load per
 // lane), so each warp keeps four independent bucket probes in flight.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -13,6 +14,11 @@
 #include "hive_kernels.cuh"
 
 namespace hive {
+
+// Claim placement inside a bucket (placement is not observable): 0 = the
+// lowest free slot of the lowest lane with one (first-fit), 1 = a per-key
+// rotated lane, 2 = rotated lane and slot.  Set from HIVE_CLAIM_ROT.
+static __constant__ uint32_t c_claim_rot;
 
 // --------------------------------------------------------------------------------
 // small helpers
@@ -687,7 +693,9 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             b2 = tv.addr(h2);
         }
         // per-key start of the free-slot search (lane, slot): independent of b1
-        const uint32_t lrot = (h2 >> 24) % G, srot = (h2 >> 27) % WG::SPL;
+        // (c_claim_rot: 0 = lowest free, 1 = rotated lane, 2 = lane and slot)
+        const uint32_t lrot = c_claim_rot >= 1 ? (h2 >> 24) % G : 0u;
+        const uint32_t srot = c_claim_rot >= 2 ? (h2 >> 27) % WG::SPL : 0u;
         bool two = valid && b2 != b1;
         const uint64_t fp = spill_fp(k);
         // one bucket view: b1, later overwritten by b2 (b1's scan results are
@@ -720,7 +728,10 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             // Step 1: b1 (one scan gives the match and the first free slot); then
             // -- only if b1's spill word allows k to live elsewhere -- b2 and the
             // stash.
-            if (valid) scan_slots_rot<SPL>(sv_, k, srot, jm1, jf1);
+            if (valid) {
+                if (c_claim_rot >= 2) scan_slots_rot<SPL>(sv_, k, srot, jm1, jf1);
+                else scan_slots<SPL>(sv_, k, jm1, jf1);
+            }
             if (__any_sync(FULL, wg.ballot(jm1 < SPL) != 0))
                 done = wcme_cas<G>(wg, sv_, tv.bucket(b1), k, kv, valid, ab);
             const bool maybe = valid && !done && (spill_w & fp) == fp;
@@ -756,7 +767,10 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         pend = false;
         // Step 2: optimistic WABC claim in b1, then b2 (first-fit, A-21); b2 is
         // read only if b1 is full.
-        if (place_only && valid) scan_slots_rot<SPL>(sv_, INVALID_KEY, srot, jm1, jf1);
+        if (place_only && valid) {
+            if (c_claim_rot >= 2) scan_slots_rot<SPL>(sv_, INVALID_KEY, srot, jm1, jf1);
+            else scan_slots<SPL>(sv_, INVALID_KEY, jm1, jf1);
+        }
         bool placed = wabc_claim_issue<G>(wg, jf1, tv.bucket(b1), kv, valid && !done, pend, pend_prev,
                                           pend_item, op, ab, lrot);
         const bool want2 = two && !done && !placed;
@@ -764,7 +778,10 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             if (want2 && !have2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), sv_);
             if (want2 && !have2 && wg.gl == 0) ab += 256;
             int jm2, jf2 = SPL;
-            if (want2) scan_slots_rot<SPL>(sv_, INVALID_KEY, srot, jm2, jf2);
+            if (want2) {
+                if (c_claim_rot >= 2) scan_slots_rot<SPL>(sv_, INVALID_KEY, srot, jm2, jf2);
+                else scan_slots<SPL>(sv_, INVALID_KEY, jm2, jf2);
+            }
             const bool p2 = wabc_claim_issue<G>(wg, jf2, tv.bucket(b2), kv, want2, pend, pend_prev,
                                                 pend_item, op, ab, lrot);
             if (p2 && wg.gl == 0) {
@@ -807,11 +824,14 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
 // rotates with the round (reading A-6 allows any victim rule; placement is not
 // observable).
 // --------------------------------------------------------------------------------
-template <int G, int MINB, bool PROF = false>
-__global__ void __launch_bounds__(BLOCK, MINB)
-k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
-              const uint64_t* __restrict__ kvs, const uint32_t* __restrict__ leftover,
-              TableView tv, StashView sv, uint32_t max_evictions, uint8_t* __restrict__ status) {
+// The Step 3-4 work loop as a device function: k_insert_slow runs it alone,
+// the monolithic mixed kernel (k_mixed_mono) runs it as its eviction stage.
+// Every thread of the grid must call it (block-level counter reductions).
+template <int G, bool PROF>
+__device__ __forceinline__ void insert_slow_body(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                                 const uint64_t* __restrict__ kvs,
+                                                 const uint32_t* __restrict__ leftover, TableView tv, StashView sv,
+                                                 uint32_t max_evictions, uint8_t* __restrict__ status) {
     using WG = WarpGroup<G>;
     constexpr int SPL = WG::SPL;
     WG wg;
@@ -989,6 +1009,14 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
     block_add(&sv.ctrl->step3, st3);
 }
 
+template <int G, int MINB, bool PROF = false>
+__global__ void __launch_bounds__(BLOCK, MINB)
+k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+              const uint64_t* __restrict__ kvs, const uint32_t* __restrict__ leftover,
+              TableView tv, StashView sv, uint32_t max_evictions, uint8_t* __restrict__ status) {
+    insert_slow_body<G, PROF>(keys, vals, kvs, leftover, tv, sv, max_evictions, status);
+}
+
 // --------------------------------------------------------------------------------
 // ERASE (Alg. 4 ScanBucketAndDelete): WCME, winner CAS -> EMPTY;
 // b2 only on a miss; then the stash.
@@ -1073,6 +1101,242 @@ k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uin
     }
     block_add(&sv.ctrl->count, 0ull - removed);
     block_add(&sv.ctrl->abytes[AB_ERASE], ab);
+}
+
+// --------------------------------------------------------------------------------
+// NEXT-4: the monolithic concurrent mixed kernel (the paper's
+// single-kernel model).  One cooperative launch per mixed
+// batch; its stages are separated by grid-wide barriers:
+//   0. clear the per-batch group table and duplicate flags;
+//   1. per-key group election: all inserts of a key form one insert group and
+//      all erases one erase group; the highest op index of a group is its
+//      owner (A-15: without it, same-key inserts would both claim a slot);
+//   2. every op runs CONCURRENTLY in one pass, finds, erases and inserts
+//      interleaved in the same warps: finds read b1 (b2 / stash only when the
+//      spill word allows), group owners apply their group as ONE atomic
+//      operation (erase: CAS -> EMPTY; insert: replace CAS or a blocking
+//      claim CAS with the owner's value), inserts whose candidate buckets are
+//      both full go to the leftover list;
+//   3. bounded eviction + stash for the leftovers (Steps 3-4), i.e. AFTER
+//      every find and erase of the batch: no lookup can observe an entry in
+//      an eviction chain's hand (A-16), so no seqlock is needed;
+//   4. duplicates copy their group owner's result.
+// Contract (include/hive.h hive_mixed_concurrent): every op of a key takes
+// effect atomically in some order -- the batch is linearizable per key with
+// each group one atomic step whose members all report the presence before
+// the group.  Single-type batches therefore give exactly the PHASED results.
+// --------------------------------------------------------------------------------
+constexpr uint32_t MONO_ERASE_BIT = 0x80000000u;   // group class in the table word's op field
+__device__ __forceinline__ uint32_t mono_hash(uint32_t k, uint32_t cls) {
+    return fmix32(k ^ DEDUP_SEED ^ (cls ? 0x9E3779B9u : 0u));
+}
+// Owner (highest op) of the (k, cls) group; `self` if the table has no entry.
+__device__ __forceinline__ uint32_t mono_owner(const uint64_t* tab, uint64_t mask, uint32_t k, uint32_t cls,
+                                               uint32_t self) {
+    uint64_t h = mono_hash(k, cls) & mask;
+    const uint32_t tag = cls ? MONO_ERASE_BIT : 0u;
+    for (uint64_t probe = 0; probe <= mask; ++probe) {
+        const uint64_t e = tab[h];
+        if (e == EMPTY) return self;
+        if ((uint32_t)(e >> 32) == k && ((uint32_t)e & MONO_ERASE_BIT) == tag) return (uint32_t)e & ~MONO_ERASE_BIT;
+        h = (h + 1) & mask;
+    }
+    return self;
+}
+
+template <int G, int GS>
+__global__ void __launch_bounds__(BLOCK, 4)
+k_mixed_mono(const uint8_t* __restrict__ opc, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+             uint64_t n, TableView tv, StashView sv, uint64_t* __restrict__ tab, uint64_t tab_mask,
+             uint8_t* __restrict__ flag, uint32_t* __restrict__ owner_of, uint32_t* __restrict__ leftover,
+             uint32_t max_evictions, uint8_t* __restrict__ result, uint32_t* __restrict__ vals_out) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t tid = (uint64_t)blockIdx.x * BLOCK + threadIdx.x;
+    const uint64_t nthreads = (uint64_t)gridDim.x * BLOCK;
+    const int lane = threadIdx.x & 31;
+    // ---- stage 0: clear ----
+    for (uint64_t i = tid; i <= tab_mask; i += nthreads) tab[i] = EMPTY;
+    for (uint64_t i = tid; i < n; i += nthreads) flag[i] = 0;
+    grid.sync();
+    // ---- stage 1: group election (insert-if-absent, atomicMax keeps the max op) ----
+    uint32_t ab = 0;
+    for (uint64_t t0 = tid & ~31ull; t0 < n; t0 += nthreads) {
+        const uint64_t t = t0 + lane;
+        const uint32_t o = t < n ? opc[t] : 0u;
+        const uint32_t k = t < n ? keys[t] : INVALID_KEY;
+        const bool part = t < n && (o == 1 || o == 2) && k != INVALID_KEY;
+        const uint32_t cls = o == 2 ? 1u : 0u;
+        // lanes of this warp with the same (key, class): pre-reduce to the max op
+        const uint32_t grp = __match_any_sync(FULL, part ? ((uint64_t)k << 1 | cls) : ~0ull);
+        if (!part) continue;
+        if (__popc(grp) > 1) flag[t] = 1;
+        if ((31 - __clz(grp)) != lane) continue;
+        const uint64_t word = ((uint64_t)k << 32) | (cls ? MONO_ERASE_BIT : 0u) | (uint32_t)t;
+        uint64_t h = mono_hash(k, cls) & tab_mask;
+        for (uint64_t probe = 0; probe <= tab_mask; ++probe) {
+            const uint64_t prev = cas64(&tab[h], EMPTY, word);
+            ab += 32;
+            if (prev == EMPTY) break;
+            if ((prev >> 32) == k && (((uint32_t)prev & MONO_ERASE_BIT) != 0) == (cls != 0)) {
+                flag[t] = 1;
+                flag[(uint32_t)prev & ~MONO_ERASE_BIT] = 1;
+                if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
+                break;
+            }
+            h = (h + 1) & tab_mask;
+        }
+    }
+    grid.sync();
+    // ---- stage 2: all ops concurrently (one G-lane group per op) ----
+    {
+        using WG = WarpGroup<G>;
+        constexpr int SPL = WG::SPL;
+        __shared__ uint32_t lbuf[WARPS_PER_BLOCK][32];
+        WG wg;
+        WarpList wl{lbuf[threadIdx.x >> 5], 0};
+        const bool stash_on = sv.ctrl->stash_tail != 0;
+        unsigned long long added = 0, removed = 0;
+        const uint64_t warp = tid >> 5, nw = nthreads >> 5;
+        for (uint64_t base = warp * WG::GPW; base < n; base += nw * WG::GPW) {
+            const uint64_t t = base + wg.gi;
+            const bool active = t < n;
+            const uint32_t o = active ? opc[t] : 3u;
+            const uint32_t k = active ? keys[t] : INVALID_KEY;
+            const uint32_t v = active && o == 1 ? vals[t] : 0u;
+            bool valid = o < 3 && k != INVALID_KEY;
+            if (active && wg.gl == 0) {
+                vals_out[t] = 0;
+                if (!valid) result[t] = (o == 1) ? 2 : 0;        // reserved key / unknown opcode
+                ab += 4 + 1 + 1 + 4 + (o == 1 ? 4 : 0);
+            }
+            // group members other than the owner only copy its result (stage 4)
+            uint32_t own = (uint32_t)t;
+            if (valid && o != 0 && wg.gl == 0 && flag[t]) {
+                own = mono_owner(tab, tab_mask, k, o == 2 ? 1u : 0u, (uint32_t)t);
+                owner_of[t] = own;
+            }
+            if (wg.bcast(own, 0) != (uint32_t)t) valid = false;
+            const bool is_find = valid && o == 0, is_ins = valid && o == 1, is_era = valid && o == 2;
+            uint32_t b1 = 0, b2 = 0, h2 = 0;
+            if (valid) {
+                b1 = tv.addr(tv.h1(k));
+                h2 = tv.h2(k);
+                b2 = tv.addr(h2);
+            }
+            const uint32_t lrot = c_claim_rot >= 1 ? (h2 >> 24) % G : 0u;
+            const uint32_t srot = c_claim_rot >= 2 ? (h2 >> 27) % SPL : 0u;
+            const uint64_t fp = spill_fp(k), kv = pack(k, v);
+            // one bucket view (b1, later possibly b2), as in k_insert_fast
+            uint64_t sl[SPL];
+            uint64_t spill_w = 0;
+            int jm1 = SPL, jf1 = SPL;
+            if (valid) {
+                load_slots<SPL>(wg.slot_ptr(tv.bucket(b1)), sl);
+                spill_w = tv.spill[b1];
+                if (wg.gl == 0) ab += 256 + 8;
+                scan_slots_rot<SPL>(sl, k, srot, jm1, jf1);
+            } else {
+                fill_empty<SPL>(sl);
+            }
+            // WCME on b1: finds read, erase / insert owners CAS the match
+            uint32_t val = 0;
+            bool done = wcme_value<G>(wg, sl, k, is_find, &val);
+            if (__any_sync(FULL, (is_ins || is_era) && jm1 < SPL))
+                done |= wcme_cas<G>(wg, sl, tv.bucket(b1), k, is_era ? EMPTY : kv, is_ins || is_era, ab);
+            const bool maybe = valid && !done && (spill_w & fp) == fp;
+            const bool need2 = maybe && b2 != b1;
+            bool have2 = false;
+            if (__any_sync(FULL, need2)) {
+                if (need2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), sl);
+                else fill_empty<SPL>(sl);
+                if (need2 && wg.gl == 0) ab += 256;
+                have2 = need2;
+                done |= wcme_value<G>(wg, sl, k, need2 && is_find, &val);
+                done |= wcme_cas<G>(wg, sl, tv.bucket(b2), k, is_era ? EMPTY : kv, need2 && !is_find, ab);
+            }
+            if (stash_on) {
+                bool sdone = false;
+                uint32_t sval = 0;
+                if (maybe && !done && wg.gl == 0) {
+                    uint64_t sw;
+                    ab += 16;
+                    int64_t pos = stash_lookup(sv, k, &sw);
+                    if (is_find) {
+                        if (pos >= 0) { sdone = true; sval = val_of(sw); }
+                    } else {
+                        while (pos >= 0) {
+                            const uint64_t prev = cas64(&sv.ring[pos], sw, is_era ? EMPTY : kv);
+                            if (prev == sw) { sdone = true; break; }
+                            pos = stash_lookup(sv, k, &sw);
+                        }
+                    }
+                }
+                sdone = wg.bcast(sdone, 0);
+                sval = wg.bcast(sval, 0);
+                if (sdone && is_find) val = sval;
+                done |= sdone;
+            }
+            // inserts of absent keys: claim in b1 at the slot the Step-1 scan
+            // found free (rotated lane / slot), checked at once; a lost claim
+            // re-reads b1 and claims by the WABC loop; then b2 (first-fit, A-21)
+            const bool want1 = is_ins && !done;
+            bool placed = false;
+            {
+                const uint32_t F = wg.ballot(want1 && jf1 < SPL);
+                bool ok = false;
+                if (want1 && F && wg.gl == first_rot<G>(F, lrot)) {
+                    ok = cas64(wg.slot_ptr(tv.bucket(b1)) + jf1, EMPTY, kv) == EMPTY;
+                    ab += 32;
+                }
+                placed = wg.ballot(ok) != 0;
+                const bool retry = want1 && F != 0 && !placed;
+                if (__any_sync(FULL, retry)) {
+                    if (retry) load_slots<SPL>(wg.slot_ptr(tv.bucket(b1)), sl);
+                    else fill_empty<SPL>(sl);
+                    if (retry && wg.gl == 0) ab += 256;
+                    have2 = false;
+                    placed |= wabc_claim<G>(wg, sl, tv.bucket(b1), kv, retry, ab);
+                }
+            }
+            const bool want2 = want1 && !placed && b2 != b1;
+            if (__any_sync(FULL, want2)) {
+                if (want2 && !have2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), sl);
+                else if (!want2) fill_empty<SPL>(sl);
+                if (want2 && !have2 && wg.gl == 0) ab += 256;
+                const bool p2 = wabc_claim<G>(wg, sl, tv.bucket(b2), kv, want2, ab);
+                if (p2 && wg.gl == 0) {
+                    atomicOr((unsigned long long*)&tv.spill[b1], (unsigned long long)fp);
+                    ab += 8;
+                }
+                placed |= p2;
+            }
+            if (valid && wg.gl == 0) {
+                if (is_find) {
+                    result[t] = done ? 1 : 0;
+                    vals_out[t] = done ? val : 0u;
+                } else {
+                    result[t] = done ? 1 : 0;                 // presence before the group
+                    if (is_ins && !done) ++added;
+                    if (is_era && done) ++removed;
+                }
+            }
+            wl.push(want1 && !placed && wg.gl == 0, (uint32_t)t, leftover, &sv.ctrl->n_left);
+        }
+        wl.flush(leftover, &sv.ctrl->n_left);
+        block_add(&sv.ctrl->count, added - removed);
+    }
+    block_add(&sv.ctrl->abytes[AB_INSERT], ab);
+    grid.sync();
+    // ---- stage 3: Steps 3-4 for the leftovers, after every find and erase ----
+    insert_slow_body<GS, false>(keys, vals, nullptr, leftover, tv, sv, max_evictions, result);
+    grid.sync();
+    // ---- stage 4: group members copy their owner's result ----
+    for (uint64_t t = tid; t < n; t += nthreads)
+        if (flag[t] && opc[t] != 0 && keys[t] != INVALID_KEY) {
+            const uint32_t own = owner_of[t];
+            if (own != (uint32_t)t) result[t] = result[own];
+        }
 }
 
 // Duplicates copy their owner's outcome (PHASED contract, A-17).
@@ -1592,6 +1856,8 @@ cudaError_t init_hash_tables() {
     }
     cudaError_t e = cudaMemcpyToSymbol(c_crc32_tab, t32, sizeof(t32));
     if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_crc64_tab, t64, sizeof(t64));
+    const uint32_t rot = getenv("HIVE_CLAIM_ROT") ? (uint32_t)atoi(getenv("HIVE_CLAIM_ROT")) : CLAIM_ROT_DEFAULT;
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_claim_rot, &rot, sizeof(rot));
     return e;
 }
 
@@ -1684,6 +1950,37 @@ cudaError_t launch_erase(const Grids& gr, cudaStream_t s, const uint32_t* keys, 
 #define L_ERA(G, MB) k_erase<G, MB><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, dd, erased, vals_zero)
     HIVE_DISPATCH_GM(gr.g_erase, gr.minb, L_ERA)
     return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(BLOCK)
+k_count_ops(const uint8_t* __restrict__ ops, uint64_t n, uint8_t code, unsigned long long* __restrict__ out) {
+    unsigned long long c = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (uint64_t)gridDim.x * BLOCK)
+        c += ops[i] == code;
+    block_add(out, c);
+}
+cudaError_t launch_count_ops(cudaStream_t s, const uint8_t* ops, uint64_t n, uint8_t code,
+                             unsigned long long* out) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    k_count_ops<<<clamp_grid(148 * 4, n, BLOCK), BLOCK, 0, s>>>(ops, n, code, out);
+    return cudaGetLastError();
+}
+
+int mono_grid(int num_sms) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)k_mixed_mono<G_INSERT, G_SLOW>, BLOCK, 0);
+    return (nb > 0 ? nb : 1) * num_sms;
+}
+
+cudaError_t launch_mixed_mono(int grid, cudaStream_t s, const uint8_t* ops, const uint32_t* keys,
+                              const uint32_t* vals, uint64_t n, TableView tv, StashView sv, uint64_t* tab,
+                              uint64_t tab_mask, uint8_t* flag, uint32_t* owner_of, uint32_t* leftover,
+                              uint32_t max_evictions, uint8_t* result, uint32_t* vals_out) {
+    void* args[] = {(void*)&ops, (void*)&keys, (void*)&vals, (void*)&n, (void*)&tv, (void*)&sv, (void*)&tab,
+                    (void*)&tab_mask, (void*)&flag, (void*)&owner_of, (void*)&leftover, (void*)&max_evictions,
+                    (void*)&result, (void*)&vals_out};
+    return cudaLaunchCooperativeKernel((const void*)k_mixed_mono<G_INSERT, G_SLOW>, grid, BLOCK, args, 0, s);
 }
 
 cudaError_t launch_dup_copy(int grid, cudaStream_t s, const uint32_t* idx, uint64_t n,

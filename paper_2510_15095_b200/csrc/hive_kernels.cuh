@@ -18,6 +18,7 @@ constexpr int MINB_DEFAULT = 4;          // 4 blocks/SM => <= 64 registers (ncu:
 constexpr int PART_CHUNK = 8192;         // max elements per warp in the stable partition
 constexpr int PART_UNROLL = 4;           // rows of 32 elements whose loads are in flight together
 constexpr int MAX_PARTS = 64;
+constexpr uint32_t CLAIM_ROT_DEFAULT = 1;   // claim placement (hive_kernels.cu c_claim_rot)
 
 enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1, PART_ELECT = 2, PART_ROUTE_KEYS = 3, PART_ROUTE_P2P = 4,
                 PART_ROUTE_PAD = 5 };
@@ -78,6 +79,18 @@ cudaError_t launch_insert_slow(const Grids& gr, cudaStream_t s, const uint32_t* 
 cudaError_t launch_erase(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                          uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
                          DedupView dd, uint8_t* erased, uint32_t* vals_zero);
+
+// NEXT-4 monolithic concurrent mixed kernel (one cooperative launch).
+// tab: the per-batch group table (tab_mask + 1 words, a power of two >= 2n);
+// flag uint8[n], owner_of / leftover uint32[n]; ctrl n_left and slow_next
+// must be zero.  mono_grid: the co-resident grid for this device.
+int mono_grid(int num_sms);
+cudaError_t launch_mixed_mono(int grid, cudaStream_t s, const uint8_t* ops, const uint32_t* keys,
+                              const uint32_t* vals, uint64_t n, TableView tv, StashView sv, uint64_t* tab,
+                              uint64_t tab_mask, uint8_t* flag, uint32_t* owner_of, uint32_t* leftover,
+                              uint32_t max_evictions, uint8_t* result, uint32_t* vals_out);
+cudaError_t launch_count_ops(cudaStream_t s, const uint8_t* ops, uint64_t n, uint8_t code,
+                             unsigned long long* out);
 
 cudaError_t launch_dup_copy(int grid, cudaStream_t s, const uint32_t* idx, uint64_t n,
                             const uint64_t* n_dev, DedupView dd, uint8_t* out);

@@ -59,6 +59,7 @@ SIGNATURES = {
     "hive_find": (_int, [_vp, _vp, _u64, _vp, _vp, _vp]),
     "hive_erase": (_int, [_vp, _vp, _u64, _vp, _vp]),
     "hive_mixed": (_int, [_vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp]),
+    "hive_mixed_concurrent": (_int, [_vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp]),
     "hive_clear": (_int, [_vp, _vp]),
     "hive_insert_host": (_int, [_vp, _vp, _vp, _u64, _vp, _vp]),
     "hive_find_host": (_int, [_vp, _vp, _u64, _vp, _vp, _vp]),
@@ -233,6 +234,20 @@ class HiveTable:
             result = torch.empty(n, dtype=torch.uint8, device=keys.device)
         _check(self._L.hive_mixed(self._h, _p(ops), _p(keys), _p(vals), n, _p(vals_out), _p(result),
                                   _stream(stream)), "hive_mixed")
+        return vals_out, result
+
+    def mixed_concurrent(self, ops: torch.Tensor, keys: torch.Tensor, vals: torch.Tensor, vals_out=None,
+                         result=None, stream=None):
+        """hive_mixed_concurrent: the whole batch in one cooperative launch,
+        linearizable per key (include/hive.h)."""
+        ops, keys, vals = _dev(ops, 1), _dev(keys, 4), _dev(vals, 4)
+        n = keys.numel()
+        if vals_out is None:
+            vals_out = torch.empty(n, dtype=torch.uint32, device=keys.device)
+        if result is None:
+            result = torch.empty(n, dtype=torch.uint8, device=keys.device)
+        _check(self._L.hive_mixed_concurrent(self._h, _p(ops), _p(keys), _p(vals), n, _p(vals_out), _p(result),
+                                             _stream(stream)), "hive_mixed_concurrent")
         return vals_out, result
 
     # ---- end-to-end variants: host tensors in, host tensors out -----------------------

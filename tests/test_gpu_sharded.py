@@ -38,7 +38,7 @@ def test_sharded_handle_world1_vs_oracle(pg, grow):
     from paper_2510_15095_b200 import u8, u32
     from paper_2510_15095_b200.sharded import ShardedHive
     cfg = dict(resize_k=16) if grow else dict(lf_grow=2.0, lf_shrink=0)
-    sh = ShardedHive(256 * 32 if grow else 2048 * 32, batch_max=40000, **cfg)
+    sh = ShardedHive(256 * 32 if grow else 2048 * 32, batch_max=60000, **cfg)
     o = oracle.OracleTable(256 * 32 if grow else 2048 * 32, **cfg)
     assert sh.table.shard_info()[:2] == (1, 0)
     rng = np.random.default_rng(9)
