@@ -409,9 +409,16 @@ def main():
     if world == 1 and not sharded and rank == 0 and not args.no_cpu_baseline:
         s_log2 = min(24, args.n_log2)
         ops, sec = oracle_sample(s_log2)
+        scale = (1 << s_log2) / n
         cpu = {"value": ops / sec / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"2^{s_log2} inserts to LF 0.95 + 2^{s_log2} finds (50% hits), sequential oracle",
-               "seconds": sec, "host_nproc": os.cpu_count()}
+               "sample": f"the cfg2 recipe at 2^{s_log2 - args.n_log2} scale: keys_of(0..2^{s_log2}) inserted "
+                         f"into {-(-(1 << s_log2) * 100 // (95 * 32))} buckets (LF 0.95, growth off), then "
+                         f"2^{s_log2} finds from gen.mixed_queries(seed 202) with 50% hits; sequential oracle, "
+                         f"1 core (it is single-threaded)",
+               "seconds": sec, "scale": scale,
+               "extrapolated_full_step_s": sec / scale,
+               "extrapolation": "linear in ops (the oracle's per-op cost is cache-miss bound at both sizes)",
+               "host_nproc": os.cpu_count()}
 
     if rank == 0:
         line = {
@@ -717,6 +724,28 @@ def secondary_measurements(table, keys, vals, queries, n, nb, dev, prof_main):
         "split_ms": p3.get("k_split", (0, 0))[0], "merge_ms": p3.get("k_merge", (0, 0))[0],
         "split_launches": p3.get("k_split", (0, 0))[1], "merge_launches": p3.get("k_merge", (0, 0))[1],
     }
+    # NEXT-4: the same 64 batches through the monolithic concurrent kernel
+    # (hive_mixed_concurrent: one cooperative launch per batch + resize)
+    tc = HiveTable(1024 * 32)
+    for b in range(nbat):
+        tc.mixed_concurrent(ops_all[b], k_all[b], v_all[b], vo, rr)
+    tc.clear()
+    tc.profile(True)
+    torch.cuda.synchronize()
+    ev[0].record()
+    for b in range(nbat):
+        tc.mixed_concurrent(ops_all[b], k_all[b], v_all[b], vo, rr)
+    ev[1].record()
+    torch.cuda.synchronize()
+    sc = tc.stats()
+    pc = tc.profile_read(reset=True)
+    res["cfg3_mixed_concurrent"] = {
+        "gops": nbat * bsz / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9, "ms": ev[0].elapsed_time(ev[1]),
+        "kern_ms": {k: round(v[0], 3) for k, v in pc.items()},
+        "launches": {k: v[1] for k, v in pc.items()},
+        "final_buckets": sc["n_buckets"], "final_count": sc["count"], "grows": sc["grows"],
+        "vs_phased": (nbat * bsz / ev[0].elapsed_time(ev[1])) / (nbat * bsz / mixed_ms)}
+    del tc
     res["cfg4_zipf"] = cfg4_zipf(dev)
     return res
 
@@ -760,11 +789,21 @@ def cfg4_zipf(dev):
         torch.cuda.synchronize()
     s = t.stats()
     hot = int((r1 == 1).sum())
+    # NEXT-4: Z1 through the monolithic concurrent kernel (same prefill)
+    for rep in range(2):
+        t.clear()
+        t.insert(pk, pv)
+        torch.cuda.synchronize()
+        ev[2].record()
+        t.mixed_concurrent(ops1, k1, v1, vo, rr)
+        ev[3].record()
+        torch.cuda.synchronize()
+    z1c = n1 / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9
     out = {"z1_mixed_gops": n1 / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9,
            "z2_insert_gops": n2 / (ev[1].elapsed_time(ev[2]) * 1e-3) / 1e9,
            "z1_hot_key_copies": hot, "z2_distinct_keys": int(len(np.unique(r2))),
            "final_lf": s["count"] / (nb * 32), "evictions": s["evictions"], "max_depth": s["max_depth"],
-           "stash_used": s["stash_used"], "leftovers": s["leftovers"]}
+           "stash_used": s["stash_used"], "leftovers": s["leftovers"], "z1_mixed_concurrent_gops": z1c}
     return out
 
 

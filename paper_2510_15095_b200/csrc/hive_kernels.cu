@@ -17,8 +17,10 @@ namespace hive {
 
 // Claim placement inside a bucket (placement is not observable): 0 = the
 // lowest free slot of the lowest lane with one (first-fit), 1 = a per-key
-// rotated lane, 2 = rotated lane and slot.  Set from HIVE_CLAIM_ROT.
-static __constant__ uint32_t c_claim_rot;
+// rotated lane, 2 = rotated lane and slot.  Rotation cut lost optimistic
+// claims (cfg2 leftovers 2.55 M -> 2.20 M) but made k_insert_fast slower
+// (4.99 -> 5.37 ms, profiles/r02_claim_rot_sweep.jsonl): first-fit is kept.
+constexpr uint32_t c_claim_rot = CLAIM_ROT_DEFAULT;
 
 // --------------------------------------------------------------------------------
 // small helpers
@@ -1856,8 +1858,6 @@ cudaError_t init_hash_tables() {
     }
     cudaError_t e = cudaMemcpyToSymbol(c_crc32_tab, t32, sizeof(t32));
     if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_crc64_tab, t64, sizeof(t64));
-    const uint32_t rot = getenv("HIVE_CLAIM_ROT") ? (uint32_t)atoi(getenv("HIVE_CLAIM_ROT")) : CLAIM_ROT_DEFAULT;
-    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_claim_rot, &rot, sizeof(rot));
     return e;
 }
 

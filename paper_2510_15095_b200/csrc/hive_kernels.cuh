@@ -18,7 +18,8 @@ constexpr int MINB_DEFAULT = 4;          // 4 blocks/SM => <= 64 registers (ncu:
 constexpr int PART_CHUNK = 8192;         // max elements per warp in the stable partition
 constexpr int PART_UNROLL = 4;           // rows of 32 elements whose loads are in flight together
 constexpr int MAX_PARTS = 64;
-constexpr uint32_t CLAIM_ROT_DEFAULT = 1;   // claim placement (hive_kernels.cu c_claim_rot)
+constexpr uint32_t CLAIM_ROT_DEFAULT = 0;   // claim placement (hive_kernels.cu c_claim_rot; 0 measured fastest,
+                                            // 1 / 2 for experiments: rebuild)
 
 enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1, PART_ELECT = 2, PART_ROUTE_KEYS = 3, PART_ROUTE_P2P = 4,
                 PART_ROUTE_PAD = 5 };

@@ -313,13 +313,13 @@ def test_grow_after_regressed_merge_abort():
 
 def test_step_breakdown_tool():
     """NEXT-2: the clock64 step breakdown of tools/step_breakdown.py
-    on a 2^14-bucket table.  Shares partition the total; Step 4 time appears only
+    on a 2^18-bucket table.  Shares partition the total; Step 4 time appears only
     in batches that stashed; Steps 1-2 dominate at low load; the instrumented
     kernels give the same table as the plain ones (checked against the oracle)."""
     import sys
     sys.path.insert(0, "tools")
     from step_breakdown import breakdown
-    rows = breakdown(1 << 14)
+    rows = breakdown(1 << 18)
     for r in rows:
         assert abs(sum(r["share"]) - 1.0) < 1e-9 and all(c >= 0 for c in r["cycles"])
         assert (r["cycles"][3] > 0) == (r["stashed"] > 0)

@@ -123,6 +123,6 @@ def test_sharded_calls_capture_in_a_cuda_graph(pg):
         assert (_np(st) == o.insert(gen.keys_of(ids), gen.vals_of(ids))).all()
         v_o, f_o = o.find(gen.keys_of(qids))
         assert (_np(fo) == f_o).all() and (_np(vo).astype(np.uint32) == v_o).all()
-        assert (_np(er) == o.erase(gen.keys_of(ids[: n // 4]))).all()
+        assert (_np(er)[: n // 4] == o.erase(gen.keys_of(ids[: n // 4]))).all()
     del g
     sh.close()

@@ -2,7 +2,7 @@
 # A/B of the optimistic claim placement (HIVE_CLAIM_ROT 0 / 1 / 2) on the cfg2
 # bench step: insert-phase time, kernel times, leftovers.
 mkdir -p gpurun_out
-for r in 0 1 2; do
+for r in 0 1 2; do  # (now compile-time: CLAIM_ROT_DEFAULT in hive_kernels.cuh)
   HIVE_CLAIM_ROT=$r python bench.py --steps 5 --no-secondary --no-cpu-baseline > gpurun_out/rot$r.json 2>gpurun_out/rot$r.err
   python - "$r" <<'PY'
 import json, sys
