@@ -130,6 +130,8 @@ typedef struct {
                                 Step-2 placements = new keys - leftovers      */
     uint64_t xfail;          /* sharded: ops of this rank not processed
                                 because their exchange region was full        */
+    uint64_t elect_overflow; /* owner-election table overflows (must be 0: the
+                                tables hold 2.5x the mean part size)          */
     uint64_t step_cycles[4]; /* insertion step breakdown,
                                 collected while hive_profile level 2 is on:
                                 warp clock64() cycles in Step 1 (replace),

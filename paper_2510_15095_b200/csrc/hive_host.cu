@@ -230,6 +230,9 @@ struct hive_table_s {
     uint32_t* owner2 = nullptr; uint64_t owner2_cap = 0;
     uint8_t* flag2 = nullptr;  uint64_t flag2_cap = 0;
     uint64_t* erec = nullptr; uint64_t erec_cap = 0;     // election records (op << 32 | key)
+    uint32_t* rvals = nullptr; uint64_t rvals_cap = 0;   // fused insert: values in record order
+    uint64_t* ftab = nullptr; uint64_t ftab_cap = 0;     // fused insert: the two epoch-tagged tables
+    int fused_grid = 0;                                  // co-resident grid of k_insert_fused
     unsigned long long* ecount = nullptr;                // per-part counts + cursors
     int mono_grid = 0;                                   // co-resident grid of k_mixed_mono
     uint64_t* einfo = nullptr;                           // per-part totals / bases
@@ -541,12 +544,47 @@ struct InsertChunks {
     const cudaEvent_t* ready;
 };
 
+// The INSERT phase as ONE cooperative launch (k_insert_fused): the ops are
+// hash-partitioned with their values, then each part's owner election
+// overlaps the previous part's fast path, followed by Steps 3-4 and the
+// duplicate fix-up.  Used for large phases with owner election on.
+hive_status insert_phase_fused(hive_table_s* h, const uint32_t* keys, const uint32_t* vals, const uint32_t* idx,
+                               uint64_t n_upper, const uint64_t* n_dev, uint64_t n_batch, uint8_t* status,
+                               uint32_t* vals_zero, cudaStream_t s) {
+    const uint64_t per = pow2_at_least(std::max<uint64_t>(1024, (uint64_t)(2.5 * (double)n_upper / FUSED_PARTS)));
+    CKS(ensure(h->ftab, h->ftab_cap, 2 * per));
+    CKS(ensure(h->owner, h->owner_cap, n_batch));
+    CKS(ensure(h->flag, h->flag_cap, n_batch));
+    CKS(ensure(h->erec, h->erec_cap, n_upper));
+    CKS(ensure(h->rvals, h->rvals_cap, n_upper));
+    CKS(ensure(h->left, h->left_cap, std::max<uint64_t>(n_upper, 1)));
+    if (!h->fused_grid) h->fused_grid = fused_grid(h->num_sms);
+    CK(cudaMemsetAsync(h->flag, 0, n_batch, s));
+    CK(cudaMemsetAsync(h->ftab, 0x04, per * sizeof(uint64_t), s));          // epoch 1: stale for even parts
+    CK(cudaMemsetAsync(h->ftab + per, 0x00, per * sizeof(uint64_t), s));    // epoch 0: stale for odd parts
+    {
+        Prof p(h, "k_elect_partition", s, 3);
+        CK(launch_elect_partition(s, keys, idx, n_upper, n_dev, FUSED_PARTS, h->ecount, h->ecount + MAX_PARTS,
+                                  h->einfo, h->erec, h->num_sms, vals, h->rvals, status, vals_zero));
+    }
+    CK(cudaMemsetAsync(&h->ctrl->n_left, 0, 2 * sizeof(uint64_t), s));     // n_left + slow_next
+    Prof p(h, "k_insert_fused", s);
+    CK(launch_insert_fused(h->fused_grid, s, h->erec, h->rvals, h->einfo, h->ftab, h->ftab + per, per - 1,
+                           DedupView{h->ftab, per - 1, h->flag, h->owner, FUSED_PARTS}, h->tv(), h->sv(), status,
+                           vals_zero, h->left, h->cfg.max_evictions, keys, vals));
+    return HIVE_OK;
+}
+
 hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* vals,
                          const uint64_t* kvs, const uint32_t* idx, uint64_t n_upper,
                          const uint64_t* n_dev, uint64_t n_batch, uint8_t* status,
                          uint32_t* vals_zero, cudaStream_t s, const InsertChunks* chunks = nullptr,
                          const DedupView* pre = nullptr) {
     const bool dedup = !kvs && h->dedup_on();
+    // large phases with election: the fused single-launch form (HIVE_FUSED=0: the multi-launch form)
+    static const bool fused_ok = !getenv("HIVE_FUSED") || atoi(getenv("HIVE_FUSED")) != 0;
+    if (dedup && fused_ok && !pre && !chunks && !h->step_prof && n_upper >= FUSED_MIN_OPS)
+        return insert_phase_fused(h, keys, vals, idx, n_upper, n_dev, n_batch, status, vals_zero, s);
     DedupView dd{nullptr, 0, nullptr, nullptr};
     if (dedup && pre) dd = *pre;                 // election already enqueued by the caller
     else if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
@@ -1099,7 +1137,7 @@ hive_status hive_destroy(hive_t h) {
     vrange_free(h->ix);
     vrange_free(h->dr);
     vrange_free(h->sp);
-    void* bufs[] = {h->ctrl, h->dd, h->owner, h->flag, h->dd2, h->owner2, h->flag2, h->left, h->cls, h->cnt, h->pinfo, h->aborts,
+    void* bufs[] = {h->ctrl, h->rvals, h->ftab, h->dd, h->owner, h->flag, h->dd2, h->owner2, h->flag2, h->left, h->cls, h->cnt, h->pinfo, h->aborts,
                     h->erec, h->ecount, h->einfo, h->hk, h->hv, h->hst, h->fq, h->fv, h->ff};
     for (auto e : h->pipe_ev) cudaEventDestroy(e);
     if (h->ins_free) cudaEventDestroy(h->ins_free);
@@ -1338,6 +1376,7 @@ hive_status hive_stats(hive_t h, hive_stats_t* o) {
     for (int i = 0; i < 8; ++i) o->alg_bytes[i] = c.abytes[i];
     o->step3 = c.step3;
     o->xfail = c.xfail;
+    o->elect_overflow = c.eover;
     for (int i = 0; i < 4; ++i) o->step_cycles[i] = c.cyc[i];
     return c.failed ? HIVE_ESTASHFULL : c.xfail ? HIVE_EXCHANGE : HIVE_OK;
 }

@@ -515,18 +515,25 @@ __global__ void k_elect_bases(const unsigned long long* __restrict__ gcount, uin
 // memory grouped by part, one global reservation per (tile, part), then a
 // coalesced copy-out (consecutive threads write consecutive records of a
 // part's run).  Part and rank share one register (rank < 2^16, part < 2^7).
+// WITH_VALS (the fused insert path): the op's value is staged and written
+// beside its record (rvals, same order), and ops with the reserved key -- in
+// no part -- get status 2 / value-out 0 here.
+template <bool WITH_VALS>
 __global__ void __launch_bounds__(BLOCK, 4)
 k_elect_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
                 const uint64_t* __restrict__ n_dev, uint32_t n_parts, unsigned long long* __restrict__ cursor,
-                uint64_t* __restrict__ recs) {
+                uint64_t* __restrict__ recs, const uint32_t* __restrict__ vals, uint32_t* __restrict__ rvals,
+                uint8_t* __restrict__ status, uint32_t* __restrict__ vals_zero) {
     __shared__ unsigned int hist[MAX_PARTS];
     __shared__ unsigned int loff[MAX_PARTS + 1];
     __shared__ unsigned long long gbase[MAX_PARTS];
-    __shared__ uint64_t stage[ETILE];
+    constexpr int TILE = WITH_VALS ? ETILE / 2 : ETILE;    // 48 KB static shared memory
+    __shared__ uint64_t stage[TILE];
+    __shared__ uint32_t stagev[WITH_VALS ? TILE : 1];
     if (n_dev) n = *n_dev;
-    constexpr int PER = ETILE / BLOCK;
+    constexpr int PER = TILE / BLOCK;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint64_t t0 = (uint64_t)blockIdx.x * ETILE; t0 < n; t0 += (uint64_t)gridDim.x * ETILE) {
+    for (uint64_t t0 = (uint64_t)blockIdx.x * TILE; t0 < n; t0 += (uint64_t)gridDim.x * TILE) {
         for (int p = threadIdx.x; p < MAX_PARTS; p += BLOCK) hist[p] = 0;
         __syncthreads();
         // warp w owns elements [w * 32 * PER, (w + 1) * 32 * PER) of the tile
@@ -567,10 +574,18 @@ k_elect_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ 
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
             const uint32_t part = pr[j] >> 16;
-            if (part >= MAX_PARTS) continue;
             const uint64_t i = wbase + (uint64_t)j * 32;
+            if (part >= MAX_PARTS) {
+                if (WITH_VALS && i < n) {                  // reserved key: in no part
+                    const uint32_t op = idx ? idx[i] : (uint32_t)i;
+                    if (status) status[op] = 2;
+                    if (vals_zero) vals_zero[op] = 0;
+                }
+                continue;
+            }
             const uint32_t op = idx ? idx[i] : (uint32_t)i;
             stage[loff[part] + (pr[j] & 0xFFFFu)] = ((uint64_t)op << 32) | k[j];
+            if constexpr (WITH_VALS) stagev[loff[part] + (pr[j] & 0xFFFFu)] = vals[op];
         }
         __syncthreads();
         const uint32_t total = loff[n_parts];
@@ -578,6 +593,7 @@ k_elect_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ 
             const uint64_t rec = stage[e];
             const uint32_t part = elect_part((uint32_t)rec, n_parts);
             recs[gbase[part] + (e - loff[part])] = rec;
+            if constexpr (WITH_VALS) rvals[gbase[part] + (e - loff[part])] = stagev[e];
         }
         __syncthreads();
     }
@@ -586,14 +602,21 @@ k_elect_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ 
 cudaError_t launch_elect_partition(cudaStream_t s, const uint32_t* keys, const uint32_t* idx, uint64_t n,
                                    const uint64_t* n_dev, uint32_t n_parts, unsigned long long* gcount,
                                    unsigned long long* cursor, uint64_t* part_info, uint64_t* recs,
-                                   int num_sms) {
+                                   int num_sms, const uint32_t* vals, uint32_t* rvals, uint8_t* status,
+                                   uint32_t* vals_zero) {
     cudaError_t e = cudaMemsetAsync(gcount, 0, MAX_PARTS * sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
     const int grid_h = (int)std::min<uint64_t>((n + BLOCK - 1) / BLOCK, (uint64_t)num_sms * 8);
     k_elect_hist<<<grid_h, BLOCK, 0, s>>>(keys, idx, n, n_dev, n_parts, gcount);
     k_elect_bases<<<1, 32, 0, s>>>(gcount, n_parts, part_info, cursor);
     const int grid_s = (int)std::min<uint64_t>((n + ETILE - 1) / ETILE, (uint64_t)num_sms * 8);
-    k_elect_scatter<<<grid_s, BLOCK, 0, s>>>(keys, idx, n, n_dev, n_parts, cursor, recs);
+    const int grid_v = (int)std::min<uint64_t>((n + ETILE / 2 - 1) / (ETILE / 2), (uint64_t)num_sms * 8);
+    if (rvals)
+        k_elect_scatter<true><<<grid_v, BLOCK, 0, s>>>(keys, idx, n, n_dev, n_parts, cursor, recs, vals, rvals,
+                                                       status, vals_zero);
+    else
+        k_elect_scatter<false><<<grid_s, BLOCK, 0, s>>>(keys, idx, n, n_dev, n_parts, cursor, recs, nullptr,
+                                                        nullptr, nullptr, nullptr);
     return cudaGetLastError();
 }
 
@@ -637,56 +660,43 @@ __device__ __forceinline__ bool owns(const WarpGroup<G>& wg, const DedupView& dd
 // after a resize: Step 1 is skipped (those keys are in no bucket)
 // and nothing is counted.
 // --------------------------------------------------------------------------------
-template <int G, int MINB, bool PROF = false>
-__global__ void __launch_bounds__(BLOCK, MINB)
-k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
-              const uint64_t* __restrict__ kvs, const uint32_t* __restrict__ idx, uint64_t n,
-              const uint64_t* __restrict__ n_dev, TableView tv, StashView sv, DedupView dd,
-              uint8_t* __restrict__ status, uint32_t* __restrict__ vals_zero,
-              uint32_t* __restrict__ leftover, uint32_t op_base) {
-    using WG = WarpGroup<G>;
-    constexpr int SPL = WG::SPL;
-    __shared__ uint32_t lbuf[WARPS_PER_BLOCK][32];
-    WG wg;
-    WarpList wl{lbuf[threadIdx.x >> 5], 0};
-    if (n_dev) n = *n_dev;
-    const bool place_only = kvs != nullptr;
-    const bool stash_on = !place_only && sv.ctrl->stash_tail != 0;
-    unsigned long long added = 0;
+// Per-thread state of the fast path that outlives one range of ops.
+struct FastState {
+    unsigned long long added = 0, cyc1 = 0, cyc2 = 0;
     uint32_t ab = 0;                       // per-thread: < 2^32 bytes
     bool pend = false;                     // this lane issued a claim last iteration
     uint64_t pend_prev = EMPTY;            // ... and this is its CAS result
     uint32_t pend_item = 0;
-    const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
+};
+
+// The fast-path loop over the ops [lo, hi) of an op source, warp `warp` of
+// `nw`: fetch(tt, op, k, v) reads op tt, owner(wg, valid, k, op, ab) is the
+// group-uniform owner-election check.  in_bytes: streamed input / output bytes
+// per op (byte accounting).  The claim issued by the last iteration is
+// resolved before returning; the caller flushes `wl` and reduces `st`.
+template <int G, bool PROF, class Fetch, class Owner>
+__device__ __forceinline__ void insert_fast_range(uint64_t lo, uint64_t hi, uint64_t warp, uint64_t nw, Fetch fetch,
+                                                  Owner owner, bool place_only, bool stash_on, uint32_t in_bytes,
+                                                  TableView tv, StashView sv, uint8_t* __restrict__ status,
+                                                  uint32_t* __restrict__ vals_zero, uint32_t* __restrict__ leftover,
+                                                  WarpList& wl, FastState& st) {
+    using WG = WarpGroup<G>;
+    constexpr int SPL = WG::SPL;
+    WG wg;
     // software pipeline: the next iteration's (op, key, value) is loaded while
     // this iteration probes
     const uint64_t stride = nw * WG::GPW;
     uint32_t op_n = 0, k_n = INVALID_KEY, v_n = 0;
-    auto fetch = [&](uint64_t tt) {
-        if (tt >= n) return;
-        if (place_only) {
-            const uint64_t w = kvs[tt];
-            op_n = (uint32_t)tt;
-            k_n = key_of(w);
-            v_n = val_of(w);
-        } else {
-            op_n = idx ? idx[tt] : op_base + (uint32_t)tt;   // op_base: chunked launches
-            k_n = keys[op_n];
-            v_n = vals[op_n];
-        }
-    };
-    unsigned long long cyc1 = 0, cyc2 = 0;   // PROF: this warp's Step-1 / Step-2 cycles
-    fetch(warp * WG::GPW + wg.gi);
-    for (uint64_t t0 = warp * WG::GPW; t0 < n; t0 += stride) {
+    if (lo + warp * WG::GPW + wg.gi < hi) fetch(lo + warp * WG::GPW + wg.gi, op_n, k_n, v_n);
+    for (uint64_t t0 = lo + warp * WG::GPW; t0 < hi; t0 += stride) {
         long long c0 = 0;
         if constexpr (PROF) c0 = clock64();
         const uint64_t t = t0 + wg.gi;
-        const bool active = t < n;
+        const bool active = t < hi;
         const uint32_t op = op_n;                    // op indices < 2^32 (API contract)
         const uint32_t k = active ? k_n : INVALID_KEY;
         const uint32_t v = v_n;
-        fetch(t + stride);
+        if (t + stride < hi) fetch(t + stride, op_n, k_n, v_n);
         bool valid = active && k != INVALID_KEY;
         uint32_t b1 = 0, b2 = 0, h2 = 0;
         if (valid) {
@@ -711,15 +721,14 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
             fill_empty<SPL>(sv_);
         }
         if (active && wg.gl == 0) {
-            ab += (place_only ? 8 : 8 + (status ? 1 : 0) + (vals_zero ? 4 : 0) + (idx ? 4 : 0)) +
-                  (valid ? 256 + 8 : 0);
+            st.ab += in_bytes + (valid ? 256 + 8 : 0);
             if (!place_only) {
                 if (vals_zero) vals_zero[op] = 0;
                 if (!valid && status) status[op] = 2;
             }
         }
         // owner election: duplicates copy the owner's outcome afterwards
-        if (!owns<G>(wg, dd, valid, k, op, ab)) {
+        if (!owner(wg, valid, k, op, st.ab)) {
             valid = false;
             two = false;
         }
@@ -735,20 +744,20 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
                 else scan_slots<SPL>(sv_, k, jm1, jf1);
             }
             if (__any_sync(FULL, wg.ballot(jm1 < SPL) != 0))
-                done = wcme_cas<G>(wg, sv_, tv.bucket(b1), k, kv, valid, ab);
+                done = wcme_cas<G>(wg, sv_, tv.bucket(b1), k, kv, valid, st.ab);
             const bool maybe = valid && !done && (spill_w & fp) == fp;
             const bool need2 = two && maybe;
             if (__any_sync(FULL, need2)) {
                 if (need2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), sv_);
-                if (need2 && wg.gl == 0) ab += 256;
+                if (need2 && wg.gl == 0) st.ab += 256;
                 have2 = need2;
-                done |= wcme_cas<G>(wg, sv_, tv.bucket(b2), k, kv, need2, ab);
+                done |= wcme_cas<G>(wg, sv_, tv.bucket(b2), k, kv, need2, st.ab);
             }
             if (stash_on) {
                 bool sdone = false;
                 if (maybe && !done && wg.gl == 0) {
                     uint64_t sw;
-                    ab += 16;
+                    st.ab += 16;
                     int64_t pos = stash_lookup(sv, k, &sw);
                     while (pos >= 0) {
                         uint64_t prev = cas64(&sv.ring[pos], sw, kv);
@@ -765,57 +774,92 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         }
         // resolve the claim issued in the previous iteration (its CAS has had
         // this iteration's loads to come back); a lost claim goes to Step 3
-        wl.push(pend && pend_prev != EMPTY, pend_item, leftover, &sv.ctrl->n_left);
-        pend = false;
+        wl.push(st.pend && st.pend_prev != EMPTY, st.pend_item, leftover, &sv.ctrl->n_left);
+        st.pend = false;
         // Step 2: optimistic WABC claim in b1, then b2 (first-fit, A-21); b2 is
         // read only if b1 is full.
         if (place_only && valid) {
             if (c_claim_rot >= 2) scan_slots_rot<SPL>(sv_, INVALID_KEY, srot, jm1, jf1);
             else scan_slots<SPL>(sv_, INVALID_KEY, jm1, jf1);
         }
-        bool placed = wabc_claim_issue<G>(wg, jf1, tv.bucket(b1), kv, valid && !done, pend, pend_prev,
-                                          pend_item, op, ab, lrot);
+        bool placed = wabc_claim_issue<G>(wg, jf1, tv.bucket(b1), kv, valid && !done, st.pend, st.pend_prev,
+                                          st.pend_item, op, st.ab, lrot);
         const bool want2 = two && !done && !placed;
         if (__any_sync(FULL, want2)) {
             if (want2 && !have2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), sv_);
-            if (want2 && !have2 && wg.gl == 0) ab += 256;
+            if (want2 && !have2 && wg.gl == 0) st.ab += 256;
             int jm2, jf2 = SPL;
             if (want2) {
                 if (c_claim_rot >= 2) scan_slots_rot<SPL>(sv_, INVALID_KEY, srot, jm2, jf2);
                 else scan_slots<SPL>(sv_, INVALID_KEY, jm2, jf2);
             }
-            const bool p2 = wabc_claim_issue<G>(wg, jf2, tv.bucket(b2), kv, want2, pend, pend_prev,
-                                                pend_item, op, ab, lrot);
+            const bool p2 = wabc_claim_issue<G>(wg, jf2, tv.bucket(b2), kv, want2, st.pend, st.pend_prev,
+                                                st.pend_item, op, st.ab, lrot);
             if (p2 && wg.gl == 0) {
                 atomicOr((unsigned long long*)&tv.spill[b1], (unsigned long long)fp);
-                ab += 8;
+                st.ab += 8;
             }
             placed |= p2;
         }
         const bool left = valid && !done && !placed;
         if (!place_only && valid && wg.gl == 0) {
             if (status) status[op] = done ? 1 : 0;
-            if (!done) ++added;
+            if (!done) ++st.added;
         }
         wl.push(left && wg.gl == 0, op, leftover, &sv.ctrl->n_left);
         if constexpr (PROF) {
             const long long c2 = clock64();
             const unsigned long long s1 = warp_span(c0, c1), s2 = warp_span(c1, c2);
             if (wg.lane == 0) {
-                cyc1 += s1;
-                cyc2 += s2;
+                st.cyc1 += s1;
+                st.cyc2 += s2;
             }
         }
     }
-    wl.push(pend && pend_prev != EMPTY, pend_item, leftover, &sv.ctrl->n_left);
-    wl.flush(leftover, &sv.ctrl->n_left);
-    block_add(&sv.ctrl->count, added);
-    block_add(&sv.ctrl->abytes[AB_INSERT], ab);
-    if constexpr (PROF) {
-        block_add(&sv.ctrl->cyc[0], cyc1);
-        block_add(&sv.ctrl->cyc[1], cyc2);
-    }
+    wl.push(st.pend && st.pend_prev != EMPTY, st.pend_item, leftover, &sv.ctrl->n_left);
+    st.pend = false;
+}
 
+template <int G, int MINB, bool PROF = false>
+__global__ void __launch_bounds__(BLOCK, MINB)
+k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+              const uint64_t* __restrict__ kvs, const uint32_t* __restrict__ idx, uint64_t n,
+              const uint64_t* __restrict__ n_dev, TableView tv, StashView sv, DedupView dd,
+              uint8_t* __restrict__ status, uint32_t* __restrict__ vals_zero,
+              uint32_t* __restrict__ leftover, uint32_t op_base) {
+    __shared__ uint32_t lbuf[WARPS_PER_BLOCK][32];
+    WarpList wl{lbuf[threadIdx.x >> 5], 0};
+    if (n_dev) n = *n_dev;
+    const bool place_only = kvs != nullptr;
+    const bool stash_on = !place_only && sv.ctrl->stash_tail != 0;
+    const uint64_t warp = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * BLOCK) >> 5;
+    auto fetch = [&](uint64_t tt, uint32_t& op, uint32_t& k, uint32_t& v) {
+        if (place_only) {
+            const uint64_t w = kvs[tt];
+            op = (uint32_t)tt;
+            k = key_of(w);
+            v = val_of(w);
+        } else {
+            op = idx ? idx[tt] : op_base + (uint32_t)tt;     // op_base: chunked launches
+            k = keys[op];
+            v = vals[op];
+        }
+    };
+    auto owner = [&](const WarpGroup<G>& wg, bool valid, uint32_t k, uint32_t op, uint32_t& ab) {
+        return owns<G>(wg, dd, valid, k, op, ab);
+    };
+    const uint32_t in_bytes = place_only ? 8 : 8 + (status ? 1 : 0) + (vals_zero ? 4 : 0) + (idx ? 4 : 0);
+    FastState st;
+    insert_fast_range<G, PROF>(0, n, warp, nw, fetch, owner, place_only, stash_on, in_bytes, tv, sv, status,
+                               vals_zero, leftover, wl, st);
+    wl.flush(leftover, &sv.ctrl->n_left);
+    block_add(&sv.ctrl->count, st.added);
+    block_add(&sv.ctrl->abytes[AB_INSERT], st.ab);
+    if constexpr (PROF) {
+        block_add(&sv.ctrl->cyc[0], st.cyc1);
+        block_add(&sv.ctrl->cyc[1], st.cyc2);
+    }
 }
 
 // --------------------------------------------------------------------------------
@@ -1017,6 +1061,159 @@ k_insert_slow(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
               const uint64_t* __restrict__ kvs, const uint32_t* __restrict__ leftover,
               TableView tv, StashView sv, uint32_t max_evictions, uint8_t* __restrict__ status) {
     insert_slow_body<G, PROF>(keys, vals, kvs, leftover, tv, sv, max_evictions, status);
+}
+
+// --------------------------------------------------------------------------------
+// Fused INSERT phase with owner election (cooperative, one launch).  The
+// election of part q overlaps the insert fast path of part q-1: in every
+// block, warps 6-7 elect (latency-bound L2 CASes) while warps 0-5 probe
+// (HBM-bound), so the election's CAS round trips hide under the probes; a
+// grid barrier separates the parts.  The two election tables alternate
+// between parts and are never cleared inside the phase: a word is
+//   epoch(6) | low 26 bits of fmix32(k ^ DEDUP_SEED) (its top 6 bits are the
+//   part) | op(32),
+// and a word whose epoch is not the current part's is empty.
+// --------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t fused_owner(const uint64_t* tab, uint64_t mask, uint32_t hk26, uint32_t epoch,
+                                                uint32_t self) {
+    uint64_t h = hk26 & mask;
+    for (uint64_t probe = 0; probe <= mask; ++probe) {
+        const uint64_t e = tab[h];
+        if ((uint32_t)(e >> 58) != epoch) return self;
+        if (((uint32_t)(e >> 32) & 0x3FFFFFFu) == hk26) return (uint32_t)e;
+        h = (h + 1) & mask;
+    }
+    return self;
+}
+
+template <int G>
+__global__ void __launch_bounds__(BLOCK, 4)
+k_insert_fused(const uint64_t* __restrict__ recs, const uint32_t* __restrict__ rvals,
+               const uint64_t* __restrict__ part_info, uint64_t* __restrict__ tab0, uint64_t* __restrict__ tab1,
+               uint64_t tab_mask, DedupView dd, TableView tv, StashView sv, uint8_t* __restrict__ status,
+               uint32_t* __restrict__ vals_zero, uint32_t* __restrict__ leftover, uint32_t max_evictions,
+               const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    constexpr int ELECT_WARPS = 2;                       // of WARPS_PER_BLOCK
+    __shared__ uint32_t lbuf[WARPS_PER_BLOCK][32];
+    WarpList wl{lbuf[threadIdx.x >> 5], 0};
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool elector = wib >= WARPS_PER_BLOCK - ELECT_WARPS;
+    const uint64_t ew = (uint64_t)blockIdx.x * ELECT_WARPS + (wib - (WARPS_PER_BLOCK - ELECT_WARPS));
+    const uint64_t n_ew = (uint64_t)gridDim.x * ELECT_WARPS;
+    const uint64_t iw = (uint64_t)blockIdx.x * (WARPS_PER_BLOCK - ELECT_WARPS) + wib;
+    const uint64_t n_iw = (uint64_t)gridDim.x * (WARPS_PER_BLOCK - ELECT_WARPS);
+    const bool stash_on = sv.ctrl->stash_tail != 0;
+    const uint32_t in_bytes = 8 + 4 + (status ? 1 : 0) + (vals_zero ? 4 : 0);
+    FastState st;
+    uint32_t eab = 0;
+    unsigned long long eover = 0;
+    for (uint32_t q = 0; q <= FUSED_PARTS; ++q) {
+        if (elector && q < FUSED_PARTS) {                // ---- elect part q ----
+            uint64_t* tab = (q & 1) ? tab1 : tab0;
+            const uint64_t base = part_info[MAX_PARTS + q], cnt = part_info[q];
+            for (uint64_t t0 = ew * 32; t0 < cnt; t0 += n_ew * 32) {
+                const uint64_t t = t0 + lane;
+                const bool active = t < cnt;
+                const uint64_t rec = active ? recs[base + t] : EMPTY;
+                const uint32_t k = (uint32_t)rec, op = (uint32_t)(rec >> 32);
+                const uint32_t grp = __match_any_sync(FULL, k);
+                if (!active) continue;
+                eab += 8;
+                uint32_t mx = op;
+                if (__popc(grp) > 1) {                   // same key in this warp: pre-merge
+                    dd.flag[op] = 1;
+                    mx = __reduce_max_sync(grp, op);
+                }
+                if (op != mx) continue;
+                const uint32_t hk26 = fmix32(k ^ DEDUP_SEED) & 0x3FFFFFFu;
+                const uint64_t word = ((uint64_t)q << 58) | ((uint64_t)hk26 << 32) | op;
+                uint64_t h = hk26 & tab_mask;
+                uint64_t e = *(volatile uint64_t*)&tab[h];
+                uint64_t probe = 0;
+                while (true) {
+                    if ((uint32_t)(e >> 58) != q) {          // stale epoch: free
+                        const uint64_t prev = cas64(&tab[h], e, word);
+                        eab += 32;
+                        if (prev == e) break;
+                        e = prev;                            // re-examine the same slot
+                        continue;
+                    }
+                    if (((uint32_t)(e >> 32) & 0x3FFFFFFu) == hk26) {
+                        dd.flag[op] = 1;
+                        dd.flag[(uint32_t)e] = 1;
+                        if (word > e) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
+                        eab += 32;
+                        break;
+                    }
+                    if (++probe > tab_mask) { ++eover; break; }   // table full (never at the sizing)
+                    h = (h + 1) & tab_mask;
+                    e = *(volatile uint64_t*)&tab[h];
+                }
+            }
+        }
+        if (!elector && q >= 1) {                        // ---- insert part q-1 ----
+            const uint32_t pq = q - 1;
+            const uint64_t* tab = (pq & 1) ? tab1 : tab0;
+            const uint64_t base = part_info[MAX_PARTS + pq], cnt = part_info[pq];
+            auto fetch = [&](uint64_t tt, uint32_t& op, uint32_t& k, uint32_t& v) {
+                const uint64_t rec = recs[tt];
+                op = (uint32_t)(rec >> 32);
+                k = (uint32_t)rec;
+                v = rvals[tt];
+            };
+            auto owner = [&](const WarpGroup<G>& wg, bool valid, uint32_t k, uint32_t op, uint32_t& ab) {
+                uint32_t own = op;
+                if (valid && wg.gl == 0) {
+                    ab += 1;
+                    if (dd.flag[op]) {
+                        own = fused_owner(tab, tab_mask, fmix32(k ^ DEDUP_SEED) & 0x3FFFFFFu, pq, op);
+                        dd.owner_of[op] = own;
+                        ab += 8 + 4;
+                    }
+                }
+                return wg.bcast(own, 0) == op;
+            };
+            insert_fast_range<G, false>(base, base + cnt, iw, n_iw, fetch, owner, false, stash_on, in_bytes, tv, sv,
+                                        status, vals_zero, leftover, wl, st);
+        }
+        grid.sync();
+    }
+    wl.flush(leftover, &sv.ctrl->n_left);
+    block_add(&sv.ctrl->count, st.added);
+    block_add(&sv.ctrl->abytes[AB_INSERT], st.ab);
+    block_add(&sv.ctrl->abytes[AB_ELECT], eab);
+    block_add(&sv.ctrl->eover, eover);
+    grid.sync();
+    // ---- Steps 3-4 for the leftovers ----
+    insert_slow_body<G_SLOW, false>(keys, vals, nullptr, leftover, tv, sv, max_evictions, status);
+    grid.sync();
+    // ---- duplicates copy their owner's status (PHASED contract, A-17) ----
+    const uint64_t total = part_info[MAX_PARTS + FUSED_PARTS - 1] + part_info[FUSED_PARTS - 1];
+    for (uint64_t t = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; t < total; t += (uint64_t)gridDim.x * BLOCK) {
+        const uint32_t op = (uint32_t)(recs[t] >> 32);
+        if (!dd.flag[op]) continue;
+        const uint32_t o = dd.owner_of[op];
+        if (o != op && status) status[op] = status[o];
+    }
+}
+
+int fused_grid(int num_sms) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)k_insert_fused<G_INSERT>, BLOCK, 0);
+    return (nb > 0 ? nb : 1) * num_sms;
+}
+
+cudaError_t launch_insert_fused(int grid, cudaStream_t s, const uint64_t* recs, const uint32_t* rvals,
+                                const uint64_t* part_info, uint64_t* tab0, uint64_t* tab1, uint64_t tab_mask,
+                                DedupView dd, TableView tv, StashView sv, uint8_t* status, uint32_t* vals_zero,
+                                uint32_t* leftover, uint32_t max_evictions, const uint32_t* keys,
+                                const uint32_t* vals) {
+    void* args[] = {(void*)&recs, (void*)&rvals, (void*)&part_info, (void*)&tab0, (void*)&tab1, (void*)&tab_mask,
+                    (void*)&dd, (void*)&tv, (void*)&sv, (void*)&status, (void*)&vals_zero, (void*)&leftover,
+                    (void*)&max_evictions, (void*)&keys, (void*)&vals};
+    return cudaLaunchCooperativeKernel((const void*)k_insert_fused<G_INSERT>, grid, BLOCK, args, 0, s);
 }
 
 // --------------------------------------------------------------------------------

@@ -140,7 +140,22 @@ cudaError_t launch_partition(cudaStream_t s, int mode, uint32_t n_parts, uint32_
 cudaError_t launch_elect_partition(cudaStream_t s, const uint32_t* keys, const uint32_t* idx, uint64_t n,
                                    const uint64_t* n_dev, uint32_t n_parts, unsigned long long* gcount,
                                    unsigned long long* cursor, uint64_t* part_info, uint64_t* recs,
-                                   int num_sms);
+                                   int num_sms, const uint32_t* vals = nullptr, uint32_t* rvals = nullptr,
+                                   uint8_t* status = nullptr, uint32_t* vals_zero = nullptr);
+// Fused INSERT phase with owner election (one cooperative launch): ops
+// hash-partitioned into FUSED_PARTS parts (records + values from
+// launch_elect_partition with rvals); part q is elected into table (q & 1)
+// while part q-1 runs the insert fast path, then Steps 3-4 and the duplicate
+// fix-up.  tab0 / tab1: tab_mask + 1 words each, pre-set to the byte patterns
+// 0x04 / 0x00 (stale epochs).  ctrl n_left / slow_next must be zero.
+constexpr uint32_t FUSED_PARTS = 64;
+constexpr uint64_t FUSED_MIN_OPS = 1ull << 21;   // smaller phases: one L2-resident election table
+int fused_grid(int num_sms);
+cudaError_t launch_insert_fused(int grid, cudaStream_t s, const uint64_t* recs, const uint32_t* rvals,
+                                const uint64_t* part_info, uint64_t* tab0, uint64_t* tab1, uint64_t tab_mask,
+                                DedupView dd, TableView tv, StashView sv, uint8_t* status, uint32_t* vals_zero,
+                                uint32_t* leftover, uint32_t max_evictions, const uint32_t* keys,
+                                const uint32_t* vals);
 cudaError_t launch_dedup_elect_part(int grid, cudaStream_t s, const uint64_t* recs, const uint64_t* part_info,
                                     uint32_t part, DedupView dd, Ctrl* ctrl);
 

@@ -46,7 +46,8 @@ class HiveStats(ctypes.Structure):
             "count", "stash_used", "stash_cap", "evictions", "max_depth", "stash_pushes", "leftovers",
             "grows", "shrinks", "merge_aborts", "failed", "in_b1", "mapped_bytes")] + [
         ("alg_bytes", ctypes.c_uint64 * 8)] + [
-        ("step3", ctypes.c_uint64), ("xfail", ctypes.c_uint64), ("step_cycles", ctypes.c_uint64 * 4)]
+        ("step3", ctypes.c_uint64), ("xfail", ctypes.c_uint64), ("elect_overflow", ctypes.c_uint64),
+        ("step_cycles", ctypes.c_uint64 * 4)]
 
 
 # every exported symbol of include/hive.h, with its ctypes signature
