@@ -581,8 +581,9 @@ hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* 
                          uint32_t* vals_zero, cudaStream_t s, const InsertChunks* chunks = nullptr,
                          const DedupView* pre = nullptr) {
     const bool dedup = !kvs && h->dedup_on();
-    // large phases with election: the fused single-launch form (HIVE_FUSED=0: the multi-launch form)
-    static const bool fused_ok = !getenv("HIVE_FUSED") || atoi(getenv("HIVE_FUSED")) != 0;
+    // large phases with election: the fused single-launch form, opt-in with
+    // HIVE_FUSED=1 (measured slower than the multi-launch form)
+    static const bool fused_ok = getenv("HIVE_FUSED") && atoi(getenv("HIVE_FUSED")) != 0;
     if (dedup && fused_ok && !pre && !chunks && !h->step_prof && n_upper >= FUSED_MIN_OPS)
         return insert_phase_fused(h, keys, vals, idx, n_upper, n_dev, n_batch, status, vals_zero, s);
     DedupView dd{nullptr, 0, nullptr, nullptr};

@@ -660,6 +660,17 @@ __device__ __forceinline__ bool owns(const WarpGroup<G>& wg, const DedupView& dd
 // after a resize: Step 1 is skipped (those keys are in no bucket)
 // and nothing is counted.
 // --------------------------------------------------------------------------------
+// EMPTY slots of the group's bucket view (all lanes of the group get the sum).
+template <int G>
+__device__ __forceinline__ uint32_t group_free(const uint64_t (&s)[WarpGroup<G>::SPL]) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < WarpGroup<G>::SPL; ++j) c += key_of(s[j]) == INVALID_KEY ? 1u : 0u;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) c += __shfl_xor_sync(FULL, c, o);
+    return c;
+}
+
 // Per-thread state of the fast path that outlives one range of ops.
 struct FastState {
     unsigned long long added = 0, cyc1 = 0, cyc2 = 0;
@@ -735,6 +746,7 @@ __device__ __forceinline__ void insert_fast_range(uint64_t lo, uint64_t hi, uint
         const uint64_t kv = pack(k, v);
         bool done = false, have2 = false;
         int jm1 = SPL, jf1 = SPL;
+        uint32_t f1 = SPL * G;                         // free slots of b1 (two-choice placement only)
         if (!place_only) {
             // Step 1: b1 (one scan gives the match and the first free slot); then
             // -- only if b1's spill word allows k to live elsewhere -- b2 and the
@@ -743,6 +755,7 @@ __device__ __forceinline__ void insert_fast_range(uint64_t lo, uint64_t hi, uint
                 if (c_claim_rot >= 2) scan_slots_rot<SPL>(sv_, k, srot, jm1, jf1);
                 else scan_slots<SPL>(sv_, k, jm1, jf1);
             }
+            if constexpr (TWO_CHOICE_T > 0) f1 = group_free<G>(sv_);
             if (__any_sync(FULL, wg.ballot(jm1 < SPL) != 0))
                 done = wcme_cas<G>(wg, sv_, tv.bucket(b1), k, kv, valid, st.ab);
             const bool maybe = valid && !done && (spill_w & fp) == fp;
@@ -776,14 +789,28 @@ __device__ __forceinline__ void insert_fast_range(uint64_t lo, uint64_t hi, uint
         // this iteration's loads to come back); a lost claim goes to Step 3
         wl.push(st.pend && st.pend_prev != EMPTY, st.pend_item, leftover, &sv.ctrl->n_left);
         st.pend = false;
+        // Thresholded two-choice placement (reading A-21; placement is not
+        // observable): when b1 has fewer than TWO_CHOICE_T free slots, b2 is
+        // read and the emptier bucket is claimed.  TWO_CHOICE_T = 0: first-fit.
+        bool choose2 = false;
+        if constexpr (TWO_CHOICE_T > 0) {
+            const bool look2 = !place_only && two && !done && f1 < TWO_CHOICE_T;
+            if (__any_sync(FULL, look2)) {
+                if (look2 && !have2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), sv_);
+                if (look2 && !have2 && wg.gl == 0) st.ab += 256;
+                if (look2) have2 = true;
+                const uint32_t f2 = group_free<G>(sv_);
+                choose2 = look2 && f2 > f1;
+            }
+        }
         // Step 2: optimistic WABC claim in b1, then b2 (first-fit, A-21); b2 is
         // read only if b1 is full.
         if (place_only && valid) {
             if (c_claim_rot >= 2) scan_slots_rot<SPL>(sv_, INVALID_KEY, srot, jm1, jf1);
             else scan_slots<SPL>(sv_, INVALID_KEY, jm1, jf1);
         }
-        bool placed = wabc_claim_issue<G>(wg, jf1, tv.bucket(b1), kv, valid && !done, st.pend, st.pend_prev,
-                                          st.pend_item, op, st.ab, lrot);
+        bool placed = wabc_claim_issue<G>(wg, jf1, tv.bucket(b1), kv, valid && !done && !choose2, st.pend,
+                                          st.pend_prev, st.pend_item, op, st.ab, lrot);
         const bool want2 = two && !done && !placed;
         if (__any_sync(FULL, want2)) {
             if (want2 && !have2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), sv_);

@@ -18,6 +18,13 @@ constexpr int MINB_DEFAULT = 4;          // 4 blocks/SM => <= 64 registers (ncu:
 constexpr int PART_CHUNK = 8192;         // max elements per warp in the stable partition
 constexpr int PART_UNROLL = 4;           // rows of 32 elements whose loads are in flight together
 constexpr int MAX_PARTS = 64;
+#ifndef HIVE_TWO_CHOICE_T
+#define HIVE_TWO_CHOICE_T 0
+#endif
+// Thresholded two-choice placement in the insert fast path (reading A-21):
+// below this many free slots in b1 the emptier of b1 / b2 is claimed; 0 =
+// first-fit b1 then b2.  Build-time (-DHIVE_TWO_CHOICE_T=t, HIVE_NVCC_DEFINES).
+constexpr uint32_t TWO_CHOICE_T = HIVE_TWO_CHOICE_T;
 constexpr uint32_t CLAIM_ROT_DEFAULT = 0;   // claim placement (hive_kernels.cu c_claim_rot; 0 measured fastest,
                                             // 1 / 2 for experiments: rebuild)
 
