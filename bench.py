@@ -747,7 +747,48 @@ def secondary_measurements(table, keys, vals, queries, n, nb, dev, prof_main):
         "vs_phased": (nbat * bsz / ev[0].elapsed_time(ev[1])) / (nbat * bsz / mixed_ms)}
     del tc
     res["cfg4_zipf"] = cfg4_zipf(dev)
+    res["imbalanced_050_030_020"] = imbalanced(dev)
     return res
+
+
+def imbalanced(dev):
+    """The paper's imbalanced workload (§V-C.2): one mixed batch
+    of n ops with insert:lookup:delete = 0.5:0.3:0.2 over ids uniform in
+    [0, n), on a table that starts at 1K buckets and grows before the batch's
+    insert phase (paper on an RTX 4090: ~2.6 -> 1.8 G ops/s as n grows; context,
+    not a target).  PHASED hive_mixed and hive_mixed_concurrent, device time of
+    the call (resize included), after a warm-up call on a cleared table."""
+    import torch
+
+    from paper_2510_15095_b200 import HiveTable, u8, u32
+    out = {}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for lg in (20, 22, 24, 26):
+        n = 1 << lg
+        ops = u8(gen.bernoulli_ops(n, 0.5, 0.2, seed=600 + lg), dev)
+        ids = gen.uniform_ids(n, n, seed=700 + lg)
+        k, v = u32(gen.keys_of(ids), dev), u32(gen.vals_of(ids), dev)
+        vo = torch.empty(n, dtype=torch.uint32, device=dev)
+        rr = torch.empty(n, dtype=torch.uint8, device=dev)
+        row = {}
+        for mode in ("phased", "concurrent"):
+            t = HiveTable(1024 * 32)
+            run = t.mixed if mode == "phased" else t.mixed_concurrent
+            best = None
+            for rep in range(3):
+                t.clear()
+                torch.cuda.synchronize()
+                ev[0].record()
+                run(ops, k, v, vo, rr)
+                ev[1].record()
+                torch.cuda.synchronize()
+                ms = ev[0].elapsed_time(ev[1])
+                if rep and (best is None or ms < best):
+                    best = ms
+            row[mode + "_gops"] = n / (best * 1e-3) / 1e9
+            del t
+        out[f"2^{lg}"] = row
+    return out
 
 
 def cfg4_zipf(dev):

@@ -126,3 +126,38 @@ def test_sharded_calls_capture_in_a_cuda_graph(pg):
         assert (_np(er)[: n // 4] == o.erase(gen.keys_of(ids[: n // 4]))).all()
     del g
     sh.close()
+
+
+def test_cfg5_sequence_world1_shard_dump_vs_oracle(pg):
+    """BASELINE configs[4] / SURVEY §8(d) cfg5 check at world size 1 and reduced
+    T: the bench's cfg5 sequence (insert 2^T keys in batches, 2^T finds with 50%
+    hits, erase 2^(T-3)) through the sharded handle, every result and the
+    shard's sorted dump against a per-shard oracle fed the ops routed to it."""
+    import oracle
+    from paper_2510_15095_b200 import u32
+    from paper_2510_15095_b200.sharded import ShardedHive
+    T, B = 22, 1 << 20
+    total = 1 << T
+    nb = -(-total * 100 // (95 * 32))
+    sh = ShardedHive(nb * 32, batch_max=B, lf_grow=2.0, lf_shrink=0)
+    o = oracle.OracleTable(nb * 32, lf_grow=2.0, lf_shrink=0)
+    rng = np.random.default_rng(505)
+    for lo in range(0, total, B):
+        ids = np.arange(lo, lo + B, dtype=np.uint32)
+        k, v = gen.keys_of(ids), gen.vals_of(ids)
+        assert (_np(sh.insert(u32(k), u32(v))) == o.insert(k, v)).all()
+    for b in range(total // B):
+        hit = rng.integers(0, total, B // 2, dtype=np.uint64)
+        miss = (1 << 31) + b * (B // 2) + np.arange(B // 2, dtype=np.uint64)
+        q = gen.keys_of(np.concatenate([hit, miss])[rng.permutation(B)].astype(np.uint32))
+        vv, ff = sh.find(u32(q))
+        v_o, f_o = o.find(q)
+        assert (_np(ff) == f_o).all() and (_np(vv).astype(np.uint32) == v_o).all() and f_o.sum() == B // 2
+    e = gen.keys_of(np.arange(total // 8, dtype=np.uint32))
+    assert (_np(sh.erase(u32(e))) == o.erase(e)).all()
+    kk, vv = sh.table.dump()
+    kk, vv = _np(kk).astype(np.uint32), _np(vv).astype(np.uint32)
+    ko, vo = o.dump()
+    og, oo = np.argsort(kk), np.argsort(ko)
+    assert (kk[og] == ko[oo]).all() and (vv[og] == vo[oo]).all() and len(kk) == total - total // 8
+    sh.close()
