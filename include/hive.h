@@ -278,6 +278,21 @@ hive_status hive_stats(hive_t h, hive_stats_t* out);
 hive_status hive_dump(hive_t h, uint32_t* d_keys, uint32_t* d_vals, uint64_t cap,
                       uint64_t* n_out, void* stream);
 
+/* Test hook (sync): replace the table's contents with an
+ * externally built image -- e.g. the CPU oracle's layout -- so that the probe
+ * kernels can be checked against a layout the GPU insert path did not make.
+ * d_slots: DEVICE uint64[n_buckets * 32] packed words (EMPTY = all ones) in
+ * bucket order; the geometry becomes (m = floor(log2 n_buckets), split =
+ * n_buckets - 2^m) with the Litwin addressing of PAPER:485-503 (A-2).
+ * d_stash: DEVICE uint64[n_stash] live stash words (nullable when 0); the
+ * stash capacity follows n_buckets.  Spill words and the stash index are
+ * rebuilt, count = live slots + n_stash, statistics reset.  Every key must sit
+ * in one of its candidate buckets or the stash, once (not checked).
+ * HIVE_EINVAL for n_buckets < 2 or above max_capacity, n_stash above the
+ * stash capacity, or a sharded handle. */
+hive_status hive_load_image(hive_t h, const uint64_t* d_slots, uint64_t n_buckets, const uint64_t* d_stash,
+                            uint64_t n_stash, void* stream);
+
 /* Per-kernel device timing (CUDA events around every launch on the call's
  * stream).  Enabled by hive_profile(h, 1); hive_profile(h, 2) additionally
  * runs the insert kernels' clock64-instrumented variants (default lane

@@ -71,6 +71,8 @@ def lib():
         L.oracle_expand.argtypes = [vp, u32]
         L.oracle_contract.argtypes = [vp, u32]
         L.oracle_contract.restype = ctypes.c_int
+        L.oracle_image.argtypes = [vp, vp, vp, u64]
+        L.oracle_image.restype = u64
         L.oracle_bucket.argtypes = [vp, u64, vp]
         L.oracle_bucket.restype = u32
         L.oracle_pack.argtypes = [u32, u32]
@@ -192,6 +194,15 @@ class OracleTable:
 
     def contract(self, k: int) -> bool:
         return bool(self._L.oracle_contract(self._h, k))
+
+    def image(self):
+        """(bucket array uint64[n_buckets * 32], live stash words uint64[k])."""
+        nb = self.stats()["n_buckets"]
+        slots = np.zeros(nb * 32, np.uint64)
+        n = self._L.oracle_image(self._h, None, None, 0)
+        stash = np.zeros(max(n, 1), np.uint64)
+        self._L.oracle_image(self._h, _ptr(slots), _ptr(stash), n)
+        return slots, stash[:n]
 
     def bucket(self, b: int):
         s = np.zeros(32, np.uint64)

@@ -767,6 +767,21 @@ uint32_t oracle_bucket(oracle_t o, uint64_t b, uint64_t* slots32) {
     return t.freeMask[b];
 }
 
+/* The whole bucket array (n_buckets * 32 packed words) and the live stash
+ * entries, for loading the oracle's layout into the GPU table (test hook). */
+uint64_t oracle_image(oracle_t o, uint64_t* slots, uint64_t* stash, uint64_t stash_cap) {
+    Table& t = o->t;
+    if (slots) std::copy(t.buckets.begin(), t.buckets.begin() + t.NB() * S, slots);
+    uint64_t n = 0;
+    for (uint64_t p = t.head; p < t.tail; ++p) {
+        uint64_t kv = t.ring[p % t.stash_cap];
+        if (kv == EMPTY) continue;
+        if (stash && n < stash_cap) stash[n] = kv;
+        ++n;
+    }
+    return n;
+}
+
 uint64_t oracle_pack(uint32_t key, uint32_t value) { return Pack(key, value); }
 uint32_t oracle_unpack_key(uint64_t pair) { return UnpackKey(pair); }
 uint32_t oracle_unpack_value(uint64_t pair) { return UnpackValue(pair); }

@@ -72,6 +72,9 @@ void oracle_expand(oracle_t t, uint32_t k);
 int  oracle_contract(oracle_t t, uint32_t k);
 /* Raw bucket view for fixtures: 32 slot words + freeMask. */
 uint32_t oracle_bucket(oracle_t t, uint64_t b, uint64_t* slots32);
+/* Bucket array (n_buckets * 32 words, may be NULL) and up to stash_cap live
+ * stash words (may be NULL); returns the number of live stash entries. */
+uint64_t oracle_image(oracle_t t, uint64_t* slots, uint64_t* stash, uint64_t stash_cap);
 
 /* Primitives exposed so the pins can test them individually. */
 uint64_t oracle_pack(uint32_t key, uint32_t value);

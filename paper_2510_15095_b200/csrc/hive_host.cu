@@ -1393,6 +1393,41 @@ hive_status hive_dump(hive_t h, uint32_t* d_keys, uint32_t* d_vals, uint64_t cap
     return HIVE_OK;
 }
 
+hive_status hive_load_image(hive_t h, const uint64_t* d_slots, uint64_t n_buckets, const uint64_t* d_stash,
+                            uint64_t n_stash, void* stream) {
+    if (!h || !d_slots || n_buckets < 2 || n_buckets > h->max_buckets || (n_stash && !d_stash)) return HIVE_EINVAL;
+    if (h->sharded()) return HIVE_EINVAL;
+    BusyGuard g(h);
+    if (!g.ok) return HIVE_EBUSY;
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last = s;
+    uint32_t m = 0;
+    while ((2ull << m) <= n_buckets) ++m;
+    CKS(map_buckets(h, n_buckets));
+    h->m = m;
+    h->split = (uint32_t)(n_buckets - (1ull << m));
+    const uint64_t cap = h->stash_cap_for(n_buckets);
+    if (n_stash > cap) return HIVE_EINVAL;
+    CK(cudaMemcpyAsync((void*)h->va, d_slots, n_buckets * SLOTS * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync((void*)h->sp.va, 0, n_buckets * sizeof(uint64_t), s));
+    CK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), s));
+    CKS(stash_reset(h, cap, s));
+    CK(launch_image(s, h->tv(), n_buckets, h->sv(), d_stash, n_stash));
+    // live count = occupied slots + stash entries: counted by the dump kernel
+    CKS(set_ctrl_word(h, &h->ctrl->dump_n, 0, s));
+    CK(launch_dump(h->grids.stream, s, h->tv(), n_buckets, h->sv(), nullptr, nullptr, 0));
+    CKS(read_ctrl(h, s));
+    h->stage_h[2] = h->ctrl_h->dump_n;      // two staging words: both copies are in flight together
+    h->stage_h[3] = n_stash;
+    CK(cudaMemcpyAsync(&h->ctrl->count, h->stage_h + 2, sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(&h->ctrl->stash_tail, h->stage_h + 3, sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    h->tail_known = n_stash;
+    h->nb_at_drain = n_buckets;
+    h->grows = h->shrinks = h->merge_aborts = 0;
+    return HIVE_OK;
+}
+
 hive_status hive_profile(hive_t h, int enable) {
     if (!h) return HIVE_EINVAL;
     h->prof = enable != 0;

@@ -2405,6 +2405,36 @@ cudaError_t launch_unroute_pad(cudaStream_t s, const uint32_t* pos, uint64_t n, 
     return cudaGetLastError();
 }
 
+// ---- test hook: load an externally built image (hive_load_image) -----------------
+// Spill words of a loaded bucket array: every key not in bucket addr(h1(k))
+// sets its fingerprint bits there; stash entries are written to the ring,
+// indexed, and flagged in their b1's spill word the same way.
+__global__ void __launch_bounds__(BLOCK)
+k_image_spill(TableView tv, uint64_t n_slots) {
+    for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < n_slots; i += (uint64_t)gridDim.x * BLOCK) {
+        const uint64_t w = tv.buckets[i];
+        if (w == EMPTY) continue;
+        const uint32_t k = key_of(w), hb = tv.addr(tv.h1(k));
+        if (hb != (uint32_t)(i / SLOTS)) atomicOr((unsigned long long*)&tv.spill[hb], (unsigned long long)spill_fp(k));
+    }
+}
+__global__ void __launch_bounds__(BLOCK)
+k_image_stash(TableView tv, StashView sv, const uint64_t* __restrict__ words, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (uint64_t)gridDim.x * BLOCK) {
+        const uint64_t w = words[i];
+        const uint32_t k = key_of(w);
+        sv.ring[i] = w;
+        stash_index_put(sv, k, i);
+        atomicOr((unsigned long long*)&tv.spill[tv.addr(tv.h1(k))], (unsigned long long)spill_fp(k));
+    }
+}
+cudaError_t launch_image(cudaStream_t s, TableView tv, uint64_t n_buckets, StashView sv, const uint64_t* stash,
+                         uint64_t n_stash) {
+    k_image_spill<<<clamp_grid(148 * 8, n_buckets * SLOTS, BLOCK), BLOCK, 0, s>>>(tv, n_buckets * SLOTS);
+    if (n_stash) k_image_stash<<<clamp_grid(148 * 8, n_stash, BLOCK), BLOCK, 0, s>>>(tv, sv, stash, n_stash);
+    return cudaGetLastError();
+}
+
 // ---- hash study (§III-C, Theorem 1 / CSR; §V-B pairs) -------------------------
 __device__ __forceinline__ uint32_t hash_fn(uint32_t fn, uint32_t k) {
     switch (fn) {

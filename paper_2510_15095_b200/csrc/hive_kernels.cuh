@@ -110,6 +110,9 @@ constexpr int MAX_SEGMENTS = 64;        // linear-hashing rounds crossed by one 
 
 cudaError_t launch_stash_reset(cudaStream_t s, StashView sv);
 
+// hive_load_image: spill words of the loaded buckets, stash ring + index + spill bits.
+cudaError_t launch_image(cudaStream_t s, TableView tv, uint64_t n_buckets, StashView sv, const uint64_t* stash,
+                         uint64_t n_stash);
 cudaError_t launch_dump(int grid, cudaStream_t s, TableView tv, uint64_t n_buckets, StashView sv,
                         uint32_t* keys, uint32_t* vals, uint64_t cap);
 cudaError_t launch_count_b1(int grid, cudaStream_t s, TableView tv, uint64_t n_buckets, Ctrl* ctrl);

@@ -68,6 +68,7 @@ SIGNATURES = {
     "hive_stats": (_int, [_vp, ctypes.POINTER(HiveStats)]),
     "hive_dump": (_int, [_vp, _vp, _vp, _u64, ctypes.POINTER(_u64), _vp]),
     "hive_profile": (_int, [_vp, _int]),
+    "hive_load_image": (_int, [_vp, _vp, _u64, _vp, _u64, _vp]),
     "hive_profile_read": (_int, [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
                                  ctypes.POINTER(_u64), _int, _int]),
     "hive_route": (_int, [_u32, _u32, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp]),
@@ -306,6 +307,15 @@ class HiveTable:
         v = torch.empty(max(n.value, 1), dtype=torch.uint32, device="cuda")
         _check(self._L.hive_dump(self._h, _p(k), _p(v), n.value, ctypes.byref(n), _stream()), "hive_dump")
         return k[:n.value], v[:n.value]
+
+    def load_image(self, slots: torch.Tensor, stash: torch.Tensor | None = None, stream=None):
+        """hive_load_image (test hook): slots = device uint64/int64 tensor of
+        n_buckets * 32 packed words, stash = live stash words."""
+        slots = _dev(slots, 8)
+        n_st = 0 if stash is None else stash.numel()
+        _check(self._L.hive_load_image(self._h, _p(slots), slots.numel() // 32,
+                                       _p(_dev(stash, 8)) if n_st else None, n_st, _stream(stream)),
+               "hive_load_image")
 
     def shard_info(self) -> tuple[int, int, int]:
         """(nranks, rank, padded exchange capacity per peer); (1, 0, 0) unsharded."""

@@ -335,3 +335,32 @@ def test_step_breakdown_tool():
     p.g.profile(False)
     sg, _ = p.check_state()
     assert sum(sg["step_cycles"]) > 0
+
+
+@pytest.mark.parametrize("hash_pair", ["bithash", "crc"])
+def test_probe_kernels_on_oracle_built_image(hash_pair):
+    """hive_load_image: the oracle's own layout -- its
+    paper-literal lowest-slot victim rule puts ~1% of the keys in the stash and
+    many in their second bucket -- is loaded into the GPU table; the GPU's find /
+    erase / insert kernels then run on a layout their insert path never made
+    and must match the oracle op by op, split-pointer addressing included
+    (2^12 + 1000 buckets)."""
+    import oracle
+    from gpu_util import Pair
+    nb = (1 << 12) + 1000
+    p = Pair(nb * 32, lf_grow=2.0, lf_shrink=0, hash=hash_pair)
+    n = int(0.95 * nb * 32)
+    keys = gen.present_keys(n)
+    p.o.insert(keys, gen.vals_of(np.arange(n)))
+    slots, stash = p.o.image()
+    assert len(stash) > 0
+    p.g.load_image(torch.from_numpy(slots.view(np.int64)).cuda(), torch.from_numpy(stash.view(np.int64)).cuda())
+    assert p.g.stats()["count"] == p.o.stats()["count"]
+    q = np.concatenate([keys, gen.absent_keys(20000)])
+    p.find(q)
+    p.erase(np.concatenate([keys[::5], gen.absent_keys(1000)]))
+    p.find(q)
+    p.insert(keys[::7], gen.vals_of(np.arange(0, n, 7)) ^ 0xABC)      # replaces, incl. stashed keys
+    p.insert(gen.absent_keys(3000), np.arange(3000, dtype=np.uint32))  # new keys into the loaded layout
+    p.find(q)
+    p.check_state()
