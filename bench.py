@@ -215,7 +215,7 @@ def main():
     if sharded:
         from paper_2510_15095_b200.sharded import P2PShardedHive, ShardedHive
         if args.exchange == "p2p":
-            sh = P2PShardedHive(nb * 32, region=n, lf_grow=2.0, lf_shrink=0)
+            sh = P2PShardedHive(nb * 32, region=P2PShardedHive.padded_region(n, world), lf_grow=2.0, lf_shrink=0)
         else:
             sh = ShardedHive(nb * 32, batch_max=n, lf_grow=2.0, lf_shrink=0)
         table = sh.table
@@ -475,7 +475,8 @@ def run_cfg5(args, rank: int, world: int, local: int):
     per = total // world
     B = min(1 << 26, per)
     nb = -(-per * 100 // (95 * 32))
-    sh = (P2PShardedHive(nb * 32, region=B, lf_grow=2.0, lf_shrink=0) if args.exchange == "p2p"
+    sh = (P2PShardedHive(nb * 32, region=P2PShardedHive.padded_region(B, world), lf_grow=2.0, lf_shrink=0)
+          if args.exchange == "p2p"
           else ShardedHive(nb * 32, batch_max=B, lf_grow=2.0, lf_shrink=0))
     rng = np.random.default_rng(505 + rank)
     ins, fnd, era = [], [], []

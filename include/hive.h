@@ -352,14 +352,36 @@ hive_status hive_unroute(const uint32_t* d_pos, uint64_t n, const uint8_t* d_in8
  * must be <= 2^32 (positions are 32-bit). */
 
 /* Stable route of this rank's batch into the owners' inboxes (shard(k) as in
- * hive_route), then cnt[rank] on every owner.  d_pos uint32[n]: p * region +
- * (position in this rank's region of owner p), the hive_unroute index into
- * res8 / res32.  d_counts uint64[n_shards]: records sent per owner (device).
- * d_ops / peer_ops nullable together.  n <= region. */
+ * hive_route), then cnt[rank] on every owner (records stored, <= region).
+ * d_pos uint32[n]: p * region + (position in this rank's region of owner p),
+ * the hive_unroute index into res8 / res32; an op past its region's capacity
+ * is not sent and gets d_pos = 0xFFFFFFFF (use hive_unroute_pad).  d_counts
+ * uint64[n_shards]: ops per owner before clipping (device).  d_ops / peer_ops
+ * nullable together. */
 hive_status hive_route_p2p(uint32_t n_shards, uint32_t rank, uint32_t seed, const uint32_t* d_keys,
                            const uint32_t* d_vals, const uint8_t* d_ops, uint64_t n, uint64_t region,
                            uint64_t* const* peer_kv, uint8_t* const* peer_ops, uint64_t* const* peer_cnt,
                            uint32_t* d_pos, uint64_t* d_counts, void* stream);
+/* Owner, device-count form (no host synchronisation): compact the n_src inbox
+ * regions by the device counts d_cnt, run this handle's op of `kind`
+ * (0 find, 1 insert, 2 erase, 3 mixed: opcodes from d_inbox_ops) on the union
+ * batch in source-rank order, and store every result straight into its
+ * source's result region (peer_res32 for find / mixed, peer_res8 always).
+ * Scratch (18 B per inbox record) is owned by the handle, grown on first use.
+ * The host waits only if the op itself needs a count (growth / contraction
+ * enabled).  HIVE_EINVAL on sharded (NCCL) handles. */
+hive_status hive_serve_inbox(hive_t h, uint32_t kind, uint32_t n_src, uint32_t rank, uint64_t region,
+                             const uint64_t* d_inbox_kv, const uint8_t* d_inbox_ops, const uint64_t* d_cnt,
+                             uint32_t* const* peer_res32, uint8_t* const* peer_res8, void* stream);
+/* hive_unroute for a route that can leave ops unsent (region capacity):
+ * pos == 0xFFFFFFFF gives out8 = miss8 and out32 = 0.  d_poison (nullable):
+ * a device word -- the peer exchange's timeout marker -- that, when non-zero
+ * at execution time, turns every out8 into 6 (peer lost) and out32 into 0,
+ * so results of an exchange that timed out are never returned as valid
+ * without a host synchronisation. */
+hive_status hive_unroute_pad(const uint32_t* d_pos, uint64_t n, const uint8_t* d_in8, uint8_t* d_out8,
+                             const uint32_t* d_in32, uint32_t* d_out32, uint8_t miss8, const uint64_t* d_poison,
+                             void* stream);
 /* Owner: concatenate the n_src inbox regions (cnt[r] records each, rank order)
  * into d_keys / d_vals / d_ops [n_total = sum cnt] (d_ops with d_inbox_ops). */
 hive_status hive_inbox_compact(uint32_t n_src, uint64_t region, const uint64_t* d_inbox_kv,

@@ -289,6 +289,15 @@ struct hive_table_s {
     } sh;
     bool sharded() const { return sh.comm != nullptr; }
 
+    // ---- peer-memory exchange (NEXT-1) owner scratch, sized n_src * region ----
+    struct Inbox {
+        uint64_t cap = 0;
+        void* base = nullptr;
+        uint32_t *kc = nullptr, *vc = nullptr, *back = nullptr, *r32c = nullptr;
+        uint8_t *oc = nullptr, *r8c = nullptr;
+        uint64_t* n_dev = nullptr;
+    } ib;
+
     uint64_t nb() const { return (1ull << m) + split; }
     TableView tv() const {
         return TableView{(uint64_t*)va, (uint32_t)((1ull << m) - 1), split, (uint64_t*)sp.va, hkind()};
@@ -908,6 +917,32 @@ hive_status a2a(hive_table_s* h, const void* send, void* recv, size_t count, int
     return HIVE_OK;
 }
 
+// The owner's PHASED batch over a compacted received batch whose length is
+// the device word n_dev (n_upper bounds it): the host waits only where the
+// phase itself needs a count (growth / contraction enabled).
+hive_status owner_phase(hive_table_s* h, int kind, const uint8_t* oc, const uint32_t* kc, const uint32_t* vc,
+                        uint64_t n_upper, const uint64_t* n_dev, uint8_t* r8c, uint32_t* r32c, cudaStream_t s) {
+    switch (kind) {
+        case SK_INSERT:
+            if (h->cfg.lf_grow < 1.0f) {             // growth needs the union batch size on the host
+                CK(cudaMemcpyAsync(h->stage_h, n_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+                CKS(read_ctrl(h, s));
+                if (h->stage_h[0]) CKS(grow_known(h, h->ctrl_h->count, h->stage_h[0], s));
+            }
+            return insert_phase(h, kc, vc, nullptr, nullptr, n_upper, n_dev, n_upper, r8c, nullptr, s);
+        case SK_FIND: {
+            Prof p(h, "k_find", s);
+            CK(launch_find(h->grids, s, kc, nullptr, n_upper, n_dev, h->tv(), h->sv(), r32c, r8c));
+            return HIVE_OK;
+        }
+        case SK_ERASE:
+            CKS(erase_phase(h, kc, nullptr, n_upper, n_dev, n_upper, r8c, nullptr, s));
+            return shrink_after(h, s);
+        default:
+            return mixed_impl(h, oc, kc, vc, n_upper, n_dev, r32c, r8c, s);
+    }
+}
+
 // One collective op of a sharded handle: route -> all-to-all -> owner phase on
 // the union batch (rank order) -> all-to-all back -> unpermute.  Stream-
 // ordered; the host waits only where the local phase itself needs a count
@@ -946,27 +981,7 @@ hive_status shard_call(hive_table_s* h, int kind, const uint8_t* d_op, const uin
         CK(launch_owner_compact(s, G, cap, S.recv_kv, mixed ? S.recv_op : nullptr, S.cnt_recv, S.kc, S.vc,
                                 mixed ? S.oc : nullptr, S.back, S.n_dev));
     }
-    switch (kind) {
-        case SK_INSERT:
-            if (h->cfg.lf_grow < 1.0f) {             // growth needs the union batch size on the host
-                CK(cudaMemcpyAsync(h->stage_h, S.n_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-                CKS(read_ctrl(h, s));
-                if (h->stage_h[0]) CKS(grow_known(h, h->ctrl_h->count, h->stage_h[0], s));
-            }
-            CKS(insert_phase(h, S.kc, S.vc, nullptr, nullptr, tot, S.n_dev, tot, S.r8c, nullptr, s));
-            break;
-        case SK_FIND: {
-            Prof p(h, "k_find", s);
-            CK(launch_find(h->grids, s, S.kc, nullptr, tot, S.n_dev, h->tv(), h->sv(), S.r32c, S.r8c));
-            break;
-        }
-        case SK_ERASE:
-            CKS(erase_phase(h, S.kc, nullptr, tot, S.n_dev, tot, S.r8c, nullptr, s));
-            CKS(shrink_after(h, s));
-            break;
-        default:
-            CKS(mixed_impl(h, S.oc, S.kc, S.vc, tot, S.n_dev, S.r32c, S.r8c, s));
-    }
+    CKS(owner_phase(h, kind, S.oc, S.kc, S.vc, tot, S.n_dev, S.r8c, S.r32c, s));
     {
         Prof p(h, "k_owner_return", s);
         CK(launch_owner_return(s, tot, S.n_dev, S.back, S.r8c, vals32 ? S.r32c : nullptr, S.ret8,
@@ -983,7 +998,7 @@ hive_status shard_call(hive_table_s* h, int kind, const uint8_t* d_op, const uin
     if (n && (out8 || out32)) {
         Prof p(h, "k_unroute_pad", s);
         CK(launch_unroute_pad(s, S.pos, n, S.rr8, out8, out32 ? S.rr32 : nullptr, out32,
-                              kind == SK_FIND ? 2 : 4));
+                              kind == SK_FIND ? 2 : 4, nullptr));
     }
     return HIVE_OK;
 }
@@ -1149,6 +1164,7 @@ hive_status hive_destroy(hive_t h) {
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (h->sh.base) cudaFree(h->sh.base);
+    if (h->ib.base) cudaFree(h->ib.base);
     if (h->ctrl_h) cudaFreeHost(h->ctrl_h);
     if (h->stage_h) cudaFreeHost(h->stage_h);
     for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -1539,7 +1555,7 @@ hive_status hive_route_p2p(uint32_t n_shards, uint32_t rank, uint32_t seed, cons
                            uint32_t* d_pos, uint64_t* d_counts, void* stream) {
     PeerDest pd;
     if (!fill_peers(pd, n_shards, region, rank) || !peer_kv || !peer_cnt || !d_counts) return HIVE_EINVAL;
-    if (n > region || (n && (!d_keys || !d_pos))) return HIVE_EINVAL;
+    if (n && (!d_keys || !d_pos)) return HIVE_EINVAL;
     for (uint32_t p = 0; p < n_shards; ++p) {
         if (!peer_kv[p] || !peer_cnt[p] || (d_ops && (!peer_ops || !peer_ops[p]))) return HIVE_EINVAL;
         pd.kv[p] = peer_kv[p];
@@ -1554,6 +1570,61 @@ hive_status hive_route_p2p(uint32_t n_shards, uint32_t rank, uint32_t seed, cons
     if (!rs.info) CK(cudaMalloc((void**)&rs.info, 2 * MAX_PARTS * sizeof(uint64_t)));
     CK(launch_route_p2p(s, n_shards, seed, d_keys, d_vals, d_ops, n, rs.cnt, rs.info, d_pos, pd));
     CK(cudaMemcpyAsync(d_counts, rs.info, n_shards * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    return HIVE_OK;
+}
+
+hive_status hive_serve_inbox(hive_t h, uint32_t kind, uint32_t n_src, uint32_t rank, uint64_t region,
+                             const uint64_t* d_inbox_kv, const uint8_t* d_inbox_ops, const uint64_t* d_cnt,
+                             uint32_t* const* peer_res32, uint8_t* const* peer_res8, void* stream) {
+    PeerDest pd;
+    if (!h || h->sharded() || kind > 3 || !fill_peers(pd, n_src, region, rank) || !d_inbox_kv || !d_cnt)
+        return HIVE_EINVAL;
+    static const int kinds[4] = {SK_FIND, SK_INSERT, SK_ERASE, SK_MIXED};    // API order -> internal
+    const int sk = kinds[kind];
+    if (sk == SK_MIXED && !d_inbox_ops) return HIVE_EINVAL;
+    const bool vals32 = sk == SK_FIND || sk == SK_MIXED;
+    for (uint32_t p = 0; p < n_src; ++p) {
+        if (!peer_res8 || !peer_res8[p] || (vals32 && (!peer_res32 || !peer_res32[p]))) return HIVE_EINVAL;
+        pd.res8[p] = peer_res8[p];
+        pd.res32[p] = vals32 ? peer_res32[p] : nullptr;
+    }
+    BusyGuard g(h);
+    if (!g.ok) return HIVE_EBUSY;
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last = s;
+    auto& I = h->ib;
+    const uint64_t tot = (uint64_t)n_src * region;
+    if (I.cap < tot) {                         // one allocation, carved (allocator calls are slow here)
+        if (I.base) CK(cudaFree(I.base));
+        I = hive_table_s::Inbox{};
+        const uint64_t a = (tot * 4 + 255) / 256 * 256, b = (tot + 255) / 256 * 256;
+        cudaError_t e = cudaMalloc(&I.base, 4 * a + 2 * b + 256);
+        if (e != cudaSuccess) { set_err(e, "cudaMalloc(inbox scratch)", __LINE__); return HIVE_ENOMEM; }
+        char* q = (char*)I.base;
+        I.kc = (uint32_t*)q; I.vc = (uint32_t*)(q + a); I.back = (uint32_t*)(q + 2 * a);
+        I.r32c = (uint32_t*)(q + 3 * a); I.oc = (uint8_t*)(q + 4 * a); I.r8c = (uint8_t*)(q + 4 * a + b);
+        I.n_dev = (uint64_t*)(q + 4 * a + 2 * b);
+        I.cap = tot;
+    }
+    {
+        Prof p(h, "k_owner_compact", s);
+        CK(launch_owner_compact(s, n_src, region, d_inbox_kv, sk == SK_MIXED ? d_inbox_ops : nullptr, d_cnt, I.kc,
+                                I.vc, sk == SK_MIXED ? I.oc : nullptr, I.back, I.n_dev));
+    }
+    CKS(owner_phase(h, sk, I.oc, I.kc, I.vc, tot, I.n_dev, I.r8c, I.r32c, s));
+    Prof p(h, "k_return_p2p", s);
+    CK(launch_return_p2p_back(s, tot, I.n_dev, region, I.back, vals32 ? I.r32c : nullptr, I.r8c, pd));
+    return HIVE_OK;
+}
+
+hive_status hive_unroute_pad(const uint32_t* d_pos, uint64_t n, const uint8_t* d_in8, uint8_t* d_out8,
+                             const uint32_t* d_in32, uint32_t* d_out32, uint8_t miss8, const uint64_t* d_poison,
+                             void* stream) {
+    if (n == 0) return HIVE_OK;
+    if (!d_pos || ((d_out8 != nullptr) != (d_in8 != nullptr)) || ((d_out32 != nullptr) != (d_in32 != nullptr)))
+        return HIVE_EINVAL;
+    CK(launch_unroute_pad((cudaStream_t)stream, d_pos, n, d_in8, d_out8, d_in32, d_out32, miss8,
+                          (const unsigned long long*)d_poison));
     return HIVE_OK;
 }
 

@@ -1927,11 +1927,16 @@ k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __rest
                 // owner p's inbox, this rank's region: a remote store over NVLink
                 // (a local one when p is this rank); the stable rank keeps the
                 // (rank, index) order the owner's PHASED batch relies on
+                // (an op past the region's capacity is not sent: pos = NO_POS)
                 const uint64_t rel = pos - part_info[MAX_PARTS + p];
-                const uint64_t at = (uint64_t)pd.rank * pd.region + rel;
-                pd.kv[p][at] = ((uint64_t)(vals ? vals[i] : 0u) << 32) | keys[i];
-                if (pd.ops[p]) pd.ops[p][at] = ops[i];
-                pos_out[i] = (uint32_t)((uint64_t)p * pd.region + rel);
+                if (rel < pd.region) {
+                    const uint64_t at = (uint64_t)pd.rank * pd.region + rel;
+                    pd.kv[p][at] = ((uint64_t)(vals ? vals[i] : 0u) << 32) | keys[i];
+                    if (pd.ops[p]) pd.ops[p][at] = ops[i];
+                    pos_out[i] = (uint32_t)((uint64_t)p * pd.region + rel);
+                } else {
+                    pos_out[i] = NO_POS;
+                }
             } else {
                 send_kv[pos] = ((uint64_t)(vals ? vals[i] : 0u) << 32) | keys[i];
                 if (send_ops) send_ops[pos] = ops[i];
@@ -2360,11 +2365,13 @@ k_owner_return(uint64_t n, const uint64_t* __restrict__ n_dev, const uint32_t* _
 __global__ void __launch_bounds__(BLOCK)
 k_unroute_pad(const uint32_t* __restrict__ pos, uint64_t n, const uint8_t* __restrict__ in8,
               uint8_t* __restrict__ out8, const uint32_t* __restrict__ in32, uint32_t* __restrict__ out32,
-              uint8_t miss8) {
+              uint8_t miss8, const unsigned long long* __restrict__ poison) {
+    // a set poison word (peer-exchange timeout marker): no result is trusted
+    const bool lost = poison && *(volatile const unsigned long long*)poison != 0;
     for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (uint64_t)gridDim.x * BLOCK) {
         const uint32_t p = pos[i];
-        const bool ok = p != NO_POS;
-        if (out8) out8[i] = ok ? in8[p] : miss8;
+        const bool ok = p != NO_POS && !lost;
+        if (out8) out8[i] = ok ? in8[p] : (lost ? HIVE_RESULT_PEER_LOST : miss8);
         if (out32) out32[i] = ok ? in32[p] : 0u;
     }
 }
@@ -2398,10 +2405,11 @@ cudaError_t launch_owner_return(cudaStream_t s, uint64_t n_upper, const uint64_t
 }
 
 cudaError_t launch_unroute_pad(cudaStream_t s, const uint32_t* pos, uint64_t n, const uint8_t* in8, uint8_t* out8,
-                               const uint32_t* in32, uint32_t* out32, uint8_t miss8) {
+                               const uint32_t* in32, uint32_t* out32, uint8_t miss8,
+                               const unsigned long long* poison) {
     if (n == 0) return cudaSuccess;
     const int grid = clamp_grid(148 * 8, n, BLOCK);
-    k_unroute_pad<<<grid, BLOCK, 0, s>>>(pos, n, in8, out8, in32, out32, miss8);
+    k_unroute_pad<<<grid, BLOCK, 0, s>>>(pos, n, in8, out8, in32, out32, miss8, poison);
     return cudaGetLastError();
 }
 
@@ -2500,10 +2508,41 @@ cudaError_t launch_stash_reset(cudaStream_t s, StashView sv) {
 // ---- NEXT-1 peer-memory exchange -------------------------------------
 // Per-source count of this rank's records, written into every owner's count
 // array (remote stores), after the scatter in stream order.
-__global__ void k_p2p_counts(const uint64_t* __restrict__ part_info, uint32_t n_shards, PeerDest pd) {
+__global__ void k_p2p_counts(const uint64_t* __restrict__ part_info, uint32_t n_shards, PeerDest pd,
+                             unsigned long long* xfail) {
     const uint32_t p = threadIdx.x;
-    if (p < n_shards) pd.cnt[p][pd.rank] = part_info[p];
+    unsigned long long over = 0;
+    if (p < n_shards) {
+        const uint64_t c = part_info[p];
+        pd.cnt[p][pd.rank] = c < pd.region ? c : pd.region;       // records actually stored
+        over = c > pd.region ? c - pd.region : 0;
+    }
+    over = warp_sum(over);
+    if (p == 0 && over && xfail) atomicAdd(xfail, over);
     __threadfence_system();
+}
+
+// Owner, device-count form: result j of the compacted inbox batch goes back to
+// the source region its record came from (back[j] = source * region + slot).
+__global__ void __launch_bounds__(BLOCK)
+k_return_p2p_back(const uint64_t* __restrict__ n_dev, uint64_t region, const uint32_t* __restrict__ back,
+                  const uint32_t* __restrict__ res32, const uint8_t* __restrict__ res8, PeerDest pd) {
+    const uint64_t n = *n_dev;
+    for (uint64_t j = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; j < n; j += (uint64_t)gridDim.x * BLOCK) {
+        const uint32_t at = back[j];
+        const uint32_t r = (uint32_t)(at / region);
+        const uint64_t dst = (uint64_t)pd.rank * region + (at - (uint64_t)r * region);
+        if (res32) pd.res32[r][dst] = res32[j];
+        if (res8) pd.res8[r][dst] = res8[j];
+    }
+    __threadfence_system();
+}
+cudaError_t launch_return_p2p_back(cudaStream_t s, uint64_t n_upper, const uint64_t* n_dev, uint64_t region,
+                                   const uint32_t* back, const uint32_t* res32, const uint8_t* res8,
+                                   const PeerDest& pd) {
+    const int grid = clamp_grid(148 * 8, n_upper, BLOCK);
+    k_return_p2p_back<<<grid, BLOCK, 0, s>>>(n_dev, region, back, res32, res8, pd);
+    return cudaGetLastError();
 }
 
 // Region prefix of the n_src per-source counts (n_src <= MAX_PEERS), per block.
@@ -2600,11 +2639,11 @@ cudaError_t launch_p2p_wait(cudaStream_t s, uint32_t n, uint32_t phase, uint64_t
 
 cudaError_t launch_route_p2p(cudaStream_t s, uint32_t n_shards, uint32_t seed, const uint32_t* keys,
                              const uint32_t* vals, const uint8_t* ops, uint64_t n, uint64_t* cnt,
-                             uint64_t* part_info, uint32_t* pos, const PeerDest& pd) {
+                             uint64_t* part_info, uint32_t* pos, const PeerDest& pd, unsigned long long* xfail) {
     cudaError_t e = launch_partition_pd(s, PART_ROUTE_P2P, n_shards, seed, keys, vals, ops, n, cnt, part_info,
                                         nullptr, 0, nullptr, nullptr, pos, nullptr, nullptr, nullptr, nullptr, pd);
     if (e != cudaSuccess) return e;
-    k_p2p_counts<<<1, 32, 0, s>>>(part_info, n_shards, pd);
+    k_p2p_counts<<<1, 32, 0, s>>>(part_info, n_shards, pd, xfail);
     return cudaGetLastError();
 }
 

@@ -124,7 +124,13 @@ uint64_t part_warps(uint64_t n);
 // (remote stores over NVLink), then each owner's per-source count.
 cudaError_t launch_route_p2p(cudaStream_t s, uint32_t n_shards, uint32_t seed, const uint32_t* keys,
                              const uint32_t* vals, const uint8_t* ops, uint64_t n, uint64_t* cnt,
-                             uint64_t* part_info, uint32_t* pos, const PeerDest& pd);
+                             uint64_t* part_info, uint32_t* pos, const PeerDest& pd,
+                             unsigned long long* xfail = nullptr);
+// Owner, device-count form of the result return (after launch_owner_compact
+// over the inbox with cap = region): result j -> source back[j] / region.
+cudaError_t launch_return_p2p_back(cudaStream_t s, uint64_t n_upper, const uint64_t* n_dev, uint64_t region,
+                                   const uint32_t* back, const uint32_t* res32, const uint8_t* res8,
+                                   const PeerDest& pd);
 // Owner: gather the per-source inbox regions into contiguous key / value / op arrays.
 cudaError_t launch_inbox_compact(cudaStream_t s, uint32_t n_src, uint64_t region, const uint64_t* inbox_kv,
                                  const uint8_t* inbox_ops, const uint64_t* cnt, uint64_t n_total,
@@ -189,9 +195,12 @@ cudaError_t launch_owner_compact(cudaStream_t s, uint32_t n_src, uint64_t cap, c
 // (ret8[back[j]] = r8[j], ret32 likewise; either pair may be null).
 cudaError_t launch_owner_return(cudaStream_t s, uint64_t n_upper, const uint64_t* n_dev, const uint32_t* back,
                                 const uint8_t* r8, const uint32_t* r32, uint8_t* ret8, uint32_t* ret32);
-// Source: out8[i] = in8[pos[i]] (pos == NO_POS: out8 = miss8, out32 = 0).
+// Source: out8[i] = in8[pos[i]] (pos == NO_POS: out8 = miss8, out32 = 0; a
+// non-zero *poison marks every op HIVE_RESULT_PEER_LOST).
+constexpr uint8_t HIVE_RESULT_PEER_LOST = 6;
 cudaError_t launch_unroute_pad(cudaStream_t s, const uint32_t* pos, uint64_t n, const uint8_t* in8, uint8_t* out8,
-                               const uint32_t* in32, uint32_t* out32, uint8_t miss8);
+                               const uint32_t* in32, uint32_t* out32, uint8_t miss8,
+                               const unsigned long long* poison = nullptr);
 
 cudaError_t launch_unroute(cudaStream_t s, const uint32_t* pos, uint64_t n, const uint8_t* in8,
                            uint8_t* out8, const uint32_t* in32, uint32_t* out32);

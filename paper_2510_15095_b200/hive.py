@@ -80,6 +80,8 @@ SIGNATURES = {
     "hive_gather_ceiling_rw": (_int, [_vp, _u64, _vp, _u64, _vp, _u32, _vp]),
     "hive_route_p2p": (_int, [_u32, _u32, _u32, _vp, _vp, _vp, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hive_inbox_compact": (_int, [_u32, _u64, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
+    "hive_serve_inbox": (_int, [_vp, _u32, _u32, _u32, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hive_unroute_pad": (_int, [_vp, _u64, _vp, _vp, _vp, _vp, ctypes.c_uint8, _vp, _vp]),
     "hive_return_p2p": (_int, [_u32, _u32, _u64, _vp, _u64, _vp, _vp, _vp, _vp, _vp]),
     "hive_p2p_signal": (_int, [_u32, _u32, _u32, _u64, _vp, _vp]),
     "hive_p2p_wait": (_int, [_u32, _u32, _u64, _vp, _u64, _vp]),
@@ -317,6 +319,14 @@ class HiveTable:
                                        _p(_dev(stash, 8)) if n_st else None, n_st, _stream(stream)),
                "hive_load_image")
 
+    def serve_inbox(self, kind: int, n_src: int, rank: int, region: int, inbox_kv: int, inbox_ops: int, cnt: int,
+                    peer_res32, peer_res8, stream=None):
+        """hive_serve_inbox: the owner's side of the peer-memory exchange with
+        device-side counts (kind 0 find, 1 insert, 2 erase, 3 mixed)."""
+        _check(self._L.hive_serve_inbox(self._h, kind, n_src, rank, region, ctypes.c_void_p(inbox_kv),
+                                        ctypes.c_void_p(inbox_ops) if inbox_ops else None, ctypes.c_void_p(cnt),
+                                        _ptrs(peer_res32), _ptrs(peer_res8), _stream(stream)), "hive_serve_inbox")
+
     def shard_info(self) -> tuple[int, int, int]:
         """(nranks, rank, padded exchange capacity per peer); (1, 0, 0) unsharded."""
         g, r, c = _int(), _int(), _u64()
@@ -487,6 +497,14 @@ def unroute_raw(pos, n, in8: int, out8, in32: int, out32, stream=None):
     """hive_unroute with raw device pointers for the inputs (exchange buffers)."""
     _check(lib().hive_unroute(_p(pos), n, ctypes.c_void_p(in8) if in8 else None, _p(out8),
                               ctypes.c_void_p(in32) if in32 else None, _p(out32), _stream(stream)), "hive_unroute")
+
+
+def unroute_pad_raw(pos, n, in8: int, out8, in32: int, out32, miss8: int, poison: int = 0, stream=None):
+    """hive_unroute_pad with raw device pointers for the inputs."""
+    _check(lib().hive_unroute_pad(_p(pos), n, ctypes.c_void_p(in8) if in8 else None, _p(out8),
+                                  ctypes.c_void_p(in32) if in32 else None, _p(out32), miss8,
+                                  ctypes.c_void_p(poison) if poison else None, _stream(stream)),
+           "hive_unroute_pad")
 
 
 def p2p_signal(n, rank, phase, epoch, peer_sig, stream=None):

@@ -96,6 +96,7 @@ class PeerBuffers:
             nbytes = {"cnt": world * 8, "sig": self.SIG_WORDS * 8}.get(name, world * region * width)
             self.ptr[name] = hive.dev_alloc(nbytes)
         _view(self.ptr["sig"], self.SIG_WORDS, torch.int64).zero_()
+        _view(self.ptr["cnt"], world, torch.int64).zero_()
         torch.cuda.synchronize()
         self.owned = True
 
@@ -117,17 +118,30 @@ class PeerBuffers:
 class P2PShardedHive:
     """Hash-partitioned table whose exchange is done by the kernels themselves:
     hive_route_p2p stores each op record straight into its owner's inbox over
-    NVLink, the owner runs one PHASED batch on the compacted inbox, and
-    hive_return_p2p stores the results straight back; the source's
-    hive_unroute restores its op order.  The phases are ordered by device-side
-    signals (hive_p2p_signal / hive_p2p_wait: release stores into the peers'
-    signal words, acquire spins), not host barriers; the one host sync per call
-    is the owner's read of its inbox counts.  Same semantics as ShardedHive: a
-    shard sees the union batch in (rank, index) order.
+    NVLink; hive_serve_inbox compacts the inbox by its DEVICE-side counts, runs
+    one PHASED batch and stores each result straight back into its source's
+    result region; the source's hive_unroute_pad restores its op order.  The
+    phases are ordered by device-side signals (hive_p2p_signal / hive_p2p_wait:
+    release stores into the peers' signal words, acquire spins): with growth
+    off a call has no host synchronisation at all.  A peer that never signals
+    sets the timeout marker, which the unroute kernel turns into result 6 for
+    every op of that call (check() raises and resets it).  Same semantics as
+    ShardedHive: a shard sees the union batch in (rank, index) order.
+
+    `region` = records per (source, owner) region; padded_region(batch_max,
+    world) sizes it like the NCCL path (batch / world * (1 + slack) + 1024), so
+    the buffers cost ~1/world of one region per batch op; an op past its region
+    is not sent (result 4, find found 2).
 
     `virtual_group` builds `world` ranks inside ONE process on one GPU (the
     peers' buffers are then plain local pointers): the tests drive the phases
     of all virtual ranks in lockstep to check the multi-rank logic."""
+
+    KIND = {"find": 0, "insert": 1, "erase": 2, "mixed": 3}        # hive_serve_inbox kinds
+
+    @staticmethod
+    def padded_region(batch_max: int, world: int, slack: float = 0.0625) -> int:
+        return min(batch_max, -(-batch_max * (1 + slack) // world) + 1024) if world > 1 else batch_max
 
     def __init__(self, capacity_per_shard: int, region: int, group=None, seed: int = SHARD_SEED,
                  _virtual=None, **cfg):
@@ -149,6 +163,7 @@ class P2PShardedHive:
         self.table = hive.HiveTable(capacity_per_shard, **cfg)
         self._state = None
         self._epoch = 0
+        self.timeout_ns = 60_000_000_000          # a phase wait gives up after this (then results are 6)
         if _virtual is None:
             dist.barrier(group=group)       # every rank's signal words are zeroed
 
@@ -171,8 +186,6 @@ class P2PShardedHive:
     # ---- the three phases (every rank runs each phase before any runs the next) ----
     def route_phase(self, kind: str, keys, vals=None, ops=None):
         n = keys.numel()
-        if n > self.region:
-            raise hive.HiveError(f"batch of {n} ops exceeds the exchange region ({self.region})")
         if vals is None:
             vals = torch.zeros(n, dtype=torch.uint32, device=keys.device)
         pos = torch.empty(n, dtype=torch.uint32, device=keys.device)
@@ -183,7 +196,10 @@ class P2PShardedHive:
         hive.p2p_signal(self.world, self.rank, 0, self._epoch, self._col("sig"))
         self._state = (kind, n, pos)
 
-    def _check_timeout(self):
+    def check(self):
+        """Raise (and reset the marker) if a peer missed a phase signal; the
+        calls themselves never wait on the host for it (results of such a call
+        are all 6)."""
         sig = _view(self.own.ptr["sig"], PeerBuffers.SIG_WORDS, torch.int64)
         if int(sig[-1].item()):
             sig[-1].zero_()                     # reset the marker: the handle stays usable
@@ -192,47 +208,30 @@ class P2PShardedHive:
 
     def serve_phase(self):
         kind = self._state[0]
-        hive.p2p_wait(self.world, 0, self._epoch, self.own.ptr["sig"])   # every source's records are in
-        cnt = _view(self.own.ptr["cnt"], self.world, torch.int64)
-        n_total = int(cnt.sum().item())
-        self._check_timeout()
-        dev = cnt.device
-        k = torch.empty(max(n_total, 1), dtype=torch.uint32, device=dev)
-        v = torch.empty(max(n_total, 1), dtype=torch.uint32, device=dev)
-        o = torch.empty(max(n_total, 1), dtype=torch.uint8, device=dev) if kind == "mixed" else None
-        hive.inbox_compact(self.world, self.region, self.own.ptr["kv"], self.own.ptr["ops"] if o is not None else 0,
-                           self.own.ptr["cnt"], n_total, k, v, o)
-        k, v = k[:n_total], v[:n_total]
-        r32 = r8 = None
-        if kind == "insert":
-            r8 = self.table.insert(k, v)
-        elif kind == "erase":
-            r8 = self.table.erase(k)
-        elif kind == "find":
-            r32, r8 = self.table.find(k)
-        else:
-            r32, r8 = self.table.mixed(o[:n_total], k, v)
-        hive.return_p2p(self.world, self.rank, self.region, self.own.ptr["cnt"], n_total, r32, r8,
-                        self._col("res32") if r32 is not None else None,
-                        self._col("res8") if r8 is not None else None)
+        hive.p2p_wait(self.world, 0, self._epoch, self.own.ptr["sig"], self.timeout_ns)   # all records are in
+        vals32 = kind in ("find", "mixed")
+        self.table.serve_inbox(self.KIND[kind], self.world, self.rank, self.region, self.own.ptr["kv"],
+                               self.own.ptr["ops"] if kind == "mixed" else 0, self.own.ptr["cnt"],
+                               self._col("res32") if vals32 else None, self._col("res8"))
         hive.p2p_signal(self.world, self.rank, 1, self._epoch, self._col("sig"))
 
     def finish_phase(self):
         kind, n, pos = self._state
         self._state = None
         dev = pos.device
-        hive.p2p_wait(self.world, 1, self._epoch, self.own.ptr["sig"])   # every owner's results are back
-        self._check_timeout()                   # never unroute stale results of a lost owner
+        hive.p2p_wait(self.world, 1, self._epoch, self.own.ptr["sig"], self.timeout_ns)   # all results are back
         out8 = torch.empty(n, dtype=torch.uint8, device=dev)
         out32 = torch.empty(n, dtype=torch.uint32, device=dev) if kind in ("find", "mixed") else None
         if n:
-            hive.unroute_raw(pos, n, self.own.ptr["res8"], out8,
-                             self.own.ptr["res32"] if out32 is not None else 0, out32)
+            # the timeout marker poisons the results instead of a host check
+            hive.unroute_pad_raw(pos, n, self.own.ptr["res8"], out8,
+                                 self.own.ptr["res32"] if out32 is not None else 0, out32,
+                                 2 if kind == "find" else 4, self.own.ptr["sig"] + 8 * (PeerBuffers.SIG_WORDS - 1))
         return out8, out32
 
     def _call(self, kind, keys, vals=None, ops=None):
-        # no host barrier: the phases are ordered by the device-side signals;
-        # the only host synchronisation is the owner's read of its inbox counts
+        # no host barrier and no host synchronisation: the phases are ordered
+        # by the device-side signals, the owner works from device-side counts
         self.route_phase(kind, keys, vals, ops)
         self.serve_phase()
         return self.finish_phase()

@@ -87,13 +87,45 @@ def test_p2p_exchange_matches_oracle_on_union_batch(world):
             t.close()
 
 
-def test_p2p_rejects_oversized_batch():
+def test_p2p_region_overflow_reports_unsent_ops():
+    """A batch larger than its (source, owner) region: the ops past the region
+    are not sent (find found = 2, insert status 4), every sent op is exact."""
+    from gpu_util import np8, np32
+    from paper_2510_15095_b200 import u32
+    from paper_2510_15095_b200.sharded import P2PShardedHive
+    ranks = P2PShardedHive.virtual_group(1, 64 * 32, 100, lf_grow=2.0, lf_shrink=0)
+    try:
+        keys = gen.present_keys(130)
+        (st, _), = _run(ranks, "insert", [(u32(keys), u32(keys))])
+        st = np8(st)
+        assert (st[:100] == 0).all() and (st[100:] == 4).all()
+        (f, v), = _run(ranks, "find", [(u32(keys),)])
+        f, v = np8(f), np32(v)
+        assert (f[:100] == 1).all() and (v[:100] == keys[:100]).all() and (f[100:] == 2).all()
+    finally:
+        for t in ranks:
+            t.close()
+
+
+def test_p2p_lost_peer_poisons_results_without_host_sync():
+    """an owner that never answers must not let stale
+    results through.  Rank 1 never routes, so rank 0's phase waits time out;
+    the unroute kernel sees the timeout marker and reports 6 for every op
+    (no host check inside the call), and check() raises and resets it."""
+    from gpu_util import np8
     from paper_2510_15095_b200 import HiveError, u32
     from paper_2510_15095_b200.sharded import P2PShardedHive
-    ranks = P2PShardedHive.virtual_group(2, 64 * 32, 100)
+    ranks = P2PShardedHive.virtual_group(2, 64 * 32, 1000)
     try:
+        r0 = ranks[0]
+        r0.timeout_ns = 2_000_000                # 2 ms
+        r0.route_phase("find", u32(gen.present_keys(500)))
+        r0.serve_phase()
+        f, _ = r0.finish_phase()
+        assert (np8(f) == 6).all()
         with pytest.raises(HiveError):
-            ranks[0].route_phase("find", u32(np.arange(101, dtype=np.uint32)))
+            r0.check()
+        r0.check()                               # the marker was reset
     finally:
         for t in ranks:
             t.close()
