@@ -329,6 +329,7 @@ def main():
                                   "8 B per spill/stash word, exact key/value/result streams"}
     if not sharded:
         roofline["ceilings"] = gather_ceiling(queries, nb, dev, per_kernel, hbm_peak)
+        roofline["byte_model"] = byte_model(table, n, st, prof, dev)
 
     # ---- e2e through the public API with host buffers (pinned) ---------------------------
     e2e = None
@@ -538,6 +539,45 @@ def run_cfg5(args, rank: int, world: int, local: int):
                        "l2": "inputs and tables larger than L2 (no flush)"},
             "clocks": clk.summary(), "count_total": int(cnt.item())}), flush=True)
     dist.destroy_process_group()
+
+
+def byte_model(table, n, st, prof, dev):
+    """DESIGN.md §6 byte model of the two probe kernels, checked against the
+    bytes the kernels count.  Rates are measured separately on the built cfg2
+    table: f_fp = share of absent-key lookups whose b1 spill word lets them read
+    b2 (the spill filter's false-positive rate), r2_hit = share of present-key
+    lookups that read b2 (= 1 - p_h1 up to the stash).  Model, per lookup of a
+    batch with hit rate h:  9 (key, value, found) + 264 (b1 + spill word)
+    + 256 * (h * r2_hit + (1 - h) * f_fp) + 16 * (stash index probes).
+    Insert (new key, owner election on), per op: 10 (key, value, status, flag)
+    + 264 + 32 (claim CAS sector) + 256 * r_b2 + 8 * r_spill, where r_b2 = share
+    of inserts that read b2 (b1 full, or a spill word allowing a b2 match) and
+    r_spill = share placed in b2 (spill-word atomicOr)."""
+    import torch
+
+    from paper_2510_15095_b200 import u32
+    m = 1 << 22
+    pres = u32(gen.keys_of(np.random.default_rng(5).integers(0, n, m, dtype=np.uint64).astype(np.uint32)), dev)
+    absn = u32(gen.absent_keys(m), dev)
+    out = {}
+    for name, q in (("present", pres), ("absent", absn)):
+        a0 = table.stats()["alg_bytes"]["find"]
+        table.find(q)
+        torch.cuda.synchronize()
+        out[name] = (table.stats()["alg_bytes"]["find"] - a0) / m
+    r2_hit = (out["present"] - 273) / 256
+    f_fp = (out["absent"] - 273) / (256 + 16)
+    counted_find = st["alg_bytes"]["find"] / n
+    pred_find = 273 + 256 * (0.5 * r2_hit + 0.5 * f_fp) + 8 * f_fp
+    counted_ins = st["alg_bytes"]["insert"] / n
+    bucket_keys = max(1, st["count"] - st["stash_used"])
+    return {"p_h1": st["in_b1"] / bucket_keys, "r2_hit": r2_hit, "f_fp": f_fp,
+            "find_counted_B_per_op": counted_find, "find_model_B_per_op": pred_find,
+            "find_model_vs_counted": pred_find / counted_find,
+            "insert_counted_B_per_op": counted_ins,
+            "insert_r_b2_plus_spill": (counted_ins - 306) / 256,
+            "lost_or_full_claims_per_op": st["leftovers"] / n,
+            "survey_two_probe_model_B_per_op": {"find": 416, "insert": 553}}
 
 
 def gather_ceiling(keys, nb, dev, per_kernel, hbm_peak, reps=5):

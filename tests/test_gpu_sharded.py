@@ -134,18 +134,24 @@ def test_cfg5_sequence_world1_shard_dump_vs_oracle(pg):
     hits, erase 2^(T-3)) through the sharded handle, every result and the
     shard's sorted dump against a per-shard oracle fed the ops routed to it."""
     import oracle
+    from gpu_util import first_diff
     from paper_2510_15095_b200 import u32
     from paper_2510_15095_b200.sharded import ShardedHive
     T, B = 22, 1 << 20
     total = 1 << T
     nb = -(-total * 100 // (95 * 32))
     sh = ShardedHive(nb * 32, batch_max=B, lf_grow=2.0, lf_shrink=0)
-    o = oracle.OracleTable(nb * 32, lf_grow=2.0, lf_shrink=0)
+    # the bench's cfg5 sizing leaves a split state (m = 17, split = 6,899): its unsplit buckets are
+    # over-subscribed and the oracle's paper-literal victim rule overflows a 2% stash there; stash
+    # capacity changes no result unless it overflows, so only the oracle gets a 30% stash
+    o = oracle.OracleTable(nb * 32, lf_grow=2.0, lf_shrink=0, stash_fraction=0.30)
     rng = np.random.default_rng(505)
     for lo in range(0, total, B):
         ids = np.arange(lo, lo + B, dtype=np.uint32)
         k, v = gen.keys_of(ids), gen.vals_of(ids)
-        assert (_np(sh.insert(u32(k), u32(v))) == o.insert(k, v)).all()
+        sg, so = _np(sh.insert(u32(k), u32(v))), o.insert(k, v)
+        assert (sg == so).all(), (lo, first_diff("insert status", sg, so, k), np.bincount(sg), np.bincount(so),
+                                  sh.table.stats())
     for b in range(total // B):
         hit = rng.integers(0, total, B // 2, dtype=np.uint64)
         miss = (1 << 31) + b * (B // 2) + np.arange(B // 2, dtype=np.uint64)
