@@ -1,5 +1,5 @@
-"""compute-sanitizer memcheck / racecheck over a small workload that touches
-every kernel family."""
+"""compute-sanitizer memcheck / racecheck / synccheck over a small workload that
+touches every kernel family."""
 import os
 import shutil
 import subprocess
@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
 def test_compute_sanitizer(tool):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")

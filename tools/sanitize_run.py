@@ -13,6 +13,14 @@ for b in range(6):
     t.mixed(u8(ops), u32(keys), u32(keys ^ 7))
 k = u32(gen.present_keys(5000))
 t.insert(k, k); t.find(k); t.erase(k[:4000])
+# NEXT-4 monolithic kernel (cooperative launch) and the NEXT-2 clock64 variants
+for b in range(3):
+    n = 3000
+    keys = rng.integers(0, 4000, n, dtype=np.uint64).astype(np.uint32)
+    t.mixed_concurrent(u8(gen.bernoulli_ops(n, 0.4, 0.2, seed=50 + b)), u32(keys), u32(keys ^ 9))
+t.profile(2)
+t.insert(u32(gen.present_keys(6000)), u32(gen.present_keys(6000)))
+t.profile(False)
 u = HiveTable(16 * 32, lf_grow=2.0, lf_shrink=0)        # overfull: Steps 3-4
 kk = u32(gen.present_keys(16 * 32 + 200))
 u.insert(kk, kk); u.find(kk); u.erase(kk[:100])
