@@ -194,6 +194,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
+    if sharded:
+        print(f"[bench] rank {rank}: torch.distributed nccl world {dist.get_world_size()}", file=sys.stderr,
+              flush=True)
 
     n = 1 << args.n_log2
     nb = -(-n * 100 // (95 * 32)) if args.n_log2 != 26 else gen.CFG2_BUCKETS
@@ -219,6 +222,9 @@ def main():
         else:
             sh = ShardedHive(nb * 32, batch_max=n, lf_grow=2.0, lf_shrink=0)
         table = sh.table
+        g_, r_, c_ = table.shard_info()
+        print(f"[bench] rank {rank}: sharded handle nranks={g_} rank={r_} cap_per_peer={c_} "
+              f"exchange={args.exchange}", file=sys.stderr, flush=True)
 
         def step():
             table.clear()

@@ -381,7 +381,8 @@ k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ id
         const uint32_t hk = fmix32(k ^ DEDUP_SEED);
         uint64_t* tab = dd.sub(hk);
         uint64_t h = hk & dd.mask;
-        for (uint64_t probe = 0; probe <= dd.mask; ++probe) {
+        uint64_t probe = 0;
+        for (; probe <= dd.mask; ++probe) {
             const uint64_t prev = cas64(&tab[h], EMPTY, word);
             ab += 32;
             if (prev == EMPTY) break;
@@ -393,6 +394,7 @@ k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ id
             }
             h = (h + 1) & dd.mask;
         }
+        if (probe > dd.mask) atomicAdd(&ctrl->eover, 1ull);   // table full: never at the sizing (stats)
     }
     block_add(&ctrl->abytes[AB_ELECT], ab);
 }
@@ -427,7 +429,8 @@ k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict
         const uint32_t hk = fmix32(k ^ DEDUP_SEED);
         uint64_t* tab = dd.sub(hk);
         uint64_t h = hk & dd.mask;
-        for (uint64_t probe = 0; probe <= dd.mask; ++probe) {
+        uint64_t probe = 0;
+        for (; probe <= dd.mask; ++probe) {
             const uint64_t prev = cas64(&tab[h], EMPTY, word);
             ab += 32;
             if (prev == EMPTY) break;
@@ -439,6 +442,7 @@ k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict
             }
             h = (h + 1) & dd.mask;
         }
+        if (probe > dd.mask) atomicAdd(&ctrl->eover, 1ull);   // table full: never at the sizing (stats)
     }
     block_add(&ctrl->abytes[AB_ELECT], ab);
 }
