@@ -1428,12 +1428,26 @@ k_mixed_mono(const uint8_t* __restrict__ opc, const uint32_t* __restrict__ keys,
         const bool stash_on = sv.ctrl->stash_tail != 0;
         unsigned long long added = 0, removed = 0;
         const uint64_t warp = tid >> 5, nw = nthreads >> 5;
-        for (uint64_t base = warp * WG::GPW; base < n; base += nw * WG::GPW) {
+        const uint64_t stride = nw * WG::GPW;
+        bool pend = false;                       // optimistic claim issued last iteration
+        uint64_t pend_prev = EMPTY;
+        uint32_t pend_item = 0;
+        // software pipeline: the next iteration's (opcode, key, value) loads are
+        // in flight while this iteration probes
+        uint32_t o_n = 3u, k_n = INVALID_KEY, v_n = 0;
+        auto fetch = [&](uint64_t tt) {
+            o_n = tt < n ? opc[tt] : 3u;
+            k_n = tt < n ? keys[tt] : INVALID_KEY;
+            v_n = tt < n ? vals[tt] : 0u;
+        };
+        fetch(warp * WG::GPW + wg.gi);
+        for (uint64_t base = warp * WG::GPW; base < n; base += stride) {
             const uint64_t t = base + wg.gi;
             const bool active = t < n;
-            const uint32_t o = active ? opc[t] : 3u;
-            const uint32_t k = active ? keys[t] : INVALID_KEY;
-            const uint32_t v = active && o == 1 ? vals[t] : 0u;
+            const uint32_t o = active ? o_n : 3u;
+            const uint32_t k = active ? k_n : INVALID_KEY;
+            const uint32_t v = o == 1 ? v_n : 0u;
+            fetch(t + stride);
             bool valid = o < 3 && k != INVALID_KEY;
             if (active && wg.gl == 0) {
                 vals_out[t] = 0;
@@ -1507,34 +1521,24 @@ k_mixed_mono(const uint8_t* __restrict__ opc, const uint32_t* __restrict__ keys,
                 if (sdone && is_find) val = sval;
                 done |= sdone;
             }
-            // inserts of absent keys: claim in b1 at the slot the Step-1 scan
-            // found free (rotated lane / slot), checked at once; a lost claim
-            // re-reads b1 and claims by the WABC loop; then b2 (first-fit, A-21)
+            // resolve last iteration's optimistic claim: a lost one goes to
+            // the Step 3-4 stage (an insert placed there is linearized after
+            // every find and erase of the batch, when its key is still absent)
+            wl.push(pend && pend_prev != EMPTY, pend_item, leftover, &sv.ctrl->n_left);
+            pend = false;
+            // inserts of absent keys: optimistic WABC claim in b1 at the slot the
+            // Step-1 scan found free, then b2 (first-fit, A-21), as k_insert_fast
             const bool want1 = is_ins && !done;
-            bool placed = false;
-            {
-                const uint32_t F = wg.ballot(want1 && jf1 < SPL);
-                bool ok = false;
-                if (want1 && F && wg.gl == first_rot<G>(F, lrot)) {
-                    ok = cas64(wg.slot_ptr(tv.bucket(b1)) + jf1, EMPTY, kv) == EMPTY;
-                    ab += 32;
-                }
-                placed = wg.ballot(ok) != 0;
-                const bool retry = want1 && F != 0 && !placed;
-                if (__any_sync(FULL, retry)) {
-                    if (retry) load_slots<SPL>(wg.slot_ptr(tv.bucket(b1)), sl);
-                    else fill_empty<SPL>(sl);
-                    if (retry && wg.gl == 0) ab += 256;
-                    have2 = false;
-                    placed |= wabc_claim<G>(wg, sl, tv.bucket(b1), kv, retry, ab);
-                }
-            }
+            bool placed = wabc_claim_issue<G>(wg, jf1, tv.bucket(b1), kv, want1, pend, pend_prev, pend_item,
+                                              (uint32_t)t, ab, lrot);
             const bool want2 = want1 && !placed && b2 != b1;
             if (__any_sync(FULL, want2)) {
                 if (want2 && !have2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), sl);
-                else if (!want2) fill_empty<SPL>(sl);
                 if (want2 && !have2 && wg.gl == 0) ab += 256;
-                const bool p2 = wabc_claim<G>(wg, sl, tv.bucket(b2), kv, want2, ab);
+                int jm2, jf2 = SPL;
+                if (want2) scan_slots<SPL>(sl, INVALID_KEY, jm2, jf2);
+                const bool p2 = wabc_claim_issue<G>(wg, jf2, tv.bucket(b2), kv, want2, pend, pend_prev, pend_item,
+                                                    (uint32_t)t, ab, lrot);
                 if (p2 && wg.gl == 0) {
                     atomicOr((unsigned long long*)&tv.spill[b1], (unsigned long long)fp);
                     ab += 8;
@@ -1553,6 +1557,7 @@ k_mixed_mono(const uint8_t* __restrict__ opc, const uint32_t* __restrict__ keys,
             }
             wl.push(want1 && !placed && wg.gl == 0, (uint32_t)t, leftover, &sv.ctrl->n_left);
         }
+        wl.push(pend && pend_prev != EMPTY, pend_item, leftover, &sv.ctrl->n_left);
         wl.flush(leftover, &sv.ctrl->n_left);
         block_add(&sv.ctrl->count, added - removed);
     }
