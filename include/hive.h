@@ -72,6 +72,15 @@ typedef enum {
                                  (reading A-26).  Default (flag clear):
                                  BitHash1 / BitHash2 (Listing 1).  Any other
                                  flag bit -> HIVE_EINVAL. */
+#define HIVE_SHARD_DEDUP 4u   /* sharded handles only: elect one owner per (key,
+                                 opcode) among each rank's local batch before
+                                 routing (SURVEY §8(e) Zipf item); only owners
+                                 are exchanged and the other ops copy their
+                                 owner's result.  Results are unchanged; under
+                                 skewed keys the hot key's region holds one
+                                 record per rank instead of all its copies.
+                                 Costs one election pass over the local batch.
+                                 Requires nccl_comm and shard_batch_max < 2^30. */
 
 typedef struct {
     uint64_t capacity;       /* initial slots; rounded up to 32-slot buckets

@@ -286,6 +286,13 @@ struct hive_table_s {
         // host-buffer calls: device staging of the local batch
         uint32_t *hk = nullptr, *hv = nullptr, *ho32 = nullptr;
         uint8_t *ho8 = nullptr, *hop = nullptr;
+        // source-side election (HIVE_SHARD_DEDUP): group table, flags, owners, send list
+        void* sbase = nullptr;
+        uint64_t* stab = nullptr;
+        uint64_t smask = 0;
+        uint8_t* sflag = nullptr;
+        uint32_t *sowner = nullptr, *slist = nullptr;
+        unsigned long long* snlist = nullptr;
     } sh;
     bool sharded() const { return sh.comm != nullptr; }
 
@@ -957,12 +964,34 @@ hive_status shard_call(hive_table_s* h, int kind, const uint8_t* d_op, const uin
     const uint32_t G = (uint32_t)S.nranks;
     const uint64_t cap = S.cap, tot = S.tot;
     const bool mixed = kind == SK_MIXED, vals32 = kind == SK_FIND || kind == SK_MIXED;
+    // source-side owner election (HIVE_SHARD_DEDUP): route one op per (key, opcode)
+    const bool src_dedup = (h->cfg.flags & HIVE_SHARD_DEDUP) && n;
+    if (src_dedup) {
+        if (!S.sbase) {
+            const uint64_t tabn = pow2_at_least(std::max<uint64_t>(1024, 2 * S.batch_max));
+            const uint64_t a = tabn * 8, b = (S.batch_max + 255) / 256 * 256, c = (S.batch_max * 4 + 255) / 256 * 256;
+            cudaError_t e = cudaMalloc(&S.sbase, a + b + 2 * c + 256);
+            if (e != cudaSuccess) { set_err(e, "cudaMalloc(source election)", __LINE__); return HIVE_ENOMEM; }
+            char* q = (char*)S.sbase;
+            S.stab = (uint64_t*)q;
+            S.smask = tabn - 1;
+            S.sflag = (uint8_t*)(q + a);
+            S.sowner = (uint32_t*)(q + a + b);
+            S.slist = (uint32_t*)(q + a + b + c);
+            S.snlist = (unsigned long long*)(q + a + b + 2 * c);
+        }
+        Prof p(h, "k_src_elect", s, 2);
+        static const uint8_t kind_op[4] = {1, 0, 2, 0};            // SK_INSERT, SK_FIND, SK_ERASE, (mixed: opcodes)
+        CK(launch_src_elect(s, mixed ? d_op : nullptr, kind_op[kind], d_keys, n, S.stab, S.smask, S.sflag, S.sowner,
+                            S.slist, S.snlist, h->ctrl));
+    }
     {
         Prof p(h, "k_route_pad", s, 3);
         if (n) {
             CK(launch_route_pad(s, G, HIVE_SHARD_SEED, d_keys, kind == SK_INSERT || mixed ? d_vals : nullptr,
                                 mixed ? d_op : nullptr, n, cap, S.pcnt, S.pinfo, S.send_kv,
-                                mixed ? S.send_op : nullptr, S.pos, S.cnt_send, h->ctrl));
+                                mixed ? S.send_op : nullptr, S.pos, S.cnt_send, h->ctrl,
+                                src_dedup ? S.slist : nullptr, src_dedup ? (const uint64_t*)S.snlist : nullptr));
         } else {
             CK(cudaMemsetAsync(S.cnt_send, 0, G * sizeof(uint64_t), s));
         }
@@ -996,9 +1025,11 @@ hive_status shard_call(hive_table_s* h, int kind, const uint8_t* d_op, const uin
         CKS(st);
     }
     if (n && (out8 || out32)) {
-        Prof p(h, "k_unroute_pad", s);
+        Prof p(h, "k_unroute_pad", s, src_dedup ? 2 : 1);
         CK(launch_unroute_pad(s, S.pos, n, S.rr8, out8, out32 ? S.rr32 : nullptr, out32,
-                              kind == SK_FIND ? 2 : 4, nullptr));
+                              kind == SK_FIND ? 2 : 4, nullptr, src_dedup ? S.slist : nullptr,
+                              src_dedup ? (const uint64_t*)S.snlist : nullptr));
+        if (src_dedup) CK(launch_src_copy(s, n, S.sflag, S.sowner, out8, out32));
     }
     return HIVE_OK;
 }
@@ -1045,7 +1076,9 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
     if (!cfg || !out || cfg->capacity == 0 || cfg->stash_fraction < 0.0f) return HIVE_EINVAL;
     if (cfg->lf_grow < 1.0f && cfg->lf_shrink > 0.0f && cfg->lf_shrink >= cfg->lf_grow) return HIVE_EINVAL;
     if (cfg->lf_grow <= 0.0f) return HIVE_EINVAL;
-    if (cfg->flags & ~(HIVE_KEYS_UNIQUE | HIVE_HASH_CRC)) return HIVE_EINVAL;
+    if (cfg->flags & ~(HIVE_KEYS_UNIQUE | HIVE_HASH_CRC | HIVE_SHARD_DEDUP)) return HIVE_EINVAL;
+    if ((cfg->flags & HIVE_SHARD_DEDUP) && (!cfg->nccl_comm || cfg->shard_batch_max >= (1ull << 30)))
+        return HIVE_EINVAL;
     if (cfg->nccl_comm && (cfg->shard_batch_max == 0 || cfg->shard_slack < 0.0f)) return HIVE_EINVAL;
     *out = nullptr;
     if (!load_vmm(g_vmm)) return HIVE_ECUDA;
@@ -1164,6 +1197,7 @@ hive_status hive_destroy(hive_t h) {
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (h->sh.base) cudaFree(h->sh.base);
+    if (h->sh.sbase) cudaFree(h->sh.sbase);
     if (h->ib.base) cudaFree(h->ib.base);
     if (h->ctrl_h) cudaFreeHost(h->ctrl_h);
     if (h->stage_h) cudaFreeHost(h->stage_h);

@@ -2050,11 +2050,13 @@ k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __rest
             } else if (mode == PART_ROUTE_PAD) {
                 // region p of the padded NCCL send buffer (pd.region = cap
                 // records); an op past the region's capacity is not sent
+                // (over an index list -- source-side election -- op e is the
+                // list entry i; pos_out is indexed by the list position)
                 const uint64_t rel = pos - part_info[MAX_PARTS + p];
                 if (rel < pd.region) {
                     const uint64_t at = (uint64_t)p * pd.region + rel;
-                    send_kv[at] = ((uint64_t)(vals ? vals[i] : 0u) << 32) | keys[i];
-                    if (send_ops) send_ops[at] = ops[i];
+                    send_kv[at] = ((uint64_t)(vals ? vals[e] : 0u) << 32) | keys[e];
+                    if (send_ops) send_ops[at] = ops[e];
                     pos_out[i] = (uint32_t)at;
                 } else {
                     pos_out[i] = NO_POS;
@@ -2501,25 +2503,130 @@ k_owner_return(uint64_t n, const uint64_t* __restrict__ n_dev, const uint32_t* _
 __global__ void __launch_bounds__(BLOCK)
 k_unroute_pad(const uint32_t* __restrict__ pos, uint64_t n, const uint8_t* __restrict__ in8,
               uint8_t* __restrict__ out8, const uint32_t* __restrict__ in32, uint32_t* __restrict__ out32,
-              uint8_t miss8, const unsigned long long* __restrict__ poison) {
+              uint8_t miss8, const unsigned long long* __restrict__ poison, const uint32_t* __restrict__ idx,
+              const uint64_t* __restrict__ n_dev) {
     // a set poison word (peer-exchange timeout marker): no result is trusted
     const bool lost = poison && *(volatile const unsigned long long*)poison != 0;
+    if (n_dev) n = *n_dev;
     for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (uint64_t)gridDim.x * BLOCK) {
         const uint32_t p = pos[i];
         const bool ok = p != NO_POS && !lost;
-        if (out8) out8[i] = ok ? in8[p] : (lost ? HIVE_RESULT_PEER_LOST : miss8);
-        if (out32) out32[i] = ok ? in32[p] : 0u;
+        const uint64_t o = idx ? idx[i] : i;          // index-list route: results go to op idx[i]
+        if (out8) out8[o] = ok ? in8[p] : (lost ? HIVE_RESULT_PEER_LOST : miss8);
+        if (out32) out32[o] = ok ? in32[p] : 0u;
     }
+}
+
+// ---- source-side owner election of a sharded call (SURVEY §8(e) Zipf item) -------
+// Group of an op = (key, class); class = the op's opcode (0 find, 1 insert,
+// 2 erase; other opcodes and the reserved key are never grouped).  The highest
+// op index of a group is its owner; only owners are routed, the others copy
+// their owner's result after the exchange.  Same results as routing every op:
+// the owner's batch is PHASED and a rank's duplicates are consecutive members
+// of the union batch's groups.
+__device__ __forceinline__ uint32_t src_hash(uint32_t k, uint32_t cls) {
+    return fmix32(k ^ DEDUP_SEED ^ (cls * 0x9E3779B9u));
+}
+__global__ void __launch_bounds__(BLOCK)
+k_src_elect(const uint8_t* __restrict__ opc, uint8_t kind_op, const uint32_t* __restrict__ keys, uint64_t n,
+            uint64_t* __restrict__ tab, uint64_t mask, uint8_t* __restrict__ flag, Ctrl* ctrl) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t t0 = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) & ~31ull; t0 < n;
+         t0 += (uint64_t)gridDim.x * BLOCK) {
+        const uint64_t t = t0 + lane;
+        const uint32_t o = t < n ? (opc ? opc[t] : kind_op) : 3u;
+        const uint32_t k = t < n ? keys[t] : INVALID_KEY;
+        const bool part = o < 3 && k != INVALID_KEY;
+        const uint32_t grp = __match_any_sync(FULL, part ? ((uint64_t)k << 2 | o) : ~0ull);
+        if (!part) continue;
+        if (__popc(grp) > 1) flag[t] = 1;
+        if ((31 - __clz(grp)) != lane) continue;                 // warp pre-merge: the max lane
+        const uint64_t word = ((uint64_t)k << 32) | ((uint64_t)o << 30) | (uint32_t)t;
+        uint64_t h = src_hash(k, o) & mask;
+        uint64_t probe = 0;
+        for (; probe <= mask; ++probe) {
+            const uint64_t prev = cas64(&tab[h], EMPTY, word);
+            if (prev == EMPTY) break;
+            if ((prev >> 30) == (word >> 30)) {                   // same key and class
+                flag[t] = 1;
+                flag[(uint32_t)prev & 0x3FFFFFFFu] = 1;
+                if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
+                break;
+            }
+            h = (h + 1) & mask;
+        }
+        if (probe > mask) atomicAdd(&ctrl->eover, 1ull);
+    }
+}
+// The send list (owners and ungrouped ops, in no particular order) and, for
+// grouped ops, their owner.
+__global__ void __launch_bounds__(BLOCK)
+k_src_list(const uint8_t* __restrict__ opc, uint8_t kind_op, const uint32_t* __restrict__ keys, uint64_t n,
+           const uint64_t* __restrict__ tab, uint64_t mask, const uint8_t* __restrict__ flag,
+           uint32_t* __restrict__ owner_of, uint32_t* __restrict__ list, unsigned long long* __restrict__ n_list) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t t0 = ((uint64_t)blockIdx.x * BLOCK + threadIdx.x) & ~31ull; t0 < n;
+         t0 += (uint64_t)gridDim.x * BLOCK) {
+        const uint64_t t = t0 + lane;
+        bool send = t < n;
+        if (send && flag[t]) {
+            const uint32_t o = opc ? opc[t] : kind_op, k = keys[t];
+            uint64_t h = src_hash(k, o) & mask;
+            uint32_t own = (uint32_t)t;
+            for (uint64_t probe = 0; probe <= mask; ++probe) {
+                const uint64_t e = tab[h];
+                if (e == EMPTY) break;
+                if ((e >> 32) == k && ((e >> 30) & 3u) == o) { own = (uint32_t)e & 0x3FFFFFFFu; break; }
+                h = (h + 1) & mask;
+            }
+            owner_of[t] = own;
+            send = own == (uint32_t)t;
+        }
+        const uint32_t bal = __ballot_sync(FULL, send);
+        unsigned long long base = 0;
+        if (lane == 0 && bal) base = atomicAdd(n_list, (unsigned long long)__popc(bal));
+        base = __shfl_sync(FULL, base, 0);
+        if (send) list[base + __popc(bal & lanemask_lt())] = (uint32_t)t;
+    }
+}
+__global__ void __launch_bounds__(BLOCK)
+k_src_copy(uint64_t n, const uint8_t* __restrict__ flag, const uint32_t* __restrict__ owner_of,
+           uint8_t* __restrict__ out8, uint32_t* __restrict__ out32) {
+    for (uint64_t t = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; t < n; t += (uint64_t)gridDim.x * BLOCK) {
+        if (!flag[t]) continue;
+        const uint32_t o = owner_of[t];
+        if (o == (uint32_t)t) continue;
+        if (out8) out8[t] = out8[o];
+        if (out32) out32[t] = out32[o];
+    }
+}
+cudaError_t launch_src_elect(cudaStream_t s, const uint8_t* opc, uint8_t kind_op, const uint32_t* keys, uint64_t n,
+                             uint64_t* tab, uint64_t mask, uint8_t* flag, uint32_t* owner_of, uint32_t* list,
+                             unsigned long long* n_list, Ctrl* ctrl) {
+    cudaError_t e = cudaMemsetAsync(tab, 0xFF, (mask + 1) * sizeof(uint64_t), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, n, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(n_list, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    const int grid = clamp_grid(148 * 8, n, BLOCK);
+    k_src_elect<<<grid, BLOCK, 0, s>>>(opc, kind_op, keys, n, tab, mask, flag, ctrl);
+    k_src_list<<<grid, BLOCK, 0, s>>>(opc, kind_op, keys, n, tab, mask, flag, owner_of, list, n_list);
+    return cudaGetLastError();
+}
+cudaError_t launch_src_copy(cudaStream_t s, uint64_t n, const uint8_t* flag, const uint32_t* owner_of, uint8_t* out8,
+                            uint32_t* out32) {
+    if (n == 0) return cudaSuccess;
+    k_src_copy<<<clamp_grid(148 * 8, n, BLOCK), BLOCK, 0, s>>>(n, flag, owner_of, out8, out32);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_route_pad(cudaStream_t s, uint32_t n_shards, uint32_t seed, const uint32_t* keys,
                              const uint32_t* vals, const uint8_t* ops, uint64_t n, uint64_t cap, uint64_t* cnt,
                              uint64_t* part_info, uint64_t* send_kv, uint8_t* send_ops, uint32_t* pos,
-                             uint64_t* cnt_send, Ctrl* ctrl) {
+                             uint64_t* cnt_send, Ctrl* ctrl, const uint32_t* idx, const uint64_t* n_dev) {
     PeerDest pd{};
     pd.region = cap;
     cudaError_t e = launch_partition_pd(s, PART_ROUTE_PAD, n_shards, seed, keys, vals, ops, n, cnt, part_info,
-                                        nullptr, 0, send_kv, send_ops, pos, nullptr, nullptr, nullptr, nullptr, pd);
+                                        nullptr, 0, send_kv, send_ops, pos, nullptr, nullptr, idx, n_dev, pd);
     if (e != cudaSuccess) return e;
     k_pad_counts<<<1, 32, 0, s>>>(part_info, n_shards, cap, cnt_send, ctrl);
     return cudaGetLastError();
@@ -2542,10 +2649,10 @@ cudaError_t launch_owner_return(cudaStream_t s, uint64_t n_upper, const uint64_t
 
 cudaError_t launch_unroute_pad(cudaStream_t s, const uint32_t* pos, uint64_t n, const uint8_t* in8, uint8_t* out8,
                                const uint32_t* in32, uint32_t* out32, uint8_t miss8,
-                               const unsigned long long* poison) {
+                               const unsigned long long* poison, const uint32_t* idx, const uint64_t* n_dev) {
     if (n == 0) return cudaSuccess;
     const int grid = clamp_grid(148 * 8, n, BLOCK);
-    k_unroute_pad<<<grid, BLOCK, 0, s>>>(pos, n, in8, out8, in32, out32, miss8, poison);
+    k_unroute_pad<<<grid, BLOCK, 0, s>>>(pos, n, in8, out8, in32, out32, miss8, poison, idx, n_dev);
     return cudaGetLastError();
 }
 

@@ -184,7 +184,18 @@ constexpr uint32_t NO_POS = 0xFFFFFFFFu;
 cudaError_t launch_route_pad(cudaStream_t s, uint32_t n_shards, uint32_t seed, const uint32_t* keys,
                              const uint32_t* vals, const uint8_t* ops, uint64_t n, uint64_t cap, uint64_t* cnt,
                              uint64_t* part_info, uint64_t* send_kv, uint8_t* send_ops, uint32_t* pos,
-                             uint64_t* cnt_send, Ctrl* ctrl);
+                             uint64_t* cnt_send, Ctrl* ctrl, const uint32_t* idx = nullptr,
+                             const uint64_t* n_dev = nullptr);
+// Source-side owner election of a sharded call: groups (key, opcode) --
+// opc == nullptr: every op has opcode kind_op -- elect the highest op index,
+// flag grouped ops, owner_of for grouped ops, and list = the ops to route
+// (*n_list of them).  tab: mask + 1 words (power of two >= 2n).
+cudaError_t launch_src_elect(cudaStream_t s, const uint8_t* opc, uint8_t kind_op, const uint32_t* keys, uint64_t n,
+                             uint64_t* tab, uint64_t mask, uint8_t* flag, uint32_t* owner_of, uint32_t* list,
+                             unsigned long long* n_list, Ctrl* ctrl);
+// After the exchange: grouped non-owners copy their owner's results.
+cudaError_t launch_src_copy(cudaStream_t s, uint64_t n, const uint8_t* flag, const uint32_t* owner_of, uint8_t* out8,
+                            uint32_t* out32);
 // Owner: the records of the G received regions (cnt_recv[r] valid in region
 // r), in source-rank order, as contiguous keys / values / opcodes; back[j] =
 // the padded position record j came from; *n_dev = the total.
@@ -200,7 +211,8 @@ cudaError_t launch_owner_return(cudaStream_t s, uint64_t n_upper, const uint64_t
 constexpr uint8_t HIVE_RESULT_PEER_LOST = 6;
 cudaError_t launch_unroute_pad(cudaStream_t s, const uint32_t* pos, uint64_t n, const uint8_t* in8, uint8_t* out8,
                                const uint32_t* in32, uint32_t* out32, uint8_t miss8,
-                               const unsigned long long* poison = nullptr);
+                               const unsigned long long* poison = nullptr, const uint32_t* idx = nullptr,
+                               const uint64_t* n_dev = nullptr);
 
 cudaError_t launch_unroute(cudaStream_t s, const uint32_t* pos, uint64_t n, const uint8_t* in8,
                            uint8_t* out8, const uint32_t* in32, uint32_t* out32);

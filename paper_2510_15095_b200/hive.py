@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_PKG, "libhive.so")
 
 HIVE_KEYS_UNIQUE = 1
 HIVE_HASH_CRC = 2
+HIVE_SHARD_DEDUP = 4
 HASH_PAIRS = {"bithash": 0, "crc": HIVE_HASH_CRC}      # (BitHash1, BitHash2) / (CRC-32, CRC-64)
 HASH_FNS = {"bithash1": 0, "bithash2": 1, "crc32": 2, "crc64": 3}
 OP_FIND, OP_INSERT, OP_ERASE = 0, 1, 2
@@ -166,7 +167,7 @@ class HiveTable:
                  lf_shrink: float = 0.25, max_evictions: int = 16, resize_k: int = 1024,
                  stash_fraction: float = 0.02, keys_unique: bool = False, hash: str = "bithash",
                  stream=None, nccl_comm: int | None = None, shard_batch_max: int = 0,
-                 shard_slack: float = 0.0625):
+                 shard_slack: float = 0.0625, shard_dedup: bool = False):
         """nccl_comm (an ncclComm_t from nccl_comm_init): create one shard of a
         hash-partitioned table; every op call is then collective over the comm
         (include/hive.h "Sharded tables")."""
@@ -178,7 +179,7 @@ class HiveTable:
         cfg.capacity, cfg.max_capacity = capacity, max_capacity
         cfg.lf_grow, cfg.lf_shrink = lf_grow, lf_shrink
         cfg.max_evictions, cfg.resize_k, cfg.stash_fraction = max_evictions, resize_k, stash_fraction
-        cfg.flags = (HIVE_KEYS_UNIQUE if keys_unique else 0) | HASH_PAIRS[hash]
+        cfg.flags = (HIVE_KEYS_UNIQUE if keys_unique else 0) | HASH_PAIRS[hash] | (HIVE_SHARD_DEDUP if shard_dedup else 0)
         cfg.nccl_comm = nccl_comm
         cfg.shard_batch_max, cfg.shard_slack = shard_batch_max, shard_slack
         self.cfg = cfg

@@ -32,13 +32,15 @@ def _np(t):
     return t.cpu().numpy()
 
 
-@pytest.mark.parametrize("grow", [True, False])
-def test_sharded_handle_world1_vs_oracle(pg, grow):
+@pytest.mark.parametrize("grow,dedup", [(True, False), (False, False), (True, True), (False, True)])
+def test_sharded_handle_world1_vs_oracle(pg, grow, dedup):
+    """dedup: source-side owner election before routing (HIVE_SHARD_DEDUP) --
+    the batches repeat keys heavily, results must be unchanged."""
     import oracle
     from paper_2510_15095_b200 import u8, u32
     from paper_2510_15095_b200.sharded import ShardedHive
     cfg = dict(resize_k=16) if grow else dict(lf_grow=2.0, lf_shrink=0)
-    sh = ShardedHive(256 * 32 if grow else 2048 * 32, batch_max=60000, **cfg)
+    sh = ShardedHive(256 * 32 if grow else 2048 * 32, batch_max=60000, shard_dedup=dedup, **cfg)
     o = oracle.OracleTable(256 * 32 if grow else 2048 * 32, **cfg)
     assert sh.table.shard_info()[:2] == (1, 0)
     rng = np.random.default_rng(9)
@@ -166,4 +168,27 @@ def test_cfg5_sequence_world1_shard_dump_vs_oracle(pg):
     ko, vo = o.dump()
     og, oo = np.argsort(kk), np.argsort(ko)
     assert (kk[og] == ko[oo]).all() and (vv[og] == vo[oo]).all() and len(kk) == total - total // 8
+    sh.close()
+
+
+def test_sharded_source_dedup_zipf_batch(pg):
+    """HIVE_SHARD_DEDUP on a Zipf(0.99) mixed batch (the hot key ~5% of the ops):
+    statuses, values and the final table equal the oracle's; the routed record
+    count is the number of distinct (key, opcode) groups."""
+    import oracle
+    from paper_2510_15095_b200 import u8, u32
+    from paper_2510_15095_b200.sharded import ShardedHive
+    n = 1 << 18
+    sh = ShardedHive(8192 * 32, batch_max=n, shard_dedup=True, lf_grow=2.0, lf_shrink=0)
+    o = oracle.OracleTable(8192 * 32, lf_grow=2.0, lf_shrink=0)
+    for b in range(3):
+        r = gen.zipf_ranks(n, 1 << 16, 0.99, seed=90 + b)
+        keys = gen.keys_of((r - 1).astype(np.uint32))
+        ops = gen.bernoulli_ops(n, 0.5, 0.2, seed=95 + b)
+        vals = np.arange(n, dtype=np.uint32) + b * n
+        vo, res = sh.mixed(u8(ops), u32(keys), u32(vals))
+        vo_o, res_o = o.mixed(ops, keys, vals)
+        assert (_np(res) == res_o).all() and (_np(vo).astype(np.uint32) == vo_o).all(), b
+    k, v = sh.table.dump()
+    assert dict(zip(_np(k).astype(np.uint32).tolist(), _np(v).astype(np.uint32).tolist())) == o.dump_dict()
     sh.close()
