@@ -907,16 +907,19 @@ hive_status shard_alloc(hive_table_s* h) {
 }
 
 // One all-to-all of `count` elements per peer: ncclAlltoAll (NCCL >= 2.28) or
-// a group of send / recv pairs.
+// a group of send / recv pairs.  skip_self: the rank's own block is not moved
+// (the caller reads it from the send buffer) -- NCCL would copy it locally,
+// which at 2^26-op batches costs more than the whole exchange to a peer.
 hive_status a2a(hive_table_s* h, const void* send, void* recv, size_t count, int dtype, size_t esize,
-                cudaStream_t s) {
+                cudaStream_t s, bool skip_self = false) {
     auto& S = h->sh;
-    if (g_nccl.alltoall) {
+    if (g_nccl.alltoall && !skip_self) {
         CKN(g_nccl.alltoall(send, recv, count, dtype, S.comm, s));
         return HIVE_OK;
     }
     CKN(g_nccl.group_start());
     for (int p = 0; p < S.nranks; ++p) {
+        if (skip_self && p == S.rank) continue;
         CKN(g_nccl.send((const char*)send + p * count * esize, count, dtype, p, S.comm, s));
         CKN(g_nccl.recv((char*)recv + p * count * esize, count, dtype, p, S.comm, s));
     }
@@ -1000,15 +1003,16 @@ hive_status shard_call(hive_table_s* h, int kind, const uint8_t* d_op, const uin
         Prof p(h, "nccl_alltoall(fwd)", s, 0);
         CKN(g_nccl.group_start());
         hive_status st = a2a(h, S.cnt_send, S.cnt_recv, 1, NCCL_U64, 8, s);
-        if (st == HIVE_OK) st = a2a(h, S.send_kv, S.recv_kv, cap, NCCL_U64, 8, s);
-        if (st == HIVE_OK && mixed) st = a2a(h, S.send_op, S.recv_op, cap, NCCL_U8, 1, s);
+        if (st == HIVE_OK) st = a2a(h, S.send_kv, S.recv_kv, cap, NCCL_U64, 8, s, true);
+        if (st == HIVE_OK && mixed) st = a2a(h, S.send_op, S.recv_op, cap, NCCL_U8, 1, s, true);
         CKN(g_nccl.group_end());
         CKS(st);
     }
     {
         Prof p(h, "k_owner_compact", s);
         CK(launch_owner_compact(s, G, cap, S.recv_kv, mixed ? S.recv_op : nullptr, S.cnt_recv, S.kc, S.vc,
-                                mixed ? S.oc : nullptr, S.back, S.n_dev));
+                                mixed ? S.oc : nullptr, S.back, S.n_dev, (uint32_t)S.rank, S.send_kv,
+                                mixed ? S.send_op : nullptr));
     }
     CKS(owner_phase(h, kind, S.oc, S.kc, S.vc, tot, S.n_dev, S.r8c, S.r32c, s));
     {
@@ -1019,12 +1023,17 @@ hive_status shard_call(hive_table_s* h, int kind, const uint8_t* d_op, const uin
     {
         Prof p(h, "nccl_alltoall(back)", s, 0);
         CKN(g_nccl.group_start());
-        hive_status st = a2a(h, S.ret8, S.rr8, cap, NCCL_U8, 1, s);
-        if (st == HIVE_OK && vals32) st = a2a(h, S.ret32, S.rr32, cap, NCCL_U32, 4, s);
+        hive_status st = a2a(h, S.ret8, S.rr8, cap, NCCL_U8, 1, s, true);
+        if (st == HIVE_OK && vals32) st = a2a(h, S.ret32, S.rr32, cap, NCCL_U32, 4, s, true);
         CKN(g_nccl.group_end());
         CKS(st);
     }
     if (n && (out8 || out32)) {
+        // the own region's results stayed in ret8 / ret32: place them where the
+        // unpermute reads (a device copy of one region, not an NCCL transfer)
+        const uint64_t off = (uint64_t)S.rank * cap;
+        CK(cudaMemcpyAsync(S.rr8 + off, S.ret8 + off, cap, cudaMemcpyDeviceToDevice, s));
+        if (vals32) CK(cudaMemcpyAsync(S.rr32 + off, S.ret32 + off, cap * 4, cudaMemcpyDeviceToDevice, s));
         Prof p(h, "k_unroute_pad", s, src_dedup ? 2 : 1);
         CK(launch_unroute_pad(s, S.pos, n, S.rr8, out8, out32 ? S.rr32 : nullptr, out32,
                               kind == SK_FIND ? 2 : 4, nullptr, src_dedup ? S.slist : nullptr,

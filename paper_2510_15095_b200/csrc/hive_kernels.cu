@@ -2241,6 +2241,10 @@ Grids query_grids(int num_sms) {
 #define OCC_SLOW(G, MB) g.insert_slow = occ((const void*)k_insert_slow<G, MB>) * num_sms
 #define OCC_ERA(G, MB) g.erase = occ((const void*)k_erase<G, MB>) * num_sms
     HIVE_DISPATCH_GM8(g.g_find, g.minb_find, OCC_FIND)
+    // HIVE_FIND_BPS: cap the persistent k_find grid at this many blocks per SM
+    // (experiments; tools/sector_bench.cu found random 256 B gathers fastest
+    // at 4 resident blocks of 256 threads)
+    if (getenv("HIVE_FIND_BPS")) g.find = std::min(g.find, atoi(getenv("HIVE_FIND_BPS")) * num_sms);
     HIVE_DISPATCH_GM(g.g_insert, g.minb, OCC_INS)
     HIVE_DISPATCH_GM(g.g_slow, g.minb, OCC_SLOW)
     HIVE_DISPATCH_GM(g.g_erase, g.minb, OCC_ERA)
@@ -2470,7 +2474,8 @@ __global__ void __launch_bounds__(BLOCK)
 k_owner_compact(uint32_t n_src, uint64_t cap, const uint64_t* __restrict__ recv_kv,
                 const uint8_t* __restrict__ recv_ops, const uint64_t* __restrict__ cnt,
                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint8_t* __restrict__ ops,
-                uint32_t* __restrict__ back, uint64_t* __restrict__ n_dev) {
+                uint32_t* __restrict__ back, uint64_t* __restrict__ n_dev, uint32_t self,
+                const uint64_t* __restrict__ self_kv, const uint8_t* __restrict__ self_ops) {
     __shared__ uint64_t start[MAX_PARTS + 1];
     pad_starts(cnt, n_src, cap, start);
     if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = start[n_src];
@@ -2480,10 +2485,13 @@ k_owner_compact(uint32_t n_src, uint64_t cap, const uint64_t* __restrict__ recv_
         const uint64_t o = j - (uint64_t)r * cap;
         if (start[r] + o >= start[r + 1]) continue;          // padding
         const uint64_t li = start[r] + o;
-        const uint64_t w = recv_kv[j];
+        // this rank's own region never went through the exchange: it is read
+        // from the send buffer (same padded layout)
+        const bool own = self_kv && r == self;
+        const uint64_t w = own ? self_kv[j] : recv_kv[j];
         keys[li] = key_of(w);
         vals[li] = val_of(w);
-        if (ops) ops[li] = recv_ops[j];
+        if (ops) ops[li] = own ? self_ops[j] : recv_ops[j];
         back[li] = (uint32_t)j;
     }
 }
@@ -2634,9 +2642,11 @@ cudaError_t launch_route_pad(cudaStream_t s, uint32_t n_shards, uint32_t seed, c
 
 cudaError_t launch_owner_compact(cudaStream_t s, uint32_t n_src, uint64_t cap, const uint64_t* recv_kv,
                                  const uint8_t* recv_ops, const uint64_t* cnt_recv, uint32_t* keys, uint32_t* vals,
-                                 uint8_t* ops, uint32_t* back, uint64_t* n_dev) {
+                                 uint8_t* ops, uint32_t* back, uint64_t* n_dev, uint32_t self,
+                                 const uint64_t* self_kv, const uint8_t* self_ops) {
     const int grid = clamp_grid(148 * 8, (uint64_t)n_src * cap, BLOCK);
-    k_owner_compact<<<grid, BLOCK, 0, s>>>(n_src, cap, recv_kv, recv_ops, cnt_recv, keys, vals, ops, back, n_dev);
+    k_owner_compact<<<grid, BLOCK, 0, s>>>(n_src, cap, recv_kv, recv_ops, cnt_recv, keys, vals, ops, back, n_dev,
+                                           self, self_kv, self_ops);
     return cudaGetLastError();
 }
 

@@ -199,9 +199,12 @@ cudaError_t launch_src_copy(cudaStream_t s, uint64_t n, const uint8_t* flag, con
 // Owner: the records of the G received regions (cnt_recv[r] valid in region
 // r), in source-rank order, as contiguous keys / values / opcodes; back[j] =
 // the padded position record j came from; *n_dev = the total.
+// self_kv (nullable): region `self` is read from this buffer (the local send
+// buffer: the rank's own records skip the exchange), self_ops likewise.
 cudaError_t launch_owner_compact(cudaStream_t s, uint32_t n_src, uint64_t cap, const uint64_t* recv_kv,
                                  const uint8_t* recv_ops, const uint64_t* cnt_recv, uint32_t* keys, uint32_t* vals,
-                                 uint8_t* ops, uint32_t* back, uint64_t* n_dev);
+                                 uint8_t* ops, uint32_t* back, uint64_t* n_dev, uint32_t self = 0,
+                                 const uint64_t* self_kv = nullptr, const uint8_t* self_ops = nullptr);
 // Owner: results of the compacted batch back into the padded layout
 // (ret8[back[j]] = r8[j], ret32 likewise; either pair may be null).
 cudaError_t launch_owner_return(cudaStream_t s, uint64_t n_upper, const uint64_t* n_dev, const uint32_t* back,
