@@ -447,6 +447,71 @@ k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict
     block_add(&ctrl->abytes[AB_ELECT], ab);
 }
 
+// The same election with two independent records per lane per iteration:
+// both first CASes are issued back to back, so each lane keeps two L2 atomic
+// round trips in flight (the one-record kernel is CAS-latency bound: 97% warps
+// active, 64 long-scoreboard stalls per issue).  Collisions fall back to the
+// sequential probe loop of their record.
+__device__ __forceinline__ void elect_resolve(const DedupView& dd, uint64_t* tab, uint64_t h, uint64_t prev,
+                                              uint64_t word, uint32_t k, uint32_t op, uint32_t& ab, Ctrl* ctrl) {
+    for (uint64_t probe = 0;; ) {
+        if (prev == EMPTY) return;
+        if ((uint32_t)(prev >> 32) == k) {
+            dd.flag[op] = 1;
+            dd.flag[(uint32_t)prev] = 1;
+            if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
+            return;
+        }
+        if (++probe > dd.mask) { atomicAdd(&ctrl->eover, 1ull); return; }
+        h = (h + 1) & dd.mask;
+        prev = cas64(&tab[h], EMPTY, word);
+        ab += 32;
+    }
+}
+template <int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
+k_dedup_elect_part2(const uint64_t* __restrict__ recs, const uint64_t* __restrict__ part_info, uint32_t part,
+                    DedupView dd, Ctrl* ctrl) {
+    const uint64_t n = part_info[part];
+    const uint64_t base = part_info[MAX_PARTS + part];
+    const int lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * BLOCK * 2;
+    uint32_t ab = 0;
+    for (uint64_t t0 = ((uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u)) * 2; t0 < n; t0 += stride) {
+        const uint64_t ta = t0 + lane, tb = t0 + 32 + lane;
+        const uint64_t wa = ta < n ? recs[base + ta] : EMPTY;
+        const uint64_t wb = tb < n ? recs[base + tb] : EMPTY;
+        const uint32_t ka = (uint32_t)wa, opa = (uint32_t)(wa >> 32);
+        const uint32_t kb = (uint32_t)wb, opb = (uint32_t)(wb >> 32);
+        const uint32_t ga = __match_any_sync(FULL, ka), gb = __match_any_sync(FULL, kb);
+        bool da = ta < n, db = tb < n;
+        ab += (da ? 8 : 0) + (db ? 8 : 0);
+        if (da && __popc(ga) > 1) {
+            dd.flag[opa] = 1;
+            da = __reduce_max_sync(ga, opa) == opa;
+        } else if (__popc(ga) > 1) {
+            (void)__reduce_max_sync(ga, opa);               // every lane of the group takes part
+        }
+        if (db && __popc(gb) > 1) {
+            dd.flag[opb] = 1;
+            db = __reduce_max_sync(gb, opb) == opb;
+        } else if (__popc(gb) > 1) {
+            (void)__reduce_max_sync(gb, opb);
+        }
+        const uint64_t worda = ((uint64_t)ka << 32) | opa, wordb = ((uint64_t)kb << 32) | opb;
+        const uint32_t hka = fmix32(ka ^ DEDUP_SEED), hkb = fmix32(kb ^ DEDUP_SEED);
+        uint64_t* taba = dd.sub(hka);
+        uint64_t* tabb = dd.sub(hkb);
+        const uint64_t ha = hka & dd.mask, hb = hkb & dd.mask;
+        uint64_t pa = EMPTY, pb = EMPTY;
+        if (da) { pa = cas64(&taba[ha], EMPTY, worda); ab += 32; }
+        if (db) { pb = cas64(&tabb[hb], EMPTY, wordb); ab += 32; }
+        if (da) elect_resolve(dd, taba, ha, pa, worda, ka, opa, ab, ctrl);
+        if (db) elect_resolve(dd, tabb, hb, pb, wordb, kb, opb, ab, ctrl);
+    }
+    block_add(&ctrl->abytes[AB_ELECT], ab);
+}
+
 // Hash partition of one phase's ops for the election (order inside a part is
 // arbitrary; the election is order-free): pass 1 per-block histograms,
 // pass 2 per-part bases, pass 3 a 4096-op tile per block written part by part
@@ -2272,7 +2337,20 @@ cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, c
 
 cudaError_t launch_dedup_elect_part(int grid, cudaStream_t s, const uint64_t* recs, const uint64_t* part_info,
                                     uint32_t part, DedupView dd, Ctrl* ctrl) {
-    k_dedup_elect_part<<<grid, BLOCK, 0, s>>>(recs, part_info, part, dd, ctrl);
+    // HIVE_ELECT_ILP: 1 = one record per lane; 2 = two (40 registers, 6 blocks
+    // per SM); 3 = two, capped at 32 registers (8 blocks per SM)
+    static const int ilp = getenv("HIVE_ELECT_ILP") ? atoi(getenv("HIVE_ELECT_ILP")) : 1;
+    static int g2 = 0, g3 = 0;
+    int dev = 0, sms = 0;
+    if (ilp >= 2 && (!g2 || !g3)) {
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        g2 = occ((const void*)k_dedup_elect_part2<1>) * sms;
+        g3 = occ((const void*)k_dedup_elect_part2<8>) * sms;
+    }
+    if (ilp == 2) k_dedup_elect_part2<1><<<g2, BLOCK, 0, s>>>(recs, part_info, part, dd, ctrl);
+    else if (ilp >= 3) k_dedup_elect_part2<8><<<g3, BLOCK, 0, s>>>(recs, part_info, part, dd, ctrl);
+    else k_dedup_elect_part<<<grid, BLOCK, 0, s>>>(recs, part_info, part, dd, ctrl);
     return cudaGetLastError();
 }
 
