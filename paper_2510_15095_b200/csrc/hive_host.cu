@@ -1001,9 +1001,11 @@ hive_status shard_call(hive_table_s* h, int kind, const uint8_t* d_op, const uin
     }
     {
         Prof p(h, "nccl_alltoall(fwd)", s, 0);
+        // the counts collective in its own call, then one group of point-to-point
+        // transfers for the records (and opcodes) to the peers
+        CKS(a2a(h, S.cnt_send, S.cnt_recv, 1, NCCL_U64, 8, s));
         CKN(g_nccl.group_start());
-        hive_status st = a2a(h, S.cnt_send, S.cnt_recv, 1, NCCL_U64, 8, s);
-        if (st == HIVE_OK) st = a2a(h, S.send_kv, S.recv_kv, cap, NCCL_U64, 8, s, true);
+        hive_status st = a2a(h, S.send_kv, S.recv_kv, cap, NCCL_U64, 8, s, true);
         if (st == HIVE_OK && mixed) st = a2a(h, S.send_op, S.recv_op, cap, NCCL_U8, 1, s, true);
         CKN(g_nccl.group_end());
         CKS(st);
