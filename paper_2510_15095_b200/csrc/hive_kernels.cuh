@@ -25,8 +25,12 @@ constexpr int MAX_PARTS = 64;
 // below this many free slots in b1 the emptier of b1 / b2 is claimed; 0 =
 // first-fit b1 then b2.  Build-time (-DHIVE_TWO_CHOICE_T=t, HIVE_NVCC_DEFINES).
 constexpr uint32_t TWO_CHOICE_T = HIVE_TWO_CHOICE_T;
-constexpr uint32_t CLAIM_ROT_DEFAULT = 0;   // claim placement (hive_kernels.cu c_claim_rot; 0 measured fastest,
-                                            // 1 / 2 for experiments: rebuild)
+#ifndef HIVE_CLAIM_ROT
+#define HIVE_CLAIM_ROT 0
+#endif
+// claim placement (hive_kernels.cu c_claim_rot; 0 measured fastest; 1 / 2 for
+// experiments: -DHIVE_CLAIM_ROT=r through HIVE_NVCC_DEFINES)
+constexpr uint32_t CLAIM_ROT_DEFAULT = HIVE_CLAIM_ROT;
 
 enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1, PART_ELECT = 2, PART_ROUTE_KEYS = 3, PART_ROUTE_P2P = 4,
                 PART_ROUTE_PAD = 5 };

@@ -1,9 +1,10 @@
 #!/bin/bash
-# A/B of the optimistic claim placement (HIVE_CLAIM_ROT 0 / 1 / 2) on the cfg2
-# bench step: insert-phase time, kernel times, leftovers.
+# A/B of the optimistic claim placement (-DHIVE_CLAIM_ROT=0 / 1 / 2, a rebuild
+# each) on the cfg2 bench step: insert-phase time, kernel times, leftovers.
 mkdir -p gpurun_out
-for r in 0 1 2; do  # (now compile-time: CLAIM_ROT_DEFAULT in hive_kernels.cuh)
-  HIVE_CLAIM_ROT=$r python bench.py --steps 5 --no-secondary --no-cpu-baseline > gpurun_out/rot$r.json 2>gpurun_out/rot$r.err
+for r in 0 1 2; do
+  HIVE_NVCC_DEFINES="-DHIVE_CLAIM_ROT=$r" python -m paper_2510_15095_b200.build --force > /dev/null
+  python bench.py --steps 5 --no-secondary --no-cpu-baseline > gpurun_out/rot$r.json 2>gpurun_out/rot$r.err
   python - "$r" <<'PY'
 import json, sys
 r = sys.argv[1]
@@ -15,3 +16,4 @@ print(json.dumps({"rot": int(r), "value": round(d["value"], 3), "updates": round
                   "evictions": d["table_stats"]["evictions"]}))
 PY
 done
+python -m paper_2510_15095_b200.build --force > /dev/null
