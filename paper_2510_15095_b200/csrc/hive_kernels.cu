@@ -729,6 +729,10 @@ __device__ __forceinline__ bool owns(const WarpGroup<G>& wg, const DedupView& dd
 // after a resize: Step 1 is skipped (those keys are in no bucket)
 // and nothing is counted.
 // --------------------------------------------------------------------------------
+// Two-choice threshold test (signed, so a threshold of 0 compiles without a
+// pointless-comparison warning).
+__device__ __forceinline__ bool below_two_choice_t(uint32_t f) { return (int64_t)f < (int64_t)TWO_CHOICE_T; }
+
 // EMPTY slots of the group's bucket view (all lanes of the group get the sum).
 template <int G>
 __device__ __forceinline__ uint32_t group_free(const uint64_t (&s)[WarpGroup<G>::SPL]) {
@@ -815,7 +819,7 @@ __device__ __forceinline__ void insert_fast_range(uint64_t lo, uint64_t hi, uint
         const uint64_t kv = pack(k, v);
         bool done = false, have2 = false;
         int jm1 = SPL, jf1 = SPL;
-        uint32_t f1 = SPL * G;                         // free slots of b1 (two-choice placement only)
+        [[maybe_unused]] uint32_t f1 = SPL * G;        // free slots of b1 (two-choice placement only)
         if (!place_only) {
             // Step 1: b1 (one scan gives the match and the first free slot); then
             // -- only if b1's spill word allows k to live elsewhere -- b2 and the
@@ -863,7 +867,7 @@ __device__ __forceinline__ void insert_fast_range(uint64_t lo, uint64_t hi, uint
         // read and the emptier bucket is claimed.  TWO_CHOICE_T = 0: first-fit.
         bool choose2 = false;
         if constexpr (TWO_CHOICE_T > 0) {
-            const bool look2 = !place_only && two && !done && f1 < TWO_CHOICE_T;
+            const bool look2 = !place_only && two && !done && below_two_choice_t(f1);
             if (__any_sync(FULL, look2)) {
                 if (look2 && !have2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), sv_);
                 if (look2 && !have2 && wg.gl == 0) st.ab += 256;
@@ -1003,11 +1007,13 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         const uint64_t kv = pack(k, v);
         bool done = false, have2 = false;
         int jm1 = SPL, jf1 = SPL;
+        [[maybe_unused]] uint32_t f1 = SPL * G;        // free slots of b1 (two-choice placement only)
         if (!place_only) {
             // Step 1: b1 (one scan gives the match and the first free slot); then
             // -- only if b1's spill word allows k to live elsewhere -- b2 and the
             // stash.
             if (valid) scan_slots<SPL>(sv_, k, jm1, jf1);
+            if constexpr (TWO_CHOICE_T > 0) f1 = group_free<G>(sv_);
             if (__any_sync(FULL, wg.ballot(jm1 < SPL) != 0))
                 done = wcme_cas<G>(wg, sv_, tv.bucket(b1), k, kv, valid, ab);
             const bool maybe = valid && !done && (spill_w & fp) == fp;
@@ -1039,10 +1045,24 @@ k_insert_fast(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ va
         // this iteration's loads to come back); a lost claim goes to Step 3
         wl.push(pend && pend_prev != EMPTY, pend_item, leftover, &sv.ctrl->n_left);
         pend = false;
+        // Thresholded two-choice placement (reading A-21; build-time, off by
+        // default -- measured, §5): below TWO_CHOICE_T free slots in b1, read b2
+        // and claim the emptier bucket.
+        bool choose2 = false;
+        if constexpr (TWO_CHOICE_T > 0) {
+            const bool look2 = !place_only && two && !done && below_two_choice_t(f1);
+            if (__any_sync(FULL, look2)) {
+                if (look2 && !have2) load_slots<SPL>(wg.slot_ptr(tv.bucket(b2)), sv_);
+                if (look2 && !have2 && wg.gl == 0) ab += 256;
+                if (look2) have2 = true;
+                const uint32_t f2 = group_free<G>(sv_);
+                choose2 = look2 && f2 > f1;
+            }
+        }
         // Step 2: optimistic WABC claim in b1, then b2 (first-fit, A-21); b2 is
         // read only if b1 is full.
         if (place_only && valid) scan_slots<SPL>(sv_, INVALID_KEY, jm1, jf1);
-        bool placed = wabc_claim_issue<G>(wg, jf1, tv.bucket(b1), kv, valid && !done, pend, pend_prev,
+        bool placed = wabc_claim_issue<G>(wg, jf1, tv.bucket(b1), kv, valid && !done && !choose2, pend, pend_prev,
                                           pend_item, op, ab);
         const bool want2 = two && !done && !placed;
         if (__any_sync(FULL, want2)) {
