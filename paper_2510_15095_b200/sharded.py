@@ -14,6 +14,8 @@ duplicates across ranks therefore resolve to the op with the largest
 """
 from __future__ import annotations
 
+import math
+
 import torch
 import torch.distributed as dist
 
@@ -141,7 +143,10 @@ class P2PShardedHive:
 
     @staticmethod
     def padded_region(batch_max: int, world: int, slack: float = 0.0625) -> int:
-        return min(batch_max, -(-batch_max * (1 + slack) // world) + 1024) if world > 1 else batch_max
+        """Records per (source, owner) region: the NCCL handle's per-peer capacity."""
+        if world <= 1:
+            return int(batch_max)
+        return int(min(batch_max, math.ceil(batch_max * (1 + slack) / world) + 1024))
 
     def __init__(self, capacity_per_shard: int, region: int, group=None, seed: int = SHARD_SEED,
                  _virtual=None, **cfg):

@@ -216,3 +216,17 @@ def test_padded_exchange_world2_gloo(cap):
                 assert (np.asarray(gc).astype(np.int64) == np.asarray(ec).astype(np.int64)).all(), (r, b)
             overflowed += int((np.asarray(g[0]) == 4).sum())
     assert (overflowed > 0) == (cap == 600)
+
+
+def test_padded_region_sizing():
+    """Host logic of the peer-memory regions (A-32): the NCCL handle's formula,
+    ceil(batch / G * (1 + slack)) + 1024, never above the batch, the whole batch
+    at G = 1."""
+    from paper_2510_15095_b200.sharded import P2PShardedHive
+    pr = P2PShardedHive.padded_region
+    assert pr(1 << 26, 1) == 1 << 26
+    assert pr(1 << 26, 8) == 8_913_920 and isinstance(pr(1 << 26, 8), int)      # 2^23 * 1.0625 + 1024
+    assert pr(1000, 8) == 1000                                                 # capped at the batch
+    for g in (2, 3, 4, 8):
+        r = pr(1 << 24, g)
+        assert isinstance(r, int) and (1 << 24) / g < r <= (1 << 24)
