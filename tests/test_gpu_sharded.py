@@ -192,3 +192,27 @@ def test_sharded_source_dedup_zipf_batch(pg):
     k, v = sh.table.dump()
     assert dict(zip(_np(k).astype(np.uint32).tolist(), _np(v).astype(np.uint32).tolist())) == o.dump_dict()
     sh.close()
+
+
+@pytest.mark.parametrize("flags", [dict(hash="crc"), dict(keys_unique=True)])
+def test_sharded_handle_with_table_flags(pg, flags):
+    """Sharded handles take the table flags: the CRC-32 / CRC-64 hash pair (A-26)
+    and HIVE_KEYS_UNIQUE (no owner election; batches here are duplicate-free)."""
+    import oracle
+    from paper_2510_15095_b200 import u32
+    from paper_2510_15095_b200.sharded import ShardedHive
+    n = 40000
+    sh = ShardedHive(4096 * 32, batch_max=n, lf_grow=2.0, lf_shrink=0, **flags)
+    o = oracle.OracleTable(4096 * 32, lf_grow=2.0, lf_shrink=0, **({"hash": flags["hash"]} if "hash" in flags else {}))
+    ids = np.arange(n, dtype=np.uint32)
+    k, v = gen.keys_of(ids), gen.vals_of(ids)
+    assert (_np(sh.insert(u32(k), u32(v))) == o.insert(k, v)).all()
+    qids, _ = gen.mixed_queries(n // 2, n // 2, n, seed=77)
+    q = gen.keys_of(qids)
+    vv, ff = sh.find(u32(q))
+    v_o, f_o = o.find(q)
+    assert (_np(ff) == f_o).all() and (_np(vv).astype(np.uint32) == v_o).all()
+    assert (_np(sh.erase(u32(k[::3]))) == o.erase(k[::3])).all()
+    kk, vv2 = sh.table.dump()
+    assert dict(zip(_np(kk).astype(np.uint32).tolist(), _np(vv2).astype(np.uint32).tolist())) == o.dump_dict()
+    sh.close()
