@@ -184,24 +184,9 @@ struct DedupView {
     uint8_t* flag;       // per op (indexed like the keys), zeroed per phase
     uint32_t* owner_of;  // per op, written for flagged ops only
     uint32_t n_parts;    // sub-tables (power of two)
-    // List of flagged ops (nullable): the duplicate fix-up visits only these.
-    // An op may appear twice (two threads flag it at once); *fcount > fcap
-    // means the list overflowed and the fix-up scans every op instead.
-    uint32_t* flist = nullptr;
-    unsigned long long* fcount = nullptr;
-    uint64_t fcap = 0;
     __device__ __forceinline__ uint64_t* sub(uint32_t h) const {
         const uint32_t part = n_parts > 1 ? (uint32_t)(((uint64_t)h * n_parts) >> 32) : 0u;
         return slots + (uint64_t)part * (mask + 1);
-    }
-    // Flag op as a duplicate (and list it once flagged for the first time).
-    __device__ __forceinline__ void mark(uint32_t op) const {
-        if (flag[op]) return;
-        flag[op] = 1;
-        if (flist) {
-            const unsigned long long at = atomicAdd(fcount, 1ull);
-            if (at < fcap) flist[at] = op;
-        }
     }
 };
 

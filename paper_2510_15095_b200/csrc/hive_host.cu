@@ -227,10 +227,6 @@ struct hive_table_s {
     // second set: hive_mixed elects its ERASE phase before the control wait
     // (small batches only: one sub-table, no partition scratch)
     uint64_t* dd2 = nullptr;   uint64_t dd2_cap = 0;
-    // lists of flagged (duplicate) ops of the two election sets + their counts
-    uint32_t* flist = nullptr;  uint64_t flist_cap = 0;
-    uint32_t* flist2 = nullptr; uint64_t flist2_cap = 0;
-    unsigned long long* fcnt = nullptr;                  // [0] set 1, [1] set 2
     uint32_t* owner2 = nullptr; uint64_t owner2_cap = 0;
     uint8_t* flag2 = nullptr;  uint64_t flag2_cap = 0;
     uint64_t* erec = nullptr; uint64_t erec_cap = 0;     // election records (op << 32 | key)
@@ -502,10 +498,8 @@ hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* 
     CKS(ensure(h->dd, h->dd_cap, sub * parts));
     CKS(ensure(h->owner, h->owner_cap, n_batch));
     CKS(ensure(h->flag, h->flag_cap, n_batch));
-    CKS(ensure(h->flist, h->flist_cap, 2 * n_upper + 64));
-    *dd = DedupView{h->dd, sub - 1, h->flag, h->owner, parts, h->flist, h->fcnt, h->flist_cap};
+    *dd = DedupView{h->dd, sub - 1, h->flag, h->owner, parts};
     CK(cudaMemsetAsync(h->flag, 0, n_batch, s));
-    CK(cudaMemsetAsync(h->fcnt, 0, sizeof(unsigned long long), s));
     if (parts == 1 || !jit) CK(cudaMemsetAsync(h->dd, 0xFF, sub * parts * sizeof(uint64_t), s));
     if (parts == 1) {
         Prof p(h, "k_dedup_elect", s);
@@ -544,10 +538,8 @@ bool elect_owners_set2(hive_table_s* h, const uint32_t* keys, const uint32_t* id
     if (hive_status e = ensure(h->dd2, h->dd2_cap, sub); e != HIVE_OK) return fail(e);
     if (hive_status e = ensure(h->owner2, h->owner2_cap, n_batch); e != HIVE_OK) return fail(e);
     if (hive_status e = ensure(h->flag2, h->flag2_cap, n_batch); e != HIVE_OK) return fail(e);
-    if (hive_status e = ensure(h->flist2, h->flist2_cap, 2 * n_upper + 64); e != HIVE_OK) return fail(e);
-    *dd = DedupView{h->dd2, sub - 1, h->flag2, h->owner2, 1, h->flist2, h->fcnt + 1, h->flist2_cap};
+    *dd = DedupView{h->dd2, sub - 1, h->flag2, h->owner2, 1};
     cudaError_t e = cudaMemsetAsync(h->flag2, 0, n_batch, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(h->fcnt + 1, 0, sizeof(unsigned long long), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(h->dd2, 0xFF, sub * sizeof(uint64_t), s);
     if (e == cudaSuccess) {
         Prof p(h, "k_dedup_elect", s);
@@ -1157,7 +1149,6 @@ hive_status hive_create(const hive_config* cfg, void* stream, hive_t* out) {
         return fail(HIVE_ENOMEM);
     if (cudaMalloc((void**)&h->aborts, MAX_SEGMENTS * sizeof(unsigned long long)) != cudaSuccess)
         return fail(HIVE_ENOMEM);
-    if (cudaMalloc((void**)&h->fcnt, 2 * sizeof(unsigned long long)) != cudaSuccess) return fail(HIVE_ENOMEM);
     memset(h->ctrl_h, 0, sizeof(Ctrl));
     if (cfg->nccl_comm) {                     // one shard of a hash-partitioned table
         if (!load_nccl()) return fail(HIVE_ENCCL);
@@ -1206,7 +1197,7 @@ hive_status hive_destroy(hive_t h) {
     vrange_free(h->ix);
     vrange_free(h->dr);
     vrange_free(h->sp);
-    void* bufs[] = {h->ctrl, h->flist, h->flist2, h->fcnt, h->rvals, h->ftab, h->dd, h->owner, h->flag, h->dd2, h->owner2, h->flag2, h->left, h->cls, h->cnt, h->pinfo, h->aborts,
+    void* bufs[] = {h->ctrl, h->rvals, h->ftab, h->dd, h->owner, h->flag, h->dd2, h->owner2, h->flag2, h->left, h->cls, h->cnt, h->pinfo, h->aborts,
                     h->erec, h->ecount, h->einfo, h->hk, h->hv, h->hst, h->fq, h->fv, h->ff};
     for (auto e : h->pipe_ev) cudaEventDestroy(e);
     if (h->ins_free) cudaEventDestroy(h->ins_free);

@@ -375,7 +375,7 @@ k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ id
         const uint32_t grp = __match_any_sync(FULL, k);
         if (active) ab += 4 + (idx ? 4 : 0);
         if (k == INVALID_KEY) continue;
-        if (__popc(grp) > 1) dd.mark(op);
+        if (__popc(grp) > 1) dd.flag[op] = 1;
         if ((31 - __clz(grp)) != lane) continue;
         const uint64_t word = ((uint64_t)k << 32) | op;
         const uint32_t hk = fmix32(k ^ DEDUP_SEED);
@@ -387,8 +387,8 @@ k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ id
             ab += 32;
             if (prev == EMPTY) break;
             if ((uint32_t)(prev >> 32) == k) {
-                dd.mark(op);
-                dd.mark((uint32_t)prev);
+                dd.flag[op] = 1;
+                dd.flag[(uint32_t)prev] = 1;
                 if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
                 break;
             }
@@ -421,7 +421,7 @@ k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict
         // lanes holding the same key
         uint32_t mx = op;
         if (__popc(grp) > 1) {
-            dd.mark(op);
+            dd.flag[op] = 1;
             mx = __reduce_max_sync(grp, op);
         }
         if (op != mx) continue;
@@ -435,8 +435,8 @@ k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict
             ab += 32;
             if (prev == EMPTY) break;
             if ((uint32_t)(prev >> 32) == k) {
-                dd.mark(op);
-                dd.mark((uint32_t)prev);
+                dd.flag[op] = 1;
+                dd.flag[(uint32_t)prev] = 1;
                 if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
                 break;
             }
@@ -457,8 +457,8 @@ __device__ __forceinline__ void elect_resolve(const DedupView& dd, uint64_t* tab
     for (uint64_t probe = 0;; ) {
         if (prev == EMPTY) return;
         if ((uint32_t)(prev >> 32) == k) {
-            dd.mark(op);
-            dd.mark((uint32_t)prev);
+            dd.flag[op] = 1;
+            dd.flag[(uint32_t)prev] = 1;
             if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
             return;
         }
@@ -487,13 +487,13 @@ k_dedup_elect_part2(const uint64_t* __restrict__ recs, const uint64_t* __restric
         bool da = ta < n, db = tb < n;
         ab += (da ? 8 : 0) + (db ? 8 : 0);
         if (da && __popc(ga) > 1) {
-            dd.mark(opa);
+            dd.flag[opa] = 1;
             da = __reduce_max_sync(ga, opa) == opa;
         } else if (__popc(ga) > 1) {
             (void)__reduce_max_sync(ga, opa);               // every lane of the group takes part
         }
         if (db && __popc(gb) > 1) {
-            dd.mark(opb);
+            dd.flag[opb] = 1;
             db = __reduce_max_sync(gb, opb) == opb;
         } else if (__popc(gb) > 1) {
             (void)__reduce_max_sync(gb, opb);
@@ -1366,7 +1366,7 @@ k_insert_fused(const uint64_t* __restrict__ recs, const uint32_t* __restrict__ r
                 eab += 8;
                 uint32_t mx = op;
                 if (__popc(grp) > 1) {                   // same key in this warp: pre-merge
-                    dd.mark(op);
+                    dd.flag[op] = 1;
                     mx = __reduce_max_sync(grp, op);
                 }
                 if (op != mx) continue;
@@ -1384,8 +1384,8 @@ k_insert_fused(const uint64_t* __restrict__ recs, const uint32_t* __restrict__ r
                         continue;
                     }
                     if (((uint32_t)(e >> 32) & 0x3FFFFFFu) == hk26) {
-                        dd.mark(op);
-                        dd.mark((uint32_t)e);
+                        dd.flag[op] = 1;
+                        dd.flag[(uint32_t)e] = 1;
                         if (word > e) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
                         eab += 32;
                         break;
@@ -1791,15 +1791,6 @@ __global__ void __launch_bounds__(BLOCK)
 k_dup_copy(const uint32_t* __restrict__ idx, uint64_t n, const uint64_t* __restrict__ n_dev,
            DedupView dd, uint8_t* __restrict__ out) {
     if (n_dev) n = *n_dev;
-    if (dd.flist && *dd.fcount <= dd.fcap) {   // only the listed (flagged) ops
-        const uint64_t nl = *dd.fcount;
-        for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < nl; i += (uint64_t)gridDim.x * BLOCK) {
-            const uint32_t op = dd.flist[i];
-            const uint32_t o = dd.owner_of[op];
-            if (o != op) out[op] = out[o];
-        }
-        return;
-    }
     if (!idx) {                             // contiguous ops: 16 flags per load
         const uint64_t nv = n / 16;
         const uint4* f4 = reinterpret_cast<const uint4*>(dd.flag);
