@@ -36,15 +36,26 @@ for dedup in (False, True):
     sh.find_host(kh)
     torch.cuda.synchronize()
     sh.close()
-# hive_load_image: a table's own dump layout reloaded into another table
-t = HiveTable(64 * 32, lf_grow=2.0, lf_shrink=0)
-k = u32(gen.present_keys(1800))
-t.insert(k, k)
-slots = torch.full((64 * 32,), -1, dtype=torch.int64, device="cuda")
-kk, vv = t.dump()
+# hive_load_image: keys placed first-fit in their b1 bucket (64 buckets, split 0), the rest in the stash
+from paper_2510_15095_b200 import hive
+keys = gen.present_keys(1800)
+h1 = hive.hash_keys("bithash1", u32(keys)).cpu().numpy().view(np.uint32)
+slots = np.full(64 * 32, np.uint64(0xFFFFFFFFFFFFFFFF), np.uint64)
+fill = np.zeros(64, np.int64)
+stash = []
+for k, h in zip(keys.tolist(), h1.tolist()):
+    b = h & 63
+    w = np.uint64((k << 32) | k)
+    if fill[b] < 32:
+        slots[b * 32 + fill[b]] = w
+        fill[b] += 1
+    else:
+        stash.append(w)
 u = HiveTable(64 * 32, lf_grow=2.0, lf_shrink=0)
-u.insert(kk, vv)
-u.find(k)
+u.load_image(torch.from_numpy(slots.view(np.int64)).cuda(),
+             torch.from_numpy(np.array(stash, np.uint64).view(np.int64)).cuda() if stash else None)
+v, f = u.find(u32(keys))
+assert bool(f.all().item())
 torch.cuda.synchronize()
 dist.destroy_process_group()
 print("ok")
