@@ -184,6 +184,7 @@ struct DedupView {
     uint8_t* flag;       // per op (indexed like the keys), zeroed per phase
     uint32_t* owner_of;  // per op, written for flagged ops only
     uint32_t n_parts;    // sub-tables (power of two)
+    uint8_t* any = nullptr;  // set to 1 by the election if it flags any op (zeroed with flag)
     __device__ __forceinline__ uint64_t* sub(uint32_t h) const {
         const uint32_t part = n_parts > 1 ? (uint32_t)(((uint64_t)h * n_parts) >> 32) : 0u;
         return slots + (uint64_t)part * (mask + 1);

@@ -497,9 +497,9 @@ hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* 
         1024, parts == 1 ? 2 * n_upper : (uint64_t)(fill * (double)n_upper / parts)));
     CKS(ensure(h->dd, h->dd_cap, sub * parts));
     CKS(ensure(h->owner, h->owner_cap, n_batch));
-    CKS(ensure(h->flag, h->flag_cap, n_batch));
-    *dd = DedupView{h->dd, sub - 1, h->flag, h->owner, parts};
-    CK(cudaMemsetAsync(h->flag, 0, n_batch, s));
+    CKS(ensure(h->flag, h->flag_cap, n_batch + 1));
+    *dd = DedupView{h->dd, sub - 1, h->flag, h->owner, parts, h->flag + n_batch};
+    CK(cudaMemsetAsync(h->flag, 0, n_batch + 1, s));
     if (parts == 1 || !jit) CK(cudaMemsetAsync(h->dd, 0xFF, sub * parts * sizeof(uint64_t), s));
     if (parts == 1) {
         Prof p(h, "k_dedup_elect", s);
@@ -513,8 +513,10 @@ hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* 
                                   h->einfo, h->erec, h->num_sms));
     }
     // Each part's sub-table is cleared right before its launch: the memset
-    // leaves its lines in L2, where the election's CASes then hit.  The
-    // sub-tables stay intact for the probe kernels' owner lookups.
+    // leaves its lines in L2, where the election's CASes then hit (clearing on
+    // a side stream that overlaps the partition and the earlier parts measured
+    // slower: the parts then miss L2).  The sub-tables stay
+    // intact for the probe kernels' owner lookups.
     Prof p(h, "k_dedup_elect", s, parts);
     for (uint32_t q = 0; q < parts; ++q) {
         if (jit) CK(cudaMemsetAsync(h->dd + (uint64_t)q * sub, 0xFF, sub * sizeof(uint64_t), s));
@@ -537,9 +539,9 @@ bool elect_owners_set2(hive_table_s* h, const uint32_t* keys, const uint32_t* id
     auto fail = [&](hive_status e) { *st = e; return false; };
     if (hive_status e = ensure(h->dd2, h->dd2_cap, sub); e != HIVE_OK) return fail(e);
     if (hive_status e = ensure(h->owner2, h->owner2_cap, n_batch); e != HIVE_OK) return fail(e);
-    if (hive_status e = ensure(h->flag2, h->flag2_cap, n_batch); e != HIVE_OK) return fail(e);
-    *dd = DedupView{h->dd2, sub - 1, h->flag2, h->owner2, 1};
-    cudaError_t e = cudaMemsetAsync(h->flag2, 0, n_batch, s);
+    if (hive_status e = ensure(h->flag2, h->flag2_cap, n_batch + 1); e != HIVE_OK) return fail(e);
+    *dd = DedupView{h->dd2, sub - 1, h->flag2, h->owner2, 1, h->flag2 + n_batch};
+    cudaError_t e = cudaMemsetAsync(h->flag2, 0, n_batch + 1, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(h->dd2, 0xFF, sub * sizeof(uint64_t), s);
     if (e == cudaSuccess) {
         Prof p(h, "k_dedup_elect", s);
@@ -628,7 +630,10 @@ hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* 
     }
     if (dedup && status) {
         Prof p(h, "k_dup_copy", s);
-        CK(launch_dup_copy(h->grids.stream, s, idx, n_upper, n_dev, dd, status));
+        // flags are set only for this phase's ops (the array is per phase), so
+        // the dense scan of flag[0, n_batch) replaces a walk of the op list
+        // (16 flags per load instead of one random byte per listed op)
+        CK(launch_dup_copy(h->grids.stream, s, nullptr, n_batch, nullptr, dd, status));
     }
     return HIVE_OK;
 }
@@ -778,7 +783,7 @@ hive_status erase_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* i
     }
     if (dedup && out) {
         Prof p(h, "k_dup_copy", s);
-        CK(launch_dup_copy(h->grids.stream, s, idx, n_upper, n_dev, dd, out));
+        CK(launch_dup_copy(h->grids.stream, s, nullptr, n_batch, nullptr, dd, out));   // dense scan
     }
     return HIVE_OK;
 }
@@ -825,13 +830,12 @@ namespace {
 hive_status mixed_impl(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, const uint32_t* d_vals,
                        uint64_t n, const uint64_t* n_dev, uint32_t* d_vals_out, uint8_t* d_result,
                        cudaStream_t s) {
-    // classify: stable partition of op indices by opcode (3 regions of n)
+    // classify: op indices by opcode into 3 regions of n (one pass; order
+    // inside a region is not the op order -- every phase is order-free)
     CKS(ensure(h->cls, h->cls_cap, 3 * n));
-    CKS(ensure(h->cnt, h->cnt_cap, 3 * part_warps(n) + 1));
     {
-        Prof p(h, "k_classify", s, 3);
-        CK(launch_partition(s, PART_CLASSIFY, 3, 0, d_keys, d_vals, d_op, n, h->cnt, h->pinfo, h->cls, n,
-                            nullptr, nullptr, nullptr, d_result, d_vals_out, nullptr, n_dev));
+        Prof p(h, "k_classify", s);
+        CK(launch_classify(s, d_op, n, n_dev, h->pinfo, h->cls, n, d_result, d_vals_out, h->num_sms));
     }
     const uint64_t* n_find = h->pinfo + 0;
     const uint64_t* n_ins = h->pinfo + 1;

@@ -354,74 +354,35 @@ k_find(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint
 // --------------------------------------------------------------------------------
 // Owner election for in-batch duplicates (reading A-15):
 // insert-if-absent of (key << 32 | op) into a per-batch table; atomicMax keeps
-// the highest op per key (the oracle's last write).  Ops inside a warp are
-// increasing with the lane (identity or stable lists), so __match_any_sync's
-// highest lane is the warp-local maximum.  Every op whose key occurs more than
-// once gets flag[op] = 1 (the first conflicting arrival flags the creator), so
-// the phase kernels consult the table only for those ops.
+// the highest op per key (the oracle's last write).  Lanes of a warp holding
+// the same key elect their highest op first (op lists are in no particular
+// order).  Every op whose key occurs more than once gets flag[op] = 1 (the
+// first conflicting arrival flags the creator), so the phase kernels consult
+// the table only for those ops; *dd.any = 1 once any op is flagged.
 // --------------------------------------------------------------------------------
+__device__ __forceinline__ void mark_any(const DedupView& dd, bool flagged) {
+    if (__syncthreads_or(flagged) && threadIdx.x == 0 && dd.any) *dd.any = 1;
+}
 __global__ void __launch_bounds__(BLOCK)
 k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
               const uint64_t* __restrict__ n_dev, DedupView dd, Ctrl* ctrl) {
     if (n_dev) n = *n_dev;
     uint32_t ab = 0;                       // per-thread: < 2^32 bytes
+    bool flagged = false;
     const int lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
     for (uint64_t t0 = (uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u); t0 < n; t0 += stride) {
         const uint64_t t = t0 + lane;
         const bool active = t < n;
-        const uint64_t op = active ? (idx ? (uint64_t)idx[t] : t) : 0;
+        const uint32_t op = active ? (idx ? idx[t] : (uint32_t)t) : 0u;    // < 2^32 (API)
         const uint32_t k = active ? keys[op] : INVALID_KEY;
         const uint32_t grp = __match_any_sync(FULL, k);
         if (active) ab += 4 + (idx ? 4 : 0);
         if (k == INVALID_KEY) continue;
-        if (__popc(grp) > 1) dd.flag[op] = 1;
-        if ((31 - __clz(grp)) != lane) continue;
-        const uint64_t word = ((uint64_t)k << 32) | op;
-        const uint32_t hk = fmix32(k ^ DEDUP_SEED);
-        uint64_t* tab = dd.sub(hk);
-        uint64_t h = hk & dd.mask;
-        uint64_t probe = 0;
-        for (; probe <= dd.mask; ++probe) {
-            const uint64_t prev = cas64(&tab[h], EMPTY, word);
-            ab += 32;
-            if (prev == EMPTY) break;
-            if ((uint32_t)(prev >> 32) == k) {
-                dd.flag[op] = 1;
-                dd.flag[(uint32_t)prev] = 1;
-                if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
-                break;
-            }
-            h = (h + 1) & dd.mask;
-        }
-        if (probe > dd.mask) atomicAdd(&ctrl->eover, 1ull);   // table full: never at the sizing (stats)
-    }
-    block_add(&ctrl->abytes[AB_ELECT], ab);
-}
-
-// Election over one part of a hash-partitioned phase: input = the part's
-// (op << 32 | key) records in op order (stable partition), sub-table L2-resident.
-__global__ void __launch_bounds__(BLOCK)
-k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict__ part_info, uint32_t part,
-                   DedupView dd, Ctrl* ctrl) {
-    const uint64_t n = part_info[part];
-    const uint64_t base = part_info[MAX_PARTS + part];
-    const int lane = threadIdx.x & 31;
-    const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
-    uint32_t ab = 0;                       // per-thread: < 2^32 bytes
-    for (uint64_t t0 = (uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u); t0 < n; t0 += stride) {
-        const uint64_t t = t0 + lane;
-        const bool active = t < n;
-        const uint64_t w = active ? recs[base + t] : EMPTY;
-        const uint32_t k = (uint32_t)w, op = (uint32_t)(w >> 32);
-        const uint32_t grp = __match_any_sync(FULL, k);
-        if (active) ab += 8;
-        if (!active) continue;
-        // input order inside a warp is arbitrary here: elect the max op of the
-        // lanes holding the same key
         uint32_t mx = op;
         if (__popc(grp) > 1) {
             dd.flag[op] = 1;
+            flagged = true;
             mx = __reduce_max_sync(grp, op);
         }
         if (op != mx) continue;
@@ -437,6 +398,7 @@ k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict
             if ((uint32_t)(prev >> 32) == k) {
                 dd.flag[op] = 1;
                 dd.flag[(uint32_t)prev] = 1;
+                flagged = true;
                 if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
                 break;
             }
@@ -445,6 +407,59 @@ k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict
         if (probe > dd.mask) atomicAdd(&ctrl->eover, 1ull);   // table full: never at the sizing (stats)
     }
     block_add(&ctrl->abytes[AB_ELECT], ab);
+    mark_any(dd, flagged);
+}
+
+// Election over one part of a hash-partitioned phase: input = the part's
+// (op << 32 | key) records in op order (stable partition), sub-table L2-resident.
+__global__ void __launch_bounds__(BLOCK)
+k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict__ part_info, uint32_t part,
+                   DedupView dd, Ctrl* ctrl) {
+    const uint64_t n = part_info[part];
+    const uint64_t base = part_info[MAX_PARTS + part];
+    const int lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
+    uint32_t ab = 0;                       // per-thread: < 2^32 bytes
+    bool flagged = false;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u); t0 < n; t0 += stride) {
+        const uint64_t t = t0 + lane;
+        const bool active = t < n;
+        const uint64_t w = active ? recs[base + t] : EMPTY;
+        const uint32_t k = (uint32_t)w, op = (uint32_t)(w >> 32);
+        const uint32_t grp = __match_any_sync(FULL, k);
+        if (active) ab += 8;
+        if (!active) continue;
+        // input order inside a warp is arbitrary here: elect the max op of the
+        // lanes holding the same key
+        uint32_t mx = op;
+        if (__popc(grp) > 1) {
+            dd.flag[op] = 1;
+            flagged = true;
+            mx = __reduce_max_sync(grp, op);
+        }
+        if (op != mx) continue;
+        const uint64_t word = ((uint64_t)k << 32) | op;
+        const uint32_t hk = fmix32(k ^ DEDUP_SEED);
+        uint64_t* tab = dd.sub(hk);
+        uint64_t h = hk & dd.mask;
+        uint64_t probe = 0;
+        for (; probe <= dd.mask; ++probe) {
+            const uint64_t prev = cas64(&tab[h], EMPTY, word);
+            ab += 32;
+            if (prev == EMPTY) break;
+            if ((uint32_t)(prev >> 32) == k) {
+                dd.flag[op] = 1;
+                dd.flag[(uint32_t)prev] = 1;
+                flagged = true;
+                if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
+                break;
+            }
+            h = (h + 1) & dd.mask;
+        }
+        if (probe > dd.mask) atomicAdd(&ctrl->eover, 1ull);   // table full: never at the sizing (stats)
+    }
+    block_add(&ctrl->abytes[AB_ELECT], ab);
+    mark_any(dd, flagged);
 }
 
 // The same election with two independent records per lane per iteration:
@@ -459,6 +474,7 @@ __device__ __forceinline__ void elect_resolve(const DedupView& dd, uint64_t* tab
         if ((uint32_t)(prev >> 32) == k) {
             dd.flag[op] = 1;
             dd.flag[(uint32_t)prev] = 1;
+            if (dd.any) *dd.any = 1;                         // rare: a duplicate across warps
             if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
             return;
         }
@@ -488,12 +504,14 @@ k_dedup_elect_part2(const uint64_t* __restrict__ recs, const uint64_t* __restric
         ab += (da ? 8 : 0) + (db ? 8 : 0);
         if (da && __popc(ga) > 1) {
             dd.flag[opa] = 1;
+            if (dd.any) *dd.any = 1;
             da = __reduce_max_sync(ga, opa) == opa;
         } else if (__popc(ga) > 1) {
             (void)__reduce_max_sync(ga, opa);               // every lane of the group takes part
         }
         if (db && __popc(gb) > 1) {
             dd.flag[opb] = 1;
+            if (dd.any) *dd.any = 1;
             db = __reduce_max_sync(gb, opb) == opb;
         } else if (__popc(gb) > 1) {
             (void)__reduce_max_sync(gb, opb);
@@ -1790,6 +1808,7 @@ k_mixed_mono(const uint8_t* __restrict__ opc, const uint32_t* __restrict__ keys,
 __global__ void __launch_bounds__(BLOCK)
 k_dup_copy(const uint32_t* __restrict__ idx, uint64_t n, const uint64_t* __restrict__ n_dev,
            DedupView dd, uint8_t* __restrict__ out) {
+    if (dd.any && *dd.any == 0) return;     // the election flagged nothing
     if (n_dev) n = *n_dev;
     if (!idx) {                             // contiguous ops: 16 flags per load
         const uint64_t nv = n / 16;
@@ -2450,6 +2469,89 @@ cudaError_t launch_mixed_mono(int grid, cudaStream_t s, const uint8_t* ops, cons
                     (void*)&tab_mask, (void*)&flag, (void*)&owner_of, (void*)&leftover, (void*)&max_evictions,
                     (void*)&result, (void*)&vals_out};
     return cudaLaunchCooperativeKernel((const void*)k_mixed_mono<G_INSERT, G_SLOW>, grid, BLOCK, args, 0, s);
+}
+
+// PHASED classification in ONE pass: the op indices of each
+// opcode class (0 find, 1 insert, 2 erase) go to region c of out_idx (stride
+// `stride`); ops with another opcode get result 0 / value 0 in place.  Each
+// tile of CTILE ops reserves its runs with one atomicAdd per class on
+// counts[0..2] (zeroed by the caller), so a region is ordered tile by tile in
+// reservation order, not in op order: every consumer is order-free (the
+// elections keep the highest op index, reading A-15; finds and erases are
+// independent per op).  Replaces the count / single-block scan / scatter
+// partition for this 3-class case (three launches, ~36 us per 2^20-op batch).
+constexpr int CTILE = 4096;
+__global__ void __launch_bounds__(BLOCK)
+k_classify(const uint8_t* __restrict__ ops, uint64_t n, const uint64_t* __restrict__ n_dev,
+           unsigned long long* __restrict__ counts, uint32_t* __restrict__ out_idx, uint64_t stride,
+           uint8_t* __restrict__ result_zero, uint32_t* __restrict__ vals_zero) {
+    constexpr int PER = CTILE / BLOCK;                   // rows of 32 ops per warp
+    __shared__ uint32_t wtot[WARPS_PER_BLOCK][3];
+    __shared__ unsigned long long woff[WARPS_PER_BLOCK][3];
+    if (n_dev) n = *n_dev;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt = lanemask_lt();
+    for (uint64_t t0 = (uint64_t)blockIdx.x * CTILE; t0 < n; t0 += (uint64_t)gridDim.x * CTILE) {
+        const uint64_t wbase = t0 + (uint64_t)warp * 32 * PER + lane;
+        uint32_t cls[PER];
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const uint64_t i = wbase + (uint64_t)r * 32;
+            cls[r] = i < n ? (ops[i] < 3 ? ops[i] : 3u) : 4u;
+        }
+        // per row: rank of the lane inside its class (ballots), running warp totals
+        uint32_t c0 = 0, c1 = 0, c2 = 0;
+        uint32_t rank[PER];
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const uint32_t b0 = __ballot_sync(FULL, cls[r] == 0), b1 = __ballot_sync(FULL, cls[r] == 1),
+                           b2 = __ballot_sync(FULL, cls[r] == 2);
+            const uint32_t bm = cls[r] == 0 ? b0 : cls[r] == 1 ? b1 : b2;
+            const uint32_t run = cls[r] == 0 ? c0 : cls[r] == 1 ? c1 : c2;
+            rank[r] = run + __popc(bm & lt);
+            c0 += __popc(b0);
+            c1 += __popc(b1);
+            c2 += __popc(b2);
+        }
+        if (lane == 0) {
+            wtot[warp][0] = c0;
+            wtot[warp][1] = c1;
+            wtot[warp][2] = c2;
+        }
+        __syncthreads();
+        if (threadIdx.x < 3) {                            // one reservation per class per tile
+            const int c = threadIdx.x;
+            uint32_t tot = 0;
+            for (int w = 0; w < WARPS_PER_BLOCK; ++w) tot += wtot[w][c];
+            unsigned long long base = tot ? atomicAdd(&counts[c], (unsigned long long)tot) : 0ull;
+            for (int w = 0; w < WARPS_PER_BLOCK; ++w) {
+                woff[w][c] = base;
+                base += wtot[w][c];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const uint64_t i = wbase + (uint64_t)r * 32;
+            if (cls[r] < 3) {
+                out_idx[cls[r] * stride + woff[warp][cls[r]] + rank[r]] = (uint32_t)i;
+            } else if (cls[r] == 3) {
+                if (result_zero) result_zero[i] = 0;
+                if (vals_zero) vals_zero[i] = 0;
+            }
+        }
+        __syncthreads();                                  // wtot / woff reuse
+    }
+}
+cudaError_t launch_classify(cudaStream_t s, const uint8_t* ops, uint64_t n, const uint64_t* n_dev,
+                            uint64_t* counts, uint32_t* out_idx, uint64_t stride, uint8_t* result_zero,
+                            uint32_t* vals_zero, int num_sms) {
+    cudaError_t e = cudaMemsetAsync(counts, 0, 3 * sizeof(uint64_t), s);
+    if (e != cudaSuccess || n == 0) return e;
+    const int grid = (int)std::min<uint64_t>((n + CTILE - 1) / CTILE, (uint64_t)num_sms * 8);
+    k_classify<<<grid, BLOCK, 0, s>>>(ops, n, n_dev, reinterpret_cast<unsigned long long*>(counts), out_idx, stride,
+                                      result_zero, vals_zero);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_dup_copy(int grid, cudaStream_t s, const uint32_t* idx, uint64_t n,

@@ -106,6 +106,12 @@ cudaError_t launch_count_ops(cudaStream_t s, const uint8_t* ops, uint64_t n, uin
 
 cudaError_t launch_dup_copy(int grid, cudaStream_t s, const uint32_t* idx, uint64_t n,
                             const uint64_t* n_dev, DedupView dd, uint8_t* out);
+// PHASED classification in one pass: counts[c] (zeroed here) = ops of class c
+// (0 find, 1 insert, 2 erase), their indices in out_idx[c * stride ...] in
+// tile reservation order (not op order); other opcodes: result / value 0.
+cudaError_t launch_classify(cudaStream_t s, const uint8_t* ops, uint64_t n, const uint64_t* n_dev,
+                            uint64_t* counts, uint32_t* out_idx, uint64_t stride, uint8_t* result_zero,
+                            uint32_t* vals_zero, int num_sms);
 
 cudaError_t launch_split(cudaStream_t s, TableView tv, uint32_t n_pairs, Ctrl* ctrl);
 cudaError_t launch_merge(cudaStream_t s, TableView tv, uint32_t n_pairs, unsigned long long* abort_at,

@@ -58,6 +58,25 @@ def test_ragged_batches(n):
     p.check_state()
 
 
+@pytest.mark.parametrize("n", [0, 1, 7, 33, 4095, 4096, 4097, 3 * 4096 + 5, 1 << 17])
+def test_ragged_mixed_batches(n):
+    """Mixed batches of every tile shape of the one-pass classification (4096-op
+    tiles: empty, partial, exact, one over, several): opcodes 0 / 1 / 2 plus
+    invalid opcodes (3, 200: result 0, value 0), repeated keys and the reserved
+    key, with growth and shrink on -- results and state equal the oracle's."""
+    rng = np.random.default_rng(1000 + n)
+    p = _pair(64 * 32, resize_k=16)
+    for rnd in range(3):
+        ops = rng.choice(np.array([0, 1, 2, 3, 200], np.uint8), size=n, p=[0.3, 0.4, 0.2, 0.05, 0.05])
+        ids = rng.integers(0, max(2, n // 2), n, dtype=np.uint64).astype(np.uint32)
+        keys = gen.keys_of(ids)
+        if n > 10:
+            keys[rng.integers(0, n, 3)] = INVALID
+        vals = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+        p.mixed(ops, keys, vals)
+        p.check_state()
+
+
 def test_duplicates_and_reserved_keys():
     """In-batch duplicates: statuses/erase outputs identical for duplicates
     (present at phase start), value = a member of the accepted set (this
