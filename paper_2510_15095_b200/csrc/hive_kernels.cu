@@ -2340,6 +2340,9 @@ Grids query_grids(int num_sms) {
     g.g_erase = env_g("HIVE_G_ERASE", G_ERASE);
     g.minb = getenv("HIVE_MINB") ? atoi(getenv("HIVE_MINB")) : MINB_DEFAULT;
     g.minb_find = getenv("HIVE_MINB_FIND") ? atoi(getenv("HIVE_MINB_FIND")) : MINB_FIND_DEFAULT;
+    // the Step-3 kernel's residency on its own (experiments; default: as the
+    // other mutating kernels)
+    g.minb_slow = getenv("HIVE_MINB_SLOW") ? atoi(getenv("HIVE_MINB_SLOW")) : g.minb;
 #define OCC_FIND(G, MB) g.find = occ((const void*)k_find<G, MB>) * num_sms
 #define OCC_INS(G, MB) g.insert_fast = occ((const void*)k_insert_fast<G, MB>) * num_sms
 #define OCC_SLOW(G, MB) g.insert_slow = occ((const void*)k_insert_slow<G, MB>) * num_sms
@@ -2350,7 +2353,7 @@ Grids query_grids(int num_sms) {
     // at 4 resident blocks of 256 threads)
     if (getenv("HIVE_FIND_BPS")) g.find = std::min(g.find, atoi(getenv("HIVE_FIND_BPS")) * num_sms);
     HIVE_DISPATCH_GM(g.g_insert, g.minb, OCC_INS)
-    HIVE_DISPATCH_GM(g.g_slow, g.minb, OCC_SLOW)
+    HIVE_DISPATCH_GM(g.g_slow, g.minb_slow, OCC_SLOW)
     HIVE_DISPATCH_GM(g.g_erase, g.minb, OCC_ERA)
 #define OCC_GATHER(G, MB) g.gather = occ((const void*)k_gather<G, MB>) * num_sms
     HIVE_DISPATCH_GM8(g.g_find, g.minb_find, OCC_GATHER)
@@ -2427,7 +2430,7 @@ cudaError_t launch_insert_slow(const Grids& gr, cudaStream_t s, const uint32_t* 
     }
 #define L_SLOW(G, MB) k_insert_slow<G, MB><<<gr.insert_slow, BLOCK, 0, s>>>(keys, vals, kvs, leftover, tv, sv, \
                                                                     max_evictions, status)
-    HIVE_DISPATCH_GM(gr.g_slow, gr.minb, L_SLOW)
+    HIVE_DISPATCH_GM(gr.g_slow, gr.minb_slow, L_SLOW)
     return cudaGetLastError();
 }
 

@@ -58,6 +58,7 @@ struct Grids {                           // persistent grid sizes (blocks)
     int g_find, g_insert, g_slow, g_erase;   // lanes per operation
     int minb;                                // min resident blocks/SM for the mutating kernels
     int minb_find;                           // ... and for k_find
+    int minb_slow;                           // ... and for k_insert_slow (HIVE_MINB_SLOW)
 };
 
 // Occupancy-derived persistent grid sizes for this device.
