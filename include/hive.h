@@ -313,8 +313,9 @@ hive_status hive_profile(hive_t h, int enable);
 int hive_profile_read(hive_t h, const char** names, double* ms, uint64_t* launches,
                       int max, int reset);
 
-/* ---- stable partition (used for mixed classification and for routing a
- * batch across hash-partitioned shards) -------------------- */
+/* ---- stable partition (routing a batch across hash-partitioned shards,
+ * SURVEY §8(e)); hive_mixed classifies its ops with a separate one-pass,
+ * order-free kernel -------------------------------------------------------- */
 
 /* Route a batch to n_shards shards: shard(k) = (fmix32(k ^ seed) * n_shards)
  * >> 32.  Stable (rank order preserved inside each shard).

@@ -191,6 +191,16 @@ struct DedupView {
     }
 };
 
+// A phase's duplicate fix-up (out[op] = out[owner_of[op]] for flagged ops)
+// handed to the next phase's kernel of a mixed batch; flag == nullptr: none.
+struct DupFix {
+    const uint8_t* flag = nullptr;
+    const uint32_t* owner_of = nullptr;
+    const uint8_t* any = nullptr;   // nullable: the election's any-flag word
+    uint8_t* out = nullptr;
+    uint64_t n = 0;                 // ops of the batch (flags are indexed by op)
+};
+
 // ---- memory access -----------------------------------------------------------------
 // Bucket loads: 256-bit vector loads (LDG.E.ENL2.256 on sm_100a), bypassing L1
 // allocation (random, no reuse; also no stale L1 lines across the CAS traffic of

@@ -597,7 +597,7 @@ hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* 
                          const uint64_t* kvs, const uint32_t* idx, uint64_t n_upper,
                          const uint64_t* n_dev, uint64_t n_batch, uint8_t* status,
                          uint32_t* vals_zero, cudaStream_t s, const InsertChunks* chunks = nullptr,
-                         const DedupView* pre = nullptr) {
+                         const DedupView* pre = nullptr, DupFix* defer = nullptr) {
     const bool dedup = !kvs && h->dedup_on();
     // large phases with election: the fused single-launch form, opt-in with
     // HIVE_FUSED=1 (measured slower than the multi-launch form)
@@ -628,7 +628,10 @@ hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* 
         CK(launch_insert_slow(h->grids, s, keys, vals, kvs, h->left, h->tv(), h->sv(),
                               h->cfg.max_evictions, status, h->step_prof));
     }
-    if (dedup && status) {
+    if (dedup && status && defer) {
+        // a mixed batch: the next phase's kernel runs the fix-up first
+        *defer = DupFix{dd.flag, dd.owner_of, dd.any, status, n_batch};
+    } else if (dedup && status) {
         Prof p(h, "k_dup_copy", s);
         // flags are set only for this phase's ops (the array is per phase), so
         // the dense scan of flag[0, n_batch) replaces a walk of the op list
@@ -771,7 +774,8 @@ hive_status shrink_after(hive_table_s* h, cudaStream_t s, int64_t count_lb = -1)
 
 hive_status erase_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* idx, uint64_t n_upper,
                         const uint64_t* n_dev, uint64_t n_batch, uint8_t* out, uint32_t* vals_zero,
-                        cudaStream_t s, const DedupView* pre = nullptr) {
+                        cudaStream_t s, const DedupView* pre = nullptr, const DupFix* carry = nullptr,
+                        DupFix* defer = nullptr) {
     const bool dedup = h->dedup_on();
     DedupView dd{nullptr, 0, nullptr, nullptr};
     if (dedup && pre) dd = *pre;                 // election already enqueued by the caller
@@ -779,9 +783,11 @@ hive_status erase_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* i
     {
         Prof p(h, "k_erase", s);
         CK(launch_erase(h->grids, s, keys, idx, n_upper, n_dev, h->tv(), h->sv(), dd, out,
-                        vals_zero));
+                        vals_zero, carry));
     }
-    if (dedup && out) {
+    if (dedup && out && defer) {
+        *defer = DupFix{dd.flag, dd.owner_of, dd.any, out, n_batch};     // into the FIND kernel
+    } else if (dedup && out) {
         Prof p(h, "k_dup_copy", s);
         CK(launch_dup_copy(h->grids.stream, s, nullptr, n_batch, nullptr, dd, out));   // dense scan
     }
@@ -867,12 +873,19 @@ hive_status mixed_impl(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
         count_lb = count0 > n_erase ? (int64_t)(count0 - n_erase) : 0;
         if (h->stage_h[1]) CKS(grow_known(h, count0, h->stage_h[1], s));
     }
+    // each phase's duplicate fix-up runs as the prologue of the next phase's
+    // kernel (they write results of different op classes): two launches less.
+    // The INSERT fix-up rides in k_erase only when the ERASE phase was elected
+    // into the second scratch set (pre_era); otherwise that election reuses
+    // the first set's flags and the fix-up must run before it.
+    DupFix fix_ins, fix_era;
     CKS(insert_phase(h, d_keys, d_vals, nullptr, h->cls + n, n, n_ins, n, d_result, d_vals_out, s, nullptr,
-                     pre ? &dd_ins : nullptr));
-    CKS(erase_phase(h, d_keys, h->cls + 2 * n, n, n_era, n, d_result, d_vals_out, s, pre_era ? &dd_era : nullptr));
+                     pre ? &dd_ins : nullptr, pre_era ? &fix_ins : nullptr));
+    CKS(erase_phase(h, d_keys, h->cls + 2 * n, n, n_era, n, d_result, d_vals_out, s, pre_era ? &dd_era : nullptr,
+                    pre_era ? &fix_ins : nullptr, &fix_era));
     CKS(shrink_after(h, s, count_lb));
     Prof p(h, "k_find", s);
-    CK(launch_find(h->grids, s, d_keys, h->cls, n, n_find, h->tv(), h->sv(), d_vals_out, d_result));
+    CK(launch_find(h->grids, s, d_keys, h->cls, n, n_find, h->tv(), h->sv(), d_vals_out, d_result, &fix_era));
     return HIVE_OK;
 }
 

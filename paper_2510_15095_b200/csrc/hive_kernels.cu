@@ -274,6 +274,28 @@ __device__ __forceinline__ bool wcme_value(const WarpGroup<G>& wg, const uint64_
     return M != 0;
 }
 
+// Duplicate fix-up body (k_dup_copy's dense form; see there).
+__device__ __forceinline__ void dup_fix(const DupFix& fx) {
+    if (fx.any && *fx.any == 0) return;     // the election flagged nothing
+    const uint64_t n = fx.n, nv = n / 16;
+    const uint4* f4 = reinterpret_cast<const uint4*>(fx.flag);
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 w = f4[v];
+        if ((w.x | w.y | w.z | w.w) == 0) continue;
+        for (int j = 0; j < 16; ++j) {
+            const uint64_t op = v * 16 + j;
+            if (!fx.flag[op]) continue;
+            const uint32_t o = fx.owner_of[op];
+            if (o != (uint32_t)op) fx.out[op] = fx.out[o];
+        }
+    }
+    for (uint64_t op = nv * 16 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; op < n;
+         op += (uint64_t)gridDim.x * blockDim.x) {
+        if (!fx.flag[op]) continue;
+        const uint32_t o = fx.owner_of[op];
+        if (o != (uint32_t)op) fx.out[op] = fx.out[o];
+    }
+}
 // --------------------------------------------------------------------------------
 // FIND: WCME on b1, then b2 only on a miss, then the stash
 // index only when the stash is non-empty.  Read-only phase.
@@ -282,10 +304,11 @@ template <int G, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB)
 k_find(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
        const uint64_t* __restrict__ n_dev, TableView tv, StashView sv,
-       uint32_t* __restrict__ vals_out, uint8_t* __restrict__ found_out) {
+       uint32_t* __restrict__ vals_out, uint8_t* __restrict__ found_out, DupFix fx) {
     using WG = WarpGroup<G>;
     constexpr int SPL = WG::SPL;
     WG wg;
+    if (fx.flag) dup_fix(fx);               // the ERASE phase's duplicate fix-up (mixed batch)
     if (n_dev) n = *n_dev;
     const bool stash_on = sv.ctrl->stash_tail != 0;
     uint32_t ab = 0;                       // per-thread: < 2^32 bytes
@@ -1485,10 +1508,11 @@ template <int G, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB)
 k_erase(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
         const uint64_t* __restrict__ n_dev, TableView tv, StashView sv, DedupView dd,
-        uint8_t* __restrict__ erased_out, uint32_t* __restrict__ vals_zero) {
+        uint8_t* __restrict__ erased_out, uint32_t* __restrict__ vals_zero, DupFix fx) {
     using WG = WarpGroup<G>;
     constexpr int SPL = WG::SPL;
     WG wg;
+    if (fx.flag) dup_fix(fx);               // the INSERT phase's duplicate fix-up (mixed batch)
     if (n_dev) n = *n_dev;
     const bool stash_on = sv.ctrl->stash_tail != 0;
     unsigned long long removed = 0;
@@ -1804,31 +1828,17 @@ k_mixed_mono(const uint8_t* __restrict__ opc, const uint32_t* __restrict__ keys,
         }
 }
 
-// Duplicates copy their owner's outcome (PHASED contract, A-17).
+// Duplicates copy their owner's outcome (PHASED contract, A-17): the dense
+// form scans flag[0, n) (16 flags per load); flags are set only for the
+// phase's own ops.  Also run as the prologue of the next phase's kernel in a
+// mixed batch (DupFix): the two touch result entries of different op classes.
 __global__ void __launch_bounds__(BLOCK)
 k_dup_copy(const uint32_t* __restrict__ idx, uint64_t n, const uint64_t* __restrict__ n_dev,
            DedupView dd, uint8_t* __restrict__ out) {
     if (dd.any && *dd.any == 0) return;     // the election flagged nothing
     if (n_dev) n = *n_dev;
-    if (!idx) {                             // contiguous ops: 16 flags per load
-        const uint64_t nv = n / 16;
-        const uint4* f4 = reinterpret_cast<const uint4*>(dd.flag);
-        for (uint64_t v = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * BLOCK) {
-            const uint4 w = f4[v];
-            if ((w.x | w.y | w.z | w.w) == 0) continue;
-            for (int j = 0; j < 16; ++j) {
-                const uint64_t op = v * 16 + j;
-                if (!dd.flag[op]) continue;
-                const uint32_t o = dd.owner_of[op];
-                if (o != (uint32_t)op) out[op] = out[o];
-            }
-        }
-        for (uint64_t op = nv * 16 + (uint64_t)blockIdx.x * BLOCK + threadIdx.x; op < n;
-             op += (uint64_t)gridDim.x * BLOCK) {
-            if (!dd.flag[op]) continue;
-            const uint32_t o = dd.owner_of[op];
-            if (o != (uint32_t)op) out[op] = out[o];
-        }
+    if (!idx) {
+        dup_fix(DupFix{dd.flag, dd.owner_of, dd.any, out, n});
         return;
     }
     for (uint64_t t = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; t < n;
@@ -2370,9 +2380,10 @@ static inline int clamp_grid(int grid, uint64_t n, uint64_t per_block) {
 
 cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                         uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
-                        uint32_t* vals_out, uint8_t* found) {
-    const int grid = n_dev ? gr.find : clamp_grid(gr.find, n, BLOCK / gr.g_find);
-#define L_FIND(G, MB) k_find<G, MB><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, vals_out, found)
+                        uint32_t* vals_out, uint8_t* found, const DupFix* fix) {
+    const DupFix fx = fix ? *fix : DupFix{};
+    const int grid = (n_dev || fx.flag) ? gr.find : clamp_grid(gr.find, n, BLOCK / gr.g_find);
+#define L_FIND(G, MB) k_find<G, MB><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, vals_out, found, fx)
     HIVE_DISPATCH_GM8(gr.g_find, gr.minb_find, L_FIND)
     return cudaGetLastError();
 }
@@ -2436,9 +2447,10 @@ cudaError_t launch_insert_slow(const Grids& gr, cudaStream_t s, const uint32_t* 
 
 cudaError_t launch_erase(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                          uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
-                         DedupView dd, uint8_t* erased, uint32_t* vals_zero) {
-    const int grid = n_dev ? gr.erase : clamp_grid(gr.erase, n, BLOCK / gr.g_erase);
-#define L_ERA(G, MB) k_erase<G, MB><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, dd, erased, vals_zero)
+                         DedupView dd, uint8_t* erased, uint32_t* vals_zero, const DupFix* fix) {
+    const DupFix fx = fix ? *fix : DupFix{};
+    const int grid = (n_dev || fx.flag) ? gr.erase : clamp_grid(gr.erase, n, BLOCK / gr.g_erase);
+#define L_ERA(G, MB) k_erase<G, MB><<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, tv, sv, dd, erased, vals_zero, fx)
     HIVE_DISPATCH_GM(gr.g_erase, gr.minb, L_ERA)
     return cudaGetLastError();
 }

@@ -72,9 +72,10 @@ cudaError_t init_hash_tables();
 cudaError_t launch_gather(const Grids& gr, cudaStream_t s, const uint32_t* keys, uint64_t n,
                           const uint64_t* blocks, uint64_t n_blocks, uint32_t* out, uint32_t mode);
 
+// fix (nullable): the previous phase's duplicate fix-up, run first (mixed batches)
 cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                         uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
-                        uint32_t* vals_out, uint8_t* found);
+                        uint32_t* vals_out, uint8_t* found, const DupFix* fix = nullptr);
 
 cudaError_t launch_dedup_elect(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                                uint64_t n, const uint64_t* n_dev, DedupView dd, Ctrl* ctrl);
@@ -91,7 +92,7 @@ cudaError_t launch_insert_slow(const Grids& gr, cudaStream_t s, const uint32_t* 
 
 cudaError_t launch_erase(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
                          uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
-                         DedupView dd, uint8_t* erased, uint32_t* vals_zero);
+                         DedupView dd, uint8_t* erased, uint32_t* vals_zero, const DupFix* fix = nullptr);
 
 // NEXT-4 monolithic concurrent mixed kernel (one cooperative launch).
 // tab: the per-batch group table (tab_mask + 1 words, a power of two >= 2n);
