@@ -525,30 +525,38 @@ hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* 
     return HIVE_OK;
 }
 
-// Owner election of a phase small enough for one sub-table, into the second
-// scratch set (hive_mixed's ERASE phase, elected before the control wait).
-// Returns false (nothing enqueued) when the phase would need partitioning.
-bool elect_owners_set2(hive_table_s* h, const uint32_t* keys, const uint32_t* idx, uint64_t n_upper,
-                       const uint64_t* n_dev, uint64_t n_batch, DedupView* dd, cudaStream_t s,
-                       hive_status* st) {
+// Both elections of a mixed batch whose phases each fit one sub-table, in ONE
+// launch (hive_mixed, before the control wait): the INSERT list into the first
+// scratch set, the ERASE list into the second.  Returns false (nothing
+// enqueued) when a phase would need the partitioned election.
+bool elect_pair(hive_table_s* h, const uint32_t* keys, const uint32_t* idx_ins, const uint64_t* n_ins,
+                const uint32_t* idx_era, const uint64_t* n_era, uint64_t n_upper, uint64_t n_batch,
+                DedupView* dd_ins, DedupView* dd_era, cudaStream_t s, hive_status* st) {
     static const uint64_t sub_bytes = getenv("HIVE_ELECT_MB") ? (uint64_t)atoi(getenv("HIVE_ELECT_MB")) << 20
                                                               : (32ull << 20);
     *st = HIVE_OK;
     if (2 * n_upper * sizeof(uint64_t) > sub_bytes) return false;
     const uint64_t sub = pow2_at_least(std::max<uint64_t>(1024, 2 * n_upper));
     auto fail = [&](hive_status e) { *st = e; return false; };
+    if (hive_status e = ensure(h->dd, h->dd_cap, sub); e != HIVE_OK) return fail(e);
+    if (hive_status e = ensure(h->owner, h->owner_cap, n_batch); e != HIVE_OK) return fail(e);
+    if (hive_status e = ensure(h->flag, h->flag_cap, n_batch + 1); e != HIVE_OK) return fail(e);
     if (hive_status e = ensure(h->dd2, h->dd2_cap, sub); e != HIVE_OK) return fail(e);
     if (hive_status e = ensure(h->owner2, h->owner2_cap, n_batch); e != HIVE_OK) return fail(e);
     if (hive_status e = ensure(h->flag2, h->flag2_cap, n_batch + 1); e != HIVE_OK) return fail(e);
-    *dd = DedupView{h->dd2, sub - 1, h->flag2, h->owner2, 1, h->flag2 + n_batch};
-    cudaError_t e = cudaMemsetAsync(h->flag2, 0, n_batch + 1, s);
+    *dd_ins = DedupView{h->dd, sub - 1, h->flag, h->owner, 1, h->flag + n_batch};
+    *dd_era = DedupView{h->dd2, sub - 1, h->flag2, h->owner2, 1, h->flag2 + n_batch};
+    cudaError_t e = cudaMemsetAsync(h->flag, 0, n_batch + 1, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->dd, 0xFF, sub * sizeof(uint64_t), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->flag2, 0, n_batch + 1, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(h->dd2, 0xFF, sub * sizeof(uint64_t), s);
     if (e == cudaSuccess) {
         Prof p(h, "k_dedup_elect", s);
-        e = launch_dedup_elect(h->grids.dedup, s, keys, idx, n_upper, n_dev, *dd, h->ctrl);
+        e = launch_dedup_elect(h->grids.dedup, s, keys, idx_ins, n_upper, n_ins, *dd_ins, h->ctrl, idx_era, n_era,
+                               dd_era);
     }
     if (e != cudaSuccess) {
-        set_err(e, "elect_owners_set2", __LINE__);
+        set_err(e, "elect_pair", __LINE__);
         return fail(HIVE_ECUDA);
     }
     return true;
@@ -858,11 +866,14 @@ hive_status mixed_impl(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
         // geometry: enqueue it before waiting, so the GPU has work while the
         // host plans the resize from the count it just read.
         if (h->dedup_on()) {
-            CKS(elect_owners(h, d_keys, h->cls + n, n, n_ins, n, &dd_ins, s));
-            pre = true;
             hive_status e2 = HIVE_OK;
-            pre_era = elect_owners_set2(h, d_keys, h->cls + 2 * n, n, n_era, n, &dd_era, s, &e2);
+            pre = pre_era = elect_pair(h, d_keys, h->cls + n, n_ins, h->cls + 2 * n, n_era, n, n, &dd_ins, &dd_era,
+                                       s, &e2);
             CKS(e2);
+            if (!pre) {                      // large batch: the INSERT phase's partitioned election
+                CKS(elect_owners(h, d_keys, h->cls + n, n, n_ins, n, &dd_ins, s));
+                pre = true;
+            }
         }
         {
             Trace tr("read_ctrl", 0);

@@ -388,49 +388,63 @@ __device__ __forceinline__ void mark_any(const DedupView& dd, bool flagged) {
 }
 __global__ void __launch_bounds__(BLOCK)
 k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
-              const uint64_t* __restrict__ n_dev, DedupView dd, Ctrl* ctrl) {
+              const uint64_t* __restrict__ n_dev, DedupView dd, Ctrl* ctrl,
+              const uint32_t* __restrict__ idx2, const uint64_t* __restrict__ n_dev2, DedupView dd2) {
+    // job 1: the ops of idx (or 0..n-1) into dd; job 2 (idx2 != nullptr, a
+    // mixed batch's ERASE list next to its INSERT list): the ops of idx2 into
+    // dd2, starting at a warp-aligned virtual index so no warp mixes the jobs
     if (n_dev) n = *n_dev;
+    const uint64_t n2 = idx2 ? *n_dev2 : 0;
+    const uint64_t ra = (n + 31) & ~31ull;
     uint32_t ab = 0;                       // per-thread: < 2^32 bytes
-    bool flagged = false;
+    bool flagged = false, flagged2 = false;
     const int lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
-    for (uint64_t t0 = (uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u); t0 < n; t0 += stride) {
-        const uint64_t t = t0 + lane;
-        const bool active = t < n;
-        const uint32_t op = active ? (idx ? idx[t] : (uint32_t)t) : 0u;    // < 2^32 (API)
+    for (uint64_t v0 = (uint64_t)blockIdx.x * BLOCK + (threadIdx.x & ~31u); v0 < ra + n2; v0 += stride) {
+        const bool second = v0 >= ra;                               // warp-uniform
+        const DedupView& d = second ? dd2 : dd;
+        const uint64_t t = (second ? v0 - ra : v0) + lane;
+        const bool active = t < (second ? n2 : n);
+        const uint32_t* li = second ? idx2 : idx;
+        const uint32_t op = active ? (li ? li[t] : (uint32_t)t) : 0u;    // < 2^32 (API)
         const uint32_t k = active ? keys[op] : INVALID_KEY;
         const uint32_t grp = __match_any_sync(FULL, k);
-        if (active) ab += 4 + (idx ? 4 : 0);
+        if (active) ab += 4 + (li ? 4 : 0);
         if (k == INVALID_KEY) continue;
+        bool fl = false;
         uint32_t mx = op;
         if (__popc(grp) > 1) {
-            dd.flag[op] = 1;
-            flagged = true;
+            d.flag[op] = 1;
+            fl = true;
             mx = __reduce_max_sync(grp, op);
         }
-        if (op != mx) continue;
-        const uint64_t word = ((uint64_t)k << 32) | op;
-        const uint32_t hk = fmix32(k ^ DEDUP_SEED);
-        uint64_t* tab = dd.sub(hk);
-        uint64_t h = hk & dd.mask;
-        uint64_t probe = 0;
-        for (; probe <= dd.mask; ++probe) {
-            const uint64_t prev = cas64(&tab[h], EMPTY, word);
-            ab += 32;
-            if (prev == EMPTY) break;
-            if ((uint32_t)(prev >> 32) == k) {
-                dd.flag[op] = 1;
-                dd.flag[(uint32_t)prev] = 1;
-                flagged = true;
-                if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
-                break;
+        if (op == mx) {
+            const uint64_t word = ((uint64_t)k << 32) | op;
+            const uint32_t hk = fmix32(k ^ DEDUP_SEED);
+            uint64_t* tab = d.sub(hk);
+            uint64_t h = hk & d.mask;
+            uint64_t probe = 0;
+            for (; probe <= d.mask; ++probe) {
+                const uint64_t prev = cas64(&tab[h], EMPTY, word);
+                ab += 32;
+                if (prev == EMPTY) break;
+                if ((uint32_t)(prev >> 32) == k) {
+                    d.flag[op] = 1;
+                    d.flag[(uint32_t)prev] = 1;
+                    fl = true;
+                    if (word > prev) atomicMax((unsigned long long*)&tab[h], (unsigned long long)word);
+                    break;
+                }
+                h = (h + 1) & d.mask;
             }
-            h = (h + 1) & dd.mask;
+            if (probe > d.mask) atomicAdd(&ctrl->eover, 1ull);   // table full: never at the sizing (stats)
         }
-        if (probe > dd.mask) atomicAdd(&ctrl->eover, 1ull);   // table full: never at the sizing (stats)
+        if (second) flagged2 |= fl;
+        else flagged |= fl;
     }
     block_add(&ctrl->abytes[AB_ELECT], ab);
     mark_any(dd, flagged);
+    if (idx2) mark_any(dd2, flagged2);
 }
 
 // Election over one part of a hash-partitioned phase: input = the part's
@@ -1261,7 +1275,35 @@ __device__ __forceinline__ void insert_slow_body(const uint32_t* __restrict__ ke
         // preferring residents in their second bucket raised p_h1 to 0.93 but
         // doubled evictions and grew the stash 5x -- a net loss).
         const bool evicting = busy && !placed;
-        const int vs = (int)((seed + r * 11u) & 31u);
+        int vs = (int)((seed + r * 11u) & 31u);
+        if constexpr (VICTIM_LOOK > 0) {
+            // Split-aware victim (A-6 allows any rule; placement is not
+            // observable): VICTIM_LOOK candidate slots, VICTIM_LOOK / G per
+            // lane -- lane l's j-th candidate is its slot (vs + j) mod SPL --
+            // and the first (in (j, l) order) whose resident's other bucket is
+            // a split one (b < split or b > mask) is evicted: under linear
+            // hashing those hold half the keys of the unsplit buckets, so the
+            // chain likely ends there.  None: the rotating slot vs.
+            constexpr int PER_LANE = VICTIM_LOOK / G > 0 ? VICTIM_LOOK / G : 1;
+            uint32_t good = 0;
+#pragma unroll
+            for (int j = 0; j < PER_LANE; ++j) {
+                const int sl = (vs + j) % SPL;                 // this lane's candidate
+                bool g = false;
+                if (evicting) {
+                    const uint64_t cand = pick<SPL>(s, sl);
+                    if (cand != EMPTY) {
+                        const uint32_t a = tv.alt(key_of(cand), b);
+                        g = a != b && (a < tv.split || a > tv.mask);
+                    }
+                }
+                good |= wg.ballot(g) << (j * G);              // bit j * G + lane
+            }
+            if (good) {
+                const int f = __ffs(good) - 1;
+                vs = (f % G) * SPL + (vs + f / G) % SPL;
+            }
+        }
         const int vl = vs / SPL;
         const uint64_t victim = wg.bcast(pick<SPL>(s, vs % SPL), vl);
         const bool can = evicting && victim != EMPTY;
@@ -2408,9 +2450,10 @@ cudaError_t launch_dedup_elect_part(int grid, cudaStream_t s, const uint64_t* re
 }
 
 cudaError_t launch_dedup_elect(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
-                               uint64_t n, const uint64_t* n_dev, DedupView dd, Ctrl* ctrl) {
+                               uint64_t n, const uint64_t* n_dev, DedupView dd, Ctrl* ctrl,
+                               const uint32_t* idx2, const uint64_t* n_dev2, const DedupView* dd2) {
     if (!n_dev) grid = clamp_grid(grid, n, BLOCK);
-    k_dedup_elect<<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, dd, ctrl);
+    k_dedup_elect<<<grid, BLOCK, 0, s>>>(keys, idx, n, n_dev, dd, ctrl, idx2, n_dev2, dd2 ? *dd2 : DedupView{});
     return cudaGetLastError();
 }
 

@@ -32,6 +32,15 @@ constexpr uint32_t TWO_CHOICE_T = HIVE_TWO_CHOICE_T;
 // experiments: -DHIVE_CLAIM_ROT=r through HIVE_NVCC_DEFINES)
 constexpr uint32_t CLAIM_ROT_DEFAULT = HIVE_CLAIM_ROT;
 
+#ifndef HIVE_VICTIM_LOOK
+#define HIVE_VICTIM_LOOK 8
+#endif
+// Step 3 victim choice: 0 = rotating slot; v > 0 = the first of v candidate
+// slots (v / G per lane) whose resident's other bucket is a split one.  8 from
+// the A/B in profiles/r02b_victim_ab.txt (cfg2 Step 3 1.22 -> 0.88 ms, cfg3
+// 3.58 -> 3.91 G ops/s); build-time -DHIVE_VICTIM_LOOK=v for experiments.
+constexpr int VICTIM_LOOK = HIVE_VICTIM_LOOK;
+
 enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1, PART_ELECT = 2, PART_ROUTE_KEYS = 3, PART_ROUTE_P2P = 4,
                 PART_ROUTE_PAD = 5 };
 
@@ -77,8 +86,12 @@ cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, c
                         uint64_t n, const uint64_t* n_dev, TableView tv, StashView sv,
                         uint32_t* vals_out, uint8_t* found, const DupFix* fix = nullptr);
 
+// idx2 / n_dev2 / dd2 (nullable): a second op list elected in the same launch
+// into its own scratch set (a mixed batch's ERASE list beside its INSERT list).
 cudaError_t launch_dedup_elect(int grid, cudaStream_t s, const uint32_t* keys, const uint32_t* idx,
-                               uint64_t n, const uint64_t* n_dev, DedupView dd, Ctrl* ctrl);
+                               uint64_t n, const uint64_t* n_dev, DedupView dd, Ctrl* ctrl,
+                               const uint32_t* idx2 = nullptr, const uint64_t* n_dev2 = nullptr,
+                               const DedupView* dd2 = nullptr);
 
 cudaError_t launch_insert_fast(const Grids& gr, cudaStream_t s, const uint32_t* keys, const uint32_t* vals,
                                const uint64_t* kvs, const uint32_t* idx, uint64_t n,
