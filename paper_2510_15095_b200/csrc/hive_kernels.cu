@@ -1276,7 +1276,9 @@ __device__ __forceinline__ void insert_slow_body(const uint32_t* __restrict__ ke
         // doubled evictions and grew the stash 5x -- a net loss).
         const bool evicting = busy && !placed;
         int vs = (int)((seed + r * 11u) & 31u);
-        if constexpr (VICTIM_LOOK > 0) {
+        // (not for the lookup-based CRC pair: its constant-memory hashes cost
+        // more than the shorter chains save -- CRC inserts 4.28 -> 3.35 G/s)
+        if (VICTIM_LOOK > 0 && tv.hkind != HASH_CRC) {
             // Split-aware victim (A-6 allows any rule; placement is not
             // observable): VICTIM_LOOK candidate slots, VICTIM_LOOK / G per
             // lane -- lane l's j-th candidate is its slot (vs + j) mod SPL --
