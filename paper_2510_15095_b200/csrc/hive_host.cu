@@ -517,10 +517,14 @@ hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* 
     // a side stream that overlaps the partition and the earlier parts measured
     // slower: the parts then miss L2).  The sub-tables stay
     // intact for the probe kernels' owner lookups.
+    // HIVE_ELECT_CHAIN=1: part q's launch clears part q+1's sub-table in its
+    // tail instead of a memset between the launches (A/B)
+    static const bool chain = getenv("HIVE_ELECT_CHAIN") && atoi(getenv("HIVE_ELECT_CHAIN")) != 0;
     Prof p(h, "k_dedup_elect", s, parts);
     for (uint32_t q = 0; q < parts; ++q) {
-        if (jit) CK(cudaMemsetAsync(h->dd + (uint64_t)q * sub, 0xFF, sub * sizeof(uint64_t), s));
-        CK(launch_dedup_elect_part(h->grids.dedup, s, h->erec, h->einfo, q, *dd, h->ctrl));
+        if (jit && (!chain || q == 0)) CK(cudaMemsetAsync(h->dd + (uint64_t)q * sub, 0xFF, sub * sizeof(uint64_t), s));
+        uint64_t* next = (jit && chain && q + 1 < parts) ? h->dd + (uint64_t)(q + 1) * sub : nullptr;
+        CK(launch_dedup_elect_part(h->grids.dedup, s, h->erec, h->einfo, q, *dd, h->ctrl, next, next ? sub : 0));
     }
     return HIVE_OK;
 }

@@ -451,7 +451,7 @@ k_dedup_elect(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ id
 // (op << 32 | key) records in op order (stable partition), sub-table L2-resident.
 __global__ void __launch_bounds__(BLOCK)
 k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict__ part_info, uint32_t part,
-                   DedupView dd, Ctrl* ctrl) {
+                   DedupView dd, Ctrl* ctrl, uint4* __restrict__ clear_next, uint64_t clear_n16) {
     const uint64_t n = part_info[part];
     const uint64_t base = part_info[MAX_PARTS + part];
     const int lane = threadIdx.x & 31;
@@ -496,6 +496,13 @@ k_dedup_elect_part(const uint64_t* __restrict__ recs, const uint64_t* __restrict
         if (probe > dd.mask) atomicAdd(&ctrl->eover, 1ull);   // table full: never at the sizing (stats)
     }
     block_add(&ctrl->abytes[AB_ELECT], ab);
+    // clear the NEXT part's sub-table (EMPTY = all ones) in this launch's
+    // tail: the election is L2-atomic bound, so the writes use idle HBM time
+    // and leave the next table's lines in L2 for its launch
+    if (clear_next) {
+        const uint4 e = make_uint4(~0u, ~0u, ~0u, ~0u);
+        for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < clear_n16; i += stride) clear_next[i] = e;
+    }
     mark_any(dd, flagged);
 }
 
@@ -2433,7 +2440,8 @@ cudaError_t launch_find(const Grids& gr, cudaStream_t s, const uint32_t* keys, c
 }
 
 cudaError_t launch_dedup_elect_part(int grid, cudaStream_t s, const uint64_t* recs, const uint64_t* part_info,
-                                    uint32_t part, DedupView dd, Ctrl* ctrl) {
+                                    uint32_t part, DedupView dd, Ctrl* ctrl, uint64_t* clear_next,
+                                    uint64_t clear_words) {
     // HIVE_ELECT_ILP: 1 = one record per lane; 2 = two (40 registers, 6 blocks
     // per SM); 3 = two, capped at 32 registers (8 blocks per SM)
     static const int ilp = getenv("HIVE_ELECT_ILP") ? atoi(getenv("HIVE_ELECT_ILP")) : 1;
@@ -2445,9 +2453,14 @@ cudaError_t launch_dedup_elect_part(int grid, cudaStream_t s, const uint64_t* re
         g2 = occ((const void*)k_dedup_elect_part2<1>) * sms;
         g3 = occ((const void*)k_dedup_elect_part2<8>) * sms;
     }
+    if (ilp >= 2 && clear_next) {                 // the two-record variants do not clear
+        cudaError_t e = cudaMemsetAsync(clear_next, 0xFF, clear_words * sizeof(uint64_t), s);
+        if (e != cudaSuccess) return e;
+    }
     if (ilp == 2) k_dedup_elect_part2<1><<<g2, BLOCK, 0, s>>>(recs, part_info, part, dd, ctrl);
     else if (ilp >= 3) k_dedup_elect_part2<8><<<g3, BLOCK, 0, s>>>(recs, part_info, part, dd, ctrl);
-    else k_dedup_elect_part<<<grid, BLOCK, 0, s>>>(recs, part_info, part, dd, ctrl);
+    else k_dedup_elect_part<<<grid, BLOCK, 0, s>>>(recs, part_info, part, dd, ctrl,
+                                                   reinterpret_cast<uint4*>(clear_next), clear_words / 2);
     return cudaGetLastError();
 }
 

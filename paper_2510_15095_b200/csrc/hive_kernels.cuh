@@ -197,8 +197,11 @@ cudaError_t launch_insert_fused(int grid, cudaStream_t s, const uint64_t* recs, 
                                 DedupView dd, TableView tv, StashView sv, uint8_t* status, uint32_t* vals_zero,
                                 uint32_t* leftover, uint32_t max_evictions, const uint32_t* keys,
                                 const uint32_t* vals);
+// clear_next (nullable, clear_words even): a sub-table the launch sets to
+// EMPTY in its tail (the next part's, so its clear overlaps this election).
 cudaError_t launch_dedup_elect_part(int grid, cudaStream_t s, const uint64_t* recs, const uint64_t* part_info,
-                                    uint32_t part, DedupView dd, Ctrl* ctrl);
+                                    uint32_t part, DedupView dd, Ctrl* ctrl, uint64_t* clear_next = nullptr,
+                                    uint64_t clear_words = 0);
 
 // ---- sharded table over NCCL (include/hive.h "Sharded tables") ------
 // Stable route into a padded send buffer of G regions of `cap` records

@@ -121,6 +121,30 @@ def test_high_load_steps_3_and_4():
     p.check_state()
 
 
+@pytest.mark.parametrize("split", [1, 1536, 4095])
+def test_high_load_split_geometry(split):
+    """LF 0.97 on a table in the middle of a linear-hashing round (n_b = 2^12 +
+    split, so the split-aware eviction victim has split buckets to aim at --
+    few, many, all but one): every result, the stash-visible finds and the
+    final dump equal the oracle's, and Step 3 did run."""
+    nb = (1 << 12) + split
+    p = _pair(nb * 32, lf_grow=2.0, lf_shrink=0)
+    n = int(0.97 * nb * 32)
+    keys = gen.present_keys(n)
+    for lo in range(0, n, n // 3 + 1):
+        hi = min(n, lo + n // 3 + 1)
+        p.insert(keys[lo:hi], gen.vals_of(np.arange(lo, hi)))
+    sg, so = p.check_state()
+    assert sg["n_buckets"] == nb and sg["split"] == split
+    assert sg["leftovers"] > 0 and sg["evictions"] > 0
+    q = np.concatenate([keys, gen.absent_keys(20000)])
+    p.find(q)
+    p.erase(keys[1::4])
+    p.insert(keys[1::4], gen.vals_of(np.arange(1, n, 4)) ^ 0xA5A5)
+    p.find(q)
+    p.check_state()
+
+
 @pytest.mark.parametrize("resize_k", [1024, 7])
 def test_mixed_grow_and_shrink(resize_k):
     """BASELINE config 3 shape at small scale: 1K buckets, 40/20/40 mixed
