@@ -517,9 +517,12 @@ hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* 
     // a side stream that overlaps the partition and the earlier parts measured
     // slower: the parts then miss L2).  The sub-tables stay
     // intact for the probe kernels' owner lookups.
-    // HIVE_ELECT_CHAIN=1: part q's launch clears part q+1's sub-table in its
-    // tail instead of a memset between the launches (A/B)
-    static const bool chain = getenv("HIVE_ELECT_CHAIN") && atoi(getenv("HIVE_ELECT_CHAIN")) != 0;
+    // Part q's launch clears part q+1's sub-table in its tail (the election is
+    // L2-atomic bound, so the writes use idle HBM time and leave the next
+    // table's lines in L2): cfg2 elections 1.51 -> 1.31 ms
+    // (profiles/r02c_elect_chain_ab.txt).  HIVE_ELECT_CHAIN=0: a memset before
+    // each part instead.
+    static const bool chain = !getenv("HIVE_ELECT_CHAIN") || atoi(getenv("HIVE_ELECT_CHAIN")) != 0;
     Prof p(h, "k_dedup_elect", s, parts);
     for (uint32_t q = 0; q < parts; ++q) {
         if (jit && (!chain || q == 0)) CK(cudaMemsetAsync(h->dd + (uint64_t)q * sub, 0xFF, sub * sizeof(uint64_t), s));
@@ -1588,8 +1591,8 @@ static hive_status route_impl(int mode, uint32_t n_shards, uint32_t seed, const 
     const uint64_t E = (uint64_t)n_shards * part_warps(n) + 1;
     CKS(ensure(rs.cnt, rs.cap, E));
     if (!rs.info) CK(cudaMalloc((void**)&rs.info, 2 * MAX_PARTS * sizeof(uint64_t)));
-    CK(launch_partition(s, mode, n_shards, seed, d_keys, d_vals, d_ops, n, rs.cnt, rs.info, nullptr, 0,
-                        d_send_kv, d_send_ops, d_pos, nullptr, nullptr));
+    CK(launch_partition(s, mode, n_shards, seed, d_keys, d_vals, d_ops, n, rs.cnt, rs.info, d_send_kv, d_send_ops,
+                        d_pos));
     CK(cudaMemcpyAsync(d_counts, rs.info, n_shards * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
     return HIVE_OK;
 }

@@ -2025,23 +2025,13 @@ k_count_b1(TableView tv, uint64_t n_slots, Ctrl* ctrl) {
     block_add(&ctrl->in_b1, c);
 }
 
-__device__ __forceinline__ uint32_t part_of(int mode, uint32_t n_parts, uint32_t seed,
-                                            const uint32_t* keys, const uint8_t* ops, uint64_t i) {
-    if (mode == PART_CLASSIFY) {
-        const uint32_t o = ops[i];
-        return o < 3 ? o : 3u;
-    }
-    if (mode == PART_ELECT) {                    // election sub-table of the key
-        const uint32_t k = keys[i];
-        if (k == INVALID_KEY) return MAX_PARTS;
-        return (uint32_t)(((uint64_t)fmix32(k ^ DEDUP_SEED) * (uint64_t)n_parts) >> 32);
-    }
-    // shard(k) = (fmix32(k ^ seed) * G) >> 32
+// shard(k) = (fmix32(k ^ seed) * G) >> 32 of op i
+__device__ __forceinline__ uint32_t shard_of(uint32_t n_parts, uint32_t seed, const uint32_t* keys, uint64_t i) {
     return (uint32_t)(((uint64_t)fmix32(keys[i] ^ seed) * (uint64_t)n_parts) >> 32);
 }
 
 // Lanes of the warp holding the same label q (all lanes call).  Labels below
-// 16 (classify: 3 opcodes + invalid, routing: <= 8 shards + invalid) take 4
+// 16 (routing: <= 8 shards + the out-of-range label) take 4
 // ballots; larger label sets use __match_any_sync (measured ~3x slower).
 __device__ __forceinline__ uint32_t same_label(uint32_t q, bool small) {
     if (!small) return __match_any_sync(FULL, q);
@@ -2078,7 +2068,7 @@ k_part_count(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __restri
             for (int u = 0; u < PART_UNROLL; ++u) {
                 const uint64_t i = i0 + u * 32 + lane;
                 const uint64_t e = i < hi ? (idx ? (uint64_t)idx[i] : i) : 0;
-                pp[u] = i < hi ? part_of(mode, n_parts, seed, keys, ops, e) : MAX_PARTS;
+                pp[u] = i < hi ? shard_of(n_parts, seed, keys, e) : MAX_PARTS;
             }
 #pragma unroll
             for (int u = 0; u < PART_UNROLL; ++u) {
@@ -2160,10 +2150,8 @@ __global__ void __launch_bounds__(BLOCK)
 k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __restrict__ keys,
                const uint32_t* __restrict__ vals, const uint8_t* __restrict__ ops, uint64_t n,
                uint64_t n_warps, const uint64_t* __restrict__ off,
-               const uint64_t* __restrict__ part_info, uint32_t* __restrict__ out_idx,
-               uint64_t idx_stride, uint64_t* __restrict__ send_kv, uint8_t* __restrict__ send_ops,
-               uint32_t* __restrict__ pos_out, uint8_t* __restrict__ result_zero,
-               uint32_t* __restrict__ vals_zero, const uint32_t* __restrict__ idx,
+               const uint64_t* __restrict__ part_info, uint64_t* __restrict__ send_kv,
+               uint8_t* __restrict__ send_ops, uint32_t* __restrict__ pos_out, const uint32_t* __restrict__ idx,
                const uint64_t* __restrict__ n_dev, uint32_t chunk, PeerDest pd) {
     __shared__ uint64_t run[WARPS_PER_BLOCK][MAX_PARTS + 1];
     const bool small = n_parts < 16;
@@ -2182,7 +2170,7 @@ k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __rest
         for (int u = 0; u < PART_UNROLL; ++u) {                  // all rows' loads first
             const uint64_t i = r0 + u * 32 + lane;
             ee[u] = i < hi ? (idx ? (uint64_t)idx[i] : i) : 0;
-            pp[u] = i < hi ? part_of(mode, n_parts, seed, keys, ops, ee[u]) : MAX_PARTS;
+            pp[u] = i < hi ? shard_of(n_parts, seed, keys, ee[u]) : MAX_PARTS;
         }
 #pragma unroll
         for (int u = 0; u < PART_UNROLL; ++u) {                  // then rank the rows in order
@@ -2200,16 +2188,7 @@ k_part_scatter(int mode, uint32_t n_parts, uint32_t seed, const uint32_t* __rest
             if (in && p < n_parts && (__ffs(grp) - 1) == lane) run[wib][p] += __popc(grp);
             __syncwarp();
             if (!in) continue;
-            if (mode == PART_ELECT) {
-                if (p < n_parts) send_kv[pos] = (e << 32) | keys[e];
-            } else if (mode == PART_CLASSIFY) {
-                if (p < n_parts) {
-                    out_idx[(uint64_t)p * idx_stride + (pos - part_info[MAX_PARTS + p])] = (uint32_t)i;
-                } else {
-                    if (result_zero) result_zero[i] = 0;
-                    if (vals_zero) vals_zero[i] = 0;
-                }
-            } else if (mode == PART_ROUTE_KEYS) {
+            if (mode == PART_ROUTE_KEYS) {
                 reinterpret_cast<uint32_t*>(send_kv)[pos] = keys[i];
                 pos_out[i] = (uint32_t)pos;
             } else if (mode == PART_ROUTE_PAD) {
@@ -2674,28 +2653,22 @@ uint64_t part_warps(uint64_t n) { const uint64_t c = part_chunk(n); return (n + 
 
 cudaError_t launch_partition_pd(cudaStream_t s, int mode, uint32_t n_parts, uint32_t seed,
                                 const uint32_t* keys, const uint32_t* vals, const uint8_t* ops,
-                                uint64_t n, uint64_t* cnt, uint64_t* part_info,
-                                uint32_t* out_idx, uint64_t idx_stride, uint64_t* send_kv,
-                                uint8_t* send_ops, uint32_t* pos, uint8_t* result_zero,
-                                uint32_t* vals_zero, const uint32_t* idx, const uint64_t* n_dev,
+                                uint64_t n, uint64_t* cnt, uint64_t* part_info, uint64_t* send_kv,
+                                uint8_t* send_ops, uint32_t* pos, const uint32_t* idx, const uint64_t* n_dev,
                                 const PeerDest& pd);
 
 cudaError_t launch_partition(cudaStream_t s, int mode, uint32_t n_parts, uint32_t seed,
                              const uint32_t* keys, const uint32_t* vals, const uint8_t* ops,
-                             uint64_t n, uint64_t* cnt, uint64_t* part_info,
-                             uint32_t* out_idx, uint64_t idx_stride, uint64_t* send_kv,
-                             uint8_t* send_ops, uint32_t* pos, uint8_t* result_zero,
-                             uint32_t* vals_zero, const uint32_t* idx, const uint64_t* n_dev) {
-    return launch_partition_pd(s, mode, n_parts, seed, keys, vals, ops, n, cnt, part_info, out_idx, idx_stride,
-                               send_kv, send_ops, pos, result_zero, vals_zero, idx, n_dev, PeerDest{});
+                             uint64_t n, uint64_t* cnt, uint64_t* part_info, uint64_t* send_kv,
+                             uint8_t* send_ops, uint32_t* pos, const uint32_t* idx, const uint64_t* n_dev) {
+    return launch_partition_pd(s, mode, n_parts, seed, keys, vals, ops, n, cnt, part_info, send_kv, send_ops, pos,
+                               idx, n_dev, PeerDest{});
 }
 
 cudaError_t launch_partition_pd(cudaStream_t s, int mode, uint32_t n_parts, uint32_t seed,
                                 const uint32_t* keys, const uint32_t* vals, const uint8_t* ops,
-                                uint64_t n, uint64_t* cnt, uint64_t* part_info,
-                                uint32_t* out_idx, uint64_t idx_stride, uint64_t* send_kv,
-                                uint8_t* send_ops, uint32_t* pos, uint8_t* result_zero,
-                                uint32_t* vals_zero, const uint32_t* idx, const uint64_t* n_dev,
+                                uint64_t n, uint64_t* cnt, uint64_t* part_info, uint64_t* send_kv,
+                                uint8_t* send_ops, uint32_t* pos, const uint32_t* idx, const uint64_t* n_dev,
                                 const PeerDest& pd) {
     const uint64_t nw = part_warps(n);
     const uint32_t chunk = part_chunk(n);
@@ -2704,8 +2677,7 @@ cudaError_t launch_partition_pd(cudaStream_t s, int mode, uint32_t n_parts, uint
     k_part_scan<<<1, 1024, 0, s>>>(cnt, (uint64_t)n_parts * nw, n_parts, nw, part_info);
     if (nw)
         k_part_scatter<<<grid, BLOCK, 0, s>>>(mode, n_parts, seed, keys, vals, ops, n, nw, cnt, part_info,
-                                              out_idx, idx_stride, send_kv, send_ops, pos, result_zero,
-                                              vals_zero, idx, n_dev, chunk, pd);
+                                              send_kv, send_ops, pos, idx, n_dev, chunk, pd);
     return cudaGetLastError();
 }
 
@@ -2907,7 +2879,7 @@ cudaError_t launch_route_pad(cudaStream_t s, uint32_t n_shards, uint32_t seed, c
     PeerDest pd{};
     pd.region = cap;
     cudaError_t e = launch_partition_pd(s, PART_ROUTE_PAD, n_shards, seed, keys, vals, ops, n, cnt, part_info,
-                                        nullptr, 0, send_kv, send_ops, pos, nullptr, nullptr, idx, n_dev, pd);
+                                        send_kv, send_ops, pos, idx, n_dev, pd);
     if (e != cudaSuccess) return e;
     k_pad_counts<<<1, 32, 0, s>>>(part_info, n_shards, cap, cnt_send, ctrl);
     return cudaGetLastError();
@@ -3167,7 +3139,7 @@ cudaError_t launch_route_p2p(cudaStream_t s, uint32_t n_shards, uint32_t seed, c
                              const uint32_t* vals, const uint8_t* ops, uint64_t n, uint64_t* cnt,
                              uint64_t* part_info, uint32_t* pos, const PeerDest& pd, unsigned long long* xfail) {
     cudaError_t e = launch_partition_pd(s, PART_ROUTE_P2P, n_shards, seed, keys, vals, ops, n, cnt, part_info,
-                                        nullptr, 0, nullptr, nullptr, pos, nullptr, nullptr, nullptr, nullptr, pd);
+                                        nullptr, nullptr, pos, nullptr, nullptr, pd);
     if (e != cudaSuccess) return e;
     k_p2p_counts<<<1, 32, 0, s>>>(part_info, n_shards, pd, xfail);
     return cudaGetLastError();

@@ -41,8 +41,10 @@ constexpr uint32_t CLAIM_ROT_DEFAULT = HIVE_CLAIM_ROT;
 // 3.58 -> 3.91 G ops/s); build-time -DHIVE_VICTIM_LOOK=v for experiments.
 constexpr int VICTIM_LOOK = HIVE_VICTIM_LOOK;
 
-enum PartMode { PART_CLASSIFY = 0, PART_ROUTE = 1, PART_ELECT = 2, PART_ROUTE_KEYS = 3, PART_ROUTE_P2P = 4,
-                PART_ROUTE_PAD = 5 };
+// Modes of the stable partition (shard routing).  Mixed-batch classification
+// and the election's hash partition have their own kernels (k_classify,
+// k_elect_hist / k_elect_scatter); values 0 and 2 are retired.
+enum PartMode { PART_ROUTE = 1, PART_ROUTE_KEYS = 3, PART_ROUTE_P2P = 4, PART_ROUTE_PAD = 5 };
 
 // Peer-memory exchange: the owners' inbox / count /
 // result buffers of up to MAX_PEERS shards, passed by value.  Every buffer is
@@ -173,10 +175,8 @@ cudaError_t launch_p2p_wait(cudaStream_t s, uint32_t n, uint32_t phase, uint64_t
 
 cudaError_t launch_partition(cudaStream_t s, int mode, uint32_t n_parts, uint32_t seed,
                              const uint32_t* keys, const uint32_t* vals, const uint8_t* ops,
-                             uint64_t n, uint64_t* cnt, uint64_t* part_info,
-                             uint32_t* out_idx, uint64_t idx_stride, uint64_t* send_kv,
-                             uint8_t* send_ops, uint32_t* pos, uint8_t* result_zero,
-                             uint32_t* vals_zero, const uint32_t* idx = nullptr,
+                             uint64_t n, uint64_t* cnt, uint64_t* part_info, uint64_t* send_kv,
+                             uint8_t* send_ops, uint32_t* pos, const uint32_t* idx = nullptr,
                              const uint64_t* n_dev = nullptr);
 cudaError_t launch_elect_partition(cudaStream_t s, const uint32_t* keys, const uint32_t* idx, uint64_t n,
                                    const uint64_t* n_dev, uint32_t n_parts, unsigned long long* gcount,

@@ -126,9 +126,13 @@ def test_high_load_split_geometry(split):
     """LF 0.97 on a table in the middle of a linear-hashing round (n_b = 2^12 +
     split, so the split-aware eviction victim has split buckets to aim at --
     few, many, all but one): every result, the stash-visible finds and the
-    final dump equal the oracle's, and Step 3 did run."""
+    final dump equal the oracle's, and Step 3 did run.  The oracle alone gets
+    a 30% stash: its paper-literal lowest-slot victim overflows the 2% stash in
+    split states (stash size changes no result unless it overflows; the GPU's
+    own stash stays at 2% and must not overflow)."""
+    from gpu_util import Pair
     nb = (1 << 12) + split
-    p = _pair(nb * 32, lf_grow=2.0, lf_shrink=0)
+    p = Pair(nb * 32, oracle_cfg={"stash_fraction": 0.30}, lf_grow=2.0, lf_shrink=0)
     n = int(0.97 * nb * 32)
     keys = gen.present_keys(n)
     for lo in range(0, n, n // 3 + 1):
@@ -256,11 +260,12 @@ def test_partitioned_owner_election_large_batches():
     p.find(rng.integers(0, 1 << 22, 1 << 20, dtype=np.uint64).astype(np.uint32))
 
 
-@pytest.mark.parametrize("env", [{}, {"HIVE_ELECT_JIT": "0"}, {"HIVE_ELECT_F": "1.2"}])
+@pytest.mark.parametrize("env", [{}, {"HIVE_ELECT_CHAIN": "0"}, {"HIVE_ELECT_JIT": "0"}, {"HIVE_ELECT_F": "1.2"}])
 def test_election_modes_over_many_phases(env):
     """Five rounds of duplicate-heavy 2^22-op partitioned phases (plus small
-    single-table phases in between) against the oracle: sub-tables cleared just
-    in time (default) or up front, and a denser sub-table (longer probes)."""
+    single-table phases in between) against the oracle: each part's sub-table
+    cleared by the previous part's launch (default), by a memset just before
+    it, or all up front; and a denser sub-table (longer probes)."""
     import os
     import subprocess
     import sys
