@@ -1282,44 +1282,74 @@ __device__ __forceinline__ void insert_slow_body(const uint32_t* __restrict__ ke
         // preferring residents in their second bucket raised p_h1 to 0.93 but
         // doubled evictions and grew the stash 5x -- a net loss).
         const bool evicting = busy && !placed;
-        int vs = (int)((seed + r * 11u) & 31u);
+        const int vrot = (int)((seed + r * 11u) & 31u);       // the rotating slot
+        int vs = vrot;
+        uint64_t victim;
+        bool alt_known = false;                              // nb_alt holds the victim's other bucket
+        uint32_t nb_alt = 0;
         // (not for the lookup-based CRC pair: its constant-memory hashes cost
         // more than the shorter chains save -- CRC inserts 4.28 -> 3.35 G/s)
         if (VICTIM_LOOK > 0 && tv.hkind != HASH_CRC) {
             // Split-aware victim (A-6 allows any rule; placement is not
-            // observable): VICTIM_LOOK candidate slots, VICTIM_LOOK / G per
-            // lane -- lane l's j-th candidate is its slot (vs + j) mod SPL --
-            // and the first (in (j, l) order) whose resident's other bucket is
-            // a split one (b < split or b > mask) is evicted: under linear
-            // hashing those hold half the keys of the unsplit buckets, so the
-            // chain likely ends there.  None: the rotating slot vs.
-            constexpr int PER_LANE = VICTIM_LOOK / G > 0 ? VICTIM_LOOK / G : 1;
-            uint32_t good = 0;
+            // observable): each lane offers NC candidates, its slots
+            // o, o + ST, o + 2 ST, ... (ST = SPL / NC, o = the rotating slot's
+            // offset mod ST, so a candidate is an ST-way select, not an
+            // SPL-way one); the first (in (j, lane) order) whose resident's
+            // other bucket is a split one (b < split or b > mask) is evicted --
+            // under linear hashing those hold half the keys of the unsplit
+            // buckets, so the chain likely ends there.  None: the rotating slot.
+            constexpr int NC = VICTIM_LOOK / G > 0 ? (VICTIM_LOOK / G < SPL ? VICTIM_LOOK / G : SPL) : 1;
+            constexpr int ST = SPL / NC;
+            const int o = vrot % ST;
+            uint64_t cand[NC];
+            uint32_t good = 0, first_alt = 0;                // this lane's first good candidate's bucket
+            bool found = false;
 #pragma unroll
-            for (int j = 0; j < PER_LANE; ++j) {
-                const int sl = (vs + j) % SPL;                 // this lane's candidate
+            for (int j = 0; j < NC; ++j) {
+                uint64_t c = s[j * ST];
+#pragma unroll
+                for (int i = 1; i < ST; ++i)
+                    if (i == o) c = s[j * ST + i];
+                cand[j] = c;
                 bool g = false;
-                if (evicting) {
-                    const uint64_t cand = pick<SPL>(s, sl);
-                    if (cand != EMPTY) {
-                        const uint32_t a = tv.alt(key_of(cand), b);
-                        g = a != b && (a < tv.split || a > tv.mask);
+                if (evicting && c != EMPTY) {
+                    const uint32_t a = tv.alt(key_of(c), b);
+                    g = a != b && (a < tv.split || a > tv.mask);
+                    if (g && !found) {
+                        first_alt = a;
+                        found = true;
                     }
                 }
                 good |= wg.ballot(g) << (j * G);              // bit j * G + lane
             }
+            int jv, lv;
             if (good) {
                 const int f = __ffs(good) - 1;
-                vs = (f % G) * SPL + (vs + f / G) % SPL;
+                jv = f / G;
+                lv = f % G;
+            } else {                                         // the rotating slot (its offset is o)
+                jv = (vrot % SPL) / ST;
+                lv = vrot / SPL;
             }
+            uint64_t w = cand[0];
+#pragma unroll
+            for (int j = 1; j < NC; ++j)
+                if (j == jv) w = cand[j];
+            vs = lv * SPL + jv * ST + o;
+            victim = wg.bcast(w, lv);
+            // the chosen (jv, lv) is lane lv's first good candidate (order is
+            // j first), so its bucket is that lane's first_alt
+            nb_alt = wg.bcast(first_alt, lv);
+            alt_known = good != 0;
+        } else {
+            victim = wg.bcast(pick<SPL>(s, vs % SPL), vs / SPL);
         }
         const int vl = vs / SPL;
-        const uint64_t victim = wg.bcast(pick<SPL>(s, vs % SPL), vl);
         const bool can = evicting && victim != EMPTY;
         // The victim's next bucket is known now: its load is issued right after
         // the swap CAS, so a round costs max(load, CAS) latency, not the sum.
         // A lost CAS discards the prefetched view (the round reloads b).
-        const uint32_t nb = can ? tv.alt(key_of(victim), b) : b;
+        const uint32_t nb = can ? (alt_known ? nb_alt : tv.alt(key_of(victim), b)) : b;
         uint64_t prev = victim;
         if (can && wg.gl == vl) {
             prev = cas64(tv.bucket(b) + vs, victim, kv);
