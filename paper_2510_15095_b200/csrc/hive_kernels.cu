@@ -660,6 +660,7 @@ k_elect_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ 
     __shared__ unsigned long long gbase[MAX_PARTS];
     constexpr int TILE = WITH_VALS ? ETILE / 2 : ETILE;    // 48 KB static shared memory
     __shared__ uint64_t stage[TILE];
+    __shared__ uint8_t stagep[TILE];                         // each staged record's part
     __shared__ uint32_t stagev[WITH_VALS ? TILE : 1];
     if (n_dev) n = *n_dev;
     constexpr int PER = TILE / BLOCK;
@@ -716,13 +717,14 @@ k_elect_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ 
             }
             const uint32_t op = idx ? idx[i] : (uint32_t)i;
             stage[loff[part] + (pr[j] & 0xFFFFu)] = ((uint64_t)op << 32) | k[j];
+            stagep[loff[part] + (pr[j] & 0xFFFFu)] = (uint8_t)part;
             if constexpr (WITH_VALS) stagev[loff[part] + (pr[j] & 0xFFFFu)] = vals[op];
         }
         __syncthreads();
         const uint32_t total = loff[n_parts];
         for (uint32_t e = threadIdx.x; e < total; e += BLOCK) {
             const uint64_t rec = stage[e];
-            const uint32_t part = elect_part((uint32_t)rec, n_parts);
+            const uint32_t part = stagep[e];
             recs[gbase[part] + (e - loff[part])] = rec;
             if constexpr (WITH_VALS) rvals[gbase[part] + (e - loff[part])] = stagev[e];
         }
