@@ -77,6 +77,59 @@ def test_ragged_mixed_batches(n):
         p.check_state()
 
 
+@pytest.mark.parametrize("n", [1 << 18, (1 << 22) + 4097])
+def test_mixed_batches_capture_in_a_cuda_graph(n):
+    """With growth and contraction off a PHASED mixed batch never waits on the
+    host (classification, elections -- single-table and partitioned with the
+    chained sub-table clears -- probes, fix-ups are all stream work), so two
+    batches capture into one CUDA graph.  Each replay, with new contents in
+    the same input buffers, gives the oracle's results for those batches."""
+    import oracle
+    from paper_2510_15095_b200 import HiveTable, u8, u32
+    cap = -(-n * 2 // 32) * 32 * 2
+    g = HiveTable(cap, lf_grow=2.0, lf_shrink=0)
+    o = oracle.OracleTable(cap, lf_grow=2.0, lf_shrink=0)
+    dev = torch.device("cuda")
+    bufs = [(torch.empty(n, dtype=torch.uint8, device=dev), torch.empty(n, dtype=torch.uint32, device=dev),
+             torch.empty(n, dtype=torch.uint32, device=dev), torch.empty(n, dtype=torch.uint32, device=dev),
+             torch.empty(n, dtype=torch.uint8, device=dev)) for _ in range(2)]
+    rng = np.random.default_rng(n)
+
+    def fill():
+        host = []
+        for ops_t, k_t, v_t, _, _ in bufs:
+            ops = rng.choice(np.array([0, 1, 2], np.uint8), size=n, p=[0.4, 0.4, 0.2])
+            keys = gen.keys_of(rng.integers(0, n, n, dtype=np.uint64).astype(np.uint32))   # duplicates
+            vals = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+            ops_t.copy_(u8(ops)); k_t.copy_(u32(keys)); v_t.copy_(u32(vals))
+            host.append((ops, keys, vals))
+        return host
+
+    s = torch.cuda.Stream()
+    fill()
+    with torch.cuda.stream(s):               # warm-up: sizes every scratch buffer, then reset
+        for ops_t, k_t, v_t, vo_t, r_t in bufs:
+            g.mixed(ops_t, k_t, v_t, vo_t, r_t, stream=s)
+    torch.cuda.synchronize()
+    g.clear()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        for ops_t, k_t, v_t, vo_t, r_t in bufs:
+            g.mixed(ops_t, k_t, v_t, vo_t, r_t, stream=s)
+    for rep in range(2):                     # the table carries over between replays
+        host = fill()
+        torch.cuda.synchronize()
+        graph.replay()
+        torch.cuda.synchronize()
+        for (ops, keys, vals), (_, _, _, vo_t, r_t) in zip(host, bufs):
+            v_o, r_o = o.mixed(ops, keys, vals)
+            assert (r_t.cpu().numpy() == r_o).all(), f"replay {rep}: mixed results"
+            assert (vo_t.cpu().numpy().astype(np.uint32) == v_o).all(), f"replay {rep}: mixed values"
+    assert g.stats()["count"] == o.stats()["count"]
+    del graph
+
+
 def test_duplicates_and_reserved_keys():
     """In-batch duplicates: statuses/erase outputs identical for duplicates
     (present at phase start), value = a member of the accepted set (this
