@@ -49,7 +49,7 @@ def num(row, units, m):
     return float(v.replace(",", "")) * SCALE.get(units.get(m, ""), 1)
 
 
-def main(tag, reps, ops=None):
+def main(tag, reps, ops=None, write_traffic=True):
     ops = ops or {}
     lines = [f"# ncu summary ({tag})", "", "Captured with `ncu --set full --clock-control none --import-source on` "
              "(cold cache, serialised replays: compare shares, not absolutes).", ""]
@@ -92,7 +92,8 @@ def main(tag, reps, ops=None):
                           f"{'' if at is None or not t else f'{at / t / 1e9:.1f}'} |")
     lines += per_op
     open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
-    json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+    if write_traffic:   # the cfg2 step kernels' DRAM bytes: bench.py's roofline.traffic source
+        json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
     print("\n".join(lines))
     print(json.dumps(traffic))
 
@@ -106,7 +107,9 @@ if __name__ == "__main__":
             k, v = args[i + 1].split("=")
             ops[k] = int(v)
             i += 2
+        elif args[i] == "--no-traffic":
+            i += 1
         else:
             reps.append(args[i])
             i += 1
-    main(sys.argv[1], reps, ops)
+    main(sys.argv[1], reps, ops, write_traffic="--no-traffic" not in sys.argv)
