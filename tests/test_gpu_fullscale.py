@@ -90,3 +90,37 @@ def test_cfg4_zipf_insert_to_lf_095():
     # every key, including the stashed ones, is found with the oracle's value
     allk = np.concatenate([gen.keys_of(ids[::7]), np.unique(k2)])
     p.find(allk)
+
+
+def test_cfg2_full_scale_vs_oracle():
+    """Config 2 -- the headline bench step -- at full size against the oracle,
+    not only its closed form: 2^26 keys into 2,207,529 buckets (LF 0.95, growth
+    off) in one batch, then the bench's 2^26 queries (50% hits); every insert
+    status, every lookup value / hit and the final key -> value set (sorted
+    dumps) are equal.  The oracle alone gets a 30% stash (its paper-literal
+    victim overflows 2% in split geometries; stash size changes no result
+    unless it overflows), and the GPU must not have dropped an entry."""
+    import oracle
+    from paper_2510_15095_b200 import HiveTable, u32
+    n = 1 << 26
+    cap = gen.CFG2_BUCKETS * 32
+    t = HiveTable(cap, lf_grow=2.0, lf_shrink=0)
+    o = oracle.OracleTable(cap, lf_grow=2.0, lf_shrink=0, stash_fraction=0.30)
+    ids = np.arange(n, dtype=np.uint32)
+    keys, vals = gen.keys_of(ids), gen.vals_of(ids)
+    st = t.insert(u32(keys), u32(vals)).cpu().numpy()
+    st_o = o.insert(keys, vals)
+    assert (st == st_o).all()
+    qids, _ = gen.mixed_queries(n // 2, n // 2, n, seed=202)
+    q = gen.keys_of(qids)
+    v, f = t.find(u32(q))
+    v_o, f_o = o.find(q)
+    assert (f.cpu().numpy() == f_o).all()
+    assert (v.cpu().numpy().astype(np.uint32) == v_o).all()
+    s = t.stats()
+    assert s["failed"] == 0 and s["count"] == o.stats()["count"] == n
+    kg, vg = t.dump()
+    kg, vg = kg.cpu().numpy().astype(np.uint32), vg.cpu().numpy().astype(np.uint32)
+    ko, vo = o.dump()
+    og, oo = np.argsort(kg, kind="stable"), np.argsort(ko, kind="stable")
+    assert (kg[og] == ko[oo]).all() and (vg[og] == vo[oo]).all()
