@@ -224,11 +224,8 @@ struct hive_table_s {
     uint64_t* dd = nullptr;   uint64_t dd_cap = 0;
     uint32_t* owner = nullptr; uint64_t owner_cap = 0;
     uint8_t* flag = nullptr;  uint64_t flag_cap = 0;
-    // second set: hive_mixed elects its ERASE phase before the control wait
-    // (small batches only: one sub-table, no partition scratch)
-    uint64_t* dd2 = nullptr;   uint64_t dd2_cap = 0;
-    uint32_t* owner2 = nullptr; uint64_t owner2_cap = 0;
-    uint8_t* flag2 = nullptr;  uint64_t flag2_cap = 0;
+    // (hive_mixed's paired election carves a second set -- its ERASE phase's
+    // table, owner ids and flags -- from the upper halves of these three)
     uint64_t* erec = nullptr; uint64_t erec_cap = 0;     // election records (op << 32 | key)
     uint32_t* rvals = nullptr; uint64_t rvals_cap = 0;   // fused insert: values in record order
     uint64_t* ftab = nullptr; uint64_t ftab_cap = 0;     // fused insert: the two epoch-tagged tables
@@ -545,18 +542,17 @@ bool elect_pair(hive_table_s* h, const uint32_t* keys, const uint32_t* idx_ins, 
     if (2 * n_upper * sizeof(uint64_t) > sub_bytes) return false;
     const uint64_t sub = pow2_at_least(std::max<uint64_t>(1024, 2 * n_upper));
     auto fail = [&](hive_status e) { *st = e; return false; };
-    if (hive_status e = ensure(h->dd, h->dd_cap, sub); e != HIVE_OK) return fail(e);
-    if (hive_status e = ensure(h->owner, h->owner_cap, n_batch); e != HIVE_OK) return fail(e);
-    if (hive_status e = ensure(h->flag, h->flag_cap, n_batch + 1); e != HIVE_OK) return fail(e);
-    if (hive_status e = ensure(h->dd2, h->dd2_cap, sub); e != HIVE_OK) return fail(e);
-    if (hive_status e = ensure(h->owner2, h->owner2_cap, n_batch); e != HIVE_OK) return fail(e);
-    if (hive_status e = ensure(h->flag2, h->flag2_cap, n_batch + 1); e != HIVE_OK) return fail(e);
+    // both scratch sets carved from one allocation each (tables, owner ids,
+    // flags), so each is cleared by ONE memset; the ERASE set's flags start
+    // 16-byte aligned (the duplicate fix-up scans them 16 per load)
+    const uint64_t fstride = (n_batch + 1 + 15) & ~15ull;
+    if (hive_status e = ensure(h->dd, h->dd_cap, 2 * sub); e != HIVE_OK) return fail(e);
+    if (hive_status e = ensure(h->owner, h->owner_cap, 2 * n_batch); e != HIVE_OK) return fail(e);
+    if (hive_status e = ensure(h->flag, h->flag_cap, 2 * fstride); e != HIVE_OK) return fail(e);
     *dd_ins = DedupView{h->dd, sub - 1, h->flag, h->owner, 1, h->flag + n_batch};
-    *dd_era = DedupView{h->dd2, sub - 1, h->flag2, h->owner2, 1, h->flag2 + n_batch};
-    cudaError_t e = cudaMemsetAsync(h->flag, 0, n_batch + 1, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(h->dd, 0xFF, sub * sizeof(uint64_t), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(h->flag2, 0, n_batch + 1, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(h->dd2, 0xFF, sub * sizeof(uint64_t), s);
+    *dd_era = DedupView{h->dd + sub, sub - 1, h->flag + fstride, h->owner + n_batch, 1, h->flag + fstride + n_batch};
+    cudaError_t e = cudaMemsetAsync(h->flag, 0, 2 * fstride, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->dd, 0xFF, 2 * sub * sizeof(uint64_t), s);
     if (e == cudaSuccess) {
         Prof p(h, "k_dedup_elect", s);
         e = launch_dedup_elect(h->grids.dedup, s, keys, idx_ins, n_upper, n_ins, *dd_ins, h->ctrl, idx_era, n_era,
@@ -1232,7 +1228,7 @@ hive_status hive_destroy(hive_t h) {
     vrange_free(h->ix);
     vrange_free(h->dr);
     vrange_free(h->sp);
-    void* bufs[] = {h->ctrl, h->rvals, h->ftab, h->dd, h->owner, h->flag, h->dd2, h->owner2, h->flag2, h->left, h->cls, h->cnt, h->pinfo, h->aborts,
+    void* bufs[] = {h->ctrl, h->rvals, h->ftab, h->dd, h->owner, h->flag, h->left, h->cls, h->cnt, h->pinfo, h->aborts,
                     h->erec, h->ecount, h->einfo, h->hk, h->hv, h->hst, h->fq, h->fv, h->ff};
     for (auto e : h->pipe_ev) cudaEventDestroy(e);
     if (h->ins_free) cudaEventDestroy(h->ins_free);
