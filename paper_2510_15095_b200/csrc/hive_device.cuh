@@ -109,6 +109,7 @@ struct Ctrl {
     unsigned long long step3;          // entries placed by the Step-3 loop (cumulative)
     unsigned long long xfail;          // sharded: ops not sent (padded exchange region full), sticky
     unsigned long long eover;          // fused election: a part's table overflowed (sticky; never expected)
+    unsigned long long cls_n[3];       // hive_mixed: ops per class (find, insert, erase) of the batch
     unsigned long long pad[1];
     // Algorithmic bytes touched, per kernel family: 256 per
     // bucket probe, 32 per CAS / atomic sector, 8 per spill word or stash word,

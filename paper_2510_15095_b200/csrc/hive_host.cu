@@ -224,6 +224,7 @@ struct hive_table_s {
     uint64_t* dd = nullptr;   uint64_t dd_cap = 0;
     uint32_t* owner = nullptr; uint64_t owner_cap = 0;
     uint8_t* flag = nullptr;  uint64_t flag_cap = 0;
+    uint64_t drains = 0;                                 // stash drains launched (hive_mixed bookkeeping)
     // (hive_mixed's paired election carves a second set -- its ERASE phase's
     // table, owner ids and flags -- from the upper halves of these three)
     uint64_t* erec = nullptr; uint64_t erec_cap = 0;     // election records (op << 32 | key)
@@ -531,11 +532,18 @@ hive_status elect_owners(hive_table_s* h, const uint32_t* keys, const uint32_t* 
 
 // Both elections of a mixed batch whose phases each fit one sub-table, in ONE
 // launch (hive_mixed, before the control wait): the INSERT list into the first
-// scratch set, the ERASE list into the second.  Returns false (nothing
-// enqueued) when a phase would need the partitioned election.
-bool elect_pair(hive_table_s* h, const uint32_t* keys, const uint32_t* idx_ins, const uint64_t* n_ins,
-                const uint32_t* idx_era, const uint64_t* n_era, uint64_t n_upper, uint64_t n_batch,
-                DedupView* dd_ins, DedupView* dd_era, cudaStream_t s, hive_status* st) {
+// scratch set, the ERASE list into the second.  pair_prepare sizes the sets and
+// returns the views plus the byte ranges to clear (flags to 0, tables to all
+// ones, done by the batch's k_batch_prep); false when a phase would need the
+// partitioned election.
+struct PairScratch {
+    DedupView ins{nullptr, 0, nullptr, nullptr}, era{nullptr, 0, nullptr, nullptr};
+    uint8_t* flag = nullptr;
+    uint64_t fbytes = 0;
+    uint64_t* dd = nullptr;
+    uint64_t dwords = 0;
+};
+bool pair_prepare(hive_table_s* h, uint64_t n_upper, uint64_t n_batch, PairScratch* ps, hive_status* st) {
     static const uint64_t sub_bytes = getenv("HIVE_ELECT_MB") ? (uint64_t)atoi(getenv("HIVE_ELECT_MB")) << 20
                                                               : (32ull << 20);
     *st = HIVE_OK;
@@ -543,25 +551,18 @@ bool elect_pair(hive_table_s* h, const uint32_t* keys, const uint32_t* idx_ins, 
     const uint64_t sub = pow2_at_least(std::max<uint64_t>(1024, 2 * n_upper));
     auto fail = [&](hive_status e) { *st = e; return false; };
     // both scratch sets carved from one allocation each (tables, owner ids,
-    // flags), so each is cleared by ONE memset; the ERASE set's flags start
-    // 16-byte aligned (the duplicate fix-up scans them 16 per load)
+    // flags); the ERASE set's flags start 16-byte aligned (the duplicate
+    // fix-up scans them 16 per load)
     const uint64_t fstride = (n_batch + 1 + 15) & ~15ull;
     if (hive_status e = ensure(h->dd, h->dd_cap, 2 * sub); e != HIVE_OK) return fail(e);
     if (hive_status e = ensure(h->owner, h->owner_cap, 2 * n_batch); e != HIVE_OK) return fail(e);
     if (hive_status e = ensure(h->flag, h->flag_cap, 2 * fstride); e != HIVE_OK) return fail(e);
-    *dd_ins = DedupView{h->dd, sub - 1, h->flag, h->owner, 1, h->flag + n_batch};
-    *dd_era = DedupView{h->dd + sub, sub - 1, h->flag + fstride, h->owner + n_batch, 1, h->flag + fstride + n_batch};
-    cudaError_t e = cudaMemsetAsync(h->flag, 0, 2 * fstride, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(h->dd, 0xFF, 2 * sub * sizeof(uint64_t), s);
-    if (e == cudaSuccess) {
-        Prof p(h, "k_dedup_elect", s);
-        e = launch_dedup_elect(h->grids.dedup, s, keys, idx_ins, n_upper, n_ins, *dd_ins, h->ctrl, idx_era, n_era,
-                               dd_era);
-    }
-    if (e != cudaSuccess) {
-        set_err(e, "elect_pair", __LINE__);
-        return fail(HIVE_ECUDA);
-    }
+    ps->ins = DedupView{h->dd, sub - 1, h->flag, h->owner, 1, h->flag + n_batch};
+    ps->era = DedupView{h->dd + sub, sub - 1, h->flag + fstride, h->owner + n_batch, 1, h->flag + fstride + n_batch};
+    ps->flag = h->flag;
+    ps->fbytes = 2 * fstride;
+    ps->dd = h->dd;
+    ps->dwords = 2 * sub;
     return true;
 }
 
@@ -608,7 +609,7 @@ hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* 
                          const uint64_t* kvs, const uint32_t* idx, uint64_t n_upper,
                          const uint64_t* n_dev, uint64_t n_batch, uint8_t* status,
                          uint32_t* vals_zero, cudaStream_t s, const InsertChunks* chunks = nullptr,
-                         const DedupView* pre = nullptr, DupFix* defer = nullptr) {
+                         const DedupView* pre = nullptr, DupFix* defer = nullptr, bool left_zeroed = false) {
     const bool dedup = !kvs && h->dedup_on();
     // large phases with election: the fused single-launch form, opt-in with
     // HIVE_FUSED=1 (measured slower than the multi-launch form)
@@ -620,7 +621,7 @@ hive_status insert_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* 
     else if (dedup) CKS(elect_owners(h, keys, idx, n_upper, n_dev, n_batch, &dd, s));
     CKS(ensure(h->left, h->left_cap, std::max<uint64_t>(n_upper, 1)));
     static_assert(offsetof(Ctrl, slow_next) == offsetof(Ctrl, n_left) + sizeof(uint64_t), "adjacent");
-    CK(cudaMemsetAsync(&h->ctrl->n_left, 0, 2 * sizeof(uint64_t), s));     // n_left + slow_next
+    if (!left_zeroed) CK(cudaMemsetAsync(&h->ctrl->n_left, 0, 2 * sizeof(uint64_t), s));   // n_left + slow_next
     if (chunks) {
         Prof p(h, "k_insert_fast", s);
         for (uint64_t off = 0, c = 0; off < n_upper; off += chunks->chunk, ++c) {
@@ -674,6 +675,7 @@ hive_status drain_reinsert(hive_table_s* h, cudaStream_t s, bool growing = false
         4 * h->tail_known < h->stash_cap && h->tail_known + n_ins / 16 < h->stash_cap)
         return HIVE_OK;
     h->nb_at_drain = h->nb();
+    ++h->drains;                       // hive_mixed: the Step-3 cursors are no longer zero
     const uint64_t used = std::min<uint64_t>(h->tail_known, h->stash_cap);
     Trace tr("drain", used);
     CKS(vrange_map(h, h->dr, used * sizeof(uint64_t)));
@@ -850,42 +852,57 @@ hive_status mixed_impl(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
     // classify: op indices by opcode into 3 regions of n (one pass; order
     // inside a region is not the op order -- every phase is order-free)
     CKS(ensure(h->cls, h->cls_cap, 3 * n));
+    // one launch resets the batch's counters and the paired election's
+    // scratch (the class counts live in the control block, so the control
+    // read below brings them along)
+    const bool early = h->cfg.lf_grow < 1.0f;       // elections before the control wait
+    PairScratch ps;
+    bool pair = false;
+    if (early && h->dedup_on()) {
+        hive_status e2 = HIVE_OK;
+        pair = pair_prepare(h, n, n, &ps, &e2);
+        CKS(e2);
+    }
+    CK(launch_batch_prep(s, h->ctrl, true, pair ? ps.flag : nullptr, pair ? ps.fbytes : 0, pair ? ps.dd : nullptr,
+                         pair ? ps.dwords : 0, h->num_sms));
+    const uint64_t drains0 = h->drains;
+    uint64_t* cls_n = reinterpret_cast<uint64_t*>(h->ctrl->cls_n);
     {
         Prof p(h, "k_classify", s);
-        CK(launch_classify(s, d_op, n, n_dev, h->pinfo, h->cls, n, d_result, d_vals_out, h->num_sms));
+        CK(launch_classify(s, d_op, n, n_dev, cls_n, h->cls, n, d_result, d_vals_out, h->num_sms, true));
     }
-    const uint64_t* n_find = h->pinfo + 0;
-    const uint64_t* n_ins = h->pinfo + 1;
-    const uint64_t* n_era = h->pinfo + 2;
+    const uint64_t* n_find = cls_n + 0;
+    const uint64_t* n_ins = cls_n + 1;
+    const uint64_t* n_era = cls_n + 2;
     int64_t count_lb = -1;
     DedupView dd_ins{nullptr, 0, nullptr, nullptr}, dd_era{nullptr, 0, nullptr, nullptr};
     bool pre = false, pre_era = false;
-    if (h->cfg.lf_grow < 1.0f) {           // one wait: phase sizes + counters
+    if (early) {                           // one wait: phase sizes + counters
         if (!h->ctrl_ev) CK(cudaEventCreateWithFlags(&h->ctrl_ev, cudaEventDisableTiming));
-        CK(cudaMemcpyAsync(h->stage_h, h->pinfo, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(h->ctrl_h, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
         CK(cudaEventRecord(h->ctrl_ev, s));
-        // The insert phase's owner election does not depend on the table
-        // geometry: enqueue it before waiting, so the GPU has work while the
-        // host plans the resize from the count it just read.
-        if (h->dedup_on()) {
-            hive_status e2 = HIVE_OK;
-            pre = pre_era = elect_pair(h, d_keys, h->cls + n, n_ins, h->cls + 2 * n, n_era, n, n, &dd_ins, &dd_era,
-                                       s, &e2);
-            CKS(e2);
-            if (!pre) {                      // large batch: the INSERT phase's partitioned election
-                CKS(elect_owners(h, d_keys, h->cls + n, n, n_ins, n, &dd_ins, s));
-                pre = true;
-            }
+        // The owner elections do not depend on the table geometry: enqueue
+        // them before waiting, so the GPU has work while the host plans the
+        // resize from the count it just read.
+        if (pair) {
+            dd_ins = ps.ins;
+            dd_era = ps.era;
+            Prof p(h, "k_dedup_elect", s);
+            CK(launch_dedup_elect(h->grids.dedup, s, d_keys, h->cls + n, n, n_ins, dd_ins, h->ctrl, h->cls + 2 * n,
+                                  n_era, &dd_era));
+            pre = pre_era = true;
+        } else if (h->dedup_on()) {          // large batch: the INSERT phase's partitioned election
+            CKS(elect_owners(h, d_keys, h->cls + n, n, n_ins, n, &dd_ins, s));
+            pre = true;
         }
         {
             Trace tr("read_ctrl", 0);
             CK(cudaEventSynchronize(h->ctrl_ev));
         }
         h->tail_known = h->ctrl_h->stash_tail;
-        const uint64_t count0 = h->ctrl_h->count, n_erase = h->stage_h[2];
+        const uint64_t count0 = h->ctrl_h->count, n_erase = h->ctrl_h->cls_n[2], n_insert = h->ctrl_h->cls_n[1];
         count_lb = count0 > n_erase ? (int64_t)(count0 - n_erase) : 0;
-        if (h->stage_h[1]) CKS(grow_known(h, count0, h->stage_h[1], s));
+        if (n_insert) CKS(grow_known(h, count0, n_insert, s));
     }
     // each phase's duplicate fix-up runs as the prologue of the next phase's
     // kernel (they write results of different op classes): two launches less.
@@ -894,7 +911,7 @@ hive_status mixed_impl(hive_t h, const uint8_t* d_op, const uint32_t* d_keys, co
     // the first set's flags and the fix-up must run before it.
     DupFix fix_ins, fix_era;
     CKS(insert_phase(h, d_keys, d_vals, nullptr, h->cls + n, n, n_ins, n, d_result, d_vals_out, s, nullptr,
-                     pre ? &dd_ins : nullptr, pre_era ? &fix_ins : nullptr));
+                     pre ? &dd_ins : nullptr, pre_era ? &fix_ins : nullptr, h->drains == drains0));
     CKS(erase_phase(h, d_keys, h->cls + 2 * n, n, n_era, n, d_result, d_vals_out, s, pre_era ? &dd_era : nullptr,
                     pre_era ? &fix_ins : nullptr, &fix_era));
     CKS(shrink_after(h, s, count_lb));

@@ -2627,10 +2627,34 @@ k_classify(const uint8_t* __restrict__ ops, uint64_t n, const uint64_t* __restri
         __syncthreads();                                  // wtot / woff reuse
     }
 }
+// Per-batch scratch reset of hive_mixed in ONE launch (each cudaMemsetAsync
+// on this path cost a few microseconds of GPU time per batch): the class
+// counts, the Step-3 list cursor pair, the paired election's flags (zero) and
+// sub-tables (all ones).  fbytes and dwords are multiples of 16 and 2.
+__global__ void __launch_bounds__(BLOCK)
+k_batch_prep(Ctrl* ctrl, int zero_left, uint4* __restrict__ flag, uint64_t f16, uint4* __restrict__ dd, uint64_t d16) {
+    const uint64_t tid = (uint64_t)blockIdx.x * BLOCK + threadIdx.x, stride = (uint64_t)gridDim.x * BLOCK;
+    if (tid == 0) {
+        ctrl->cls_n[0] = ctrl->cls_n[1] = ctrl->cls_n[2] = 0;
+        if (zero_left) ctrl->n_left = ctrl->slow_next = 0;
+    }
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u), o = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (uint64_t i = tid; i < f16; i += stride) flag[i] = z;
+    for (uint64_t i = tid; i < d16; i += stride) dd[i] = o;
+}
+cudaError_t launch_batch_prep(cudaStream_t s, Ctrl* ctrl, bool zero_left, uint8_t* flag, uint64_t fbytes,
+                              uint64_t* dd, uint64_t dwords, int num_sms) {
+    const uint64_t work = std::max<uint64_t>(fbytes / 16, dwords / 2);
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((work + BLOCK - 1) / BLOCK, (uint64_t)num_sms * 8));
+    k_batch_prep<<<grid, BLOCK, 0, s>>>(ctrl, zero_left ? 1 : 0, reinterpret_cast<uint4*>(flag), fbytes / 16,
+                                        reinterpret_cast<uint4*>(dd), dwords / 2);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_classify(cudaStream_t s, const uint8_t* ops, uint64_t n, const uint64_t* n_dev,
                             uint64_t* counts, uint32_t* out_idx, uint64_t stride, uint8_t* result_zero,
-                            uint32_t* vals_zero, int num_sms) {
-    cudaError_t e = cudaMemsetAsync(counts, 0, 3 * sizeof(uint64_t), s);
+                            uint32_t* vals_zero, int num_sms, bool counts_zeroed) {
+    cudaError_t e = counts_zeroed ? cudaSuccess : cudaMemsetAsync(counts, 0, 3 * sizeof(uint64_t), s);
     if (e != cudaSuccess || n == 0) return e;
     const int grid = (int)std::min<uint64_t>((n + CTILE - 1) / CTILE, (uint64_t)num_sms * 8);
     k_classify<<<grid, BLOCK, 0, s>>>(ops, n, n_dev, reinterpret_cast<unsigned long long*>(counts), out_idx, stride,

@@ -128,7 +128,11 @@ cudaError_t launch_dup_copy(int grid, cudaStream_t s, const uint32_t* idx, uint6
 // tile reservation order (not op order); other opcodes: result / value 0.
 cudaError_t launch_classify(cudaStream_t s, const uint8_t* ops, uint64_t n, const uint64_t* n_dev,
                             uint64_t* counts, uint32_t* out_idx, uint64_t stride, uint8_t* result_zero,
-                            uint32_t* vals_zero, int num_sms);
+                            uint32_t* vals_zero, int num_sms, bool counts_zeroed = false);
+// hive_mixed's per-batch reset in one launch: ctrl->cls_n, (zero_left) the
+// Step-3 cursors, flag[0, fbytes) = 0, dd[0, dwords) = ~0 (either nullable).
+cudaError_t launch_batch_prep(cudaStream_t s, Ctrl* ctrl, bool zero_left, uint8_t* flag, uint64_t fbytes,
+                              uint64_t* dd, uint64_t dwords, int num_sms);
 
 cudaError_t launch_split(cudaStream_t s, TableView tv, uint32_t n_pairs, Ctrl* ctrl);
 cudaError_t launch_merge(cudaStream_t s, TableView tv, uint32_t n_pairs, unsigned long long* abort_at,
