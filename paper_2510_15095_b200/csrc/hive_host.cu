@@ -254,6 +254,11 @@ struct hive_table_s {
 
     uint64_t grows = 0, shrinks = 0, merge_aborts = 0;
     uint64_t tail_known = 0;           // stash_tail at the last synchronising read
+    // The stash has had no push since its last full reset, which left ring
+    // words [0, ring_clean) and index words [0, idx_clean) EMPTY: a resize
+    // then clears only the newly exposed words.
+    bool stash_clean = false;
+    uint64_t ring_clean = 0, idx_clean = 0;
     unsigned long long* aborts = nullptr;   // per-segment first aborting merge pair
 
     // profiling
@@ -474,6 +479,30 @@ hive_status stash_reset(hive_table_s* h, uint64_t cap, cudaStream_t s) {
     CK(launch_stash_reset(s, h->sv()));
     CKS(set_ctrl_word(h, &h->ctrl->stash_tail, 0, s));
     h->tail_known = 0;
+    h->stash_clean = true;
+    h->ring_clean = cap;
+    h->idx_clean = ic;
+    return HIVE_OK;
+}
+
+// Resize of an EMPTY stash (tail read as 0 at this phase, so no push since its
+// last full reset): the ring and the index are all EMPTY up to the cleared
+// extents and the index holds nothing to rehash, so only the words the new
+// capacity exposes are cleared (one launch), and stash_tail is already 0.
+hive_status stash_resize_empty(hive_table_s* h, uint64_t cap, cudaStream_t s) {
+    if (!h->stash_clean) return stash_reset(h, cap, s);
+    const uint64_t ic = pow2_at_least(2 * cap);
+    CKS(vrange_map(h, h->rg, cap * sizeof(uint64_t)));
+    CKS(vrange_map(h, h->dr, cap * sizeof(uint64_t)));
+    CKS(vrange_map(h, h->ix, ic * sizeof(uint64_t)));
+    h->ring = (uint64_t*)h->rg.va;
+    h->sidx = (uint64_t*)h->ix.va;
+    const uint64_t r0 = std::min(h->ring_clean, cap), i0 = std::min(h->idx_clean, ic);
+    CK(launch_fill2(s, h->ring + r0, cap - r0, h->sidx + i0, ic - i0, h->num_sms));
+    h->ring_clean = std::max(h->ring_clean, cap);
+    h->idx_clean = std::max(h->idx_clean, ic);
+    h->stash_cap = cap;
+    h->idx_cap = ic;
     return HIVE_OK;
 }
 
@@ -667,7 +696,7 @@ hive_status drain_reinsert(hive_table_s* h, cudaStream_t s, bool growing = false
     static const bool every = getenv("HIVE_DRAIN_EVERY") && atoi(getenv("HIVE_DRAIN_EVERY")) != 0;
     const uint64_t new_cap = h->stash_cap_for(h->nb());
     if (h->tail_known == 0) {
-        if (new_cap != h->stash_cap) CKS(stash_reset(h, new_cap, s));
+        if (new_cap != h->stash_cap) CKS(stash_resize_empty(h, new_cap, s));
         h->nb_at_drain = h->nb();
         return HIVE_OK;
     }
@@ -1522,6 +1551,7 @@ hive_status hive_load_image(hive_t h, const uint64_t* d_slots, uint64_t n_bucket
     CK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), s));
     CKS(stash_reset(h, cap, s));
     CK(launch_image(s, h->tv(), n_buckets, h->sv(), d_stash, n_stash));
+    if (n_stash) h->stash_clean = false;
     // live count = occupied slots + stash entries: counted by the dump kernel
     CKS(set_ctrl_word(h, &h->ctrl->dump_n, 0, s));
     CK(launch_dump(h->grids.stream, s, h->tv(), n_buckets, h->sv(), nullptr, nullptr, 0));

@@ -3053,6 +3053,23 @@ cudaError_t launch_unpack(cudaStream_t s, const uint64_t* kv, uint64_t n, uint32
     return cudaGetLastError();
 }
 
+// Two word ranges set to EMPTY in one launch (the growth of a clean stash:
+// only the newly exposed ring and index words).
+__global__ void __launch_bounds__(BLOCK)
+k_fill2(uint64_t* __restrict__ a, uint64_t na, uint64_t* __restrict__ b, uint64_t nb) {
+    const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
+    for (uint64_t i = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; i < na + nb; i += stride) {
+        if (i < na) a[i] = EMPTY;
+        else b[i - na] = EMPTY;
+    }
+}
+cudaError_t launch_fill2(cudaStream_t s, uint64_t* a, uint64_t na, uint64_t* b, uint64_t nb, int num_sms) {
+    if (na + nb == 0) return cudaSuccess;
+    const int grid = (int)std::min<uint64_t>((na + nb + BLOCK - 1) / BLOCK, (uint64_t)num_sms * 4);
+    k_fill2<<<grid, BLOCK, 0, s>>>(a, na, b, nb);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_stash_reset(cudaStream_t s, StashView sv) {
     cudaError_t e = cudaMemsetAsync(sv.ring, 0xFF, sv.cap * sizeof(uint64_t), s);
     if (e != cudaSuccess) return e;

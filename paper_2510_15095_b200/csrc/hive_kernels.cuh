@@ -140,6 +140,8 @@ cudaError_t launch_merge(cudaStream_t s, TableView tv, uint32_t n_pairs, unsigne
 constexpr int MAX_SEGMENTS = 64;        // linear-hashing rounds crossed by one resize phase
 
 cudaError_t launch_stash_reset(cudaStream_t s, StashView sv);
+// a[0, na) and b[0, nb) (64-bit words) set to EMPTY in one launch.
+cudaError_t launch_fill2(cudaStream_t s, uint64_t* a, uint64_t na, uint64_t* b, uint64_t nb, int num_sms);
 
 // hive_load_image: spill words of the loaded buckets, stash ring + index + spill bits.
 cudaError_t launch_image(cudaStream_t s, TableView tv, uint64_t n_buckets, StashView sv, const uint64_t* stash,
