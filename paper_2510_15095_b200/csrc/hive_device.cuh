@@ -57,18 +57,24 @@ __device__ __forceinline__ uint32_t bithash2(uint32_t key) {
 // bytes; the CRC-64 result is reduced to its low 32 bits.  The tables are
 // filled by init_hash_tables() (hive_kernels.cu) — only that translation unit's
 // copy is ever read.
-static __constant__ uint32_t c_crc32_tab[256];
-static __constant__ uint64_t c_crc64_tab[256];
+// The tables live in global memory and are read through the read-only L1
+// path (__ldg), not in __constant__ memory as in the paper's design: the 32
+// lanes of a warp index a table at 32 different bytes, which the constant
+// cache serves one address at a time, while L1 serves them as a few sector
+// wavefronts.
+static __device__ uint32_t c_crc32_tab[256];
+static __device__ uint64_t c_crc64_tab[256];
 __device__ __forceinline__ uint32_t crc32_key(uint32_t key) {
     uint32_t c = 0xFFFFFFFFu;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) c = c_crc32_tab[(c ^ (key >> (8 * i))) & 0xFFu] ^ (c >> 8);
+    for (int i = 0; i < 4; ++i) c = __ldg(&c_crc32_tab[(c ^ (key >> (8 * i))) & 0xFFu]) ^ (c >> 8);
     return ~c;
 }
 __device__ __forceinline__ uint32_t crc64_key(uint32_t key) {
     uint64_t c = ~0ull;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) c = c_crc64_tab[(c ^ (key >> (8 * i))) & 0xFFu] ^ (c >> 8);
+    for (int i = 0; i < 4; ++i)
+        c = __ldg(reinterpret_cast<const unsigned long long*>(&c_crc64_tab[(c ^ (key >> (8 * i))) & 0xFFu])) ^ (c >> 8);
     return (uint32_t)~c;
 }
 enum HashKind : uint32_t { HASH_BITHASH = 0, HASH_CRC = 1 };
