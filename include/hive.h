@@ -68,7 +68,7 @@ typedef enum {
 #define HIVE_HASH_CRC    2u   /* use the lookup-based hash pair of §V-B
                                  (PAPER:569-574): h1 = CRC-32/IEEE, h2 = low 32
                                  bits of CRC-64/XZ, over the 4 little-endian key
-                                 bytes, byte-wise tables in constant memory
+                                 bytes, byte-wise tables read through the L1 read-only path
                                  (reading A-26).  Default (flag clear):
                                  BitHash1 / BitHash2 (Listing 1).  Any other
                                  flag bit -> HIVE_EINVAL. */
@@ -426,7 +426,7 @@ hive_status hive_ipc_close(void* d_ptr);
 /* ---- hash study (§III-C Listing 1 / Theorem 1 / CSR, §V-B pairs) -------------
  * Hash functions by id: BitHash1 / BitHash2 (Listing 1), CRC-32
  * (IEEE) and the low 32 bits of CRC-64 (XZ), both over the 4 little-endian key
- * bytes from constant-memory tables (reading A-26). */
+ * bytes from 256-entry tables (reading A-26; read-only L1 path, not constant memory). */
 #define HIVE_FN_BITHASH1 0u
 #define HIVE_FN_BITHASH2 1u
 #define HIVE_FN_CRC32    2u

@@ -840,7 +840,7 @@ hive_status erase_phase(hive_table_s* h, const uint32_t* keys, const uint32_t* i
 
 // ---- host-buffer pipeline -----------------------------------------------------------
 namespace {
-// CRC constant tables are per device (module constant memory): fill them once.
+// CRC constant tables are per device (module __device__ arrays): fill them once.
 bool ensure_hash_tables() {
     static std::mutex mu;
     static bool done[64] = {};

@@ -1289,8 +1289,9 @@ __device__ __forceinline__ void insert_slow_body(const uint32_t* __restrict__ ke
         uint64_t victim;
         bool alt_known = false;                              // nb_alt holds the victim's other bucket
         uint32_t nb_alt = 0;
-        // (not for the lookup-based CRC pair: its constant-memory hashes cost
-        // more than the shorter chains save -- CRC inserts 4.28 -> 3.35 G/s)
+        // (not for the lookup-based CRC pair: on, it lifts CRC inserts
+        // 8.15 -> 8.33 G/s but the extra branch costs the default BitHash
+        // kernels ~0.5%, profiles/r02f_crc_victim_ab.txt)
         if (VICTIM_LOOK > 0 && tv.hkind != HASH_CRC) {
             // Split-aware victim (A-6 allows any rule; placement is not
             // observable): each lane offers NC candidates, its slots
@@ -2385,7 +2386,7 @@ static int env_g(const char* name, int dflt) {
     }
 
 // Byte-wise CRC tables of the §V-B lookup-based pair (reading A-26), written
-// to this module's constant memory on the current device.
+// to this module's __device__ arrays on the current device.
 cudaError_t init_hash_tables() {
     uint32_t t32[256];
     uint64_t t64[256];
